@@ -1,0 +1,203 @@
+/*
+ * gfb.h -- C ABI of the B200-native SSSP hot path ("graflow-b200").
+ *
+ * This is the drop-in boundary for the reference's BSP single-source shortest
+ * path (graflow, arXiv 2212.08200; paths below are relative to the
+ * reference's proj/ directory).  The reference is header-only C++20; its
+ * device execution policy (include/graflow_b200/device.hpp in this repo) is
+ * the binding a graflow maintainer adds, and it calls exactly these entry
+ * points.  Plain pointers and sizes only; no exceptions cross the ABI.
+ *
+ * Conventions
+ *  - Every function returns a gfb_status.  On failure gfb_last_error() holds
+ *    a thread-local message.  The C++ shim maps GFB_EINVAL ->
+ *    std::invalid_argument, GFB_ERANGE -> std::out_of_range, GFB_ELOGIC ->
+ *    std::logic_error, everything else -> std::runtime_error, mirroring the
+ *    reference's throw sites (cited per function).
+ *  - Host arrays are caller-owned and only read/written during the call.
+ *    Device memory is owned by the opaque handles and released by the
+ *    matching _free/_destroy.
+ *  - Calls are synchronous at operator granularity: no device work of a call
+ *    is still running when it returns (the reference's barrier contract,
+ *    operators.hpp:248-254; test_operators.cpp:104-117).
+ *  - One gfb_ctx per host thread (it owns one CUDA stream).
+ */
+#ifndef GFB_H
+#define GFB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GFB_NIL 0xFFFFFFFFu /* types.hpp:13 no_predecessor */
+
+typedef enum gfb_status {
+  GFB_OK = 0,
+  GFB_EINVAL = 1, /* std::invalid_argument */
+  GFB_ERANGE = 2, /* std::out_of_range */
+  GFB_ELOGIC = 3, /* std::logic_error */
+  GFB_ECUDA = 4,  /* std::runtime_error (CUDA) */
+  GFB_ENOMEM = 5, /* std::runtime_error (device memory) */
+  GFB_ENCCL = 6   /* std::runtime_error (NCCL) */
+} gfb_status;
+
+/* Edge-weight / distance arithmetic.  The reference computes in double
+ * (types.hpp:10 weight_t = double).  GFB_W_F64 reproduces it bit for bit;
+ * GFB_W_U32 is exact for integer weights (dist widened to double on read);
+ * GFB_W_F32 is the bandwidth mode (fp32 fixpoint). */
+typedef enum gfb_wtype { GFB_W_U32 = 0, GFB_W_F32 = 1, GFB_W_F64 = 2 } gfb_wtype;
+
+/* algorithms.hpp:467 Direction, plus AUTO (device push<->pull switch). */
+typedef enum gfb_direction {
+  GFB_DIR_PUSH = 0,
+  GFB_DIR_PULL = 1,
+  GFB_DIR_AUTO = 2
+} gfb_direction;
+
+/* frontier.hpp:18 FrontierRepr (queue is the async model: out of scope). */
+typedef enum gfb_repr { GFB_SPARSE = 0, GFB_DENSE = 1 } gfb_repr;
+
+/* Operator conditions.  Host C++ lambdas cannot cross a C ABI, so the device
+ * policy accepts these recognised conditions (include/graflow_b200/ops.hpp):
+ *   RELAX_MIN -- the SSSP relax lambda, algorithms.hpp:586-593;
+ *   RECORD    -- record every (src,dst,edge) invocation, return false
+ *                (test_operators.cpp:151-171 eligibility recorder);
+ *   ALWAYS    -- return true (test_operators.cpp:27 `always`). */
+typedef enum gfb_op { GFB_OP_RELAX_MIN = 0, GFB_OP_RECORD = 1, GFB_OP_ALWAYS = 2 } gfb_op;
+
+typedef struct gfb_ctx gfb_ctx;
+typedef struct gfb_graph gfb_graph;
+typedef struct gfb_frontier gfb_frontier;
+typedef struct gfb_dist gfb_dist;     /* device distance map + relax counter */
+typedef struct gfb_record gfb_record; /* device (src,dst,edge) recorder */
+
+/* ---- errors / version -------------------------------------------------- */
+int gfb_version(void);
+const char* gfb_last_error(void);
+
+/* ---- context (one CUDA stream on one device) ---------------------------- */
+int gfb_ctx_create(int device, gfb_ctx** out);
+int gfb_ctx_destroy(gfb_ctx* ctx);
+int gfb_ctx_num_sms(gfb_ctx* ctx, int* out);
+
+/* ---- graph store (graph.hpp:63-145 Graph) --------------------------------
+ * gfb_graph_upload takes the reference Graph's CSR arrays as they are
+ * (row_offsets(), column_indices(), values(): graph.hpp:94-96; values are
+ * `double` in the reference, or u32/f32 for the typed modes) and builds the
+ * device CSR (interleaved {dst, weight} records) and, when build_csc != 0,
+ * the CSC view of build_transpose (graph.hpp:184-211; slot order ascending
+ * (src, CSR edge id), with the edge-id back-map).  `wtype` is the device
+ * arithmetic; `w_host_type` the element type of `w` (GFB_W_F64 when passing
+ * the reference's values() directly).
+ * Validation mirrors build_csr (graph.hpp:152-160): a dst >= n, a negative or
+ * non-finite weight, or an inconsistent row_offsets array -> GFB_EINVAL
+ * naming the first offending edge.  -0.0 weights are canonicalised to +0.0. */
+int gfb_graph_upload(gfb_ctx* ctx, uint64_t n, uint64_t m,
+                     const uint32_t* row_offsets, const uint32_t* col,
+                     const void* w, int w_host_type, int wtype, int build_csc,
+                     gfb_graph** out);
+/* Re-copy new CSR contents of the same shape into an existing graph. */
+int gfb_graph_refill(gfb_graph* g, const uint32_t* row_offsets,
+                     const uint32_t* col, const void* w, int w_host_type);
+int gfb_graph_free(gfb_graph* g);
+int gfb_graph_info(const gfb_graph* g, uint64_t* n, uint64_t* m, int* wtype,
+                   int* has_csc);
+/* Copy the device CSR back (w in the graph's wtype; any pointer may be 0). */
+int gfb_graph_download(gfb_graph* g, uint32_t* row_offsets, uint32_t* col,
+                       void* w);
+/* Device-side synthetic graphs: counter-based RMAT
+ * (A/B/C/D = .57/.19/.19/.05, unpermuted, duplicates and self-loops kept;
+ * wtype U32 -> U{0..255}, F32 -> U[0,1) on a 2^-24 grid) and the 4-neighbour
+ * grid.  Built on the device in build_csr's layout (graph.hpp:162-179). */
+int gfb_graph_generate_rmat(gfb_ctx* ctx, int scale, int edgefactor,
+                            uint64_t seed, int wtype, int build_csc,
+                            gfb_graph** out);
+int gfb_graph_generate_grid(gfb_ctx* ctx, uint32_t side, uint64_t seed,
+                            int build_csc, gfb_graph** out);
+
+/* ---- frontier (frontier.hpp:37-218 Frontier, sparse + dense) ------------ */
+int gfb_frontier_create(gfb_ctx* ctx, uint64_t n, int repr, gfb_frontier** out);
+int gfb_frontier_free(gfb_frontier* f);
+/* add_vertex semantics (frontier.hpp:73-96): sparse keeps duplicates and
+ * order, dense is a set.  Vertex >= n -> GFB_ERANGE. */
+int gfb_frontier_assign(gfb_frontier* f, const uint32_t* vertices, uint64_t k);
+/* size() (frontier.hpp:57-67): sparse counts duplicates, dense set bits. */
+int gfb_frontier_size(gfb_frontier* f, uint64_t* size);
+/* Contents: sparse in insertion order (device order for device-produced
+ * frontiers), dense ascending (get_active_vertex, frontier.hpp:100-122). */
+int gfb_frontier_read(gfb_frontier* f, uint32_t* out, uint64_t cap, uint64_t* k);
+int gfb_frontier_repr(gfb_frontier* f, int* repr);
+
+/* ---- operator state ------------------------------------------------------ */
+int gfb_dist_create(gfb_ctx* ctx, const gfb_graph* g, gfb_dist** out);
+int gfb_dist_free(gfb_dist* d);
+/* dist = +inf everywhere, dist[source] = 0 (algorithms.hpp:579-583). */
+int gfb_dist_init(gfb_dist* d, uint32_t source);
+/* Widened to double (exact for every wtype); relaxations may be 0. */
+int gfb_dist_read(gfb_dist* d, double* dist, uint64_t* relaxations);
+int gfb_record_create(gfb_ctx* ctx, uint64_t capacity, gfb_record** out);
+int gfb_record_free(gfb_record* r);
+int gfb_record_read(gfb_record* r, uint32_t* src, uint32_t* dst, uint32_t* edge,
+                    uint64_t cap, uint64_t* count);
+
+/* ---- operators (operators.hpp) -------------------------------------------
+ * Push advance, operators.hpp:255-288 neighbors_expand: for every frontier
+ * element (duplicates included) and every out-edge, cond exactly once; the
+ * output has one entry per true cond (sparse) or is a set (dense); output
+ * representation = input representation.  `state` is a gfb_dist* for
+ * RELAX_MIN, a gfb_record* for RECORD, unused for ALWAYS. */
+int gfb_advance_push(gfb_ctx* ctx, const gfb_graph* g, gfb_frontier* in,
+                     gfb_frontier* out, int op, void* state);
+/* Pull advance, operators.hpp:296-334 neighbors_expand_pull: input must be
+ * dense (else GFB_EINVAL, :301-302), graph must have the CSC (else
+ * GFB_EINVAL, :299-300); cond runs for every eligible in-edge; output dense. */
+int gfb_advance_pull(gfb_ctx* ctx, const gfb_graph* g, gfb_frontier* in,
+                     gfb_frontier* out, int op, void* state);
+/* uniquify, operators.hpp:411-420: sparse in (else GFB_EINVAL), ascending
+ * duplicate-free sparse out.  Bitmap dedup + warp-ballot compaction. */
+int gfb_filter_unique(gfb_ctx* ctx, gfb_frontier* in, gfb_frontier* out);
+
+/* ---- the entry point: sssp() (algorithms.hpp:569-623) -------------------- */
+typedef struct gfb_sssp_opts {
+  uint32_t struct_size;  /* sizeof(gfb_sssp_opts) */
+  int32_t direction;     /* gfb_direction; AUTO default */
+  float pull_alpha;      /* AUTO: pull when frontier edges > m / pull_alpha */
+  int32_t device_loop;   /* 1: device-side convergence (CUDA graph) */
+  double delta;          /* >0: near-far filter with this width; 0: plain BSP */
+  int32_t compute_pred;  /* 1: fill pred (tight-edge tree) */
+  int32_t reserved[7];
+} gfb_sssp_opts;
+
+void gfb_sssp_opts_default(gfb_sssp_opts* o);
+
+typedef struct gfb_sssp_stats {
+  uint64_t supersteps;    /* SsspResult::supersteps, algorithms.hpp:494 */
+  uint64_t relaxations;   /* SsspResult::relaxations, algorithms.hpp:495 */
+  uint64_t n_reach;       /* vertices with finite dist */
+  uint64_t m_reach;       /* sum of out-degrees of reached vertices */
+  uint64_t push_steps, pull_steps;
+  uint64_t pred_fallback; /* vertices whose pred needed the repair pass */
+  double device_ms;       /* CUDA-event time: init .. last superstep + pred */
+  double advance_ms;      /* CUDA-event time of the advance launches (sum) */
+  uint64_t advance_launches;
+} gfb_sssp_stats;
+
+/* Runs init, the BSP loop and the predecessor pass on the device.  dist is
+ * written widened to double (n entries), pred as u32 with GFB_NIL for the
+ * source and unreachable vertices; either may be NULL to leave the result on
+ * the device (gfb_sssp_read fetches it later).  source >= n -> GFB_ERANGE
+ * (algorithms.hpp:572); PULL without CSC -> GFB_EINVAL (:573-574). */
+int gfb_sssp(gfb_ctx* ctx, gfb_graph* g, uint32_t source,
+             const gfb_sssp_opts* opts, double* dist, uint32_t* pred,
+             gfb_sssp_stats* stats);
+/* Result of the last gfb_sssp on g: dist widened to double and/or in the
+ * graph's native type (u32 / f32 / f64 bytes). */
+int gfb_sssp_read(gfb_graph* g, double* dist, void* dist_native, uint32_t* pred);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GFB_H */

@@ -1,0 +1,371 @@
+// capi.cu -- the extern "C" boundary (include/gfb.h).  Every entry point
+// catches internal errors and returns a status; gfb_last_error() holds the
+// thread-local message (no exception crosses the ABI).
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "impl.hpp"
+
+namespace gfb {
+
+static thread_local std::string g_last_error;
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  cudaGetLastError();
+  int code = e == cudaErrorMemoryAllocation ? GFB_ENOMEM : GFB_ECUDA;
+  fail(code, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ops.cu / graph.cu
+Graph* graph_upload(Ctx*, uint64_t, uint64_t, const uint32_t*, const uint32_t*, const void*, int,
+                    int, int);
+void graph_refill(Graph*, const uint32_t*, const uint32_t*, const void*, int);
+Graph* graph_generate_rmat(Ctx*, int, int, uint64_t, int, int);
+Graph* graph_generate_grid(Ctx*, uint32_t, uint64_t, int);
+void graph_download(Graph*, uint32_t*, uint32_t*, void*);
+Frontier* frontier_create(Ctx*, uint64_t, int);
+void frontier_assign(Frontier*, const uint32_t*, uint64_t);
+uint64_t frontier_size(Frontier*);
+void frontier_read(Frontier*, uint32_t*, uint64_t, uint64_t*);
+void advance_push(Ctx*, const Graph*, Frontier*, Frontier*, int, void*);
+void advance_pull(Ctx*, const Graph*, Frontier*, Frontier*, int, void*);
+void filter_unique(Ctx*, Frontier*, Frontier*);
+Dist* dist_create(Ctx*, const Graph*);
+void dist_init(Dist*, uint32_t);
+void dist_read(Dist*, double*, uint64_t*);
+Record* record_create(Ctx*, uint64_t);
+void record_read(Record*, uint32_t*, uint32_t*, uint32_t*, uint64_t, uint64_t*);
+
+template <class F>
+static int guard(F&& f) {
+  try {
+    f();
+    return GFB_OK;
+  } catch (const Error& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return GFB_ENOMEM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return GFB_ECUDA;
+  }
+}
+
+static void set_device(Ctx* c) { GFB_CUDA(cudaSetDevice(c->device)); }
+
+}  // namespace gfb
+
+using namespace gfb;
+
+struct gfb_ctx : Ctx {};
+struct gfb_graph : Graph {};
+struct gfb_frontier : Frontier {};
+struct gfb_dist : Dist {};
+struct gfb_record : Record {};
+
+#define NEED(p)                                          \
+  do {                                                   \
+    if (!(p)) fail(GFB_EINVAL, "null argument: " #p);    \
+  } while (0)
+
+extern "C" {
+
+int gfb_version(void) { return 1; }
+
+const char* gfb_last_error(void) { return g_last_error.c_str(); }
+
+int gfb_ctx_create(int device, gfb_ctx** out) {
+  return guard([&] {
+    NEED(out);
+    int count = 0;
+    GFB_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) fail(GFB_EINVAL, "ctx: no CUDA device " + std::to_string(device));
+    GFB_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    GFB_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      fail(GFB_ECUDA, std::string("ctx: libgfb is built for sm_100a; device is ") + prop.name);
+    auto* c = new gfb_ctx();
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    try {
+      GFB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      for (auto& e : c->ev) GFB_CUDA(cudaEventCreate(&e));
+      GFB_CUDA(cudaMallocHost(&c->ctl_host, sizeof(Ctl)));
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int gfb_ctx_destroy(gfb_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    set_device(ctx);
+    cudaStreamSynchronize(ctx->stream);
+    delete ctx;
+  });
+}
+
+int gfb_ctx_num_sms(gfb_ctx* ctx, int* out) {
+  return guard([&] {
+    NEED(ctx);
+    NEED(out);
+    *out = ctx->num_sms;
+  });
+}
+
+int gfb_graph_upload(gfb_ctx* ctx, uint64_t n, uint64_t m, const uint32_t* ro, const uint32_t* col,
+                     const void* w, int w_host_type, int wtype, int build_csc, gfb_graph** out) {
+  return guard([&] {
+    NEED(ctx);
+    NEED(out);
+    set_device(ctx);
+    *out = static_cast<gfb_graph*>(graph_upload(ctx, n, m, ro, col, w, w_host_type, wtype, build_csc));
+  });
+}
+
+int gfb_graph_refill(gfb_graph* g, const uint32_t* ro, const uint32_t* col, const void* w,
+                     int w_host_type) {
+  return guard([&] {
+    NEED(g);
+    set_device(g->ctx);
+    graph_refill(g, ro, col, w, w_host_type);
+  });
+}
+
+int gfb_graph_free(gfb_graph* g) {
+  return guard([&] {
+    if (!g) return;
+    set_device(g->ctx);
+    g->ctx->sync();
+    delete static_cast<Graph*>(g);
+  });
+}
+
+int gfb_graph_info(const gfb_graph* g, uint64_t* n, uint64_t* m, int* wtype, int* has_csc) {
+  return guard([&] {
+    NEED(g);
+    if (n) *n = g->n;
+    if (m) *m = g->m;
+    if (wtype) *wtype = g->wtype;
+    if (has_csc) *has_csc = g->has_csc ? 1 : 0;
+  });
+}
+
+int gfb_graph_download(gfb_graph* g, uint32_t* ro, uint32_t* col, void* w) {
+  return guard([&] {
+    NEED(g);
+    set_device(g->ctx);
+    graph_download(g, ro, col, w);
+  });
+}
+
+int gfb_graph_generate_rmat(gfb_ctx* ctx, int scale, int ef, uint64_t seed, int wtype, int csc,
+                            gfb_graph** out) {
+  return guard([&] {
+    NEED(ctx);
+    NEED(out);
+    set_device(ctx);
+    *out = static_cast<gfb_graph*>(graph_generate_rmat(ctx, scale, ef, seed, wtype, csc));
+  });
+}
+
+int gfb_graph_generate_grid(gfb_ctx* ctx, uint32_t side, uint64_t seed, int csc, gfb_graph** out) {
+  return guard([&] {
+    NEED(ctx);
+    NEED(out);
+    set_device(ctx);
+    *out = static_cast<gfb_graph*>(graph_generate_grid(ctx, side, seed, csc));
+  });
+}
+
+int gfb_frontier_create(gfb_ctx* ctx, uint64_t n, int repr, gfb_frontier** out) {
+  return guard([&] {
+    NEED(ctx);
+    NEED(out);
+    set_device(ctx);
+    *out = static_cast<gfb_frontier*>(frontier_create(ctx, n, repr));
+  });
+}
+
+int gfb_frontier_free(gfb_frontier* f) {
+  return guard([&] {
+    if (!f) return;
+    set_device(f->ctx);
+    delete static_cast<Frontier*>(f);
+  });
+}
+
+int gfb_frontier_assign(gfb_frontier* f, const uint32_t* v, uint64_t k) {
+  return guard([&] {
+    NEED(f);
+    if (k) NEED(v);
+    set_device(f->ctx);
+    frontier_assign(f, v, k);
+  });
+}
+
+int gfb_frontier_size(gfb_frontier* f, uint64_t* size) {
+  return guard([&] {
+    NEED(f);
+    NEED(size);
+    set_device(f->ctx);
+    *size = frontier_size(f);
+  });
+}
+
+int gfb_frontier_read(gfb_frontier* f, uint32_t* out, uint64_t cap, uint64_t* k) {
+  return guard([&] {
+    NEED(f);
+    NEED(k);
+    if (cap) NEED(out);
+    set_device(f->ctx);
+    frontier_read(f, out, cap, k);
+  });
+}
+
+int gfb_frontier_repr(gfb_frontier* f, int* repr) {
+  return guard([&] {
+    NEED(f);
+    NEED(repr);
+    *repr = f->repr;
+  });
+}
+
+int gfb_dist_create(gfb_ctx* ctx, const gfb_graph* g, gfb_dist** out) {
+  return guard([&] {
+    NEED(ctx);
+    NEED(g);
+    NEED(out);
+    set_device(ctx);
+    *out = static_cast<gfb_dist*>(dist_create(ctx, g));
+  });
+}
+
+int gfb_dist_free(gfb_dist* d) {
+  return guard([&] {
+    if (!d) return;
+    set_device(d->ctx);
+    delete static_cast<Dist*>(d);
+  });
+}
+
+int gfb_dist_init(gfb_dist* d, uint32_t source) {
+  return guard([&] {
+    NEED(d);
+    set_device(d->ctx);
+    dist_init(d, source);
+  });
+}
+
+int gfb_dist_read(gfb_dist* d, double* dist, uint64_t* relax) {
+  return guard([&] {
+    NEED(d);
+    set_device(d->ctx);
+    dist_read(d, dist, relax);
+  });
+}
+
+int gfb_record_create(gfb_ctx* ctx, uint64_t cap, gfb_record** out) {
+  return guard([&] {
+    NEED(ctx);
+    NEED(out);
+    set_device(ctx);
+    *out = static_cast<gfb_record*>(record_create(ctx, cap));
+  });
+}
+
+int gfb_record_free(gfb_record* r) {
+  return guard([&] {
+    if (!r) return;
+    set_device(r->ctx);
+    delete static_cast<Record*>(r);
+  });
+}
+
+int gfb_record_read(gfb_record* r, uint32_t* s, uint32_t* d, uint32_t* e, uint64_t cap,
+                    uint64_t* count) {
+  return guard([&] {
+    NEED(r);
+    NEED(count);
+    set_device(r->ctx);
+    record_read(r, s, d, e, cap, count);
+  });
+}
+
+int gfb_advance_push(gfb_ctx* ctx, const gfb_graph* g, gfb_frontier* in, gfb_frontier* out, int op,
+                     void* state) {
+  return guard([&] {
+    NEED(ctx);
+    set_device(ctx);
+    advance_push(ctx, g, in, out, op, state);
+  });
+}
+
+int gfb_advance_pull(gfb_ctx* ctx, const gfb_graph* g, gfb_frontier* in, gfb_frontier* out, int op,
+                     void* state) {
+  return guard([&] {
+    NEED(ctx);
+    set_device(ctx);
+    advance_pull(ctx, g, in, out, op, state);
+  });
+}
+
+int gfb_filter_unique(gfb_ctx* ctx, gfb_frontier* in, gfb_frontier* out) {
+  return guard([&] {
+    NEED(ctx);
+    NEED(in);
+    NEED(out);
+    set_device(ctx);
+    filter_unique(ctx, in, out);
+  });
+}
+
+void gfb_sssp_opts_default(gfb_sssp_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->struct_size = sizeof(*o);
+  o->direction = GFB_DIR_AUTO;
+  o->pull_alpha = 4.0f;
+  o->device_loop = 1;
+  o->delta = 0.0;
+  o->compute_pred = 1;
+}
+
+int gfb_sssp(gfb_ctx* ctx, gfb_graph* g, uint32_t source, const gfb_sssp_opts* opts, double* dist,
+             uint32_t* pred, gfb_sssp_stats* stats) {
+  return guard([&] {
+    NEED(ctx);
+    NEED(g);
+    set_device(ctx);
+    gfb_sssp_opts o;
+    gfb_sssp_opts_default(&o);
+    if (opts) {
+      if (opts->struct_size != sizeof(gfb_sssp_opts)) fail(GFB_EINVAL, "sssp: opts struct_size mismatch");
+      o = *opts;
+    }
+    gfb_sssp_stats st{};
+    sssp_run(ctx, g, source, &o, &st);
+    if (dist || pred) sssp_read(g, dist, nullptr, pred);
+    if (stats) *stats = st;
+  });
+}
+
+int gfb_sssp_read(gfb_graph* g, double* dist, void* dist_native, uint32_t* pred) {
+  return guard([&] {
+    NEED(g);
+    set_device(g->ctx);
+    sssp_read(g, dist, dist_native, pred);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,572 @@
+// graph.cu -- device graph store: upload (graph.hpp:150-180 layout and
+// validation), device build_transpose (graph.hpp:184-211), the static pull
+// plan, and the device-side synthetic generators (RMAT, grid).
+#include <cub/cub.cuh>
+
+#include <cstring>
+#include <string>
+
+#include "impl.hpp"
+#include "rmat.cuh"
+
+namespace gfb {
+
+void DBuf::alloc(size_t b, cudaStream_t stream) {
+  release();
+  s = stream;
+  if (b == 0) b = 16;
+  cudaError_t e = cudaMalloc(&p, b);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    p = nullptr;
+    fail(GFB_ENOMEM, "device allocation of " + std::to_string(b) + " bytes failed");
+  }
+  check_cuda(e, "cudaMalloc");
+  bytes = b;
+}
+
+void DBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+
+Ctx::~Ctx() {
+  if (ctl_host) cudaFreeHost(ctl_host);
+  for (auto& e : ev)
+    if (e) cudaEventDestroy(e);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+void Ctx::ensure_status(size_t n) {
+  if (n <= status_cap) return;
+  status.alloc(n * 8, stream);
+  qstatus.alloc(n * 8, stream);
+  status_cap = n;
+}
+
+void Ctx::sync() { GFB_CUDA(cudaStreamSynchronize(stream)); }
+
+Ctl Ctx::read_ctl(const Ctl* dctl) {
+  GFB_CUDA(cudaMemcpyAsync(ctl_host, dctl, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
+  sync();
+  return *ctl_host;
+}
+
+Graph::~Graph() = default;
+Workspace::~Workspace() {
+  if (ctl_host) cudaFreeHost(ctl_host);
+}
+
+void Frontier::reserve(uint64_t c) {
+  if (c <= cap) return;
+  DBuf nb;
+  nb.alloc(c * 4, ctx->stream);
+  if (len) GFB_CUDA(cudaMemcpyAsync(nb.p, list.p, len * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  std::swap(list.p, nb.p);
+  std::swap(list.bytes, nb.bytes);
+  cap = c;
+}
+
+// ---------------------------------------------------------------------------
+// Upload: validate + interleave {dst, weight} records.
+// ---------------------------------------------------------------------------
+template <class W>
+__device__ __forceinline__ bool conv_weight(const void* src, int htype, uint64_t e, W* out);
+
+template <>
+__device__ __forceinline__ bool conv_weight<float>(const void* src, int htype, uint64_t e,
+                                                   float* out) {
+  float w;
+  if (htype == GFB_W_F64) {
+    double d = static_cast<const double*>(src)[e];
+    if (!(d >= 0) || isinf(d)) return false;
+    w = __double2float_rn(d);
+  } else if (htype == GFB_W_F32) {
+    w = static_cast<const float*>(src)[e];
+  } else {
+    w = (float)static_cast<const uint32_t*>(src)[e];
+  }
+  if (!(w >= 0.0f) || isinf(w)) return false;
+  *out = w + 0.0f;  // canonicalise -0.0 -> +0.0
+  return true;
+}
+template <>
+__device__ __forceinline__ bool conv_weight<double>(const void* src, int htype, uint64_t e,
+                                                    double* out) {
+  double w;
+  if (htype == GFB_W_F64) w = static_cast<const double*>(src)[e];
+  else if (htype == GFB_W_F32) w = (double)static_cast<const float*>(src)[e];
+  else w = (double)static_cast<const uint32_t*>(src)[e];
+  if (!(w >= 0.0) || isinf(w)) return false;
+  *out = w + 0.0;
+  return true;
+}
+template <>
+__device__ __forceinline__ bool conv_weight<uint32_t>(const void* src, int htype, uint64_t e,
+                                                      uint32_t* out) {
+  if (htype == GFB_W_U32) {
+    *out = static_cast<const uint32_t*>(src)[e];
+    return true;
+  }
+  double d = htype == GFB_W_F64 ? static_cast<const double*>(src)[e]
+                                : (double)static_cast<const float*>(src)[e];
+  if (!(d >= 0) || isinf(d) || d > 4294967295.0 || d != floor(d)) return false;
+  *out = (uint32_t)d;
+  return true;
+}
+
+template <class W>
+__global__ void k_interleave(const uint32_t* __restrict__ col, const void* __restrict__ wsrc,
+                             int htype, EdgeRec<W>* adj, uint64_t n, uint64_t m,
+                             unsigned long long* bad_v, unsigned long long* bad_w) {
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+    uint32_t v = col[e];
+    W w{};
+    bool okw = conv_weight<W>(wsrc, htype, e, &w);
+    if (v >= n) atomicMin(bad_v, (unsigned long long)e);
+    if (!okw) atomicMin(bad_w, (unsigned long long)e);
+    EdgeRec<W> r{};
+    r.v = v;
+    r.w = w;
+    adj[e] = r;
+  }
+}
+
+__global__ void k_check_ro(const uint32_t* ro, uint64_t n, uint64_t m,
+                           unsigned long long* bad) {
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += stride) {
+    bool ok = v == 0 ? ro[0] == 0 : ro[v - 1] <= ro[v];
+    if (v == n && ro[n] != m) ok = false;
+    if (!ok) atomicMin(bad, (unsigned long long)v);
+  }
+}
+
+template <class W>
+static void launch_interleave(Graph* g, const uint32_t* dcol, const void* dw, int htype,
+                              unsigned long long* flags) {
+  Ctx* c = g->ctx;
+  k_interleave<W><<<stride_grid(c), 256, 0, c->stream>>>(
+      dcol, dw, htype, g->adj.as<EdgeRec<W>>(), g->n, g->m, flags, flags + 1);
+  GFB_CUDA(cudaGetLastError());
+}
+
+static size_t host_wsize(int htype) { return htype == GFB_W_F64 ? 8 : 4; }
+
+static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const void* w,
+                       int htype) {
+  Ctx* c = g->ctx;
+  cudaStream_t s = c->stream;
+  const uint64_t n = g->n, m = g->m;
+  if (htype < GFB_W_U32 || htype > GFB_W_F64) fail(GFB_EINVAL, "graph: bad host weight type");
+  if (!ro || (m && (!col || !w))) fail(GFB_EINVAL, "graph: null CSR array");
+  GFB_CUDA(cudaMemcpyAsync(g->ro.p, ro, (n + 1) * 4, cudaMemcpyHostToDevice, s));
+  DBuf dcol, dw, flags;
+  dcol.alloc(m * 4, s);
+  dw.alloc(m * host_wsize(htype), s);
+  flags.alloc(3 * 8, s);
+  GFB_CUDA(cudaMemsetAsync(flags.p, 0xFF, 3 * 8, s));
+  if (m) {
+    GFB_CUDA(cudaMemcpyAsync(dcol.p, col, m * 4, cudaMemcpyHostToDevice, s));
+    GFB_CUDA(cudaMemcpyAsync(dw.p, w, m * host_wsize(htype), cudaMemcpyHostToDevice, s));
+  }
+  auto* f = flags.as<unsigned long long>();
+  k_check_ro<<<stride_grid(c), 256, 0, s>>>(g->ro.as<uint32_t>(), n, m, f + 2);
+  if (m) {
+    if (g->wtype == GFB_W_F32) launch_interleave<float>(g, dcol.as<uint32_t>(), dw.p, htype, f);
+    else if (g->wtype == GFB_W_F64) launch_interleave<double>(g, dcol.as<uint32_t>(), dw.p, htype, f);
+    else launch_interleave<uint32_t>(g, dcol.as<uint32_t>(), dw.p, htype, f);
+  }
+  unsigned long long hf[3];
+  GFB_CUDA(cudaMemcpyAsync(hf, f, sizeof(hf), cudaMemcpyDeviceToHost, s));
+  c->sync();
+  if (hf[2] != ~0ull)
+    fail(GFB_EINVAL, "graph: row_offsets inconsistent at vertex " + std::to_string(hf[2]));
+  // graph.hpp:152-160 reports the first offending edge
+  if (hf[0] != ~0ull && hf[0] <= hf[1])
+    fail(GFB_EINVAL, "build_csr: edge " + std::to_string(hf[0]) + " has vertex id out of range");
+  if (hf[1] != ~0ull)
+    fail(GFB_EINVAL,
+         "build_csr: edge " + std::to_string(hf[1]) + " has negative or non-finite weight");
+  g->ws.reset();
+}
+
+Graph* graph_upload(Ctx* c, uint64_t n, uint64_t m, const uint32_t* ro, const uint32_t* col,
+                    const void* w, int htype, int wtype, int build_csc_flag) {
+  if (wtype < GFB_W_U32 || wtype > GFB_W_F64) fail(GFB_EINVAL, "graph: bad weight type");
+  if (n >= (1ull << 31) || m >= (1ull << 31))
+    fail(GFB_EINVAL, "graph: device path needs n < 2^31 and m < 2^31");
+  auto g = std::make_unique<Graph>();
+  g->ctx = c;
+  g->n = n;
+  g->m = m;
+  g->wtype = wtype;
+  g->ro.alloc((n + 1) * 4, c->stream);
+  g->adj.alloc(m * g->rec_bytes(), c->stream);
+  fill_graph(g.get(), ro, col, w, htype);
+  if (build_csc_flag) {
+    build_csc(g.get());
+    build_pull_plan(g.get());
+  }
+  return g.release();
+}
+
+void graph_refill(Graph* g, const uint32_t* ro, const uint32_t* col, const void* w, int htype) {
+  fill_graph(g, ro, col, w, htype);
+  if (g->has_csc) {
+    build_csc(g);
+    build_pull_plan(g);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Device build_transpose (graph.hpp:184-211).  A stable radix sort of the
+// CSR edge ids by destination gives exactly the reference slot order
+// (ascending source, then CSR edge id, within each destination).
+// ---------------------------------------------------------------------------
+__global__ void k_dst_keys(const void* adj, int recb, uint32_t* keys, uint32_t* ids, uint64_t m) {
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+    keys[e] = *reinterpret_cast<const uint32_t*>(static_cast<const char*>(adj) + e * recb);
+    ids[e] = (uint32_t)e;
+  }
+}
+
+__global__ void k_row_marks(const uint32_t* ro, uint32_t* mark, uint64_t n) {
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride)
+    if (ro[v + 1] > ro[v]) mark[ro[v]] = (uint32_t)v;  // one non-empty row per start
+}
+
+// offsets from sorted keys: off[v] = first index i with keys[i] >= v,
+// off[n] = m (the count+scan of graph.hpp:172-178 done from sorted keys).
+__global__ void k_offsets_from_sorted(const uint32_t* keys, uint64_t m, uint32_t* off,
+                                      uint64_t n) {
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= m; i += stride) {
+    int64_t prev = i == 0 ? -1 : (int64_t)keys[i - 1];
+    int64_t cur = i < m ? (int64_t)keys[i] : (int64_t)n;
+    for (int64_t v = prev + 1; v <= cur; ++v) off[v] = (uint32_t)i;
+  }
+}
+
+template <class W>
+__global__ void k_csc_fill(const EdgeRec<W>* adj, const uint32_t* sorted_eid,
+                           const uint32_t* src_of, EdgeRec<W>* cadj, uint32_t* ceid, uint64_t m) {
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < m; s += stride) {
+    uint32_t e = sorted_eid[s];
+    EdgeRec<W> r = adj[e];
+    r.v = src_of[e];
+    cadj[s] = r;
+    ceid[s] = e;
+  }
+}
+
+static int bits_for(uint64_t n) {
+  int b = 1;
+  while ((1ull << b) < n) ++b;
+  return b;
+}
+
+struct MaxOp {
+  __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const {
+    return a > b ? a : b;
+  }
+};
+
+// src_of[e] = source vertex of CSR edge e (row marks + inclusive max-scan).
+static void source_of_edges(Graph* g, DBuf& src_of) {
+  Ctx* c = g->ctx;
+  cudaStream_t s = c->stream;
+  src_of.alloc(g->m * 4, s);
+  GFB_CUDA(cudaMemsetAsync(src_of.p, 0, g->m * 4, s));
+  k_row_marks<<<stride_grid(c), 256, 0, s>>>(g->ro.as<uint32_t>(), src_of.as<uint32_t>(), g->n);
+  size_t tb = 0;
+  GFB_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb, src_of.as<uint32_t>(),
+                                          src_of.as<uint32_t>(), MaxOp(), (int64_t)g->m, s));
+  DBuf tmp;
+  tmp.alloc(tb, s);
+  GFB_CUDA(cub::DeviceScan::InclusiveScan(tmp.p, tb, src_of.as<uint32_t>(),
+                                          src_of.as<uint32_t>(), MaxOp(), (int64_t)g->m, s));
+}
+
+void build_csc(Graph* g) {
+  Ctx* c = g->ctx;
+  cudaStream_t s = c->stream;
+  const uint64_t n = g->n, m = g->m;
+  g->co.alloc((n + 1) * 4, s);
+  g->cadj.alloc(m * g->rec_bytes(), s);
+  g->ceid.alloc(m * 4, s);
+  if (m == 0) {
+    GFB_CUDA(cudaMemsetAsync(g->co.p, 0, (n + 1) * 4, s));
+    g->has_csc = true;
+    c->sync();
+    return;
+  }
+  DBuf keys, ids, keys2, ids2, src_of;
+  keys.alloc(m * 4, s);
+  ids.alloc(m * 4, s);
+  keys2.alloc(m * 4, s);
+  ids2.alloc(m * 4, s);
+  k_dst_keys<<<stride_grid(c), 256, 0, s>>>(g->adj.p, (int)g->rec_bytes(), keys.as<uint32_t>(),
+                                            ids.as<uint32_t>(), m);
+  size_t tb = 0;
+  GFB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<uint32_t>(), keys2.as<uint32_t>(),
+                                           ids.as<uint32_t>(), ids2.as<uint32_t>(), (int64_t)m, 0,
+                                           bits_for(n), s));
+  DBuf tmp;
+  tmp.alloc(tb, s);
+  GFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<uint32_t>(), keys2.as<uint32_t>(),
+                                           ids.as<uint32_t>(), ids2.as<uint32_t>(), (int64_t)m, 0,
+                                           bits_for(n), s));
+  tmp.release();
+  keys.release();
+  ids.release();
+  k_offsets_from_sorted<<<stride_grid(c), 256, 0, s>>>(keys2.as<uint32_t>(), m,
+                                                       g->co.as<uint32_t>(), n);
+  source_of_edges(g, src_of);
+  if (g->wtype == GFB_W_F32)
+    k_csc_fill<float><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<float>>(), ids2.as<uint32_t>(),
+                                                     src_of.as<uint32_t>(), g->cadj.as<EdgeRec<float>>(),
+                                                     g->ceid.as<uint32_t>(), m);
+  else if (g->wtype == GFB_W_F64)
+    k_csc_fill<double><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<double>>(), ids2.as<uint32_t>(),
+                                                      src_of.as<uint32_t>(), g->cadj.as<EdgeRec<double>>(),
+                                                      g->ceid.as<uint32_t>(), m);
+  else
+    k_csc_fill<uint32_t><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<uint32_t>>(), ids2.as<uint32_t>(),
+                                                        src_of.as<uint32_t>(), g->cadj.as<EdgeRec<uint32_t>>(),
+                                                        g->ceid.as<uint32_t>(), m);
+  GFB_CUDA(cudaGetLastError());
+  c->sync();
+  g->has_csc = true;
+}
+
+// Static pull plan: k_compact over the CSC offsets with an all-ones bitmap
+// drops destinations of in-degree 0 and emits the edge-tile map.
+__global__ void k_fill_ones(uint32_t* bm, uint64_t nwords, uint64_t n) {
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords; i += stride) {
+    uint64_t lo = i * 32;
+    uint32_t w = 0xFFFFFFFFu;
+    if (lo + 32 > n) w = (n > lo) ? ((1u << (n - lo)) - 1u) : 0u;
+    bm[i] = w;
+  }
+}
+
+void build_pull_plan(Graph* g) {
+  Ctx* c = g->ctx;
+  cudaStream_t s = c->stream;
+  const uint64_t n = g->n, m = g->m;
+  const uint64_t nwords = (n + 31) / 32;
+  const uint32_t ntiles = (uint32_t)((nwords + C_WORDS - 1) / C_WORDS);
+  g->pull_v.alloc((n + 1) * 4, s);
+  g->pull_off.alloc((n + 1) * 4, s);
+  g->pull_tseg.alloc((m / A_TILE + 3) * 4, s);
+  DBuf bm, ctl, status;
+  bm.alloc(nwords * 4, s);
+  ctl.alloc(sizeof(Ctl), s);
+  status.alloc((size_t)(ntiles + 1) * 8, s);
+  GFB_CUDA(cudaMemsetAsync(ctl.p, 0, sizeof(Ctl), s));
+  GFB_CUDA(cudaMemsetAsync(status.p, 0, (size_t)(ntiles + 1) * 8, s));
+  if (n == 0) {
+    g->pull_k = 0;
+    g->pull_total = 0;
+    c->sync();
+    return;
+  }
+  k_fill_ones<<<stride_grid(c), 256, 0, s>>>(bm.as<uint32_t>(), nwords, n);
+  // start and off coincide for a complete plan: start = co[v] = off
+  DBuf start;
+  start.alloc((n + 1) * 4, s);
+  Plan p{g->pull_v.as<uint32_t>(), start.as<uint32_t>(), g->pull_off.as<uint32_t>(),
+         g->pull_tseg.as<uint32_t>(), (uint32_t)(g->pull_tseg.bytes / 4)};
+  k_compact<<<ntiles, C_WARPS * 32, 0, s>>>(g->co.as<uint32_t>(), bm.as<uint32_t>(), nullptr,
+                                            (uint32_t)nwords, (uint32_t)n, p, ctl.as<Ctl>(),
+                                            status.as<unsigned long long>(), ntiles, 1);
+  GFB_CUDA(cudaGetLastError());
+  Ctl h = c->read_ctl(ctl.as<Ctl>());
+  g->pull_k = h.k;
+  g->pull_total = h.total;
+}
+
+// ---------------------------------------------------------------------------
+// Device-side synthetic graphs in build_csr layout.
+// ---------------------------------------------------------------------------
+__global__ void k_rmat_gen(int scale, uint64_t seed, int wkind, uint64_t m,
+                           unsigned long long* key, uint32_t* wbits) {
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    uint32_t s, d, w;
+    rmat_edge(scale, seed, wkind, i, &s, &d, &w);
+    key[i] = ((unsigned long long)s << 32) | d;
+    wbits[i] = w;
+  }
+}
+
+__global__ void k_unpack_sorted(const unsigned long long* key, const uint32_t* wbits,
+                                uint32_t* srcs, EdgeRec<uint32_t>* adj, uint64_t m) {
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    unsigned long long k = key[i];
+    srcs[i] = (uint32_t)(k >> 32);
+    adj[i] = EdgeRec<uint32_t>{(uint32_t)k, wbits[i]};
+  }
+}
+
+Graph* graph_generate_rmat(Ctx* c, int scale, int ef, uint64_t seed, int wtype, int csc) {
+  if (scale < 1 || scale > 30 || ef < 1) fail(GFB_EINVAL, "rmat: bad scale/edgefactor");
+  if (wtype != GFB_W_U32 && wtype != GFB_W_F32) fail(GFB_EINVAL, "rmat: wtype must be u32 or f32");
+  const uint64_t n = 1ull << scale, m = (uint64_t)ef << scale;
+  if (m >= (1ull << 31)) fail(GFB_EINVAL, "rmat: m must be < 2^31");
+  cudaStream_t s = c->stream;
+  auto g = std::make_unique<Graph>();
+  g->ctx = c;
+  g->n = n;
+  g->m = m;
+  g->wtype = wtype;
+  g->ro.alloc((n + 1) * 4, s);
+  g->adj.alloc(m * 8, s);
+  {
+    DBuf key, key2, wb, wb2;
+    key.alloc(m * 8, s);
+    key2.alloc(m * 8, s);
+    wb.alloc(m * 4, s);
+    wb2.alloc(m * 4, s);
+    k_rmat_gen<<<stride_grid(c), 256, 0, s>>>(scale, seed, wtype == GFB_W_U32 ? 0 : 1, m,
+                                              key.as<unsigned long long>(), wb.as<uint32_t>());
+    GFB_CUDA(cudaGetLastError());
+    // (src, dst, w) order: stable sort by w, then stable sort by (src, dst).
+    size_t tb1 = 0, tb2 = 0;
+    GFB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb1, wb.as<uint32_t>(), wb2.as<uint32_t>(),
+                                             key.as<unsigned long long>(),
+                                             key2.as<unsigned long long>(), (int64_t)m, 0, 32, s));
+    GFB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, key2.as<unsigned long long>(),
+                                             key.as<unsigned long long>(), wb2.as<uint32_t>(),
+                                             wb.as<uint32_t>(), (int64_t)m, 0, 32 + scale, s));
+    DBuf tmp;
+    tmp.alloc(tb1 > tb2 ? tb1 : tb2, s);
+    size_t tb = tmp.bytes;
+    GFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, wb.as<uint32_t>(), wb2.as<uint32_t>(),
+                                             key.as<unsigned long long>(),
+                                             key2.as<unsigned long long>(), (int64_t)m, 0, 32, s));
+    tb = tmp.bytes;
+    GFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, key2.as<unsigned long long>(),
+                                             key.as<unsigned long long>(), wb2.as<uint32_t>(),
+                                             wb.as<uint32_t>(), (int64_t)m, 0, 32 + scale, s));
+    tmp.release();
+    key2.release();
+    DBuf srcs;
+    srcs.alloc(m * 4, s);
+    k_unpack_sorted<<<stride_grid(c), 256, 0, s>>>(key.as<unsigned long long>(), wb.as<uint32_t>(),
+                                                   srcs.as<uint32_t>(),
+                                                   g->adj.as<EdgeRec<uint32_t>>(), m);
+    k_offsets_from_sorted<<<stride_grid(c), 256, 0, s>>>(srcs.as<uint32_t>(), m,
+                                                         g->ro.as<uint32_t>(), n);
+    GFB_CUDA(cudaGetLastError());
+    c->sync();
+  }
+  if (csc) {
+    build_csc(g.get());
+    build_pull_plan(g.get());
+  }
+  return g.release();
+}
+
+__global__ void k_grid_deg(uint32_t side, uint32_t* deg) {
+  uint64_t n = (uint64_t)side * side;
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += stride) {
+    uint32_t r = (uint32_t)(u / side), cc = (uint32_t)(u % side);
+    deg[u] = (r > 0) + (cc > 0) + (cc + 1 < side) + (r + 1 < side);
+  }
+}
+
+__global__ void k_grid_fill(uint32_t side, uint64_t seed, const uint32_t* ro,
+                            EdgeRec<uint32_t>* adj) {
+  uint64_t n = (uint64_t)side * side;
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += stride) {
+    uint32_t r = (uint32_t)(u / side), cc = (uint32_t)(u % side);
+    uint32_t e = ro[u];
+    bool ok[4] = {r > 0, cc > 0, cc + 1 < side, r + 1 < side};
+    uint64_t nb[4] = {u - side, u - 1, u + 1, u + side};
+    for (int k = 0; k < 4; ++k) {
+      if (!ok[k]) continue;
+      adj[e++] = EdgeRec<uint32_t>{(uint32_t)nb[k], grid_weight_bits(seed, u, k)};
+    }
+  }
+}
+
+Graph* graph_generate_grid(Ctx* c, uint32_t side, uint64_t seed, int csc) {
+  const uint64_t n = (uint64_t)side * side;
+  const uint64_t m = side < 2 ? 0 : 4ull * side * (side - 1);
+  if (side == 0 || n >= (1ull << 31) || m >= (1ull << 31)) fail(GFB_EINVAL, "grid: bad side");
+  cudaStream_t s = c->stream;
+  auto g = std::make_unique<Graph>();
+  g->ctx = c;
+  g->n = n;
+  g->m = m;
+  g->wtype = GFB_W_F32;
+  g->ro.alloc((n + 1) * 4, s);
+  g->adj.alloc(m * 8, s);
+  DBuf deg;
+  deg.alloc((n + 1) * 4, s);
+  GFB_CUDA(cudaMemsetAsync(deg.p, 0, (n + 1) * 4, s));
+  k_grid_deg<<<stride_grid(c), 256, 0, s>>>(side, deg.as<uint32_t>());
+  size_t tb = 0;
+  GFB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, deg.as<uint32_t>(), g->ro.as<uint32_t>(),
+                                         (int64_t)(n + 1), s));
+  DBuf tmp;
+  tmp.alloc(tb, s);
+  GFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, deg.as<uint32_t>(), g->ro.as<uint32_t>(),
+                                         (int64_t)(n + 1), s));
+  k_grid_fill<<<stride_grid(c), 256, 0, s>>>(side, seed, g->ro.as<uint32_t>(),
+                                             g->adj.as<EdgeRec<uint32_t>>());
+  GFB_CUDA(cudaGetLastError());
+  c->sync();
+  if (csc) {
+    build_csc(g.get());
+    build_pull_plan(g.get());
+  }
+  return g.release();
+}
+
+// ---------------------------------------------------------------------------
+template <class W>
+__global__ void k_split(const EdgeRec<W>* adj, uint32_t* col, W* w, uint64_t m) {
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+    EdgeRec<W> r = adj[e];
+    if (col) col[e] = r.v;
+    if (w) w[e] = r.w;
+  }
+}
+
+void graph_download(Graph* g, uint32_t* ro, uint32_t* col, void* w) {
+  Ctx* c = g->ctx;
+  cudaStream_t s = c->stream;
+  if (ro) GFB_CUDA(cudaMemcpyAsync(ro, g->ro.p, (g->n + 1) * 4, cudaMemcpyDeviceToHost, s));
+  if ((col || w) && g->m) {
+    size_t wb = g->wtype == GFB_W_F64 ? 8 : 4;
+    DBuf dc, dw;
+    dc.alloc(g->m * 4, s);
+    dw.alloc(g->m * wb, s);
+    if (g->wtype == GFB_W_F32)
+      k_split<float><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<float>>(), dc.as<uint32_t>(), dw.as<float>(), g->m);
+    else if (g->wtype == GFB_W_F64)
+      k_split<double><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<double>>(), dc.as<uint32_t>(), dw.as<double>(), g->m);
+    else
+      k_split<uint32_t><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<uint32_t>>(), dc.as<uint32_t>(), dw.as<uint32_t>(), g->m);
+    GFB_CUDA(cudaGetLastError());
+    if (col) GFB_CUDA(cudaMemcpyAsync(col, dc.p, g->m * 4, cudaMemcpyDeviceToHost, s));
+    if (w) GFB_CUDA(cudaMemcpyAsync(w, dw.p, g->m * wb, cudaMemcpyDeviceToHost, s));
+    c->sync();
+  }
+  c->sync();
+}
+
+}  // namespace gfb

@@ -1,0 +1,112 @@
+// impl.hpp -- host-side objects behind the C ABI handles.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <memory>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace gfb {
+
+// Owning device buffer (cudaMallocAsync on the context stream).
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void alloc(size_t b, cudaStream_t stream);
+  void release();
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct Ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {};
+  // operator-API scratch
+  DBuf ctl, status, qstatus;
+  size_t status_cap = 0;
+  Ctl* ctl_host = nullptr;  // pinned mirror
+  ~Ctx();
+  void ensure_status(size_t n);
+  void sync();
+  Ctl read_ctl(const Ctl* dctl);
+};
+
+struct Workspace;
+
+struct Graph {
+  Ctx* ctx = nullptr;
+  uint64_t n = 0, m = 0;
+  int wtype = GFB_W_F32;
+  bool has_csc = false;
+  DBuf ro, adj, co, cadj, ceid;
+  // static pull plan (destinations with in-degree > 0)
+  uint32_t pull_k = 0, pull_total = 0;
+  DBuf pull_v, pull_off, pull_tseg;
+  std::unique_ptr<Workspace> ws;
+  ~Graph();
+  size_t rec_bytes() const { return wtype == GFB_W_F64 ? 16 : 8; }
+};
+
+struct Frontier {
+  Ctx* ctx = nullptr;
+  uint64_t n = 0;
+  int repr = GFB_SPARSE;
+  DBuf list;      // sparse: u32[cap]
+  uint64_t len = 0, cap = 0;
+  DBuf bits;      // dense: u32[nwords]
+  uint64_t nwords() const { return (n + 31) / 32; }
+  void reserve(uint64_t c);
+};
+
+struct Dist {
+  Ctx* ctx = nullptr;
+  const Graph* g = nullptr;
+  DBuf dist, predrec, ctl;
+  unsigned long long relax = 0;
+};
+
+struct Record {
+  Ctx* ctx = nullptr;
+  uint64_t cap = 0;
+  DBuf src, dst, eid;
+  uint64_t count = 0;
+};
+
+// SSSP working memory, cached on the graph.
+struct Workspace {
+  DBuf dist, predrec, pred, res, cand;
+  DBuf bm_next, bm_cur, repair_bm;
+  DBuf pv, pstart, poff, ptseg;
+  DBuf status;
+  DBuf ctl;
+  Ctl* ctl_host = nullptr;  // pinned
+  uint32_t compact_tiles = 0;
+  uint32_t status_len = 0;
+  int wtype = -1;
+  bool has_result = false;
+  uint32_t source = 0;
+  ~Workspace();
+};
+
+// grid sizes
+inline int stride_grid(const Ctx* c) { return c->num_sms * 8; }
+inline int persist_grid(const Ctx* c, int per_sm) { return c->num_sms * per_sm; }
+
+// graph.cu
+void build_csc(Graph* g);
+void build_pull_plan(Graph* g);
+// sssp.cu
+void sssp_run(Ctx* ctx, Graph* g, uint32_t source, const gfb_sssp_opts* o, gfb_sssp_stats* st);
+void sssp_read(Graph* g, double* dist, void* dist_native, uint32_t* pred);
+Workspace* ensure_ws(Graph* g);
+
+}  // namespace gfb

@@ -1,0 +1,796 @@
+// kernels.cuh -- the sm_100a kernels of the SSSP hot path.
+//
+//   k_compact        bitmap -> ascending frontier plan (filter/uniquify,
+//                    operators.hpp:411-420 + frontier.hpp:147-165 convert):
+//                    warp-ballot compaction, degree scan, decoupled look-back,
+//                    edge-tile map for the load-balanced advance.
+//   k_plan_list      sparse list (duplicates kept) -> frontier plan, order
+//                    preserving (operators.hpp:17-24 active_vertices_of).
+//   k_advance_push   push advance (operators.hpp:255-288 neighbors_expand +
+//                    the relax lambda algorithms.hpp:586-593): merge-path
+//                    edge tiles, coalesced 8-byte record stream,
+//                    test-before-atomicMin, bitmap or ordered-queue output.
+//   k_advance_pull   pull advance (operators.hpp:296-334): CSC edge tiles,
+//                    frontier-bitmap test, shared-memory segmented min,
+//                    one global atomic per (tile, destination).
+//   k_init           algorithms.hpp:579-583 init (+ frontier seed).
+//   k_pred_*         predecessor pass (algorithms.hpp:512-528 semantics:
+//                    tight-edge tree, acyclic).
+#pragma once
+
+#include "common.cuh"
+
+namespace gfb {
+
+// ---------------------------------------------------------------------------
+// Device control block (one per workspace / operator call).
+// ---------------------------------------------------------------------------
+struct Ctl {
+  uint32_t k;          // segments in the current plan (frontier vertices, deg>0)
+  uint32_t total;      // edges of the current plan
+  uint32_t tile_ctr;   // dynamic tile counter for look-back kernels
+  uint32_t err;        // bit 0: u32 distance overflow
+  unsigned long long relax;  // sum of plan totals (cond invocations)
+  uint32_t supersteps;
+  uint32_t push_steps;
+  uint32_t pull_steps;
+  uint32_t out_count;  // ordered-queue output count
+  uint32_t rec_count;  // RECORD op output count
+  uint32_t unresolved; // predecessor pass
+  uint32_t flag;       // generic
+  uint32_t mode;       // 0 push, 1 pull (chosen by k_plan_direction)
+  unsigned long long n_reach, m_reach;
+};
+
+// Expansion plan: the frontier restricted to vertices with out-degree > 0.
+struct Plan {
+  uint32_t* v;       // vertex id
+  uint32_t* start;   // first edge of the row
+  uint32_t* off;     // exclusive prefix of degrees (off[k] = total)
+  uint32_t* tseg;    // tseg[b] = segment holding edge b*A_TILE
+  uint32_t tseg_cap; // entries allocated in tseg
+};
+
+constexpr int A_BLOCK = 256;
+constexpr int A_VT = 4;
+constexpr int A_TILE = A_BLOCK * A_VT;  // edges per advance tile
+
+constexpr int C_WARPS = 8;
+constexpr int C_WPW = 8;                 // bitmap words per warp
+constexpr int C_WORDS = C_WARPS * C_WPW; // words per compaction tile
+constexpr int C_VERTS = C_WORDS * 32;    // vertices per compaction tile
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  return x;
+}
+
+__device__ __forceinline__ uint32_t warp_sum(uint32_t x) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
+  return x;
+}
+
+// Write the tile map entries owned by segment `gi` = [eoff, eoff+deg).
+__device__ __forceinline__ void tile_map_entries(const Plan& p, uint32_t gi, uint32_t eoff,
+                                                 uint32_t deg) {
+  uint32_t b = (eoff + A_TILE - 1) / A_TILE;
+  for (uint64_t x = (uint64_t)b * A_TILE; x < (uint64_t)eoff + deg && b < p.tseg_cap;
+       x += A_TILE, ++b)
+    p.tseg[b] = gi;
+}
+
+// Finalise a plan from the inclusive totals (called by one thread).
+__device__ __forceinline__ void plan_finish(Plan p, Ctl* ctl, uint32_t K, uint32_t T) {
+  ctl->k = K;
+  ctl->total = T;
+  p.off[K] = T;
+  uint32_t sb = (T + A_TILE - 1) / A_TILE;  // sentinel past the last tile
+  if (sb < p.tseg_cap) p.tseg[sb] = K;
+  ctl->tile_ctr = 0;
+}
+
+// ---------------------------------------------------------------------------
+// k_compact: next-frontier bitmap -> plan.  One CTA per C_VERTS vertices,
+// tiles claimed in launch order (dynamic counter) so the look-back always
+// waits on a running predecessor.  Optionally copies the word into bm_cur
+// (the frontier bitmap the pull kernel tests) and clears bm_next.
+// ---------------------------------------------------------------------------
+static __global__ void __launch_bounds__(C_WARPS * 32)
+k_compact(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
+          uint32_t nwords, uint32_t n, Plan plan, Ctl* ctl, unsigned long long* status,
+          uint32_t ntiles, int clear) {
+  __shared__ uint32_t s_v[C_VERTS];
+  __shared__ uint32_t s_start[C_VERTS];
+  __shared__ uint32_t s_deg[C_VERTS];
+  __shared__ uint32_t s_wc[C_WARPS], s_we[C_WARPS];
+  __shared__ uint32_t s_tile, s_pc, s_pe;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = atomicAdd(&ctl->tile_ctr, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+
+  // ---- phase 1: warp-ballot compaction of this warp's words into smem ----
+  const uint32_t wbase = tile * C_WORDS + warp * C_WPW;
+  uint32_t my_word = 0;
+  if (lane < C_WPW && wbase + lane < nwords) {
+    my_word = bm_next[wbase + lane];
+    if (bm_cur) bm_cur[wbase + lane] = my_word;
+    if (clear) bm_next[wbase + lane] = 0;
+  }
+  uint32_t cnt = 0, edg = 0;
+  uint32_t* sv = s_v + warp * (C_WPW * 32);
+  uint32_t* ss = s_start + warp * (C_WPW * 32);
+  uint32_t* sd = s_deg + warp * (C_WPW * 32);
+#pragma unroll 1
+  for (int j = 0; j < C_WPW; ++j) {
+    uint32_t word = __shfl_sync(0xffffffffu, my_word, j);
+    if (word == 0) continue;
+    uint32_t v = (wbase + j) * 32 + lane;
+    bool bit = (word >> lane) & 1u;
+    uint32_t st = 0, deg = 0;
+    if (bit && ro) {
+      st = ro[v];
+      deg = ro[v + 1] - st;
+    }
+    bool keep = bit && (deg > 0 || !ro);  // ro == nullptr: keep every set bit
+    unsigned mask = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      uint32_t pos = cnt + __popc(mask & lanemask_lt());
+      sv[pos] = v;
+      ss[pos] = st;
+      sd[pos] = deg;
+    }
+    cnt += __popc(mask);
+    edg += warp_sum(keep ? deg : 0u);
+  }
+  if (lane == 0) {
+    s_wc[warp] = cnt;
+    s_we[warp] = edg;
+  }
+  __syncthreads();
+
+  // ---- phase 2: CTA totals, look-back for the global prefix ----
+  if (threadIdx.x == 0) {
+    uint32_t c = 0, e = 0;
+    for (int w = 0; w < C_WARPS; ++w) {
+      uint32_t tc = s_wc[w], te = s_we[w];
+      s_wc[w] = c;
+      s_we[w] = e;
+      c += tc;
+      e += te;
+    }
+    uint32_t pc, pe;
+    lb_lookback(status, tile, c, e, &pc, &pe);
+    s_pc = pc;
+    s_pe = pe;
+    if (tile == ntiles - 1) {
+      __threadfence();
+      plan_finish(plan, ctl, pc + c, pe + e);
+    }
+  }
+  __syncthreads();
+
+  // ---- phase 3: copy the stash out, ascending, with edge offsets ----
+  uint32_t gbase = s_pc + s_wc[warp];
+  uint32_t ebase = s_pe + s_we[warp];
+  for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
+    uint32_t i = i0 + lane;
+    uint32_t deg = i < cnt ? sd[i] : 0u;
+    uint32_t incl = warp_incl_scan(deg, lane);
+    if (i < cnt) {
+      uint32_t gi = gbase + i;
+      uint32_t eoff = ebase + incl - deg;
+      plan.v[gi] = sv[i];
+      plan.start[gi] = ss[i];
+      plan.off[gi] = eoff;
+      tile_map_entries(plan, gi, eoff, deg);
+    }
+    ebase += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_plan_list: sparse frontier list -> plan (duplicates and order kept,
+// deg-0 entries dropped).  C_VERTS list entries per CTA.
+// ---------------------------------------------------------------------------
+static __global__ void __launch_bounds__(C_WARPS * 32)
+k_plan_list(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ list, uint32_t len,
+            Plan plan, Ctl* ctl, unsigned long long* status, uint32_t ntiles) {
+  __shared__ uint32_t s_v[C_VERTS];
+  __shared__ uint32_t s_start[C_VERTS];
+  __shared__ uint32_t s_deg[C_VERTS];
+  __shared__ uint32_t s_wc[C_WARPS], s_we[C_WARPS];
+  __shared__ uint32_t s_tile, s_pc, s_pe;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = atomicAdd(&ctl->tile_ctr, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint32_t base = tile * C_VERTS + warp * (C_WPW * 32);
+  uint32_t cnt = 0, edg = 0;
+  uint32_t* sv = s_v + warp * (C_WPW * 32);
+  uint32_t* ss = s_start + warp * (C_WPW * 32);
+  uint32_t* sd = s_deg + warp * (C_WPW * 32);
+  for (int j = 0; j < C_WPW; ++j) {
+    uint32_t idx = base + j * 32 + lane;
+    uint32_t v = 0, st = 0, deg = 0;
+    if (idx < len) {
+      v = list[idx];
+      st = ro[v];
+      deg = ro[v + 1] - st;
+    }
+    bool keep = idx < len && deg > 0;
+    unsigned mask = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      uint32_t pos = cnt + __popc(mask & lanemask_lt());
+      sv[pos] = v;
+      ss[pos] = st;
+      sd[pos] = deg;
+    }
+    cnt += __popc(mask);
+    edg += warp_sum(keep ? deg : 0u);
+  }
+  if (lane == 0) {
+    s_wc[warp] = cnt;
+    s_we[warp] = edg;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t c = 0, e = 0;
+    for (int w = 0; w < C_WARPS; ++w) {
+      uint32_t tc = s_wc[w], te = s_we[w];
+      s_wc[w] = c;
+      s_we[w] = e;
+      c += tc;
+      e += te;
+    }
+    uint32_t pc, pe;
+    lb_lookback(status, tile, c, e, &pc, &pe);
+    s_pc = pc;
+    s_pe = pe;
+    if (tile == ntiles - 1) {
+      __threadfence();
+      plan_finish(plan, ctl, pc + c, pe + e);
+    }
+  }
+  __syncthreads();
+  uint32_t gbase = s_pc + s_wc[warp];
+  uint32_t ebase = s_pe + s_we[warp];
+  for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
+    uint32_t i = i0 + lane;
+    uint32_t deg = i < cnt ? sd[i] : 0u;
+    uint32_t incl = warp_incl_scan(deg, lane);
+    if (i < cnt) {
+      uint32_t gi = gbase + i;
+      uint32_t eoff = ebase + incl - deg;
+      plan.v[gi] = sv[i];
+      plan.start[gi] = ss[i];
+      plan.off[gi] = eoff;
+      tile_map_entries(plan, gi, eoff, deg);
+    }
+    ebase += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Advance operator arguments.
+// ---------------------------------------------------------------------------
+enum { OUT_BITMAP = 0, OUT_QUEUE = 1 };
+
+template <class W>
+struct AdvArgs {
+  using D = typename DT<W>::D;
+  const EdgeRec<W>* adj;     // CSR records (push) / CSC records (pull)
+  const uint32_t* ceid;      // CSC -> CSR edge id (pull only)
+  D* dist;
+  uint2* predrec;            // {u, csr edge} of the last improving relax
+  Plan plan;
+  Ctl* ctl;
+  uint32_t* bm_out;          // OUT_BITMAP target (next frontier)
+  const uint32_t* bm_in;     // pull: current frontier bitmap
+  uint32_t* q_out;           // OUT_QUEUE target
+  uint32_t* rec_src;         // RECORD op buffers
+  uint32_t* rec_dst;
+  uint32_t* rec_eid;
+  uint64_t rec_cap;
+  unsigned long long* status;  // zeroed here for the next look-back kernel
+  uint32_t status_len;
+  unsigned long long* qstatus; // OUT_QUEUE look-back state (zero at launch)
+  int op;                    // gfb_op
+};
+
+// Warp-aggregated append of `x` (one atomicAdd per warp).
+__device__ __forceinline__ void warp_append(uint32_t* cnt, uint32_t* q, bool want, uint32_t x,
+                                            uint64_t cap) {
+  unsigned mask = __ballot_sync(0xffffffffu, want);
+  if (!mask) return;
+  int lane = threadIdx.x & 31;
+  int leader = __ffs(mask) - 1;
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(cnt, (uint32_t)__popc(mask));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (want) {
+    uint32_t pos = base + __popc(mask & lanemask_lt());
+    if (pos < cap) q[pos] = x;
+  }
+}
+
+__device__ __forceinline__ void warp_record(Ctl* ctl, uint32_t* rs, uint32_t* rd, uint32_t* re,
+                                            uint64_t cap, bool want, uint32_t s, uint32_t d,
+                                            uint32_t e) {
+  unsigned mask = __ballot_sync(0xffffffffu, want);
+  if (!mask) return;
+  int lane = threadIdx.x & 31;
+  int leader = __ffs(mask) - 1;
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(&ctl->rec_count, (uint32_t)__popc(mask));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (want) {
+    uint64_t pos = (uint64_t)base + __popc(mask & lanemask_lt());
+    if (pos < cap) {
+      rs[pos] = s;
+      rd[pos] = d;
+      re[pos] = e;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Push advance.  Persistent grid over A_TILE-edge tiles of the plan.
+// Per tile: the segments intersecting it are staged in smem (vertex, row
+// start, dist snapshot), every thread locates the segment of its first
+// edge by binary search and walks A_VT edges to fill a local edge->segment
+// map; then edges are processed thread-strided so that consecutive lanes
+// stream consecutive records.
+// OUT_QUEUE (operator API) keeps the reference's output order
+// (frontier position, edge id): thread-contiguous edges + look-back.
+// ---------------------------------------------------------------------------
+template <class W, int OUT>
+__global__ void __launch_bounds__(A_BLOCK)
+k_advance_push(AdvArgs<W> a) {
+  using D = typename DT<W>::D;
+  __shared__ uint32_t s_off[A_TILE + 2];
+  __shared__ uint32_t s_start[A_TILE + 2];
+  __shared__ uint32_t s_u[A_TILE + 2];
+  __shared__ D s_du[A_TILE + 2];
+  __shared__ uint16_t s_seg[A_TILE];
+  __shared__ uint32_t s_tile, s_base;
+  __shared__ uint32_t s_wsum[A_BLOCK / 32];
+
+  // Zero the look-back state for the next look-back kernel (stream order
+  // guarantees the previous one has finished).
+  for (uint32_t i = blockIdx.x * A_BLOCK + threadIdx.x; i < a.status_len;
+       i += gridDim.x * A_BLOCK)
+    a.status[i] = 0;
+
+  const uint32_t total = a.ctl->total;
+  const uint32_t k = a.ctl->k;
+  const uint32_t ntiles = (total + A_TILE - 1) / A_TILE;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned* err = &a.ctl->err;
+  if (blockIdx.x == 0 && tid == 0) {
+    a.ctl->relax += total;  // one cond invocation per plan edge
+    a.ctl->supersteps += 1;
+    a.ctl->push_steps += 1;
+  }
+
+  for (uint32_t it = blockIdx.x;; it += gridDim.x) {
+    uint32_t t;
+    if (OUT == OUT_QUEUE) {
+      // dynamic tile ids (launch order) so the look-back cannot deadlock
+      if (tid == 0) s_tile = atomicAdd(&a.ctl->tile_ctr, 1u);
+      __syncthreads();
+      t = s_tile;
+    } else {
+      t = it;
+    }
+    if (t >= ntiles) break;
+    const uint32_t e0 = t * A_TILE;
+    const uint32_t cnt = min((uint32_t)A_TILE, total - e0);
+    const uint32_t s0 = a.plan.tseg[t];
+    const uint32_t s1 = (t + 1 < ntiles) ? a.plan.tseg[t + 1] : k - 1;
+    const uint32_t nseg = s1 - s0 + 1;
+    for (uint32_t j = tid; j < nseg; j += A_BLOCK) {
+      uint32_t g = s0 + j;
+      uint32_t off = a.plan.off[g];
+      uint32_t u = a.plan.v[g];
+      s_off[j] = off > e0 ? off - e0 : 0u;
+      s_start[j] = a.plan.start[g] + (off < e0 ? e0 - off : 0u);
+      s_u[j] = u;
+      s_du[j] = a.dist[u];
+    }
+    __syncthreads();
+    // edge -> segment map
+    {
+      uint32_t le0 = tid * A_VT;
+      if (le0 < cnt) {
+        uint32_t lo = 0, hi = nseg - 1;  // largest j with s_off[j] <= le0
+        while (lo < hi) {
+          uint32_t mid = (lo + hi + 1) >> 1;
+          if (s_off[mid] <= le0) lo = mid;
+          else hi = mid - 1;
+        }
+        uint32_t j = lo;
+#pragma unroll
+        for (int r = 0; r < A_VT; ++r) {
+          uint32_t le = le0 + r;
+          if (le < cnt) {
+            while (j + 1 < nseg && s_off[j + 1] <= le) ++j;
+            s_seg[le] = (uint16_t)j;
+          }
+        }
+      }
+    }
+    __syncthreads();
+
+    if (OUT == OUT_BITMAP) {
+#pragma unroll
+      for (int r = 0; r < A_VT; ++r) {
+        uint32_t le = r * A_BLOCK + tid;
+        bool act = false, live = le < cnt;
+        uint32_t e = 0, dst = 0, u = 0;
+        if (live) {
+          uint32_t j = s_seg[le];
+          e = s_start[j] + (le - s_off[j]);
+          EdgeRec<W> rec = ld_rec(a.adj + e);
+          dst = rec.v;
+          u = s_u[j];
+          if (a.op == GFB_OP_RELAX_MIN) {
+            D nd = dadd(s_du[j], rec.w, err);
+            D cur = ld_dist(a.dist + dst);
+            if (nd < cur) {
+              D old = atomic_min_d(a.dist + dst, nd);
+              if (nd < old) {
+                act = true;
+                a.predrec[dst] = make_uint2(u, e);
+              }
+            }
+          } else if (a.op == GFB_OP_ALWAYS) {
+            act = true;
+          }
+        }
+        if (a.op == GFB_OP_RECORD)
+          warp_record(a.ctl, a.rec_src, a.rec_dst, a.rec_eid, a.rec_cap, live, u, dst, e);
+        if (act) atomicOr(a.bm_out + (dst >> 5), 1u << (dst & 31));
+      }
+    } else {
+      // ordered queue output: thread owns edges [tid*A_VT, tid*A_VT + A_VT)
+      uint32_t hits[A_VT];
+      uint32_t nh = 0;
+#pragma unroll
+      for (int r = 0; r < A_VT; ++r) {
+        uint32_t le = tid * A_VT + r;
+        bool act = false, live = le < cnt;
+        uint32_t e = 0, dst = 0, u = 0;
+        if (live) {
+          uint32_t j = s_seg[le];
+          e = s_start[j] + (le - s_off[j]);
+          EdgeRec<W> rec = ld_rec(a.adj + e);
+          dst = rec.v;
+          u = s_u[j];
+          if (a.op == GFB_OP_RELAX_MIN) {
+            D nd = dadd(s_du[j], rec.w, err);
+            D cur = ld_dist(a.dist + dst);
+            if (nd < cur) {
+              D old = atomic_min_d(a.dist + dst, nd);
+              if (nd < old) {
+                act = true;
+                a.predrec[dst] = make_uint2(u, e);
+              }
+            }
+          } else if (a.op == GFB_OP_ALWAYS) {
+            act = true;
+          }
+        }
+        if (a.op == GFB_OP_RECORD)
+          warp_record(a.ctl, a.rec_src, a.rec_dst, a.rec_eid, a.rec_cap, live, u, dst, e);
+        if (act) hits[nh++] = dst;
+      }
+      // block-exclusive scan of per-thread hit counts
+      uint32_t incl = warp_incl_scan(nh, lane);
+      if (lane == 31) s_wsum[warp] = incl;
+      __syncthreads();
+      if (tid == 0) {
+        uint32_t c = 0;
+        for (int w = 0; w < A_BLOCK / 32; ++w) {
+          uint32_t x = s_wsum[w];
+          s_wsum[w] = c;
+          c += x;
+        }
+        uint32_t pc, pe;
+        lb_lookback(a.qstatus, t, c, 0u, &pc, &pe);
+        s_base = pc;
+        if (t == ntiles - 1) a.ctl->out_count = pc + c;
+      }
+      __syncthreads();
+      uint32_t pos = s_base + s_wsum[warp] + incl - nh;
+      for (uint32_t i = 0; i < nh; ++i) a.q_out[pos + i] = hits[i];
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pull advance.  Segments = destination vertices with in-degree > 0 (a
+// static plan over the CSC built at upload).  Every in-edge whose source is
+// in the current frontier bitmap is a cond invocation; RELAX_MIN reduces
+// the candidates per destination in smem (bit-pattern atomicMin) and does
+// at most one global atomicMin per (tile, destination).
+// ---------------------------------------------------------------------------
+template <class W>
+__global__ void __launch_bounds__(A_BLOCK)
+k_advance_pull(AdvArgs<W> a, uint32_t total, uint32_t k) {
+  using D = typename DT<W>::D;
+  using Bits = typename DT<W>::Bits;
+  __shared__ uint32_t s_off[A_TILE + 2];
+  __shared__ uint32_t s_start[A_TILE + 2];
+  __shared__ uint32_t s_u[A_TILE + 2];
+  __shared__ Bits s_best[A_TILE + 2];
+  __shared__ uint32_t s_slot[A_TILE + 2];
+  __shared__ uint16_t s_seg[A_TILE];
+  for (uint32_t i = blockIdx.x * A_BLOCK + threadIdx.x; i < a.status_len;
+       i += gridDim.x * A_BLOCK)
+    a.status[i] = 0;
+  const uint32_t ntiles = (total + A_TILE - 1) / A_TILE;
+  const int tid = threadIdx.x;
+  unsigned* err = &a.ctl->err;
+  if (blockIdx.x == 0 && tid == 0) {
+    a.ctl->supersteps += 1;
+    a.ctl->pull_steps += 1;
+  }
+  uint32_t n_elig = 0;
+  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint32_t e0 = t * A_TILE;
+    const uint32_t cnt = min((uint32_t)A_TILE, total - e0);
+    const uint32_t s0 = a.plan.tseg[t];
+    const uint32_t s1 = (t + 1 < ntiles) ? a.plan.tseg[t + 1] : k - 1;
+    const uint32_t nseg = s1 - s0 + 1;
+    for (uint32_t j = tid; j < nseg; j += A_BLOCK) {
+      uint32_t g = s0 + j;
+      uint32_t off = a.plan.off[g];
+      s_off[j] = off > e0 ? off - e0 : 0u;
+      s_start[j] = a.plan.start[g] + (off < e0 ? e0 - off : 0u);
+      s_u[j] = a.plan.v[g];
+      s_best[j] = (Bits)DT<W>::INF_BITS;
+      s_slot[j] = NIL;
+    }
+    __syncthreads();
+    {
+      uint32_t le0 = tid * A_VT;
+      if (le0 < cnt) {
+        uint32_t lo = 0, hi = nseg - 1;
+        while (lo < hi) {
+          uint32_t mid = (lo + hi + 1) >> 1;
+          if (s_off[mid] <= le0) lo = mid;
+          else hi = mid - 1;
+        }
+        uint32_t j = lo;
+#pragma unroll
+        for (int r = 0; r < A_VT; ++r) {
+          uint32_t le = le0 + r;
+          if (le < cnt) {
+            while (j + 1 < nseg && s_off[j + 1] <= le) ++j;
+            s_seg[le] = (uint16_t)j;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    D cand[A_VT];
+    uint32_t cslot[A_VT];
+#pragma unroll
+    for (int r = 0; r < A_VT; ++r) {
+      uint32_t le = r * A_BLOCK + tid;
+      cslot[r] = NIL;
+      bool live = le < cnt;
+      uint32_t slot = 0, src = 0, j = 0;
+      bool elig = false;
+      EdgeRec<W> rec;
+      if (live) {
+        j = s_seg[le];
+        slot = s_start[j] + (le - s_off[j]);
+        rec = ld_rec(a.adj + slot);
+        src = rec.v;
+        elig = (a.bm_in[src >> 5] >> (src & 31)) & 1u;
+        n_elig += elig;
+      }
+      if (a.op == GFB_OP_RECORD) {
+        uint32_t eid = elig ? a.ceid[slot] : 0u;
+        warp_record(a.ctl, a.rec_src, a.rec_dst, a.rec_eid, a.rec_cap, elig, src,
+                    live ? s_u[j] : 0u, eid);
+      } else if (elig) {
+        if (a.op == GFB_OP_RELAX_MIN) {
+          D nd = dadd(ld_dist(a.dist + src), rec.w, err);
+          cand[r] = nd;
+          cslot[r] = slot;
+          Bits b = *reinterpret_cast<Bits*>(&nd);
+          atomicMin(&s_best[j], b);
+        } else {  // ALWAYS: activation only
+          s_slot[j] = slot;
+        }
+      }
+    }
+    __syncthreads();
+    if (a.op == GFB_OP_RELAX_MIN) {
+#pragma unroll
+      for (int r = 0; r < A_VT; ++r) {
+        if (cslot[r] != NIL) {
+          uint32_t le = r * A_BLOCK + tid;
+          uint32_t j = s_seg[le];
+          D nd = cand[r];
+          if (*reinterpret_cast<Bits*>(&nd) == s_best[j]) s_slot[j] = cslot[r];  // any tie
+        }
+      }
+      __syncthreads();
+    }
+    for (uint32_t j = tid; j < nseg; j += A_BLOCK) {
+      uint32_t slot = s_slot[j];
+      if (slot == NIL) continue;
+      uint32_t u = s_u[j];
+      bool act = true;
+      if (a.op == GFB_OP_RELAX_MIN) {
+        Bits b = s_best[j];
+        D best = *reinterpret_cast<D*>(&b);
+        D cur = ld_dist(a.dist + u);
+        act = false;
+        if (best < cur) {
+          D old = atomic_min_d(a.dist + u, best);
+          if (best < old) {
+            act = true;
+            EdgeRec<W> rec = ld_rec(a.adj + slot);
+            a.predrec[u] = make_uint2(rec.v, a.ceid[slot]);
+          }
+        }
+      }
+      if (act) atomicOr(a.bm_out + (u >> 5), 1u << (u & 31));
+    }
+    __syncthreads();
+  }
+  n_elig = warp_sum(n_elig);  // eligible in-edges = cond invocations
+  if ((tid & 31) == 0 && n_elig) atomicAdd(&a.ctl->relax, (unsigned long long)n_elig);
+}
+
+// ---------------------------------------------------------------------------
+// Init (algorithms.hpp:579-583): dist = +inf, pred = NIL, bitmaps clear,
+// dist[source] = 0 and the source marked in the next-frontier bitmap.
+// ---------------------------------------------------------------------------
+template <class W>
+__global__ void k_init(typename DT<W>::D* dist, uint2* predrec, uint32_t* bm_next,
+                       uint32_t* bm_cur, uint32_t n, uint32_t nwords, uint32_t source,
+                       Ctl* ctl) {
+  using D = typename DT<W>::D;
+  uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    dist[i] = i == source ? D(0) : dinf<W>();
+    predrec[i] = make_uint2(NIL, NIL);
+  }
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nwords; i += stride) {
+    uint32_t w = (source >> 5) == i ? (1u << (source & 31)) : 0u;
+    bm_next[i] = w;
+    if (bm_cur) bm_cur[i] = 0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    Ctl c = {};
+    *ctl = c;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Predecessor pass.
+//  k_pred_verify: pred[v] = u of the recorded improving relax when that edge
+//    is still tight and strictly decreasing (dist[u] < dist[v]); else v goes
+//    to the repair set.  Strictly decreasing chains are acyclic.
+//  k_pred_repair: one pass over the CSR edges into repair-set vertices,
+//    round r accepts a tight edge u->v when u was resolved in an earlier
+//    round (round 1: dist[u] < dist[v]; later rounds: equal distances, the
+//    zero-weight tie classes that make a plain argmin cycle, cf.
+//    algorithms.hpp:506-511).  Smallest u wins (deterministic).
+// Also accumulates n_reach / m_reach for the bench's GTEPS.
+// ---------------------------------------------------------------------------
+template <class W>
+__global__ void k_pred_verify(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ adj,
+                              const typename DT<W>::D* __restrict__ dist,
+                              const uint2* __restrict__ predrec, uint32_t* pred, uint32_t* res,
+                              uint32_t* repair_bm, uint32_t n, uint32_t source, Ctl* ctl) {
+  using D = typename DT<W>::D;
+  uint32_t stride = gridDim.x * blockDim.x;
+  unsigned long long nr = 0, mr = 0;
+  uint32_t unres = 0;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+    D dv = dist[v];
+    uint32_t p = NIL, r = 0;
+    bool reach = !(dv == dinf<W>());
+    if (reach) {
+      ++nr;
+      mr += ro[v + 1] - ro[v];
+      if (v == source) {
+        r = 1;
+      } else {
+        uint2 pr = predrec[v];
+        if (pr.x != NIL) {
+          EdgeRec<W> rec = adj[pr.y];
+          D du = dist[pr.x];
+          if (rec.v == v && du < dv) {
+            D t = dadd(du, rec.w, nullptr);
+            if (t == dv) {
+              p = pr.x;
+              r = 1;
+            }
+          }
+        }
+        if (!r) {
+          ++unres;
+          atomicOr(repair_bm + (v >> 5), 1u << (v & 31));
+        }
+      }
+    }
+    pred[v] = p;
+    res[v] = r;
+  }
+  // block-reduce the counters (few atomics)
+  for (int d = 16; d > 0; d >>= 1) {
+    nr += __shfl_xor_sync(0xffffffffu, nr, d);
+    mr += __shfl_xor_sync(0xffffffffu, mr, d);
+    unres += __shfl_xor_sync(0xffffffffu, unres, d);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (nr) atomicAdd(&ctl->n_reach, nr);
+    if (mr) atomicAdd(&ctl->m_reach, mr);
+    if (unres) atomicAdd(&ctl->unresolved, unres);
+  }
+}
+
+// One repair round over ALL CSR rows of reached vertices (vertex-parallel,
+// warp per row).  Only runs when the verify pass left vertices unresolved.
+template <class W>
+__global__ void k_pred_repair(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ adj,
+                              const typename DT<W>::D* __restrict__ dist, uint32_t* cand,
+                              const uint32_t* res, const uint32_t* repair_bm, uint32_t n,
+                              uint32_t round) {
+  using D = typename DT<W>::D;
+  const int lane = threadIdx.x & 31;
+  uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < n; u += warps) {
+    D du = dist[u];
+    if (du == dinf<W>()) continue;
+    // round 1: strictly decreasing tight edges from any reached u;
+    // round r > 1: equal-distance tight edges from u resolved before round r
+    uint32_t ru = res[u];
+    if (round > 1 && (ru == 0 || ru > round)) continue;
+    for (uint32_t e = ro[u] + lane; e < ro[u + 1]; e += 32) {
+      EdgeRec<W> rec = adj[e];
+      uint32_t v = rec.v;
+      if (!((repair_bm[v >> 5] >> (v & 31)) & 1u)) continue;
+      if (res[v] != 0) continue;
+      D dv = dist[v];
+      bool ok = round == 1 ? du < dv : du == dv;
+      if (!ok) continue;
+      if (dadd(du, rec.w, nullptr) == dv) atomicMin(cand + v, u);
+    }
+  }
+}
+
+// Apply round `round`'s candidates; counts how many vertices were resolved.
+static __global__ void k_pred_apply(uint32_t* cand, uint32_t* pred, uint32_t* res,
+                             uint32_t* repair_bm, uint32_t n, uint32_t round, Ctl* ctl) {
+  uint32_t stride = gridDim.x * blockDim.x;
+  uint32_t done = 0;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+    uint32_t c = cand[v];
+    if (c != NIL && res[v] == 0) {
+      pred[v] = c;
+      res[v] = round + 1;
+      cand[v] = NIL;
+      atomicAnd(repair_bm + (v >> 5), ~(1u << (v & 31)));
+      ++done;
+    }
+  }
+  done = warp_sum(done);
+  if ((threadIdx.x & 31) == 0 && done) atomicAdd(&ctl->flag, done);
+}
+
+}  // namespace gfb
