@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""SSSP GTEPS bench (BASELINE.json metric) for the B200 path and the reference.
+
+Default workload: BASELINE config 3 -- RMAT scale 24, edge factor 16, fp32
+U[0,1) weights, source 0, push/pull direction switching (one B200).
+A "step" is one full sssp() (init .. last superstep .. predecessor pass).
+
+  value   GTEPS = m_reach / device time per step, graph resident in HBM
+          (CUDA events on the library's stream; max over ranks).
+  e2e     the same metric through the public C ABI with HOST buffers: each
+          step re-uploads the reference-layout CSR from pinned memory
+          (gfb_graph_refill: H2D + device CSR/CSC build), runs gfb_sssp and
+          copies dist (f64) + pred back.
+  roofline  dominant kernel = the advance: algorithmic bytes (B_alg per
+          visited edge) / CUDA-event advance time.
+  cpu_baseline  the unmodified reference (oracle/_ref) on this host's cores,
+          bounded sample (RMAT scale 20, same generator).
+
+--impl reference times the reference's own sssp() (ExecutionPolicy::parallel
+(hardware_concurrency), push, sparse: graflow_cli.cpp:34-37) per step.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SSSP GTEPS on RMAT (1/2/4/8 B200) and % of HBM roofline vs host-CPU ref"
+NOMINAL_HBM_GBS = 8000.0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks ---
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,utilization.gpu,power.draw,"
+              "clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, device=0):
+        self.device, self.rows, self.proc = device, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        load = [r for r in self.rows if len(r) >= 8 and r[2].isdigit() and int(r[2]) > 0]
+        use = load or [r for r in self.rows if len(r) >= 8]
+        if not use:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[0]) for r in use if r[0].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in use for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(use[0][1]) if use[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(use), "samples_under_load": len(load)}
+
+
+# -------------------------------------------------------------- reference ---
+def ref_graph_from_csr(ro, col, w):
+    from oracle import oracle as O
+    n = len(ro) - 1
+    src = np.repeat(np.arange(n, dtype=np.uint32), np.diff(ro).astype(np.int64))
+    t0 = time.time()
+    g = O.RefGraph(n, src, col, w.astype(np.float64))
+    log(f"[ref] build_csr n={n} m={len(col)} {time.time() - t0:.1f}s (untimed)")
+    return g
+
+
+def rmat_csr_host(scale, ef, seed):
+    """Reference-arm input: the oracle's C restatement of the generator and
+    build_csr (no product code on this path)."""
+    from oracle import oracle as O
+    s, d, wb = O.rmat_edges(scale, ef, seed=seed, wkind=1)
+    order = np.lexsort((wb.view(np.float32), d, s))
+    ro = np.zeros((1 << scale) + 1, np.int64)
+    np.add.at(ro, s.astype(np.int64) + 1, 1)
+    return np.cumsum(ro).astype(np.uint32), d[order], wb.view(np.float32)[order]
+
+
+def m_reach_of(ro, dist):
+    reach = np.isfinite(dist)
+    return int(np.diff(ro.astype(np.int64))[reach].sum()), int(reach.sum())
+
+
+def cpu_reference_runs(ro, col, w, kinds=("par", "seq", "dijkstra")):
+    """Time the unmodified reference on this host: returns {kind: (sec, cores)}."""
+    from oracle import oracle as O
+    L = O.ref()
+    if L is None:
+        return None, None
+    g = ref_graph_from_csr(ro, col, w)
+    cores = int(L.ref_hardware_concurrency())
+    out = {}
+    dist = None
+    for kind in kinds:
+        t0 = time.perf_counter()
+        if kind == "par":
+            dist, _, _, _ = g.sssp(0, mode=1, workers=cores, direction=0, repr_=0)
+            c = cores
+        elif kind == "seq":
+            dist, _, _, _ = g.sssp(0, mode=0, workers=1, direction=0, repr_=0)
+            c = 1
+        else:
+            dist, _ = g.dijkstra(0)
+            c = 1
+        out[kind] = (time.perf_counter() - t0, c)
+        log(f"[ref] {kind}: {out[kind][0]:.2f}s on {c} thread(s)")
+    return out, dist
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    if O.ref() is None:
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref/libgraflow_ref.so not built"}))
+        return
+    scale = args.ref_scale
+    ro, col, w = rmat_csr_host(scale, args.edgefactor, args.seed)
+    g = ref_graph_from_csr(ro, col, w)
+    cores = int(O.ref().ref_hardware_concurrency())
+    times, dist = [], None
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        dist, _, st, rl = g.sssp(0, mode=1, workers=cores, direction=0, repr_=0)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    m_reach, n_reach = m_reach_of(ro, dist)
+    t = sum(times) / len(times)
+    gteps = m_reach / t / 1e9
+    sample = (f"RMAT scale {scale} EF{args.edgefactor} fp32 (same generator), source 0, reference "
+              f"sssp() par({cores})/push/sparse; m_reach={m_reach}")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": gteps, "unit": "GTEPS",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args),
+        "cpu_baseline": {"value": gteps, "unit": "GTEPS", "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": gteps, "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "supersteps": st, "relaxations": rl}))
+
+
+def config_dict(args):
+    return {"workload": f"RMAT scale {args.scale} EF{args.edgefactor} fp32 U[0,1) weights, "
+                        f"source 0, direction {args.direction} (BASELINE.json configs[2])",
+            "scale": args.scale, "edgefactor": args.edgefactor, "weights": "f32",
+            "direction": args.direction, "seed": args.seed,
+            "l2": "inputs larger than L2 (CSR+CSC ~4.3 GB at scale 24 vs 126 MB L2)"}
+
+
+# ---------------------------------------------------------------- our arm ---
+def run_ours(args):
+    import paper_2212_08200_b200 as gb
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import bench_mg
+        return bench_mg.run(args, rank, world)
+    ctx = gb.Context(0)
+    t0 = time.time()
+    g = gb.rmat(args.scale, args.edgefactor, seed=args.seed, wtype="f32", transpose=True, ctx=ctx)
+    log(f"[gpu] generated RMAT s{args.scale}: n={g.num_vertices} m={g.num_edges} "
+        f"in {time.time() - t0:.1f}s")
+    kw = dict(direction=args.direction, pull_alpha=args.alpha)
+
+    sampler = ClockSampler()
+    sampler.start()
+    # warm-up (also keeps the GPU busy long enough for clock samples)
+    t_end = time.time() + args.soak
+    i = 0
+    while i < args.warmup or time.time() < t_end:
+        _, _, st = gb.sssp_stats(g, 0, want_result=False, **kw)
+        i += 1
+    # timed region: exactly K steps, device time from CUDA events
+    dev_ms, launches = [], 0
+    wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        _, _, st = gb.sssp_stats(g, 0, want_result=False, **kw)
+        dev_ms.append(st.device_ms)
+        launches += st.kernel_launches
+    wall = time.perf_counter() - wall0
+    clocks = sampler.stop()
+    m_reach, n_reach = st.m_reach, st.n_reach
+    t_ms = sum(dev_ms) / len(dev_ms)
+    gteps = m_reach / (t_ms * 1e-3) / 1e9
+    b_alg = 12.0 + 20.0 * n_reach / m_reach
+    peak, peak_kind = peaks()
+
+    # kernel roofline: advance launches, CUDA events per launch (host loop)
+    _, _, ist = gb.sssp_stats(g, 0, want_result=False, device_loop=False, **kw)
+    adv_bytes = b_alg * ist.relaxations
+    achieved = adv_bytes / (ist.advance_ms * 1e-3) / 1e9 if ist.advance_ms > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "advance_traffic.json")
+    if os.path.exists(tp):
+        tr = json.load(open(tp))
+        if tr.get("scale") == args.scale:
+            traffic = tr.get("dram_bytes_per_launch")
+
+    # correctness spot-check of the timed configuration (size-independent
+    # property: no edge can still relax; cheap on the device result)
+    dist, pred = gb.sssp_read(g, native=True)
+
+    # e2e through the public API with host buffers
+    e2e = run_e2e(gb, ctx, g, args, kw)
+
+    cpu = None
+    if not args.no_cpu:
+        cpu = cpu_baseline(gb, ctx, args)
+
+    out = {
+        "metric": METRIC, "value": gteps, "unit": "GTEPS", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (device-generated RMAT)",
+        "config": config_dict(args),
+        "e2e": e2e,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if achieved else None, "traffic": traffic,
+                     "kernel": "k_advance_push/k_advance_pull",
+                     "bytes_per_visit": b_alg, "visits_per_step": ist.relaxations,
+                     "advance_ms_per_step": ist.advance_ms,
+                     "advance_launches_per_step": ist.advance_launches,
+                     "peak_kind": peak_kind},
+        "roofline_sssp": {"b_alg_bytes_per_te": b_alg,
+                          "achieved_gbs": gteps * b_alg,
+                          "frac_of_measured": gteps * b_alg / peak,
+                          "frac_of_8tbs": gteps * b_alg / NOMINAL_HBM_GBS,
+                          "roofline_gteps_8tbs": NOMINAL_HBM_GBS / b_alg},
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "gpu_launches": launches,
+        "m_reach": m_reach, "n_reach": n_reach, "supersteps": st.supersteps,
+        "relaxations": st.relaxations, "work_inflation": st.relaxations / m_reach,
+        "push_steps": st.push_steps, "pull_steps": st.pull_steps,
+        "pred_fallback": st.pred_fallback, "wall_s_timed": wall,
+    }
+    if cpu and cpu.get("value"):
+        out["speedup_vs_cpu_best"] = gteps / cpu["value"]
+        if e2e and e2e.get("value"):
+            out["e2e_speedup_vs_cpu_best"] = e2e["value"] / cpu["value"]
+    print(json.dumps(out))
+
+
+def run_e2e(gb, ctx, g, args, kw):
+    """Public API, host buffers: refill (H2D + device build) + sssp + D2H."""
+    import torch  # pinned host memory only
+    ro, col, w = g.csr()
+    n, m = g.num_vertices, g.num_edges
+    p_ro = torch.from_numpy(ro).pin_memory().numpy()
+    p_col = torch.from_numpy(col).pin_memory().numpy()
+    p_w = torch.from_numpy(w).pin_memory().numpy()
+    dist = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
+    pred = torch.empty(n, dtype=torch.int32).pin_memory().numpy().view(np.uint32)
+    lib = gb._lib.load()
+    o = gb._opts(**kw)
+    st = gb.SsspStats()
+    times = []
+    steps = max(1, args.e2e_steps)
+    for i in range(1 + steps):
+        t0 = time.perf_counter()
+        gb.check(lib.gfb_graph_refill(g.h, C.c_void_p(p_ro.ctypes.data),
+                                      C.c_void_p(p_col.ctypes.data),
+                                      C.c_void_p(p_w.ctypes.data), gb.W_F32))
+        gb.check(lib.gfb_sssp(ctx.h, g.h, 0, C.byref(o), C.c_void_p(dist.ctypes.data),
+                              C.c_void_p(pred.ctypes.data), C.byref(st)))
+        dt = time.perf_counter() - t0
+        if i > 0:
+            times.append(dt)
+    t = sum(times) / len(times)
+    h2d = ro.nbytes + col.nbytes + w.nbytes
+    d2h = dist.nbytes + pred.nbytes
+    return {"value": st.m_reach / t / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": t * 1e3, "steps": steps,
+            "path": "gfb_graph_refill(pinned CSR, build CSC) + gfb_sssp(dist f64, pred)"}
+
+
+def cpu_baseline(gb, ctx, args):
+    from oracle import oracle as O
+    if O.ref() is None:
+        return {"value": None, "unit": "GTEPS", "cores": None, "kind": "reference",
+                "sample": "oracle/_ref not built"}
+    gs = gb.rmat(args.ref_scale, args.edgefactor, seed=args.seed, wtype="f32", transpose=False,
+                 ctx=ctx)
+    ro, col, w = gs.csr()
+    _, _, st = gb.sssp_stats(gs, 0, want_result=False)
+    runs, dist = cpu_reference_runs(ro, col, w)
+    m_reach = st.m_reach
+    best = min(runs, key=lambda k: runs[k][0])
+    res = {k: {"s": v[0], "cores": v[1], "gteps": m_reach / v[0] / 1e9} for k, v in runs.items()}
+    gpu_same = m_reach / (st.device_ms * 1e-3) / 1e9
+    return {"value": m_reach / runs[best][0] / 1e9, "unit": "GTEPS", "cores": runs[best][1],
+            "kind": "reference",
+            "sample": f"RMAT scale {args.ref_scale} EF{args.edgefactor} fp32, source 0, m_reach="
+                      f"{m_reach}; fastest of reference sssp() par/seq (push, sparse) and "
+                      f"reference_dijkstra = {best}",
+            "runs": res, "gpu_gteps_same_sample": gpu_same}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--edgefactor", type=int, default=16)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--direction", default="auto", choices=["auto", "push", "pull"])
+    ap.add_argument("--alpha", type=float, default=4.0)
+    ap.add_argument("--ref-scale", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--soak", type=float, default=1.5, help="min warm-up seconds (clock samples)")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -181,8 +181,10 @@ typedef struct gfb_sssp_stats {
   uint64_t push_steps, pull_steps;
   uint64_t pred_fallback; /* vertices whose pred needed the repair pass */
   double device_ms;       /* CUDA-event time: init .. last superstep + pred */
-  double advance_ms;      /* CUDA-event time of the advance launches (sum) */
+  double advance_ms;      /* CUDA-event time of the advance launches (sum;
+                             host-loop mode only, 0 under the device loop) */
   uint64_t advance_launches;
+  uint64_t kernel_launches; /* libgfb kernels launched by this call */
 } gfb_sssp_stats;
 
 /* Runs init, the BSP loop and the predecessor pass on the device.  dist is

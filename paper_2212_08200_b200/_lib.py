@@ -37,7 +37,8 @@ class SsspStats(C.Structure):
     _fields_ = [("supersteps", C.c_uint64), ("relaxations", C.c_uint64), ("n_reach", C.c_uint64),
                 ("m_reach", C.c_uint64), ("push_steps", C.c_uint64), ("pull_steps", C.c_uint64),
                 ("pred_fallback", C.c_uint64), ("device_ms", C.c_double),
-                ("advance_ms", C.c_double), ("advance_launches", C.c_uint64)]
+                ("advance_ms", C.c_double), ("advance_launches", C.c_uint64),
+                ("kernel_launches", C.c_uint64)]
 
 
 SIGNATURES = {

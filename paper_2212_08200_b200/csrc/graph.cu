@@ -190,7 +190,7 @@ static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const 
   if (hf[1] != ~0ull)
     fail(GFB_EINVAL,
          "build_csr: edge " + std::to_string(hf[1]) + " has negative or non-finite weight");
-  g->ws.reset();
+  if (g->ws) g->ws->has_result = false;  // same shape: keep the workspace
 }
 
 Graph* graph_upload(Ctx* c, uint64_t n, uint64_t m, const uint32_t* ro, const uint32_t* col,

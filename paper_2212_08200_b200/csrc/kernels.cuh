@@ -401,7 +401,7 @@ k_advance_push(AdvArgs<W> a) {
       s_off[j] = off > e0 ? off - e0 : 0u;
       s_start[j] = a.plan.start[g] + (off < e0 ? e0 - off : 0u);
       s_u[j] = u;
-      s_du[j] = a.dist[u];
+      s_du[j] = a.dist ? a.dist[u] : D(0);
     }
     __syncthreads();
     // edge -> segment map

@@ -48,6 +48,7 @@ struct Runner {
   Workspace* ws;
   cudaStream_t s;
   uint32_t n, nwords;
+  uint64_t kernels = 0;
 
   Plan plan() const {
     return Plan{ws->pv.as<uint32_t>(), ws->pstart.as<uint32_t>(), ws->poff.as<uint32_t>(),
@@ -104,6 +105,7 @@ struct Runner {
     const int dir = o->direction;
     const double alpha = o->pull_alpha > 0 ? o->pull_alpha : 4.0;
     uint64_t supersteps = 0, push_steps = 0, pull_steps = 0, launches = 0;
+    kernels = 2;  // k_init + first k_compact
     float adv_ms = 0;
     for (;;) {
       Ctl h = c->read_ctl(ws->ctl.as<Ctl>());
@@ -121,6 +123,7 @@ struct Runner {
       GFB_CUDA(cudaGetLastError());
       ++supersteps;
       ++launches;
+      kernels += 2;
       (pull ? pull_steps : push_steps)++;
       GFB_CUDA(cudaEventSynchronize(c->ev[3]));
       float ms = 0;
@@ -147,6 +150,7 @@ struct Runner {
       st->device_ms = ms;
       st->advance_ms = adv_ms;
       st->advance_launches = launches;
+      st->kernel_launches = kernels;
     }
   }
 
@@ -157,6 +161,7 @@ struct Runner {
         ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(), ws->repair_bm.as<uint32_t>(), n, source,
         ws->ctl.as<Ctl>());
     GFB_CUDA(cudaGetLastError());
+    ++kernels;
     if (!want) return;
     Ctl h = c->read_ctl(ws->ctl.as<Ctl>());
     *fallback = h.unresolved;
@@ -173,8 +178,12 @@ struct Runner {
                                                   ws->repair_bm.as<uint32_t>(), n, round,
                                                   ws->ctl.as<Ctl>());
       GFB_CUDA(cudaGetLastError());
+      kernels += 2;
       Ctl r = c->read_ctl(ws->ctl.as<Ctl>());
-      if (r.flag == 0) fail(GFB_ELOGIC, "sssp: predecessor repair made no progress");
+      // round 1 (strict edges) may resolve nothing when every unresolved
+      // vertex sits in a zero-weight tie class; later rounds must progress.
+      if (r.flag == 0 && round > 1)
+        fail(GFB_ELOGIC, "sssp: predecessor repair made no progress");
       left -= std::min<uint64_t>(left, r.flag);
     }
   }
