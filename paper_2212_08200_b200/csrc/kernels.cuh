@@ -695,7 +695,8 @@ template <class W>
 __global__ void k_pred_verify(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ adj,
                               const typename DT<W>::D* __restrict__ dist,
                               const uint2* __restrict__ predrec, uint32_t* pred, uint32_t* res,
-                              uint32_t* repair_bm, uint32_t n, uint32_t source, Ctl* ctl) {
+                              uint32_t* repair_bm, uint32_t* unres_list, uint32_t n,
+                              uint32_t source, Ctl* ctl) {
   using D = typename DT<W>::D;
   uint32_t stride = gridDim.x * blockDim.x;
   unsigned long long nr = 0, mr = 0;
@@ -725,6 +726,7 @@ __global__ void k_pred_verify(const uint32_t* __restrict__ ro, const EdgeRec<W>*
         if (!r) {
           ++unres;
           atomicOr(repair_bm + (v >> 5), 1u << (v & 31));
+          unres_list[atomicAdd(&ctl->flag, 1u)] = v;  // rare: races and ties
         }
       }
     }
@@ -772,6 +774,53 @@ __global__ void k_pred_repair(const uint32_t* __restrict__ ro, const EdgeRec<W>*
       if (dadd(du, rec.w, nullptr) == dv) atomicMin(cand + v, u);
     }
   }
+}
+
+// CSC repair round: one warp per unresolved vertex scans its in-edges in
+// CSC order (ascending source) and takes the FIRST acceptable tight edge,
+// i.e. the smallest source id -- deterministic, with an early exit.
+template <class W>
+__global__ void k_pred_csc_round(const uint32_t* __restrict__ co,
+                                 const EdgeRec<W>* __restrict__ cadj,
+                                 const typename DT<W>::D* __restrict__ dist, uint32_t* pred,
+                                 uint32_t* res, const uint32_t* list, uint32_t count,
+                                 uint32_t round, Ctl* ctl) {
+  using D = typename DT<W>::D;
+  const int lane = threadIdx.x & 31;
+  uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  uint32_t done = 0;
+  for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < count; i += warps) {
+    uint32_t v = list[i];
+    if (res[v] != 0) continue;  // warp-uniform
+    D dv = dist[v];
+    uint32_t found = NIL;
+    for (uint32_t base = co[v]; base < co[v + 1] && found == NIL; base += 32) {
+      uint32_t slot = base + lane;
+      bool ok = false;
+      uint32_t u = 0;
+      if (slot < co[v + 1]) {
+        EdgeRec<W> rec = cadj[slot];
+        u = rec.v;
+        D du = dist[u];
+        if (!(du == dinf<W>()) && dadd(du, rec.w, nullptr) == dv) {
+          if (round == 1) {
+            ok = du < dv;
+          } else {
+            uint32_t ru = res[u];
+            ok = du == dv && ru != 0 && ru <= round;
+          }
+        }
+      }
+      unsigned mask = __ballot_sync(0xffffffffu, ok);
+      if (mask) found = __shfl_sync(0xffffffffu, u, __ffs(mask) - 1);
+    }
+    if (found != NIL && lane == 0) {
+      pred[v] = found;
+      res[v] = round + 1;
+      ++done;
+    }
+  }
+  if (lane == 0 && done) atomicAdd(&ctl->flag, done);
 }
 
 // Apply round `round`'s candidates; counts how many vertices were resolved.

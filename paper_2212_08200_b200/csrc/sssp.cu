@@ -156,18 +156,44 @@ struct Runner {
 
   void pred_pass(uint32_t source, bool want, uint64_t* fallback) {
     GFB_CUDA(cudaMemsetAsync(ws->repair_bm.p, 0, (size_t)nwords * 4, s));
+    GFB_CUDA(cudaMemsetAsync(&ws->ctl.as<Ctl>()->flag, 0, 4, s));
     k_pred_verify<W><<<stride_grid(c), 256, 0, s>>>(
         g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(), ws->dist.as<D>(), ws->predrec.as<uint2>(),
-        ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(), ws->repair_bm.as<uint32_t>(), n, source,
-        ws->ctl.as<Ctl>());
+        ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(), ws->repair_bm.as<uint32_t>(),
+        ws->cand.as<uint32_t>(), n, source, ws->ctl.as<Ctl>());
     GFB_CUDA(cudaGetLastError());
     ++kernels;
     if (!want) return;
     Ctl h = c->read_ctl(ws->ctl.as<Ctl>());
     *fallback = h.unresolved;
     if (h.unresolved == 0) return;
-    GFB_CUDA(cudaMemsetAsync(ws->cand.p, 0xFF, (size_t)n * 4, s));
     uint64_t left = h.unresolved;
+    if (g->has_csc) {
+      // unresolved vertices were appended to ws->cand; scan their in-edges
+      const uint32_t count = h.unresolved;
+      DBuf list;
+      list.alloc((size_t)count * 4, s);
+      GFB_CUDA(cudaMemcpyAsync(list.p, ws->cand.p, (size_t)count * 4, cudaMemcpyDeviceToDevice, s));
+      for (uint32_t round = 1; left > 0; ++round) {
+        GFB_CUDA(cudaMemsetAsync(&ws->ctl.as<Ctl>()->flag, 0, 4, s));
+        uint32_t grid = std::min<uint32_t>((count + 7) / 8, c->num_sms * 8);
+        k_pred_csc_round<W><<<grid, 256, 0, s>>>(
+            g->co.as<uint32_t>(), g->cadj.as<EdgeRec<W>>(), ws->dist.as<D>(),
+            ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(), list.as<uint32_t>(), count, round,
+            ws->ctl.as<Ctl>());
+        GFB_CUDA(cudaGetLastError());
+        ++kernels;
+        Ctl r = c->read_ctl(ws->ctl.as<Ctl>());
+        // round 1 (strict edges) may resolve nothing when every unresolved
+        // vertex sits in a zero-weight tie class; later rounds must progress.
+        if (r.flag == 0 && round > 1)
+          fail(GFB_ELOGIC, "sssp: predecessor repair made no progress");
+        left -= std::min<uint64_t>(left, r.flag);
+      }
+      return;
+    }
+    // no CSC: candidate rounds over every CSR row (O(m) per round)
+    GFB_CUDA(cudaMemsetAsync(ws->cand.p, 0xFF, (size_t)n * 4, s));
     for (uint32_t round = 1; left > 0; ++round) {
       GFB_CUDA(cudaMemsetAsync(&ws->ctl.as<Ctl>()->flag, 0, 4, s));
       k_pred_repair<W><<<stride_grid(c), 256, 0, s>>>(
@@ -180,8 +206,6 @@ struct Runner {
       GFB_CUDA(cudaGetLastError());
       kernels += 2;
       Ctl r = c->read_ctl(ws->ctl.as<Ctl>());
-      // round 1 (strict edges) may resolve nothing when every unresolved
-      // vertex sits in a zero-weight tie class; later rounds must progress.
       if (r.flag == 0 && round > 1)
         fail(GFB_ELOGIC, "sssp: predecessor repair made no progress");
       left -= std::min<uint64_t>(left, r.flag);
