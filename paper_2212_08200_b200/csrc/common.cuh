@@ -145,9 +145,9 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // Status word: flag(2) | count(31) | edges(31).  The device path therefore
 // requires n < 2^31 and m < 2^31 (RMAT scale 26 EF16 has m = 1.07e9).
 // ---------------------------------------------------------------------------
-constexpr unsigned long long LB_FLAG_AGG = 1ull << 62;
-constexpr unsigned long long LB_FLAG_INC = 2ull << 62;
-constexpr unsigned long long LB_MASK31 = (1ull << 31) - 1;
+__device__ constexpr unsigned long long LB_FLAG_AGG = 1ull << 62;
+__device__ constexpr unsigned long long LB_FLAG_INC = 2ull << 62;
+__device__ constexpr unsigned long long LB_MASK31 = (1ull << 31) - 1;
 
 __device__ __forceinline__ unsigned long long lb_pack(unsigned long long flag, uint32_t c,
                                                       uint32_t e) {
@@ -179,6 +179,53 @@ __device__ inline void lb_lookback(unsigned long long* status, uint32_t tile, ui
   }
   __threadfence();
   st[tile] = lb_pack(LB_FLAG_INC, c + agg_c, e + agg_e);
+  *pre_c = c;
+  *pre_e = e;
+}
+
+// Warp-parallel variant (called by all 32 lanes of one warp; agg_* must be
+// valid in every lane): inspects 32 predecessors per step, so a chain of
+// aggregate-only predecessors costs one L2 round trip per 32 tiles.
+__device__ inline void lb_lookback_warp(unsigned long long* status, uint32_t tile, uint32_t agg_c,
+                                        uint32_t agg_e, uint32_t* pre_c, uint32_t* pre_e) {
+  volatile unsigned long long* st = status;
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st[0] = lb_pack(LB_FLAG_INC, agg_c, agg_e);
+    *pre_c = 0;
+    *pre_e = 0;
+    return;
+  }
+  if (lane == 0) {
+    st[tile] = lb_pack(LB_FLAG_AGG, agg_c, agg_e);
+    __threadfence();
+  }
+  __syncwarp();
+  uint32_t c = 0, e = 0;
+  int64_t base = (int64_t)tile - 1;
+  for (;;) {
+    int64_t j = base - lane;
+    unsigned long long sv = j >= 0 ? st[j] : LB_FLAG_INC;
+    unsigned long long flag = sv & (3ull << 62);
+    if (__any_sync(0xffffffffu, flag == 0)) continue;  // someone not published: re-read
+    unsigned inc = __ballot_sync(0xffffffffu, flag == LB_FLAG_INC);
+    int last = inc ? __ffs(inc) - 1 : 31;  // lanes 0..last contribute
+    uint32_t vc = lane <= last ? (uint32_t)((sv >> 31) & LB_MASK31) : 0u;
+    uint32_t ve = lane <= last ? (uint32_t)(sv & LB_MASK31) : 0u;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      vc += __shfl_xor_sync(0xffffffffu, vc, d);
+      ve += __shfl_xor_sync(0xffffffffu, ve, d);
+    }
+    c += vc;
+    e += ve;
+    if (inc) break;
+    base -= 32;
+  }
+  if (lane == 0) {
+    __threadfence();
+    st[tile] = lb_pack(LB_FLAG_INC, c + agg_c, e + agg_e);
+  }
   *pre_c = c;
   *pre_e = e;
 }

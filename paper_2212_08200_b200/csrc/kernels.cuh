@@ -154,23 +154,25 @@ k_compact(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
   }
   __syncthreads();
 
-  // ---- phase 2: CTA totals, look-back for the global prefix ----
-  if (threadIdx.x == 0) {
-    uint32_t c = 0, e = 0;
-    for (int w = 0; w < C_WARPS; ++w) {
-      uint32_t tc = s_wc[w], te = s_we[w];
-      s_wc[w] = c;
-      s_we[w] = e;
-      c += tc;
-      e += te;
+  // ---- phase 2: CTA totals, warp-parallel look-back for the global prefix ----
+  if (warp == 0) {
+    uint32_t tc = lane < C_WARPS ? s_wc[lane] : 0u, te = lane < C_WARPS ? s_we[lane] : 0u;
+    uint32_t ic = warp_incl_scan(tc, lane), ie = warp_incl_scan(te, lane);
+    uint32_t c = __shfl_sync(0xffffffffu, ic, 31), e = __shfl_sync(0xffffffffu, ie, 31);
+    __syncwarp();
+    if (lane < C_WARPS) {
+      s_wc[lane] = ic - tc;
+      s_we[lane] = ie - te;
     }
     uint32_t pc, pe;
-    lb_lookback(status, tile, c, e, &pc, &pe);
-    s_pc = pc;
-    s_pe = pe;
-    if (tile == ntiles - 1) {
-      __threadfence();
-      plan_finish(plan, ctl, pc + c, pe + e);
+    lb_lookback_warp(status, tile, c, e, &pc, &pe);
+    if (lane == 0) {
+      s_pc = pc;
+      s_pe = pe;
+      if (tile == ntiles - 1) {
+        __threadfence();
+        plan_finish(plan, ctl, pc + c, pe + e);
+      }
     }
   }
   __syncthreads();
@@ -239,22 +241,25 @@ k_plan_list(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ list, 
     s_we[warp] = edg;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t c = 0, e = 0;
-    for (int w = 0; w < C_WARPS; ++w) {
-      uint32_t tc = s_wc[w], te = s_we[w];
-      s_wc[w] = c;
-      s_we[w] = e;
-      c += tc;
-      e += te;
+  // ---- phase 2: CTA totals, warp-parallel look-back for the global prefix ----
+  if (warp == 0) {
+    uint32_t tc = lane < C_WARPS ? s_wc[lane] : 0u, te = lane < C_WARPS ? s_we[lane] : 0u;
+    uint32_t ic = warp_incl_scan(tc, lane), ie = warp_incl_scan(te, lane);
+    uint32_t c = __shfl_sync(0xffffffffu, ic, 31), e = __shfl_sync(0xffffffffu, ie, 31);
+    __syncwarp();
+    if (lane < C_WARPS) {
+      s_wc[lane] = ic - tc;
+      s_we[lane] = ie - te;
     }
     uint32_t pc, pe;
-    lb_lookback(status, tile, c, e, &pc, &pe);
-    s_pc = pc;
-    s_pe = pe;
-    if (tile == ntiles - 1) {
-      __threadfence();
-      plan_finish(plan, ctl, pc + c, pe + e);
+    lb_lookback_warp(status, tile, c, e, &pc, &pe);
+    if (lane == 0) {
+      s_pc = pc;
+      s_pe = pe;
+      if (tile == ntiles - 1) {
+        __threadfence();
+        plan_finish(plan, ctl, pc + c, pe + e);
+      }
     }
   }
   __syncthreads();

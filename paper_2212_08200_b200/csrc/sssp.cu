@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstring>
 
+#include "hot.cuh"
 #include "impl.hpp"
 
 namespace gfb {
@@ -82,14 +83,15 @@ struct Runner {
   }
 
   void advance(bool pull, uint32_t total) {
+    const uint32_t cap = c->num_sms * 4;  // 4 resident CTAs per SM (launch bounds)
     if (pull) {
-      uint32_t ntiles = (g->pull_total + A_TILE - 1) / A_TILE;
-      uint32_t grid = std::min<uint32_t>(std::max<uint32_t>(ntiles, 1), c->num_sms * 8);
-      k_advance_pull<W><<<grid, A_BLOCK, 0, s>>>(args(true), g->pull_total, g->pull_k);
+      uint32_t ntiles = (g->pull_total + HotCfg<W>::TILE - 1) / HotCfg<W>::TILE;
+      uint32_t grid = std::min<uint32_t>(std::max<uint32_t>(ntiles, 1), cap);
+      k_pull_relax<W><<<grid, H_BLOCK, 0, s>>>(args(true), g->pull_total, g->pull_k);
     } else {
-      uint32_t ntiles = (total + A_TILE - 1) / A_TILE;
-      uint32_t grid = std::min<uint32_t>(std::max<uint32_t>(ntiles, 1), c->num_sms * 8);
-      k_advance_push<W, OUT_BITMAP><<<grid, A_BLOCK, 0, s>>>(args(false));
+      uint32_t ntiles = (total + HotCfg<W>::TILE - 1) / HotCfg<W>::TILE;
+      uint32_t grid = std::min<uint32_t>(std::max<uint32_t>(ntiles, 1), cap);
+      k_push_relax<W><<<grid, H_BLOCK, 0, s>>>(args(false));
     }
   }
 
