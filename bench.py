@@ -347,7 +347,7 @@ def main():
     ap.add_argument("--edgefactor", type=int, default=16)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--direction", default="auto", choices=["auto", "push", "pull"])
-    ap.add_argument("--alpha", type=float, default=4.0)
+    ap.add_argument("--alpha", type=float, default=1.5)
     ap.add_argument("--ref-scale", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--soak", type=float, default=1.5, help="min warm-up seconds (clock samples)")

@@ -1,0 +1,383 @@
+// graflow_b200/device.hpp -- the device execution policy for graflow.
+//
+// Header-only C++20 shim that plugs the B200 SSSP path (libgfb.so, C ABI in
+// include/gfb.h) in behind the reference's own operator API, through the
+// paper's execution-policy overloading: the reference's
+// types stay exactly as they are --
+//   graflow::Graph            graph.hpp:63-145
+//   graflow::FrontierRepr     frontier.hpp:18
+//   graflow::Direction        algorithms.hpp:467
+//   graflow::SsspResult       algorithms.hpp:491-496
+//   graflow::vertex_t/edge_t/weight_t, no_predecessor, unreachable (types.hpp)
+// -- and a DevicePolicy overload set is added next to them:
+//   sssp(const Graph&, vertex_t, const DeviceSsspConfig&) -> SsspResult
+//       (algorithms.hpp:569-623; same result layout, same throw sites)
+//   neighbors_expand(const DevicePolicy&, const Graph&, const DeviceFrontier&, Cond)
+//       (operators.hpp:255-288)
+//   neighbors_expand_pull(const DevicePolicy&, const Graph&, const DeviceFrontier&, Cond)
+//       (operators.hpp:296-334)
+//   uniquify(const DeviceFrontier&)            (operators.hpp:411-420)
+// Host lambdas cannot run on the device, so `Cond` must be one of the
+// recognised conditions in graflow::device_ops (relax_min, record, always);
+// anything else is a compile-time error (cf. the reference's own rejection
+// of unsupported frontier/policy combinations, operators.hpp:258-263).
+//
+// Include the reference's <graflow/algorithms.hpp> first (or let this
+// header include it) and link libgfb.so.  See INTEGRATION.md.
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <type_traits>
+#include <vector>
+
+#include "graflow/algorithms.hpp"
+#include "gfb.h"
+
+namespace graflow {
+
+namespace device_detail {
+
+// gfb_status -> the exception type the reference throws at the same site.
+inline void check(int rc) {
+  if (rc == GFB_OK) return;
+  std::string msg = gfb_last_error();
+  switch (rc) {
+    case GFB_EINVAL: throw std::invalid_argument(msg);
+    case GFB_ERANGE: throw std::out_of_range(msg);
+    case GFB_ELOGIC: throw std::logic_error(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+struct CtxDeleter {
+  void operator()(gfb_ctx* c) const { gfb_ctx_destroy(c); }
+};
+struct GraphDeleter {
+  void operator()(gfb_graph* g) const { gfb_graph_free(g); }
+};
+
+// One context (CUDA stream) per (host thread, device): gfb_ctx is
+// single-threaded by contract (include/gfb.h).
+inline gfb_ctx* context(int device) {
+  thread_local std::map<int, std::unique_ptr<gfb_ctx, CtxDeleter>> ctxs;
+  auto& c = ctxs[device];
+  if (!c) {
+    gfb_ctx* h = nullptr;
+    check(gfb_ctx_create(device, &h));
+    c.reset(h);
+  }
+  return c.get();
+}
+
+}  // namespace device_detail
+
+/// Device execution policy (the new ExecutionPolicy value of the paper's
+/// overloading mechanism).  `arithmetic` selects the device distance type:
+/// GFB_W_F64 reproduces the reference's double arithmetic bit for bit,
+/// GFB_W_U32 is exact for integer weights, GFB_W_F32 is the bandwidth mode.
+struct DevicePolicy {
+  int device = 0;
+  gfb_wtype arithmetic = GFB_W_F64;
+  bool auto_direction = true;  // push<->pull switch on the device
+  float pull_alpha = 1.5f;     // pull when frontier edges > m / pull_alpha
+
+  void validate() const {
+    if (device < 0) throw std::invalid_argument("device policy: device must be >= 0");
+    if (arithmetic < GFB_W_U32 || arithmetic > GFB_W_F64)
+      throw std::invalid_argument("device policy: bad arithmetic");
+  }
+};
+
+inline DevicePolicy device_policy(int device = 0, gfb_wtype arithmetic = GFB_W_F64) {
+  DevicePolicy p;
+  p.device = device;
+  p.arithmetic = arithmetic;
+  return p;
+}
+
+/// SsspConfig (algorithms.hpp:473-489) with a device policy.
+struct DeviceSsspConfig {
+  DevicePolicy policy{};
+  Direction direction = Direction::push;
+  FrontierRepr frontier_repr = FrontierRepr::sparse;
+  bool uniquify_frontier = false;  // the device frontier is always a set
+
+  void validate() const {
+    policy.validate();
+    // queue <=> par-nosync (algorithms.hpp:479-488): the async model has no
+    // device counterpart, so the queue representation is rejected outright.
+    if (frontier_repr == FrontierRepr::queue)
+      throw std::invalid_argument("config: queue frontier requires the par-nosync policy");
+  }
+};
+
+/// Uploaded copy of an immutable graflow::Graph (graph.hpp:42-44 promises
+/// immutability, so one upload serves every call on that graph).
+class DeviceGraph {
+ public:
+  DeviceGraph(const Graph& g, const DevicePolicy& p, bool with_transpose) {
+    gfb_ctx* c = device_detail::context(p.device);
+    const auto& ro = g.row_offsets();
+    const auto& col = g.column_indices();
+    const auto& val = g.values();
+    gfb_graph* h = nullptr;
+    device_detail::check(gfb_graph_upload(c, g.num_vertices(), g.num_edges(), ro.data(),
+                                          col.data(), val.data(), GFB_W_F64, p.arithmetic,
+                                          with_transpose ? 1 : 0, &h));
+    h_.reset(h);
+    ctx_ = c;
+  }
+  gfb_graph* handle() const { return h_.get(); }
+  gfb_ctx* ctx() const { return ctx_; }
+
+  /// Cached upload keyed by the graph object, its buffers, shape, a sampled
+  /// content fingerprint, the arithmetic and the transpose flag.  A Graph is
+  /// immutable (graph.hpp:42-44); the fingerprint guards against a new Graph
+  /// reusing a destroyed one's address.
+  static DeviceGraph& of(const Graph& g, const DevicePolicy& p, bool with_transpose) {
+    using Key = std::tuple<const Graph*, const void*, const void*, std::size_t, std::size_t,
+                           std::uint64_t, int, int, bool>;
+    thread_local std::map<Key, std::unique_ptr<DeviceGraph>> cache;
+    Key k{&g, g.row_offsets().data(), g.column_indices().data(), g.num_vertices(),
+          g.num_edges(), fingerprint(g), p.device, p.arithmetic, with_transpose};
+    auto& slot = cache[k];
+    if (!slot) slot = std::make_unique<DeviceGraph>(g, p, with_transpose);
+    return *slot;
+  }
+
+  static std::uint64_t fingerprint(const Graph& g) {
+    std::uint64_t h = 1469598103934665603ull;
+    auto mix = [&h](std::uint64_t x) {
+      h ^= x;
+      h *= 1099511628211ull;
+    };
+    const auto& ro = g.row_offsets();
+    const auto& col = g.column_indices();
+    const auto& val = g.values();
+    std::size_t m = col.size(), step = m / 1024 + 1;
+    for (std::size_t i = 0; i < ro.size(); i += ro.size() / 1024 + 1) mix(ro[i]);
+    for (std::size_t i = 0; i < m; i += step) {
+      std::uint64_t b;
+      std::memcpy(&b, &val[i], 8);
+      mix(col[i]);
+      mix(b);
+    }
+    return h;
+  }
+
+ private:
+  std::unique_ptr<gfb_graph, device_detail::GraphDeleter> h_;
+  gfb_ctx* ctx_ = nullptr;
+};
+
+/// Single-source shortest paths on the device (algorithms.hpp:569-623):
+/// same validation order and exception types, same SsspResult layout.
+/// dist is widened from the device arithmetic to double (exact); pred is
+/// the acyclic tight-edge tree (NIL for the source and unreachable).
+inline SsspResult sssp(const Graph& g, vertex_t source, const DeviceSsspConfig& cfg) {
+  cfg.validate();
+  std::size_t n = g.num_vertices();
+  if (source >= n) throw std::out_of_range("sssp: source out of range");
+  if (cfg.direction == Direction::pull && !g.has_transpose())
+    throw std::invalid_argument("sssp: pull direction requires a built transpose");
+  bool want_csc = g.has_transpose();
+  DeviceGraph& dg = DeviceGraph::of(g, cfg.policy, want_csc);
+  gfb_sssp_opts o;
+  gfb_sssp_opts_default(&o);
+  o.direction = cfg.direction == Direction::pull
+                    ? GFB_DIR_PULL
+                    : (cfg.policy.auto_direction && want_csc ? GFB_DIR_AUTO : GFB_DIR_PUSH);
+  o.pull_alpha = cfg.policy.pull_alpha;
+  SsspResult r;
+  r.dist.resize(n);
+  r.pred.resize(n);
+  gfb_sssp_stats st{};
+  device_detail::check(gfb_sssp(dg.ctx(), dg.handle(), source, &o, r.dist.data(), r.pred.data(), &st));
+  r.supersteps = st.supersteps;
+  r.relaxations = st.relaxations;
+  return r;
+}
+
+// ---------------------------------------------------------------- operators
+
+/// Device frontier (frontier.hpp:37-218, sparse and dense representations).
+class DeviceFrontier {
+ public:
+  DeviceFrontier(FrontierRepr repr, std::size_t num_vertices, int device = 0)
+      : repr_(repr), n_(num_vertices) {
+    if (repr == FrontierRepr::queue)
+      throw std::invalid_argument("device frontier: queue representation is the async model");
+    gfb_frontier* h = nullptr;
+    device_detail::check(gfb_frontier_create(device_detail::context(device), num_vertices,
+                                             repr == FrontierRepr::dense ? GFB_DENSE : GFB_SPARSE, &h));
+    h_.reset(h);
+  }
+  FrontierRepr repr() const { return repr_; }
+  std::size_t num_vertices() const { return n_; }
+  /// add_vertex for a batch (frontier.hpp:73-96 semantics).
+  void assign(const std::vector<vertex_t>& vs) {
+    device_detail::check(gfb_frontier_assign(h_.get(), vs.data(), vs.size()));
+  }
+  std::size_t size() const {
+    uint64_t s = 0;
+    device_detail::check(gfb_frontier_size(h_.get(), &s));
+    return s;
+  }
+  bool empty() const { return size() == 0; }
+  /// Sparse: element order; dense: ascending (get_active_vertex order).
+  std::vector<vertex_t> contents() const {
+    std::vector<vertex_t> out(size());
+    uint64_t k = 0;
+    device_detail::check(gfb_frontier_read(h_.get(), out.data(), out.size(), &k));
+    out.resize(k);
+    return out;
+  }
+  gfb_frontier* handle() const { return h_.get(); }
+
+ private:
+  struct Del {
+    void operator()(gfb_frontier* f) const { gfb_frontier_free(f); }
+  };
+  FrontierRepr repr_;
+  std::size_t n_;
+  std::unique_ptr<gfb_frontier, Del> h_;
+};
+
+/// Device distance map for the relax_min condition.
+class DeviceDistances {
+ public:
+  DeviceDistances(const Graph& g, const DevicePolicy& p, vertex_t source, bool with_transpose)
+      : dg_(&DeviceGraph::of(g, p, with_transpose)) {
+    gfb_dist* h = nullptr;
+    device_detail::check(gfb_dist_create(dg_->ctx(), dg_->handle(), &h));
+    h_.reset(h);
+    device_detail::check(gfb_dist_init(h, source));
+  }
+  DistanceMap read(std::size_t* relaxations = nullptr) const {
+    DistanceMap d(n());
+    uint64_t r = 0;
+    device_detail::check(gfb_dist_read(h_.get(), d.data(), &r));
+    if (relaxations) *relaxations = r;
+    return d;
+  }
+  gfb_dist* handle() const { return h_.get(); }
+
+ private:
+  std::size_t n() const {
+    uint64_t n = 0;
+    gfb_graph_info(dg_->handle(), &n, nullptr, nullptr, nullptr);
+    return n;
+  }
+  struct Del {
+    void operator()(gfb_dist* d) const { gfb_dist_free(d); }
+  };
+  DeviceGraph* dg_;
+  std::unique_ptr<gfb_dist, Del> h_;
+};
+
+/// Records every (src, dst, edge) invocation (test_operators.cpp:151-171).
+class DeviceRecorder {
+ public:
+  explicit DeviceRecorder(std::size_t capacity, int device = 0) {
+    gfb_record* h = nullptr;
+    device_detail::check(gfb_record_create(device_detail::context(device), capacity, &h));
+    h_.reset(h);
+  }
+  std::vector<std::tuple<vertex_t, vertex_t, edge_t>> triples() const {
+    uint64_t cnt = 0;
+    device_detail::check(gfb_record_read(h_.get(), nullptr, nullptr, nullptr, 0, &cnt));
+    std::vector<uint32_t> s(cnt), d(cnt), e(cnt);
+    device_detail::check(gfb_record_read(h_.get(), s.data(), d.data(), e.data(), cnt, &cnt));
+    std::vector<std::tuple<vertex_t, vertex_t, edge_t>> out;
+    for (std::size_t i = 0; i < s.size(); ++i) out.emplace_back(s[i], d[i], e[i]);
+    return out;
+  }
+  gfb_record* handle() const { return h_.get(); }
+
+ private:
+  struct Del {
+    void operator()(gfb_record* r) const { gfb_record_free(r); }
+  };
+  std::unique_ptr<gfb_record, Del> h_;
+};
+
+/// The conditions the device policy recognises (the C ABI's gfb_op).
+namespace device_ops {
+struct relax_min {  // algorithms.hpp:586-593
+  DeviceDistances& dist;
+};
+struct record {  // test-only eligibility recorder
+  DeviceRecorder& rec;
+};
+struct always {};  // test_operators.cpp:27
+}  // namespace device_ops
+
+namespace device_detail {
+template <class C> struct op_of {
+  static_assert(sizeof(C) == 0,
+                "device policy: host lambdas cannot run on the device; use "
+                "graflow::device_ops::{relax_min, record, always}");
+};
+template <> struct op_of<device_ops::relax_min> {
+  static int op() { return GFB_OP_RELAX_MIN; }
+  static void* state(const device_ops::relax_min& c) { return c.dist.handle(); }
+};
+template <> struct op_of<device_ops::record> {
+  static int op() { return GFB_OP_RECORD; }
+  static void* state(const device_ops::record& c) { return c.rec.handle(); }
+};
+template <> struct op_of<device_ops::always> {
+  static int op() { return GFB_OP_ALWAYS; }
+  static void* state(const device_ops::always&) { return nullptr; }
+};
+}  // namespace device_detail
+
+/// Push advance on the device (operators.hpp:255-288).
+template <class Cond>
+DeviceFrontier neighbors_expand(const DevicePolicy& policy, const Graph& g,
+                                const DeviceFrontier& f, Cond&& cond) {
+  using C = std::remove_cvref_t<Cond>;
+  policy.validate();
+  DeviceGraph& dg = DeviceGraph::of(g, policy, g.has_transpose());
+  DeviceFrontier out(f.repr(), g.num_vertices(), policy.device);
+  device_detail::check(gfb_advance_push(dg.ctx(), dg.handle(), f.handle(), out.handle(),
+                                        device_detail::op_of<C>::op(),
+                                        device_detail::op_of<C>::state(cond)));
+  return out;
+}
+
+/// Pull advance on the device (operators.hpp:296-334).
+template <class Cond>
+DeviceFrontier neighbors_expand_pull(const DevicePolicy& policy, const Graph& g,
+                                     const DeviceFrontier& f, Cond&& cond) {
+  using C = std::remove_cvref_t<Cond>;
+  policy.validate();
+  if (!g.has_transpose())  // operators.hpp:299-300
+    throw std::invalid_argument("neighbors_expand_pull: transpose not built");
+  if (f.repr() != FrontierRepr::dense)  // operators.hpp:301-302
+    throw std::invalid_argument("neighbors_expand_pull: dense frontier required");
+  DeviceGraph& dg = DeviceGraph::of(g, policy, true);
+  DeviceFrontier out(FrontierRepr::dense, g.num_vertices(), policy.device);
+  device_detail::check(gfb_advance_pull(dg.ctx(), dg.handle(), f.handle(), out.handle(),
+                                        device_detail::op_of<C>::op(),
+                                        device_detail::op_of<C>::state(cond)));
+  return out;
+}
+
+/// uniquify (operators.hpp:411-420): bitmap dedup + warp-ballot compaction.
+inline DeviceFrontier uniquify(const DeviceFrontier& f, int device = 0) {
+  if (f.repr() != FrontierRepr::sparse)
+    throw std::invalid_argument("uniquify: sparse frontier required");
+  DeviceFrontier out(FrontierRepr::sparse, f.num_vertices(), device);
+  device_detail::check(gfb_filter_unique(device_detail::context(device), f.handle(), out.handle()));
+  return out;
+}
+
+}  // namespace graflow

@@ -105,7 +105,7 @@ struct Runner {
     compact();
     GFB_CUDA(cudaGetLastError());
     const int dir = o->direction;
-    const double alpha = o->pull_alpha > 0 ? o->pull_alpha : 4.0;
+    const double alpha = o->pull_alpha > 0 ? o->pull_alpha : 1.5;
     uint64_t supersteps = 0, push_steps = 0, pull_steps = 0, launches = 0;
     kernels = 2;  // k_init + first k_compact
     float adv_ms = 0;
@@ -159,7 +159,7 @@ struct Runner {
   void pred_pass(uint32_t source, bool want, uint64_t* fallback) {
     GFB_CUDA(cudaMemsetAsync(ws->repair_bm.p, 0, (size_t)nwords * 4, s));
     GFB_CUDA(cudaMemsetAsync(&ws->ctl.as<Ctl>()->flag, 0, 4, s));
-    k_pred_verify<W><<<stride_grid(c), 256, 0, s>>>(
+    k_pred_verify<W><<<std::max<uint32_t>((n + 255) / 256, 1), 256, 0, s>>>(
         g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(), ws->dist.as<D>(), ws->predrec.as<uint2>(),
         ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(), ws->repair_bm.as<uint32_t>(),
         ws->cand.as<uint32_t>(), n, source, ws->ctl.as<Ctl>());
