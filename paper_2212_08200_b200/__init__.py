@@ -207,7 +207,8 @@ def grid(side, seed=1, transpose=True, ctx=None):
     return Graph(h, ctx)
 
 
-def _opts(direction="auto", pull_alpha=1.5, delta=0.0, device_loop=True, compute_pred=True):
+def _opts(direction="auto", pull_alpha=1.5, delta=0.0, device_loop=True, compute_pred=True,
+          variant=0):
     o = SsspOpts()
     _lib.load().gfb_sssp_opts_default(C.byref(o))
     if direction not in _DIR:
@@ -217,6 +218,7 @@ def _opts(direction="auto", pull_alpha=1.5, delta=0.0, device_loop=True, compute
     o.delta = delta
     o.device_loop = int(device_loop)
     o.compute_pred = int(compute_pred)
+    o.reserved[0] = int(variant)  # experimental kernel shape (sssp.cu Runner::variant)
     return o
 
 

@@ -74,10 +74,10 @@ __device__ __forceinline__ uint32_t hot_stage(const Plan& plan, const D* dist, u
   return cnt;
 }
 
-template <class W>
-__global__ void __launch_bounds__(H_BLOCK, 4) k_push_relax(AdvArgs<W> a) {
+template <class W, int H_VT = HotCfg<W>::VT, int MINB = 4>
+__global__ void __launch_bounds__(H_BLOCK, MINB) k_push_relax(AdvArgs<W> a) {
   using D = typename DT<W>::D;
-  constexpr int H_VT = HotCfg<W>::VT, H_TILE = HotCfg<W>::TILE;
+  constexpr int H_TILE = H_BLOCK * H_VT;
   __shared__ uint32_t s_off[H_TILE + 2];
   __shared__ uint32_t s_start[H_TILE + 2];
   __shared__ uint32_t s_u[H_TILE + 2];

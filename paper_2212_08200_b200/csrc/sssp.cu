@@ -82,21 +82,41 @@ struct Runner {
         plan(), ws->ctl.as<Ctl>(), ws->status.as<unsigned long long>(), ws->compact_tiles, 1);
   }
 
+  int variant = 0;  // experimental kernel shape (opts.reserved[0])
+
+  template <int VT, int MINB>
+  void push_launch(uint32_t total) {
+    constexpr int TILE = H_BLOCK * VT;
+    uint32_t ntiles = (total + TILE - 1) / TILE;
+    uint32_t grid = std::min<uint32_t>(std::max<uint32_t>(ntiles, 1), c->num_sms * MINB);
+    k_push_relax<W, VT, MINB><<<grid, H_BLOCK, 0, s>>>(args(false));
+  }
+
   void advance(bool pull, uint32_t total) {
     const uint32_t cap = c->num_sms * 4;  // 4 resident CTAs per SM (launch bounds)
     if (pull) {
       uint32_t ntiles = (g->pull_total + HotCfg<W>::TILE - 1) / HotCfg<W>::TILE;
       uint32_t grid = std::min<uint32_t>(std::max<uint32_t>(ntiles, 1), cap);
       k_pull_relax<W><<<grid, H_BLOCK, 0, s>>>(args(true), g->pull_total, g->pull_k);
-    } else {
-      uint32_t ntiles = (total + HotCfg<W>::TILE - 1) / HotCfg<W>::TILE;
-      uint32_t grid = std::min<uint32_t>(std::max<uint32_t>(ntiles, 1), cap);
-      k_push_relax<W><<<grid, H_BLOCK, 0, s>>>(args(false));
+      return;
+    }
+    switch (variant) {
+      case 1: push_launch<4, 8>(total); break;
+      case 2: push_launch<4, 6>(total); break;
+      case 3: push_launch<8, 6>(total); break;
+      case 4: {  // generic operator kernel (one edge in flight per thread)
+        uint32_t ntiles = (total + A_TILE - 1) / A_TILE;
+        uint32_t grid = std::min<uint32_t>(std::max<uint32_t>(ntiles, 1), c->num_sms * 8);
+        k_advance_push<W, OUT_BITMAP><<<grid, A_BLOCK, 0, s>>>(args(false));
+        break;
+      }
+      default: push_launch<HotCfg<W>::VT, 4>(total);
     }
   }
 
   void run(uint32_t source, const gfb_sssp_opts* o, gfb_sssp_stats* st) {
     ws->has_result = false;
+    variant = o->reserved[0];
     GFB_CUDA(cudaEventRecord(c->ev[0], s));
     k_init<W><<<stride_grid(c), 256, 0, s>>>(ws->dist.as<D>(), ws->predrec.as<uint2>(),
                                              ws->bm_next.as<uint32_t>(), ws->bm_cur.as<uint32_t>(),
