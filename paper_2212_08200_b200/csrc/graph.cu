@@ -365,7 +365,7 @@ void build_pull_plan(Graph* g) {
   const uint32_t ntiles = (uint32_t)((nwords + C_WORDS - 1) / C_WORDS);
   g->pull_v.alloc((n + 1) * 4, s);
   g->pull_off.alloc((n + 1) * 4, s);
-  g->pull_tseg.alloc((m / A_TILE + 3) * 4, s);
+  g->pull_tseg.alloc((m / PLAN_GRAIN + 3) * 4, s);
   DBuf bm, ctl, status;
   bm.alloc(nwords * 4, s);
   ctl.alloc(sizeof(Ctl), s);

@@ -24,8 +24,8 @@ constexpr int H_BLOCK = 256;
 template <class W> struct HotCfg {
   static constexpr int VT = sizeof(W) == 8 ? 4 : 8;
   static constexpr int TILE = H_BLOCK * VT;
-  static constexpr int RATIO = TILE / A_TILE;
-  static_assert(TILE % A_TILE == 0, "hot tile must be a multiple of the plan tile");
+  static constexpr int RATIO = TILE / PLAN_GRAIN;
+  static_assert(TILE % PLAN_GRAIN == 0, "hot tile must be a multiple of the plan grain");
 };
 
 // Stage the plan segments of hot tile t and build the edge->segment map.
@@ -35,7 +35,7 @@ __device__ __forceinline__ uint32_t hot_stage(const Plan& plan, const D* dist, u
                                               uint32_t ntiles, uint32_t total, uint32_t k,
                                               uint32_t* s_off, uint32_t* s_start, uint32_t* s_u,
                                               D* s_du, uint16_t* s_seg, bool load_du) {
-  constexpr int H_TILE = H_BLOCK * H_VT, H_RATIO = H_TILE / A_TILE;
+  constexpr int H_TILE = H_BLOCK * H_VT, H_RATIO = H_TILE / PLAN_GRAIN;
   const int tid = threadIdx.x;
   const uint32_t e0 = t * H_TILE;
   const uint32_t cnt = min((uint32_t)H_TILE, total - e0);
@@ -224,6 +224,125 @@ __global__ void __launch_bounds__(H_BLOCK, 4) k_pull_relax(AdvArgs<W> a, uint32_
   }
   n_elig = warp_sum(n_elig);
   if ((tid & 31) == 0 && n_elig) atomicAdd(&a.ctl->relax, (unsigned long long)n_elig);
+}
+
+// ---------------------------------------------------------------------------
+// Warp-tile push advance (the default hot kernel).
+//
+// Every warp independently claims warp tiles of WT = 32*VT plan edges
+// (persistent grid, no __syncthreads anywhere).  The plan segments (frontier
+// vertices) intersecting the tile are processed in chunks of <= 32: lane j
+// holds segment j's {first plan edge, row start, vertex, dist} in registers
+// and every lane finds the segment of each of its edges with a 5-step
+// shuffle search.  Edges are mapped lane-fastest, so each warp-wide record
+// load is a contiguous run of 32 x 8 bytes; each lane keeps VT record loads,
+// then VT distance gathers, then VT atomics in flight.
+// ---------------------------------------------------------------------------
+template <class D>
+__device__ __forceinline__ D shfl_d(D x, int src) {
+  return __shfl_sync(0xffffffffu, x, src);
+}
+
+template <class W, int VT, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_push_warp(AdvArgs<W> a) {
+  using D = typename DT<W>::D;
+  constexpr int WT = 32 * VT;
+  static_assert(WT % PLAN_GRAIN == 0 || PLAN_GRAIN % WT == 0, "warp tile vs plan grain");
+  const int lane = threadIdx.x & 31;
+  const uint32_t gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.status_len;
+       i += gridDim.x * blockDim.x)
+    a.status[i] = 0;
+  const uint32_t total = a.ctl->total;
+  const uint32_t k = a.ctl->k;
+  unsigned* err = &a.ctl->err;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.ctl->relax += total;
+    a.ctl->supersteps += 1;
+    a.ctl->push_steps += 1;
+  }
+  const uint32_t ntiles = (total + WT - 1) / WT;
+  for (uint32_t t = gwarp; t < ntiles; t += nwarps) {
+    const uint32_t e0 = t * WT;
+    const uint32_t e1 = min(e0 + WT, total);
+    // first segment: the one holding edge e0 (tile map at PLAN_GRAIN)
+    uint32_t sfirst;
+    if (WT >= PLAN_GRAIN) {
+      sfirst = a.plan.tseg[e0 / PLAN_GRAIN];
+    } else {
+      // finer tile than the map: search forward from the map entry
+      uint32_t sj = a.plan.tseg[e0 / PLAN_GRAIN];
+      for (;;) {  // warp-cooperative forward scan (segments are contiguous)
+        uint32_t cand = sj + lane;
+        uint32_t off = cand < k ? a.plan.off[cand + 1] : 0xFFFFFFFFu;  // end of cand
+        unsigned m = __ballot_sync(0xffffffffu, cand < k && off > e0);
+        if (m) {
+          sfirst = sj + __ffs(m) - 1;
+          break;
+        }
+        sj += 32;
+      }
+    }
+    for (uint32_t cs = sfirst;; cs += 32) {  // chunks of <= 32 segments
+      const uint32_t j = cs + lane;
+      uint32_t off = 0xFFFFFFFFu, start = 0, u = 0;
+      D du = D(0);
+      if (j < k) {
+        off = a.plan.off[j];
+        start = a.plan.start[j];
+        u = a.plan.v[j];
+      }
+      const uint32_t c0 = max(__shfl_sync(0xffffffffu, off, 0), e0);
+      if (c0 >= e1) break;  // chunk starts past the tile
+      if (j < k && off < e1) du = ld_dist(a.dist + u);
+      // chunk end: first edge of segment cs+32 (or the tile end)
+      uint32_t nxt = (cs + 32 < k) ? a.plan.off[cs + 32] : total;
+      const uint32_t c1 = min(nxt, e1);
+      for (uint32_t x = c0; x < c1; x += 32 * VT) {
+        uint32_t dst[VT], eid[VT], srcl[VT];
+        D nd[VT], cur[VT];
+#pragma unroll
+        for (int r = 0; r < VT; ++r) {  // A: segment search + record stream
+          const uint32_t le = x + r * 32 + lane;
+          dst[r] = NIL;
+          int lo = 0;
+#pragma unroll
+          for (int step = 16; step >= 1; step >>= 1) {
+            uint32_t o = __shfl_sync(0xffffffffu, off, lo + step);
+            if (o <= le) lo += step;
+          }
+          uint32_t so = __shfl_sync(0xffffffffu, off, lo);
+          uint32_t ss = __shfl_sync(0xffffffffu, start, lo);
+          D sd = shfl_d(du, lo);
+          srcl[r] = lo;
+          if (le < c1) {
+            eid[r] = ss + (le - so);
+            EdgeRec<W> rec = ld_rec(a.adj + eid[r]);
+            dst[r] = rec.v;
+            nd[r] = dadd(sd, rec.w, err);
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < VT; ++r)  // B: distance gathers (test before atomic)
+          if (dst[r] != NIL) cur[r] = ld_dist(a.dist + dst[r]);
+#pragma unroll
+        for (int r = 0; r < VT; ++r) {  // C: atomics on candidates
+          if (dst[r] != NIL && nd[r] < cur[r]) cur[r] = atomic_min_d(a.dist + dst[r], nd[r]);
+          else dst[r] = NIL;
+        }
+#pragma unroll
+        for (int r = 0; r < VT; ++r) {  // D: winners
+          uint32_t uu = __shfl_sync(0xffffffffu, u, srcl[r]);
+          if (dst[r] != NIL && nd[r] < cur[r]) {
+            a.predrec[dst[r]] = make_uint2(uu, eid[r]);
+            atomicOr(a.bm_out + (dst[r] >> 5), 1u << (dst[r] & 31));
+          }
+        }
+      }
+      if (c1 >= e1) break;
+    }
+  }
 }
 
 }  // namespace gfb

@@ -47,13 +47,15 @@ struct Plan {
   uint32_t* v;       // vertex id
   uint32_t* start;   // first edge of the row
   uint32_t* off;     // exclusive prefix of degrees (off[k] = total)
-  uint32_t* tseg;    // tseg[b] = segment holding edge b*A_TILE
+  uint32_t* tseg;    // tseg[b] = segment holding edge b*PLAN_GRAIN
   uint32_t tseg_cap; // entries allocated in tseg
 };
 
 constexpr int A_BLOCK = 256;
 constexpr int A_VT = 4;
 constexpr int A_TILE = A_BLOCK * A_VT;  // edges per advance tile
+constexpr int PLAN_GRAIN = 256;          // edge granularity of the plan's tile map
+constexpr int A_RATIO = A_TILE / PLAN_GRAIN;
 
 constexpr int C_WARPS = 8;
 constexpr int C_WPW = 8;                 // bitmap words per warp
@@ -78,9 +80,9 @@ __device__ __forceinline__ uint32_t warp_sum(uint32_t x) {
 // Write the tile map entries owned by segment `gi` = [eoff, eoff+deg).
 __device__ __forceinline__ void tile_map_entries(const Plan& p, uint32_t gi, uint32_t eoff,
                                                  uint32_t deg) {
-  uint32_t b = (eoff + A_TILE - 1) / A_TILE;
-  for (uint64_t x = (uint64_t)b * A_TILE; x < (uint64_t)eoff + deg && b < p.tseg_cap;
-       x += A_TILE, ++b)
+  uint32_t b = (eoff + PLAN_GRAIN - 1) / PLAN_GRAIN;
+  for (uint64_t x = (uint64_t)b * PLAN_GRAIN; x < (uint64_t)eoff + deg && b < p.tseg_cap;
+       x += PLAN_GRAIN, ++b)
     p.tseg[b] = gi;
 }
 
@@ -89,7 +91,7 @@ __device__ __forceinline__ void plan_finish(Plan p, Ctl* ctl, uint32_t K, uint32
   ctl->k = K;
   ctl->total = T;
   p.off[K] = T;
-  uint32_t sb = (T + A_TILE - 1) / A_TILE;  // sentinel past the last tile
+  uint32_t sb = (T + PLAN_GRAIN - 1) / PLAN_GRAIN;  // sentinel past the last tile
   if (sb < p.tseg_cap) p.tseg[sb] = K;
   ctl->tile_ctr = 0;
 }
@@ -396,8 +398,8 @@ k_advance_push(AdvArgs<W> a) {
     if (t >= ntiles) break;
     const uint32_t e0 = t * A_TILE;
     const uint32_t cnt = min((uint32_t)A_TILE, total - e0);
-    const uint32_t s0 = a.plan.tseg[t];
-    const uint32_t s1 = (t + 1 < ntiles) ? a.plan.tseg[t + 1] : k - 1;
+    const uint32_t s0 = a.plan.tseg[t * A_RATIO];
+    const uint32_t s1 = (t + 1 < ntiles) ? a.plan.tseg[(t + 1) * A_RATIO] : k - 1;
     const uint32_t nseg = s1 - s0 + 1;
     for (uint32_t j = tid; j < nseg; j += A_BLOCK) {
       uint32_t g = s0 + j;
@@ -551,8 +553,8 @@ k_advance_pull(AdvArgs<W> a, uint32_t total, uint32_t k) {
   for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const uint32_t e0 = t * A_TILE;
     const uint32_t cnt = min((uint32_t)A_TILE, total - e0);
-    const uint32_t s0 = a.plan.tseg[t];
-    const uint32_t s1 = (t + 1 < ntiles) ? a.plan.tseg[t + 1] : k - 1;
+    const uint32_t s0 = a.plan.tseg[t * A_RATIO];
+    const uint32_t s1 = (t + 1 < ntiles) ? a.plan.tseg[(t + 1) * A_RATIO] : k - 1;
     const uint32_t nseg = s1 - s0 + 1;
     for (uint32_t j = tid; j < nseg; j += A_BLOCK) {
       uint32_t g = s0 + j;

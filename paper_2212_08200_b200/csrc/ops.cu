@@ -159,7 +159,7 @@ static Ctl build_plan(Ctx* c, const Graph* g, Frontier* in, OpPlan& p) {
   p.off.alloc((len + 1) * 4, s);
   // tile map size bound: total edges <= len * max_deg; computed after the
   // plan in a second pass when larger than the first guess.
-  uint64_t guess = std::max<uint64_t>(g->m / A_TILE + 3, 16);
+  uint64_t guess = std::max<uint64_t>(g->m / PLAN_GRAIN + 3, 16);
   p.tseg.alloc(guess * 4, s);
   for (int attempt = 0; attempt < 2; ++attempt) {
     GFB_CUDA(cudaMemsetAsync(c->ctl.p, 0, sizeof(Ctl), s));
@@ -184,7 +184,7 @@ static Ctl build_plan(Ctx* c, const Graph* g, Frontier* in, OpPlan& p) {
     }
     GFB_CUDA(cudaGetLastError());
     Ctl h = c->read_ctl(c->ctl.as<Ctl>());
-    uint64_t need = (uint64_t)h.total / A_TILE + 3;
+    uint64_t need = (uint64_t)h.total / PLAN_GRAIN + 3;
     if (need <= guess) return h;
     guess = need;
     p.tseg.alloc(guess * 4, s);

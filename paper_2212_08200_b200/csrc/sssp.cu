@@ -30,7 +30,7 @@ Workspace* ensure_ws(Graph* g) {
   ws->pv.alloc((n + 1) * 4, s);
   ws->pstart.alloc((n + 1) * 4, s);
   ws->poff.alloc((n + 1) * 4, s);
-  ws->ptseg.alloc((m / A_TILE + 3) * 4, s);
+  ws->ptseg.alloc((m / PLAN_GRAIN + 3) * 4, s);
   ws->compact_tiles = (uint32_t)((nwords + C_WORDS - 1) / C_WORDS);
   if (ws->compact_tiles == 0) ws->compact_tiles = 1;
   ws->status_len = ws->compact_tiles + 1;
@@ -92,6 +92,15 @@ struct Runner {
     k_push_relax<W, VT, MINB><<<grid, H_BLOCK, 0, s>>>(args(false));
   }
 
+  template <int VT, int MINB>
+  void warp_launch(uint32_t total) {
+    constexpr int WT = 32 * VT;
+    uint32_t ntiles = (total + WT - 1) / WT;
+    uint32_t warps_cap = c->num_sms * MINB * 8;  // 8 warps per 256-thread CTA
+    uint32_t warps = std::min<uint32_t>(std::max<uint32_t>(ntiles, 1), warps_cap);
+    k_push_warp<W, VT, MINB><<<(warps + 7) / 8, 256, 0, s>>>(args(false));
+  }
+
   void advance(bool pull, uint32_t total) {
     const uint32_t cap = c->num_sms * 4;  // 4 resident CTAs per SM (launch bounds)
     if (pull) {
@@ -101,6 +110,9 @@ struct Runner {
       return;
     }
     switch (variant) {
+      case 5: push_launch<HotCfg<W>::VT, 4>(total); break;
+      case 6: warp_launch<4, 8>(total); break;
+      case 7: warp_launch<8, 6>(total); break;
       case 1: push_launch<4, 8>(total); break;
       case 2: push_launch<4, 6>(total); break;
       case 3: push_launch<8, 6>(total); break;
@@ -110,7 +122,7 @@ struct Runner {
         k_advance_push<W, OUT_BITMAP><<<grid, A_BLOCK, 0, s>>>(args(false));
         break;
       }
-      default: push_launch<HotCfg<W>::VT, 4>(total);
+      default: warp_launch<(sizeof(W) == 8 ? 4 : 8), 4>(total);
     }
   }
 
