@@ -3,6 +3,7 @@
 // plan, and the device-side synthetic generators (RMAT, grid).
 #include <cub/cub.cuh>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -397,11 +398,16 @@ void build_pull_plan(Graph* g) {
 // Device-side synthetic graphs in build_csr layout.
 // ---------------------------------------------------------------------------
 __global__ void k_rmat_gen(int scale, uint64_t seed, int wkind, uint64_t m,
-                           unsigned long long* key, uint32_t* wbits) {
+                           unsigned long long* key, uint32_t* wbits, int permute) {
   uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint32_t mask = (uint32_t)((1ull << scale) - 1);
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
     uint32_t s, d, w;
     rmat_edge(scale, seed, wkind, i, &s, &d, &w);
+    if (permute) {  // experiment only (GFB_RMAT_PERMUTE): bijective label scramble
+      s = (s * 2654435761u + 12345u) & mask;
+      d = (d * 2654435761u + 12345u) & mask;
+    }
     key[i] = ((unsigned long long)s << 32) | d;
     wbits[i] = w;
   }
@@ -436,8 +442,10 @@ Graph* graph_generate_rmat(Ctx* c, int scale, int ef, uint64_t seed, int wtype, 
     key2.alloc(m * 8, s);
     wb.alloc(m * 4, s);
     wb2.alloc(m * 4, s);
+    const char* perm = getenv("GFB_RMAT_PERMUTE");
     k_rmat_gen<<<stride_grid(c), 256, 0, s>>>(scale, seed, wtype == GFB_W_U32 ? 0 : 1, m,
-                                              key.as<unsigned long long>(), wb.as<uint32_t>());
+                                              key.as<unsigned long long>(), wb.as<uint32_t>(),
+                                              perm && perm[0] == '1');
     GFB_CUDA(cudaGetLastError());
     // (src, dst, w) order: stable sort by w, then stable sort by (src, dst).
     size_t tb1 = 0, tb2 = 0;

@@ -20,11 +20,12 @@ ap.add_argument("--alpha", type=float, default=4.0)
 ap.add_argument("--delta", type=float, default=0.0)
 ap.add_argument("--device-loop", type=int, default=1)
 ap.add_argument("--variant", type=int, default=0)
+ap.add_argument("--source", type=int, default=0)
 a = ap.parse_args()
 ctx = gb.Context(0)
 g = gb.grid(a.grid) if a.grid else gb.rmat(a.scale, 16, seed=1, wtype="f32", transpose=True, ctx=ctx)
 for r in range(a.runs):
-    _, _, st = gb.sssp_stats(g, 0, want_result=False, direction=a.direction, pull_alpha=a.alpha,
+    _, _, st = gb.sssp_stats(g, a.source, want_result=False, direction=a.direction, pull_alpha=a.alpha,
                              delta=a.delta, device_loop=bool(a.device_loop),
                              variant=a.variant)
     print(json.dumps({k: getattr(st, k) for k, _ in gb.SsspStats._fields_}), flush=True)
