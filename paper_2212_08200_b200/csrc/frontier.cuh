@@ -1,0 +1,194 @@
+// frontier.cuh -- next-frontier bitmap -> expansion plan for the SSSP loop
+// (the filter/uniquify step, operators.hpp:411-420 + frontier.hpp:147-165:
+// bitmap dedup, ascending order) as three launches with static tiles:
+//
+//   k_fcount  per 2048-vertex tile: warp-ballot count of set bits with
+//             out-degree > 0 and their degree sum -> agg[tile]
+//   k_fscan   one CTA: exclusive scan of agg -> tile prefixes; plan totals,
+//             relaxation/superstep bookkeeping and the loop condition
+//   k_fwrite  per tile: recount, place each kept vertex at its global
+//             position (ascending), edge offsets, tile-map entries; copy the
+//             word to the current-frontier bitmap and clear it
+//
+// No global atomics and no look-back chain: the single-pass k_compact
+// (kernels.cuh) serialised 8192 CTAs on one tile counter (~50-100 us per
+// superstep at scale 24, profiles/r01_launches.md).
+#pragma once
+
+#include "kernels.cuh"
+
+namespace gfb {
+
+constexpr int F_WARPS = 8;
+constexpr int F_WPW = 8;                     // bitmap words per warp
+constexpr int F_WORDS = F_WARPS * F_WPW;     // 64 words = 2048 vertices per tile
+constexpr int F_SCAN_THREADS = 1024;
+
+// The 8 words of this warp -> per-word (mask of kept bits, row start, degree).
+struct WarpWords {
+  uint32_t keep[F_WPW];
+  uint32_t st[F_WPW];
+  uint32_t deg[F_WPW];
+};
+
+__device__ __forceinline__ void load_warp_words(const uint32_t* __restrict__ ro,
+                                                const uint32_t* bm, uint32_t nwords,
+                                                uint32_t wbase, WarpWords& w, uint32_t* raw_word) {
+  const int lane = threadIdx.x & 31;
+  uint32_t my = 0;
+  if (lane < F_WPW && wbase + lane < nwords) my = bm[wbase + lane];
+  *raw_word = my;
+  uint32_t words[F_WPW];
+#pragma unroll
+  for (int j = 0; j < F_WPW; ++j) words[j] = __shfl_sync(0xffffffffu, my, j);
+  // issue every row-offset load before consuming any (F_WPW x 2 in flight)
+#pragma unroll
+  for (int j = 0; j < F_WPW; ++j) {
+    bool bit = (words[j] >> lane) & 1u;
+    uint32_t v = (wbase + j) * 32 + lane;
+    w.st[j] = bit ? ro[v] : 0u;
+    w.deg[j] = bit ? ro[v + 1] : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < F_WPW; ++j) {
+    bool bit = (words[j] >> lane) & 1u;
+    w.deg[j] = bit ? w.deg[j] - w.st[j] : 0u;
+    w.keep[j] = __ballot_sync(0xffffffffu, w.deg[j] > 0);
+  }
+}
+
+__global__ void __launch_bounds__(F_WARPS * 32)
+k_fcount(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uint32_t nwords,
+         uint2* agg) {
+  __shared__ uint32_t s_c[F_WARPS], s_e[F_WARPS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpWords w;
+  uint32_t raw;
+  load_warp_words(ro, bm, nwords, blockIdx.x * F_WORDS + warp * F_WPW, w, &raw);
+  uint32_t c = 0, e = 0;
+#pragma unroll
+  for (int j = 0; j < F_WPW; ++j) {
+    c += __popc(w.keep[j]);
+    e += w.deg[j];
+  }
+  e = warp_sum(e);
+  if (lane == 0) {
+    s_c[warp] = c;
+    s_e[warp] = e;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t tc = 0, te = 0;
+    for (int i = 0; i < F_WARPS; ++i) {
+      tc += s_c[i];
+      te += s_e[i];
+    }
+    agg[blockIdx.x] = make_uint2(tc, te);
+  }
+}
+
+// One CTA.  agg -> exclusive prefixes (in place), plan totals, bookkeeping.
+// ctl->mode: direction of the next superstep (1 = pull when the plan's edges
+// exceed m / alpha and a CSC exists -- the push<->pull switch).
+__global__ void __launch_bounds__(F_SCAN_THREADS)
+k_fscan(uint2* agg, uint32_t tiles, Plan plan, Ctl* ctl, uint32_t m, float alpha, int can_pull,
+        int force_pull, cudaGraphConditionalHandle loop_handle,
+        cudaGraphConditionalHandle mode_handle, int use_handle) {
+  __shared__ uint32_t s_c[F_SCAN_THREADS / 32], s_e[F_SCAN_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t per = (tiles + F_SCAN_THREADS - 1) / F_SCAN_THREADS;
+  const uint32_t lo = tid * per, hi = min(lo + per, tiles);
+  uint32_t c = 0, e = 0;
+  for (uint32_t i = lo; i < hi; ++i) {
+    uint2 a = agg[i];
+    c += a.x;
+    e += a.y;
+  }
+  uint32_t ic = warp_incl_scan(c, lane), ie = warp_incl_scan(e, lane);
+  if (lane == 31) {
+    s_c[warp] = ic;
+    s_e[warp] = ie;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t wc = s_c[lane], we = s_e[lane];
+    uint32_t xc = warp_incl_scan(wc, lane), xe = warp_incl_scan(we, lane);
+    s_c[lane] = xc - wc;
+    s_e[lane] = xe - we;
+  }
+  __syncthreads();
+  uint32_t pc = s_c[warp] + ic - c, pe = s_e[warp] + ie - e;
+  for (uint32_t i = lo; i < hi; ++i) {
+    uint2 a = agg[i];
+    agg[i] = make_uint2(pc, pe);
+    pc += a.x;
+    pe += a.y;
+  }
+  if (tid == F_SCAN_THREADS - 1) {
+    // pc/pe are now the grand totals
+    const uint32_t K = pc, T = pe;
+    ctl->k = K;
+    ctl->total = T;
+    plan.off[K] = T;
+    uint32_t sb = (T + PLAN_GRAIN - 1) / PLAN_GRAIN;
+    if (sb < plan.tseg_cap) plan.tseg[sb] = K;
+    const uint32_t mode = (force_pull || (can_pull && (float)T > (float)m / alpha)) ? 1u : 0u;
+    ctl->mode = mode;
+    if (use_handle) {  // device loop: WHILE(K > 0), IF(pull)
+      cudaGraphSetConditional(loop_handle, K > 0 ? 1u : 0u);
+      if (can_pull || force_pull) cudaGraphSetConditional(mode_handle, mode);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(F_WARPS * 32)
+k_fwrite(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur, uint32_t nwords,
+         const uint2* __restrict__ prefix, Plan plan) {
+  __shared__ uint32_t s_c[F_WARPS], s_e[F_WARPS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t wbase = blockIdx.x * F_WORDS + warp * F_WPW;
+  WarpWords w;
+  uint32_t raw;
+  load_warp_words(ro, bm_next, nwords, wbase, w, &raw);
+  if (lane < F_WPW && wbase + lane < nwords) {
+    if (bm_cur) bm_cur[wbase + lane] = raw;
+    bm_next[wbase + lane] = 0;
+  }
+  uint32_t c = 0, e = 0;
+#pragma unroll
+  for (int j = 0; j < F_WPW; ++j) {
+    c += __popc(w.keep[j]);
+    e += w.deg[j];
+  }
+  e = warp_sum(e);
+  if (lane == 0) {
+    s_c[warp] = c;
+    s_e[warp] = e;
+  }
+  __syncthreads();
+  const uint2 tp = prefix[blockIdx.x];
+  uint32_t gc = tp.x, ge = tp.y;
+  for (int i = 0; i < warp; ++i) {
+    gc += s_c[i];
+    ge += s_e[i];
+  }
+#pragma unroll
+  for (int j = 0; j < F_WPW; ++j) {
+    const uint32_t keep = w.keep[j];
+    if (keep == 0) continue;  // warp-uniform
+    const bool mine = (keep >> lane) & 1u;
+    const uint32_t incl = warp_incl_scan(w.deg[j], lane);
+    if (mine) {
+      const uint32_t gi = gc + __popc(keep & lanemask_lt());
+      const uint32_t eoff = ge + incl - w.deg[j];
+      plan.v[gi] = (wbase + j) * 32 + lane;
+      plan.start[gi] = w.st[j];
+      plan.off[gi] = eoff;
+      tile_map_entries(plan, gi, eoff, w.deg[j]);
+    }
+    gc += __popc(keep);
+    ge += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+}  // namespace gfb

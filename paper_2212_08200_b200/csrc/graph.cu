@@ -34,6 +34,8 @@ void DBuf::release() {
 
 Ctx::~Ctx() {
   if (ctl_host) cudaFreeHost(ctl_host);
+  for (auto& a : aux)
+    if (a) cudaStreamDestroy(a);
   for (auto& e : ev)
     if (e) cudaEventDestroy(e);
   if (stream) cudaStreamDestroy(stream);
@@ -56,6 +58,8 @@ Ctl Ctx::read_ctl(const Ctl* dctl) {
 
 Graph::~Graph() = default;
 Workspace::~Workspace() {
+  if (loop_exec) cudaGraphExecDestroy(loop_exec);
+  if (loop_graph) cudaGraphDestroy(loop_graph);
   if (ctl_host) cudaFreeHost(ctl_host);
 }
 

@@ -30,6 +30,7 @@ struct Ctx {
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {};
+  cudaStream_t aux[2] = {};  // graph-capture helpers (device loop)
   // operator-API scratch
   DBuf ctl, status, qstatus;
   size_t status_cap = 0;
@@ -88,6 +89,13 @@ struct Workspace {
   DBuf pv, pstart, poff, ptseg;
   DBuf status;
   DBuf ctl;
+  DBuf agg;        // per-tile (count, edges) of the frontier compaction
+  DBuf src_dev;    // the source vertex (read by k_init)
+  uint32_t ftiles = 0;
+  // device loop: one instantiated CUDA graph per (direction, alpha, variant)
+  cudaGraphExec_t loop_exec = nullptr;
+  cudaGraph_t loop_graph = nullptr;
+  int loop_key[3] = {-1, -1, -1};
   Ctl* ctl_host = nullptr;  // pinned
   uint32_t compact_tiles = 0;
   uint32_t status_len = 0;

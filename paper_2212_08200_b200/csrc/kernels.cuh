@@ -667,9 +667,10 @@ k_advance_pull(AdvArgs<W> a, uint32_t total, uint32_t k) {
 // ---------------------------------------------------------------------------
 template <class W>
 __global__ void k_init(typename DT<W>::D* dist, uint2* predrec, uint32_t* bm_next,
-                       uint32_t* bm_cur, uint32_t n, uint32_t nwords, uint32_t source,
+                       uint32_t* bm_cur, uint32_t n, uint32_t nwords, const uint32_t* src_ptr,
                        Ctl* ctl) {
   using D = typename DT<W>::D;
+  const uint32_t source = *src_ptr;  // device-resident: graph launches stay source-agnostic
   uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     dist[i] = i == source ? D(0) : dinf<W>();

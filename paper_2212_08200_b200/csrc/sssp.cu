@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstring>
 
+#include "frontier.cuh"
 #include "hot.cuh"
 #include "impl.hpp"
 
@@ -31,6 +32,9 @@ Workspace* ensure_ws(Graph* g) {
   ws->pstart.alloc((n + 1) * 4, s);
   ws->poff.alloc((n + 1) * 4, s);
   ws->ptseg.alloc((m / PLAN_GRAIN + 3) * 4, s);
+  ws->ftiles = (uint32_t)std::max<uint64_t>((nwords + F_WORDS - 1) / F_WORDS, 1);
+  ws->agg.alloc((size_t)ws->ftiles * 8, s);
+  ws->src_dev.alloc(16, s);
   ws->compact_tiles = (uint32_t)((nwords + C_WORDS - 1) / C_WORDS);
   if (ws->compact_tiles == 0) ws->compact_tiles = 1;
   ws->status_len = ws->compact_tiles + 1;
@@ -50,6 +54,7 @@ struct Runner {
   cudaStream_t s;
   uint32_t n, nwords;
   uint64_t kernels = 0;
+  int variant = 0;  // experimental kernel shape (opts.reserved[0])
 
   Plan plan() const {
     return Plan{ws->pv.as<uint32_t>(), ws->pstart.as<uint32_t>(), ws->poff.as<uint32_t>(),
@@ -70,99 +75,195 @@ struct Runner {
     a.ctl = ws->ctl.as<Ctl>();
     a.bm_out = ws->bm_next.as<uint32_t>();
     a.bm_in = ws->bm_cur.as<uint32_t>();
-    a.status = ws->status.as<unsigned long long>();
-    a.status_len = ws->status_len;
+    a.status = nullptr;
+    a.status_len = 0;
     a.op = GFB_OP_RELAX_MIN;
     return a;
   }
 
-  void compact() {
-    k_compact<<<ws->compact_tiles, C_WARPS * 32, 0, s>>>(
-        g->ro.as<uint32_t>(), ws->bm_next.as<uint32_t>(), ws->bm_cur.as<uint32_t>(), nwords, n,
-        plan(), ws->ctl.as<Ctl>(), ws->status.as<unsigned long long>(), ws->compact_tiles, 1);
+  // frontier compaction: count -> scan (+ loop/direction decision) -> write
+  void compact(int dir, float alpha, cudaGraphConditionalHandle hloop,
+               cudaGraphConditionalHandle hmode, bool use_handles) {
+    const uint32_t tiles = ws->ftiles;
+    k_fcount<<<tiles, F_WARPS * 32, 0, s>>>(g->ro.as<uint32_t>(), ws->bm_next.as<uint32_t>(),
+                                            nwords, ws->agg.as<uint2>());
+    k_fscan<<<1, F_SCAN_THREADS, 0, s>>>(ws->agg.as<uint2>(), tiles, plan(), ws->ctl.as<Ctl>(),
+                                         (uint32_t)g->m, alpha,
+                                         dir == GFB_DIR_AUTO && g->has_csc ? 1 : 0,
+                                         dir == GFB_DIR_PULL ? 1 : 0, hloop, hmode,
+                                         use_handles ? 1 : 0);
+    k_fwrite<<<tiles, F_WARPS * 32, 0, s>>>(g->ro.as<uint32_t>(), ws->bm_next.as<uint32_t>(),
+                                            ws->bm_cur.as<uint32_t>(), nwords,
+                                            ws->agg.as<uint2>(), plan());
+    GFB_CUDA(cudaGetLastError());
   }
 
-  int variant = 0;  // experimental kernel shape (opts.reserved[0])
-
   template <int VT, int MINB>
-  void push_launch(uint32_t total) {
+  void push_launch(cudaStream_t st, uint32_t total) {
     constexpr int TILE = H_BLOCK * VT;
     uint32_t ntiles = (total + TILE - 1) / TILE;
     uint32_t grid = std::min<uint32_t>(std::max<uint32_t>(ntiles, 1), c->num_sms * MINB);
-    k_push_relax<W, VT, MINB><<<grid, H_BLOCK, 0, s>>>(args(false));
+    k_push_relax<W, VT, MINB><<<grid, H_BLOCK, 0, st>>>(args(false));
   }
 
+  // Persistent-grid warp kernel: the grid depends only on the device, so the
+  // same launch serves every superstep inside the captured device loop.
   template <int VT, int MINB>
-  void warp_launch(uint32_t total) {
+  void warp_launch(cudaStream_t st, uint32_t total, bool full) {
     constexpr int WT = 32 * VT;
-    uint32_t ntiles = (total + WT - 1) / WT;
     uint32_t warps_cap = c->num_sms * MINB * 8;  // 8 warps per 256-thread CTA
-    uint32_t warps = std::min<uint32_t>(std::max<uint32_t>(ntiles, 1), warps_cap);
-    k_push_warp<W, VT, MINB><<<(warps + 7) / 8, 256, 0, s>>>(args(false));
+    uint32_t warps = full ? warps_cap
+                          : std::min<uint32_t>(std::max<uint32_t>((total + WT - 1) / WT, 1),
+                                               warps_cap);
+    k_push_warp<W, VT, MINB><<<(warps + 7) / 8, 256, 0, st>>>(args(false));
   }
 
-  void advance(bool pull, uint32_t total) {
-    const uint32_t cap = c->num_sms * 4;  // 4 resident CTAs per SM (launch bounds)
-    if (pull) {
-      uint32_t ntiles = (g->pull_total + HotCfg<W>::TILE - 1) / HotCfg<W>::TILE;
-      uint32_t grid = std::min<uint32_t>(std::max<uint32_t>(ntiles, 1), cap);
-      k_pull_relax<W><<<grid, H_BLOCK, 0, s>>>(args(true), g->pull_total, g->pull_k);
-      return;
-    }
+  void pull_launch(cudaStream_t st) {
+    uint32_t ntiles = (g->pull_total + HotCfg<W>::TILE - 1) / HotCfg<W>::TILE;
+    uint32_t grid = std::min<uint32_t>(std::max<uint32_t>(ntiles, 1), c->num_sms * 4);
+    k_pull_relax<W><<<grid, H_BLOCK, 0, st>>>(args(true), g->pull_total, g->pull_k);
+  }
+
+  // total == UINT32_MAX: unknown on the host (device loop) -> full grid
+  void push(cudaStream_t st, uint32_t total) {
+    const bool full = total == 0xFFFFFFFFu;
     switch (variant) {
-      case 5: push_launch<HotCfg<W>::VT, 4>(total); break;
-      case 6: warp_launch<4, 8>(total); break;
-      case 7: warp_launch<8, 6>(total); break;
-      case 1: push_launch<4, 8>(total); break;
-      case 2: push_launch<4, 6>(total); break;
-      case 3: push_launch<8, 6>(total); break;
+      case 1: push_launch<4, 8>(st, full ? 1u << 30 : total); break;
+      case 2: push_launch<4, 6>(st, full ? 1u << 30 : total); break;
       case 4: {  // generic operator kernel (one edge in flight per thread)
-        uint32_t ntiles = (total + A_TILE - 1) / A_TILE;
+        uint32_t ntiles = full ? 1u << 20 : (total + A_TILE - 1) / A_TILE;
         uint32_t grid = std::min<uint32_t>(std::max<uint32_t>(ntiles, 1), c->num_sms * 8);
-        k_advance_push<W, OUT_BITMAP><<<grid, A_BLOCK, 0, s>>>(args(false));
+        k_advance_push<W, OUT_BITMAP><<<grid, A_BLOCK, 0, st>>>(args(false));
         break;
       }
-      default: warp_launch<(sizeof(W) == 8 ? 4 : 8), 4>(total);
+      case 6: warp_launch<4, 8>(st, total, full); break;
+      default: warp_launch<(sizeof(W) == 8 ? 4 : 8), 4>(st, total, full);
     }
+  }
+
+  void init_launch() {
+    k_init<W><<<stride_grid(c), 256, 0, s>>>(ws->dist.as<D>(), ws->predrec.as<uint2>(),
+                                             ws->bm_next.as<uint32_t>(), ws->bm_cur.as<uint32_t>(),
+                                             n, nwords, ws->src_dev.as<uint32_t>(),
+                                             ws->ctl.as<Ctl>());
+  }
+
+  // ---- device loop: init; compact; WHILE(k > 0) { IF(pull) pull ELSE push;
+  //      compact }  captured once into a CUDA graph (conditional nodes).
+  void build_loop_graph(int dir, float alpha) {
+    if (ws->loop_exec) cudaGraphExecDestroy(ws->loop_exec);
+    if (ws->loop_graph) cudaGraphDestroy(ws->loop_graph);
+    ws->loop_exec = nullptr;
+    ws->loop_graph = nullptr;
+    for (auto& a : c->aux)
+      if (!a) GFB_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+    cudaGraph_t G;
+    GFB_CUDA(cudaGraphCreate(&G, 0));
+    cudaGraphConditionalHandle hloop, hmode;
+    GFB_CUDA(cudaGraphConditionalHandleCreate(&hloop, G, 1, cudaGraphCondAssignDefault));
+    GFB_CUDA(cudaGraphConditionalHandleCreate(&hmode, G, 0, cudaGraphCondAssignDefault));
+    const bool pullable = g->has_csc && dir != GFB_DIR_PUSH;
+
+    GFB_CUDA(cudaStreamBeginCaptureToGraph(s, G, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeRelaxed));
+    init_launch();
+    compact(dir, alpha, hloop, hmode, true);
+    cudaStreamCaptureStatus cst;
+    cudaGraph_t capG;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    GFB_CUDA(cudaStreamGetCaptureInfo(s, &cst, nullptr, &capG, &deps, &ndeps));
+    cudaGraphNodeParams wp{};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = hloop;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    GFB_CUDA(cudaGraphAddNode(&wnode, capG, deps, ndeps, &wp));
+    cudaGraph_t body = wp.conditional.phGraph_out[0];
+    GFB_CUDA(cudaStreamUpdateCaptureDependencies(s, &wnode, 1, cudaStreamSetCaptureDependencies));
+    cudaGraph_t tmp;
+    GFB_CUDA(cudaStreamEndCapture(s, &tmp));
+
+    // loop body
+    cudaStream_t b = c->aux[0];
+    GFB_CUDA(cudaStreamBeginCaptureToGraph(b, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeRelaxed));
+    if (pullable) {
+      GFB_CUDA(cudaStreamGetCaptureInfo(b, &cst, nullptr, &capG, &deps, &ndeps));
+      cudaGraphNodeParams ip{};
+      ip.type = cudaGraphNodeTypeConditional;
+      ip.conditional.handle = hmode;
+      ip.conditional.type = cudaGraphCondTypeIf;
+      ip.conditional.size = 2;  // [0]: mode != 0 (pull), [1]: else (push)
+      cudaGraphNode_t inode;
+      GFB_CUDA(cudaGraphAddNode(&inode, capG, deps, ndeps, &ip));
+      cudaGraph_t gpull = ip.conditional.phGraph_out[0], gpush = ip.conditional.phGraph_out[1];
+      GFB_CUDA(cudaStreamUpdateCaptureDependencies(b, &inode, 1, cudaStreamSetCaptureDependencies));
+      cudaStream_t x = c->aux[1];
+      GFB_CUDA(cudaStreamBeginCaptureToGraph(x, gpull, nullptr, nullptr, 0,
+                                             cudaStreamCaptureModeRelaxed));
+      pull_launch(x);
+      GFB_CUDA(cudaStreamEndCapture(x, &tmp));
+      GFB_CUDA(cudaStreamBeginCaptureToGraph(x, gpush, nullptr, nullptr, 0,
+                                             cudaStreamCaptureModeRelaxed));
+      push(x, 0xFFFFFFFFu);
+      GFB_CUDA(cudaStreamEndCapture(x, &tmp));
+    } else {
+      push(b, 0xFFFFFFFFu);
+    }
+    {
+      cudaStream_t keep = s;
+      s = b;  // compact() launches on `s`
+      compact(dir, alpha, hloop, hmode, true);
+      s = keep;
+    }
+    GFB_CUDA(cudaStreamEndCapture(b, &tmp));
+    GFB_CUDA(cudaGraphInstantiate(&ws->loop_exec, G, 0));
+    ws->loop_graph = G;
   }
 
   void run(uint32_t source, const gfb_sssp_opts* o, gfb_sssp_stats* st) {
     ws->has_result = false;
     variant = o->reserved[0];
-    GFB_CUDA(cudaEventRecord(c->ev[0], s));
-    k_init<W><<<stride_grid(c), 256, 0, s>>>(ws->dist.as<D>(), ws->predrec.as<uint2>(),
-                                             ws->bm_next.as<uint32_t>(), ws->bm_cur.as<uint32_t>(),
-                                             n, nwords, source, ws->ctl.as<Ctl>());
-    GFB_CUDA(cudaMemsetAsync(ws->status.p, 0, (size_t)ws->status_len * 8, s));
-    compact();
-    GFB_CUDA(cudaGetLastError());
     const int dir = o->direction;
-    const double alpha = o->pull_alpha > 0 ? o->pull_alpha : 1.5;
-    uint64_t supersteps = 0, push_steps = 0, pull_steps = 0, launches = 0;
-    kernels = 2;  // k_init + first k_compact
+    const float alpha = o->pull_alpha > 0 ? o->pull_alpha : 1.5f;
+    // source -> device (pinned staging in ctl_host's slot)
+    GFB_CUDA(cudaMemcpyAsync(ws->src_dev.p, &source, 4, cudaMemcpyHostToDevice, s));
+    uint64_t launches = 0;
     float adv_ms = 0;
-    for (;;) {
-      Ctl h = c->read_ctl(ws->ctl.as<Ctl>());
-      if (h.err & 1u) fail(GFB_ERANGE, "sssp: u32 distance overflow (use f64 weights)");
-      if (h.k == 0) break;
-      bool pull = false;
-      if (dir == GFB_DIR_PULL) pull = true;
-      else if (dir == GFB_DIR_AUTO && g->has_csc && (double)h.total > (double)g->m / alpha)
-        pull = true;
-      GFB_CUDA(cudaEventRecord(c->ev[2], s));
-      advance(pull, h.total);
-      GFB_CUDA(cudaEventRecord(c->ev[3], s));
-      GFB_CUDA(cudaGetLastError());
-      compact();
-      GFB_CUDA(cudaGetLastError());
-      ++supersteps;
-      ++launches;
-      kernels += 2;
-      (pull ? pull_steps : push_steps)++;
-      GFB_CUDA(cudaEventSynchronize(c->ev[3]));
-      float ms = 0;
-      GFB_CUDA(cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]));
-      adv_ms += ms;
+    GFB_CUDA(cudaEventRecord(c->ev[0], s));
+    if (o->device_loop) {
+      int key[3] = {dir, (int)(alpha * 1000), variant};
+      if (!ws->loop_exec || memcmp(key, ws->loop_key, sizeof(key)) != 0) {
+        GFB_CUDA(cudaStreamSynchronize(s));
+        build_loop_graph(dir, alpha);
+        memcpy(ws->loop_key, key, sizeof(key));
+        GFB_CUDA(cudaEventRecord(c->ev[0], s));
+      }
+      GFB_CUDA(cudaGraphLaunch(ws->loop_exec, s));
+    } else {
+      cudaGraphConditionalHandle none{};
+      init_launch();
+      compact(dir, alpha, none, none, false);
+      kernels = 4;
+      for (;;) {
+        Ctl h = c->read_ctl(ws->ctl.as<Ctl>());
+        if (h.err & 1u) fail(GFB_ERANGE, "sssp: u32 distance overflow (use f64 weights)");
+        if (h.k == 0) break;
+        GFB_CUDA(cudaEventRecord(c->ev[2], s));
+        if (h.mode == 1) pull_launch(s);
+        else push(s, h.total);
+        GFB_CUDA(cudaEventRecord(c->ev[3], s));
+        GFB_CUDA(cudaGetLastError());
+        compact(dir, alpha, none, none, false);
+        ++launches;
+        kernels += 4;
+        GFB_CUDA(cudaEventSynchronize(c->ev[3]));
+        float ms = 0;
+        GFB_CUDA(cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]));
+        adv_ms += ms;
+      }
     }
     uint64_t fallback = 0;
     pred_pass(source, o->compute_pred != 0, &fallback);
@@ -171,19 +272,20 @@ struct Runner {
     if (h.err & 1u) fail(GFB_ERANGE, "sssp: u32 distance overflow (use f64 weights)");
     float ms = 0;
     GFB_CUDA(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+    if (o->device_loop) kernels += 4 + 4ull * h.supersteps;
     ws->has_result = true;
     ws->source = source;
     if (st) {
-      st->supersteps = supersteps;
+      st->supersteps = h.supersteps;
       st->relaxations = h.relax;
       st->n_reach = h.n_reach;
       st->m_reach = h.m_reach;
-      st->push_steps = push_steps;
-      st->pull_steps = pull_steps;
+      st->push_steps = h.push_steps;
+      st->pull_steps = h.pull_steps;
       st->pred_fallback = fallback;
       st->device_ms = ms;
       st->advance_ms = adv_ms;
-      st->advance_launches = launches;
+      st->advance_launches = o->device_loop ? h.supersteps : launches;
       st->kernel_launches = kernels;
     }
   }
