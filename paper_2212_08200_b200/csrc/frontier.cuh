@@ -93,7 +93,7 @@ k_fcount(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uint3
 __global__ void __launch_bounds__(F_SCAN_THREADS)
 k_fscan(uint2* agg, uint32_t tiles, Plan plan, Ctl* ctl, uint32_t m, float alpha, int can_pull,
         int force_pull, cudaGraphConditionalHandle loop_handle,
-        cudaGraphConditionalHandle mode_handle, int use_handle) {
+        cudaGraphConditionalHandle mode_handle, int set_loop, int set_mode) {
   __shared__ uint32_t s_c[F_SCAN_THREADS / 32], s_e[F_SCAN_THREADS / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t per = (tiles + F_SCAN_THREADS - 1) / F_SCAN_THREADS;
@@ -134,10 +134,9 @@ k_fscan(uint2* agg, uint32_t tiles, Plan plan, Ctl* ctl, uint32_t m, float alpha
     if (sb < plan.tseg_cap) plan.tseg[sb] = K;
     const uint32_t mode = (force_pull || (can_pull && (float)T > (float)m / alpha)) ? 1u : 0u;
     ctl->mode = mode;
-    if (use_handle) {  // device loop: WHILE(K > 0), IF(pull)
-      cudaGraphSetConditional(loop_handle, K > 0 ? 1u : 0u);
-      if (can_pull || force_pull) cudaGraphSetConditional(mode_handle, mode);
-    }
+    // device loop: WHILE(K > 0) and the IF(pull) of the next body iteration
+    if (set_loop) cudaGraphSetConditional(loop_handle, K > 0 ? 1u : 0u);
+    if (set_mode) cudaGraphSetConditional(mode_handle, mode);
   }
 }
 

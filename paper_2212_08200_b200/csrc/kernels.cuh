@@ -700,54 +700,88 @@ __global__ void k_init(typename DT<W>::D* dist, uint2* predrec, uint32_t* bm_nex
 // Also accumulates n_reach / m_reach for the bench's GTEPS.
 // ---------------------------------------------------------------------------
 template <class W>
-__global__ void k_pred_verify(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ adj,
-                              const typename DT<W>::D* __restrict__ dist,
-                              const uint2* __restrict__ predrec, uint32_t* pred, uint32_t* res,
-                              uint32_t* repair_bm, uint32_t* unres_list, uint32_t n,
-                              uint32_t source, Ctl* ctl) {
+__global__ void __launch_bounds__(256)
+k_pred_verify(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ adj,
+              const typename DT<W>::D* __restrict__ dist, const uint2* __restrict__ predrec,
+              uint32_t* pred, uint32_t* res, uint32_t* repair_bm, uint32_t* unres_list,
+              uint32_t n, uint32_t source, Ctl* ctl) {
   using D = typename DT<W>::D;
-  uint32_t stride = gridDim.x * blockDim.x;
+  constexpr int U = 4;  // vertices per thread per round, loads issued together
+  __shared__ unsigned long long s_nr[8], s_mr[8];
+  __shared__ uint32_t s_un[8];
+  const uint32_t stride = gridDim.x * blockDim.x;
   unsigned long long nr = 0, mr = 0;
   uint32_t unres = 0;
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
-    D dv = dist[v];
-    uint32_t p = NIL, r = 0;
-    bool reach = !(dv == dinf<W>());
-    if (reach) {
-      ++nr;
-      mr += ro[v + 1] - ro[v];
-      if (v == source) {
-        r = 1;
-      } else {
-        uint2 pr = predrec[v];
-        if (pr.x != NIL) {
-          EdgeRec<W> rec = adj[pr.y];
-          D du = dist[pr.x];
-          if (rec.v == v && du < dv) {
-            D t = dadd(du, rec.w, nullptr);
-            if (t == dv) {
-              p = pr.x;
-              r = 1;
-            }
-          }
-        }
-        if (!r) {
-          ++unres;
-          atomicOr(repair_bm + (v >> 5), 1u << (v & 31));
-          unres_list[atomicAdd(&ctl->flag, 1u)] = v;  // rare: races and ties
-        }
+  for (uint32_t v0 = blockIdx.x * blockDim.x + threadIdx.x; v0 < n; v0 += stride * U) {
+    D dv[U];
+    uint2 pr[U];
+    uint32_t deg[U];
+#pragma unroll
+    for (int r = 0; r < U; ++r) {
+      uint32_t v = v0 + r * stride;
+      dv[r] = v < n ? dist[v] : dinf<W>();
+      pr[r] = v < n ? predrec[v] : make_uint2(NIL, NIL);
+      deg[r] = v < n ? ro[v + 1] - ro[v] : 0u;
+    }
+    EdgeRec<W> rec[U];
+    D du[U];
+#pragma unroll
+    for (int r = 0; r < U; ++r) {
+      uint32_t v = v0 + r * stride;
+      bool look = v < n && v != source && !(dv[r] == dinf<W>()) && pr[r].x != NIL;
+      if (look) {
+        rec[r] = adj[pr[r].y];
+        du[r] = dist[pr[r].x];
       }
     }
-    pred[v] = p;
-    res[v] = r;
+#pragma unroll
+    for (int r = 0; r < U; ++r) {
+      uint32_t v = v0 + r * stride;
+      if (v >= n) continue;
+      uint32_t p = NIL, rr = 0;
+      if (!(dv[r] == dinf<W>())) {
+        ++nr;
+        mr += deg[r];
+        if (v == source) {
+          rr = 1;
+        } else {
+          if (pr[r].x != NIL && rec[r].v == v && du[r] < dv[r] &&
+              dadd(du[r], rec[r].w, nullptr) == dv[r]) {
+            p = pr[r].x;
+            rr = 1;
+          }
+          if (!rr) {
+            ++unres;
+            atomicOr(repair_bm + (v >> 5), 1u << (v & 31));
+            unres_list[atomicAdd(&ctl->flag, 1u)] = v;  // rare: races and ties
+          }
+        }
+      }
+      pred[v] = p;
+      res[v] = rr;
+    }
   }
-  // block-reduce the counters (few atomics)
+  // block reduction, then one atomic per counter per block
   for (int d = 16; d > 0; d >>= 1) {
     nr += __shfl_xor_sync(0xffffffffu, nr, d);
     mr += __shfl_xor_sync(0xffffffffu, mr, d);
     unres += __shfl_xor_sync(0xffffffffu, unres, d);
   }
-  if ((threadIdx.x & 31) == 0) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    s_nr[warp] = nr;
+    s_mr[warp] = mr;
+    s_un[warp] = unres;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    nr = mr = 0;
+    unres = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      nr += s_nr[w];
+      mr += s_mr[w];
+      unres += s_un[w];
+    }
     if (nr) atomicAdd(&ctl->n_reach, nr);
     if (mr) atomicAdd(&ctl->m_reach, mr);
     if (unres) atomicAdd(&ctl->unresolved, unres);

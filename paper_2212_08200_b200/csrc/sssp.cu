@@ -2,6 +2,8 @@
 // init -> { advance (push | pull) -> compact } until the frontier is empty
 // -> predecessor pass, all on one CUDA stream.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "frontier.cuh"
@@ -83,7 +85,7 @@ struct Runner {
 
   // frontier compaction: count -> scan (+ loop/direction decision) -> write
   void compact(int dir, float alpha, cudaGraphConditionalHandle hloop,
-               cudaGraphConditionalHandle hmode, bool use_handles) {
+               cudaGraphConditionalHandle hmode, bool set_loop, bool set_mode) {
     const uint32_t tiles = ws->ftiles;
     k_fcount<<<tiles, F_WARPS * 32, 0, s>>>(g->ro.as<uint32_t>(), ws->bm_next.as<uint32_t>(),
                                             nwords, ws->agg.as<uint2>());
@@ -91,7 +93,7 @@ struct Runner {
                                          (uint32_t)g->m, alpha,
                                          dir == GFB_DIR_AUTO && g->has_csc ? 1 : 0,
                                          dir == GFB_DIR_PULL ? 1 : 0, hloop, hmode,
-                                         use_handles ? 1 : 0);
+                                         set_loop ? 1 : 0, set_mode ? 1 : 0);
     k_fwrite<<<tiles, F_WARPS * 32, 0, s>>>(g->ro.as<uint32_t>(), ws->bm_next.as<uint32_t>(),
                                             ws->bm_cur.as<uint32_t>(), nwords,
                                             ws->agg.as<uint2>(), plan());
@@ -159,15 +161,16 @@ struct Runner {
       if (!a) GFB_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
     cudaGraph_t G;
     GFB_CUDA(cudaGraphCreate(&G, 0));
-    cudaGraphConditionalHandle hloop, hmode;
+    // a handle belongs to the graph holding its conditional node: hloop to
+    // the top-level graph, hmode to the loop body (created below)
+    cudaGraphConditionalHandle hloop, hmode{};
     GFB_CUDA(cudaGraphConditionalHandleCreate(&hloop, G, 1, cudaGraphCondAssignDefault));
-    GFB_CUDA(cudaGraphConditionalHandleCreate(&hmode, G, 0, cudaGraphCondAssignDefault));
     const bool pullable = g->has_csc && dir != GFB_DIR_PUSH;
 
     GFB_CUDA(cudaStreamBeginCaptureToGraph(s, G, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeRelaxed));
     init_launch();
-    compact(dir, alpha, hloop, hmode, true);
+    compact(dir, alpha, hloop, hmode, true, false);
     cudaStreamCaptureStatus cst;
     cudaGraph_t capG;
     const cudaGraphNode_t* deps = nullptr;
@@ -186,6 +189,8 @@ struct Runner {
     GFB_CUDA(cudaStreamEndCapture(s, &tmp));
 
     // loop body
+    if (pullable)  // first iteration expands {source}: default 0 = push
+      GFB_CUDA(cudaGraphConditionalHandleCreate(&hmode, body, 0, cudaGraphCondAssignDefault));
     cudaStream_t b = c->aux[0];
     GFB_CUDA(cudaStreamBeginCaptureToGraph(b, body, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeRelaxed));
@@ -215,7 +220,7 @@ struct Runner {
     {
       cudaStream_t keep = s;
       s = b;  // compact() launches on `s`
-      compact(dir, alpha, hloop, hmode, true);
+      compact(dir, alpha, hloop, hmode, true, pullable);
       s = keep;
     }
     GFB_CUDA(cudaStreamEndCapture(b, &tmp));
@@ -245,8 +250,10 @@ struct Runner {
     } else {
       cudaGraphConditionalHandle none{};
       init_launch();
-      compact(dir, alpha, none, none, false);
+      compact(dir, alpha, none, none, false, false);
       kernels = 4;
+      const char* tr = getenv("GFB_TRACE");
+      const bool trace = tr && tr[0] == '1';
       for (;;) {
         Ctl h = c->read_ctl(ws->ctl.as<Ctl>());
         if (h.err & 1u) fail(GFB_ERANGE, "sssp: u32 distance overflow (use f64 weights)");
@@ -256,13 +263,17 @@ struct Runner {
         else push(s, h.total);
         GFB_CUDA(cudaEventRecord(c->ev[3], s));
         GFB_CUDA(cudaGetLastError());
-        compact(dir, alpha, none, none, false);
+        compact(dir, alpha, none, none, false, false);
         ++launches;
         kernels += 4;
         GFB_CUDA(cudaEventSynchronize(c->ev[3]));
         float ms = 0;
         GFB_CUDA(cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]));
         adv_ms += ms;
+        if (trace)
+          fprintf(stderr, "[gfb] superstep %llu %s frontier=%u edges=%u advance=%.3f ms (%.1f G edges/s)\n",
+                  (unsigned long long)launches, h.mode ? "pull" : "push", h.k, h.total, ms,
+                  (h.mode ? g->pull_total : h.total) / (ms * 1e-3) / 1e9);
       }
     }
     uint64_t fallback = 0;
@@ -293,7 +304,7 @@ struct Runner {
   void pred_pass(uint32_t source, bool want, uint64_t* fallback) {
     GFB_CUDA(cudaMemsetAsync(ws->repair_bm.p, 0, (size_t)nwords * 4, s));
     GFB_CUDA(cudaMemsetAsync(&ws->ctl.as<Ctl>()->flag, 0, 4, s));
-    k_pred_verify<W><<<std::max<uint32_t>((n + 255) / 256, 1), 256, 0, s>>>(
+    k_pred_verify<W><<<c->num_sms * 8, 256, 0, s>>>(
         g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(), ws->dist.as<D>(), ws->predrec.as<uint2>(),
         ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(), ws->repair_bm.as<uint32_t>(),
         ws->cand.as<uint32_t>(), n, source, ws->ctl.as<Ctl>());
