@@ -36,6 +36,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "SSSP GTEPS on RMAT (1/2/4/8 B200) and % of HBM roofline vs host-CPU ref"
 NOMINAL_HBM_GBS = 8000.0
+# measured on this pool's B200 by tools/microbench.cu: coalesced 8-byte record
+# stream + one dependent random 4-byte gather into a 64 MB L2-resident array
+GATHER_CEILING = 263e9
 
 
 def log(*a):
@@ -262,6 +265,14 @@ def run_ours(args):
                      "advance_ms_per_step": ist.advance_ms,
                      "advance_launches_per_step": ist.advance_launches,
                      "peak_kind": peak_kind},
+        "gather_bound": {
+            "visits_per_s": ist.relaxations / (ist.advance_ms * 1e-3) if ist.advance_ms else None,
+            "ceiling_visits_per_s": GATHER_CEILING,
+            "frac": (ist.relaxations / (ist.advance_ms * 1e-3) / GATHER_CEILING
+                     if ist.advance_ms else None),
+            "note": "advance = 1 streamed 8 B record + 1 random 4 B dist gather per visit; "
+                    "ceiling = measured stream+gather rate (tools/microbench.cu, "
+                    "profiles/r01_microbench.txt)"},
         "roofline_sssp": {"b_alg_bytes_per_te": b_alg,
                           "achieved_gbs": gteps * b_alg,
                           "frac_of_measured": gteps * b_alg / peak,
@@ -347,7 +358,7 @@ def main():
     ap.add_argument("--edgefactor", type=int, default=16)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--direction", default="auto", choices=["auto", "push", "pull"])
-    ap.add_argument("--alpha", type=float, default=1.5)
+    ap.add_argument("--alpha", type=float, default=0.25)
     ap.add_argument("--ref-scale", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--soak", type=float, default=1.5, help="min warm-up seconds (clock samples)")

@@ -86,7 +86,7 @@ struct DevicePolicy {
   int device = 0;
   gfb_wtype arithmetic = GFB_W_F64;
   bool auto_direction = true;  // push<->pull switch on the device
-  float pull_alpha = 1.5f;     // pull when frontier edges > m / pull_alpha
+  float pull_alpha = 0.25f;    // pull when frontier edges > m / pull_alpha
 
   void validate() const {
     if (device < 0) throw std::invalid_argument("device policy: device must be >= 0");

@@ -207,7 +207,7 @@ def grid(side, seed=1, transpose=True, ctx=None):
     return Graph(h, ctx)
 
 
-def _opts(direction="auto", pull_alpha=1.5, delta=0.0, device_loop=True, compute_pred=True,
+def _opts(direction="auto", pull_alpha=0.25, delta=0.0, device_loop=True, compute_pred=True,
           variant=0):
     o = SsspOpts()
     _lib.load().gfb_sssp_opts_default(C.byref(o))

@@ -335,7 +335,7 @@ void gfb_sssp_opts_default(gfb_sssp_opts* o) {
   std::memset(o, 0, sizeof(*o));
   o->struct_size = sizeof(*o);
   o->direction = GFB_DIR_AUTO;
-  o->pull_alpha = 1.5f;
+  o->pull_alpha = 0.25f;
   o->device_loop = 1;
   o->delta = 0.0;
   o->compute_pred = 1;

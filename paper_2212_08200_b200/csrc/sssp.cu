@@ -232,7 +232,7 @@ struct Runner {
     ws->has_result = false;
     variant = o->reserved[0];
     const int dir = o->direction;
-    const float alpha = o->pull_alpha > 0 ? o->pull_alpha : 1.5f;
+    const float alpha = o->pull_alpha > 0 ? o->pull_alpha : 0.25f;
     // source -> device (pinned staging in ctl_host's slot)
     GFB_CUDA(cudaMemcpyAsync(ws->src_dev.p, &source, 4, cudaMemcpyHostToDevice, s));
     uint64_t launches = 0;

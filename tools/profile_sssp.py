@@ -16,7 +16,7 @@ ap.add_argument("--scale", type=int, default=24)
 ap.add_argument("--grid", type=int, default=0, help="grid side (instead of RMAT)")
 ap.add_argument("--runs", type=int, default=2)
 ap.add_argument("--direction", default="auto")
-ap.add_argument("--alpha", type=float, default=4.0)
+ap.add_argument("--alpha", type=float, default=0.25)
 ap.add_argument("--delta", type=float, default=0.0)
 ap.add_argument("--device-loop", type=int, default=1)
 ap.add_argument("--variant", type=int, default=0)
