@@ -199,6 +199,41 @@ int gfb_sssp(gfb_ctx* ctx, gfb_graph* g, uint32_t source,
  * graph's native type (u32 / f32 / f64 bytes). */
 int gfb_sssp_read(gfb_graph* g, double* dist, void* dist_native, uint32_t* pred);
 
+/* ---- 1-D partitioned SSSP: one rank's share (multi-GPU) ----
+ * No reference counterpart (the reference is single-host); mg.py drives one
+ * gfb_part per rank and exchanges the messages with torch.distributed
+ * (NCCL over NVLink/NVSwitch).  The rank holds CSR rows [lo, hi) of the
+ * global graph (ro_local rebased to 0, hi-lo+1 entries; column ids global
+ * < n_global).  Messages are 16-byte {dst_global, src_global, dist_bits, 0}
+ * records in device memory, ascending dst (= grouped by owner).  f32 / u32
+ * arithmetic only. */
+typedef struct gfb_part gfb_part;
+int gfb_part_create(gfb_ctx* ctx, uint64_t n_global, uint32_t lo, uint32_t hi,
+                    uint64_t m_local, const uint32_t* ro_local, const uint32_t* col,
+                    const void* w, int w_host_type, int wtype, gfb_part** out);
+int gfb_part_free(gfb_part* p);
+/* dist = +inf, dist[source] = 0 if the source is local; frontier = {source} */
+int gfb_part_init(gfb_part* p, uint32_t source);
+/* One superstep: expand the local frontier (relax local destinations in
+ * place, min-combine remote candidates), write the remote messages to
+ * out_dev (capacity out_cap messages), per-owner counts[nparts] (host) and
+ * the message total.  range_starts: host array of nparts+1 vertex ids. */
+int gfb_part_advance(gfb_part* p, void* out_dev, uint64_t out_cap,
+                     const uint32_t* range_starts, int nparts, uint32_t* counts,
+                     uint64_t* total);
+/* Apply received messages (device memory): atomicMin + activate. */
+int gfb_part_apply(gfb_part* p, const void* in_dev, uint64_t count);
+/* Size of the local next frontier (the allreduce operand for convergence). */
+int gfb_part_pending(gfb_part* p, uint64_t* size);
+int gfb_part_read(gfb_part* p, void* dist_native, uint64_t* relaxations,
+                  uint64_t* supersteps);
+/* Predecessor candidates from the local edges given the global distance
+ * array (device, n_global, native type): round 1 strict tight edges, round
+ * r > 1 equal-distance tight edges from sources with 1 <= res[u] <= r;
+ * cand[v] = min candidate source (device atomicMin). */
+int gfb_part_pred(gfb_part* p, const void* gdist_dev, const uint32_t* res_dev,
+                  uint32_t* cand_dev, uint32_t round);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,7 +22,7 @@ void check_cuda(cudaError_t e, const char* what) {
 
 // ops.cu / graph.cu
 Graph* graph_upload(Ctx*, uint64_t, uint64_t, const uint32_t*, const uint32_t*, const void*, int,
-                    int, int);
+                    int, int, uint64_t);
 void graph_refill(Graph*, const uint32_t*, const uint32_t*, const void*, int);
 Graph* graph_generate_rmat(Ctx*, int, int, uint64_t, int, int);
 Graph* graph_generate_grid(Ctx*, uint32_t, uint64_t, int);
@@ -68,6 +68,7 @@ struct gfb_graph : Graph {};
 struct gfb_frontier : Frontier {};
 struct gfb_dist : Dist {};
 struct gfb_record : Record {};
+struct gfb_part : Part {};
 
 #define NEED(p)                                          \
   do {                                                   \
@@ -129,7 +130,8 @@ int gfb_graph_upload(gfb_ctx* ctx, uint64_t n, uint64_t m, const uint32_t* ro, c
     NEED(ctx);
     NEED(out);
     set_device(ctx);
-    *out = static_cast<gfb_graph*>(graph_upload(ctx, n, m, ro, col, w, w_host_type, wtype, build_csc));
+    *out = static_cast<gfb_graph*>(
+        graph_upload(ctx, n, m, ro, col, w, w_host_type, wtype, build_csc, 0));
   });
 }
 
@@ -357,6 +359,81 @@ int gfb_sssp(gfb_ctx* ctx, gfb_graph* g, uint32_t source, const gfb_sssp_opts* o
     sssp_run(ctx, g, source, &o, &st);
     if (dist || pred) sssp_read(g, dist, nullptr, pred);
     if (stats) *stats = st;
+  });
+}
+
+int gfb_part_create(gfb_ctx* ctx, uint64_t n_global, uint32_t lo, uint32_t hi, uint64_t m_local,
+                    const uint32_t* ro_local, const uint32_t* col, const void* w, int w_host_type,
+                    int wtype, gfb_part** out) {
+  return guard([&] {
+    NEED(ctx);
+    NEED(out);
+    set_device(ctx);
+    *out = static_cast<gfb_part*>(
+        part_create(ctx, n_global, lo, hi, m_local, ro_local, col, w, w_host_type, wtype));
+  });
+}
+
+int gfb_part_free(gfb_part* p) {
+  return guard([&] {
+    if (!p) return;
+    set_device(p->ctx);
+    p->ctx->sync();
+    delete static_cast<Part*>(p);
+  });
+}
+
+int gfb_part_init(gfb_part* p, uint32_t source) {
+  return guard([&] {
+    NEED(p);
+    set_device(p->ctx);
+    part_init(p, source);
+  });
+}
+
+int gfb_part_advance(gfb_part* p, void* out_dev, uint64_t out_cap, const uint32_t* range_starts,
+                     int nparts, uint32_t* counts, uint64_t* total) {
+  return guard([&] {
+    NEED(p);
+    NEED(range_starts);
+    NEED(counts);
+    set_device(p->ctx);
+    uint64_t t = part_advance(p, out_dev, out_cap, range_starts, nparts, counts);
+    if (total) *total = t;
+  });
+}
+
+int gfb_part_apply(gfb_part* p, const void* in_dev, uint64_t count) {
+  return guard([&] {
+    NEED(p);
+    set_device(p->ctx);
+    part_apply(p, in_dev, count);
+  });
+}
+
+int gfb_part_pending(gfb_part* p, uint64_t* size) {
+  return guard([&] {
+    NEED(p);
+    NEED(size);
+    set_device(p->ctx);
+    *size = part_pending(p);
+  });
+}
+
+int gfb_part_read(gfb_part* p, void* dist_native, uint64_t* relaxations, uint64_t* supersteps) {
+  return guard([&] {
+    NEED(p);
+    set_device(p->ctx);
+    part_read(p, dist_native, relaxations, supersteps);
+  });
+}
+
+int gfb_part_pred(gfb_part* p, const void* gdist_dev, const uint32_t* res_dev, uint32_t* cand_dev,
+                  uint32_t round) {
+  return guard([&] {
+    NEED(p);
+    set_device(p->ctx);
+    part_pred(p, gdist_dev, res_dev, cand_dev, round);
   });
 }
 

@@ -57,7 +57,7 @@ __device__ __forceinline__ void load_warp_words(const uint32_t* __restrict__ ro,
   }
 }
 
-__global__ void __launch_bounds__(F_WARPS * 32)
+static __global__ void __launch_bounds__(F_WARPS * 32)
 k_fcount(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uint32_t nwords,
          uint2* agg) {
   __shared__ uint32_t s_c[F_WARPS], s_e[F_WARPS];
@@ -90,7 +90,7 @@ k_fcount(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uint3
 // One CTA.  agg -> exclusive prefixes (in place), plan totals, bookkeeping.
 // ctl->mode: direction of the next superstep (1 = pull when the plan's edges
 // exceed m / alpha and a CSC exists -- the push<->pull switch).
-__global__ void __launch_bounds__(F_SCAN_THREADS)
+static __global__ void __launch_bounds__(F_SCAN_THREADS)
 k_fscan(uint2* agg, uint32_t tiles, Plan plan, Ctl* ctl, uint32_t m, float alpha, int can_pull,
         int force_pull, cudaGraphConditionalHandle loop_handle,
         cudaGraphConditionalHandle mode_handle, int set_loop, int set_mode) {
@@ -140,7 +140,7 @@ k_fscan(uint2* agg, uint32_t tiles, Plan plan, Ctl* ctl, uint32_t m, float alpha
   }
 }
 
-__global__ void __launch_bounds__(F_WARPS * 32)
+static __global__ void __launch_bounds__(F_WARPS * 32)
 k_fwrite(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur, uint32_t nwords,
          const uint2* __restrict__ prefix, Plan plan) {
   __shared__ uint32_t s_c[F_WARPS], s_e[F_WARPS];

@@ -154,7 +154,8 @@ static void launch_interleave(Graph* g, const uint32_t* dcol, const void* dw, in
                               unsigned long long* flags) {
   Ctx* c = g->ctx;
   k_interleave<W><<<stride_grid(c), 256, 0, c->stream>>>(
-      dcol, dw, htype, g->adj.as<EdgeRec<W>>(), g->n, g->m, flags, flags + 1);
+      dcol, dw, htype, g->adj.as<EdgeRec<W>>(), g->col_bound ? g->col_bound : g->n, g->m, flags,
+      flags + 1);
   GFB_CUDA(cudaGetLastError());
 }
 
@@ -199,7 +200,7 @@ static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const 
 }
 
 Graph* graph_upload(Ctx* c, uint64_t n, uint64_t m, const uint32_t* ro, const uint32_t* col,
-                    const void* w, int htype, int wtype, int build_csc_flag) {
+                    const void* w, int htype, int wtype, int build_csc_flag, uint64_t col_bound) {
   if (wtype < GFB_W_U32 || wtype > GFB_W_F64) fail(GFB_EINVAL, "graph: bad weight type");
   if (n >= (1ull << 31) || m >= (1ull << 31))
     fail(GFB_EINVAL, "graph: device path needs n < 2^31 and m < 2^31");
@@ -207,6 +208,7 @@ Graph* graph_upload(Ctx* c, uint64_t n, uint64_t m, const uint32_t* ro, const ui
   g->ctx = c;
   g->n = n;
   g->m = m;
+  g->col_bound = col_bound ? col_bound : n;
   g->wtype = wtype;
   g->ro.alloc((n + 1) * 4, c->stream);
   g->adj.alloc(m * g->rec_bytes(), c->stream);

@@ -243,7 +243,7 @@ __device__ __forceinline__ D shfl_d(D x, int src) {
   return __shfl_sync(0xffffffffu, x, src);
 }
 
-template <class W, int VT, int MINB>
+template <class W, int VT, int MINB, bool PART = false>
 __global__ void __launch_bounds__(256, MINB) k_push_warp(AdvArgs<W> a) {
   using D = typename DT<W>::D;
   constexpr int WT = 32 * VT;
@@ -302,6 +302,7 @@ __global__ void __launch_bounds__(256, MINB) k_push_warp(AdvArgs<W> a) {
       for (uint32_t x = c0; x < c1; x += 32 * VT) {
         uint32_t dst[VT], eid[VT], srcl[VT];
         D nd[VT], cur[VT];
+        unsigned long long rcur[PART ? VT : 1];
 #pragma unroll
         for (int r = 0; r < VT; ++r) {  // A: segment search + record stream
           const uint32_t le = x + r * 32 + lane;
@@ -323,20 +324,48 @@ __global__ void __launch_bounds__(256, MINB) k_push_warp(AdvArgs<W> a) {
             nd[r] = dadd(sd, rec.w, err);
           }
         }
+        if constexpr (!PART) {
 #pragma unroll
-        for (int r = 0; r < VT; ++r)  // B: distance gathers (test before atomic)
-          if (dst[r] != NIL) cur[r] = ld_dist(a.dist + dst[r]);
+          for (int r = 0; r < VT; ++r)  // B: distance gathers (test before atomic)
+            if (dst[r] != NIL) cur[r] = ld_dist(a.dist + dst[r]);
 #pragma unroll
-        for (int r = 0; r < VT; ++r) {  // C: atomics on candidates
-          if (dst[r] != NIL && nd[r] < cur[r]) cur[r] = atomic_min_d(a.dist + dst[r], nd[r]);
-          else dst[r] = NIL;
-        }
+          for (int r = 0; r < VT; ++r) {  // C: atomics on candidates
+            if (dst[r] != NIL && nd[r] < cur[r]) cur[r] = atomic_min_d(a.dist + dst[r], nd[r]);
+            else dst[r] = NIL;
+          }
 #pragma unroll
-        for (int r = 0; r < VT; ++r) {  // D: winners
-          uint32_t uu = __shfl_sync(0xffffffffu, u, srcl[r]);
-          if (dst[r] != NIL && nd[r] < cur[r]) {
-            a.predrec[dst[r]] = make_uint2(uu, eid[r]);
-            atomicOr(a.bm_out + (dst[r] >> 5), 1u << (dst[r] & 31));
+          for (int r = 0; r < VT; ++r) {  // D: winners
+            uint32_t uu = __shfl_sync(0xffffffffu, u, srcl[r]);
+            if (dst[r] != NIL && nd[r] < cur[r]) {
+              a.predrec[dst[r]] = make_uint2(uu, eid[r]);
+              atomicOr(a.bm_out + (dst[r] >> 5), 1u << (dst[r] & 31));
+            }
+          }
+        } else {
+          static_assert(sizeof(D) == 4, "partitioned mode packs 32-bit distances");
+          const uint32_t span = a.hi - a.lo;
+#pragma unroll
+          for (int r = 0; r < VT; ++r) {  // B: local dist / remote staging gathers
+            if (dst[r] == NIL) continue;
+            if (dst[r] - a.lo < span) cur[r] = ld_dist(a.dist + (dst[r] - a.lo));
+            else rcur[r] = a.rbest[dst[r]];
+          }
+#pragma unroll
+          for (int r = 0; r < VT; ++r) {  // C + D
+            const uint32_t uu = __shfl_sync(0xffffffffu, u, srcl[r]) + a.lo;  // global id
+            if (dst[r] == NIL) continue;
+            if (dst[r] - a.lo < span) {
+              const uint32_t dl = dst[r] - a.lo;
+              if (nd[r] < cur[r] && nd[r] < atomic_min_d(a.dist + dl, nd[r])) {
+                a.predrec[dl] = make_uint2(uu, eid[r]);
+                atomicOr(a.bm_out + (dl >> 5), 1u << (dl & 31));
+              }
+            } else {
+              unsigned long long key =
+                  ((unsigned long long)(*reinterpret_cast<uint32_t*>(&nd[r])) << 32) | uu;
+              if (key < rcur[r] && key < atomicMin(a.rbest + dst[r], key))
+                atomicOr(a.rbm + (dst[r] >> 5), 1u << (dst[r] & 31));
+            }
           }
         }
       }

@@ -46,6 +46,7 @@ struct Workspace;
 struct Graph {
   Ctx* ctx = nullptr;
   uint64_t n = 0, m = 0;
+  uint64_t col_bound = 0;  // destination ids must be < col_bound (= n, or n_global for a partition)
   int wtype = GFB_W_F32;
   bool has_csc = false;
   DBuf ro, adj, co, cadj, ceid;
@@ -105,6 +106,19 @@ struct Workspace {
   ~Workspace();
 };
 
+// One rank of the 1-D partitioned SSSP (mg.cu).
+struct Part {
+  Ctx* ctx = nullptr;
+  std::unique_ptr<Graph> g;  // local CSR slice, global column ids
+  uint64_t n_global = 0;
+  uint32_t lo = 0, hi = 0;
+  DBuf dist, predrec, bm_next, bm_cur, pv, pstart, poff, ptseg, agg, ctl;
+  DBuf rbest, rbm, ragg, rtot, counts;
+  uint32_t ftiles = 0, rtiles = 0;
+  unsigned long long relax = 0;
+  uint32_t supersteps = 0;
+};
+
 // grid sizes
 inline int stride_grid(const Ctx* c) { return c->num_sms * 8; }
 inline int persist_grid(const Ctx* c, int per_sm) { return c->num_sms * per_sm; }
@@ -116,5 +130,15 @@ void build_pull_plan(Graph* g);
 void sssp_run(Ctx* ctx, Graph* g, uint32_t source, const gfb_sssp_opts* o, gfb_sssp_stats* st);
 void sssp_read(Graph* g, double* dist, void* dist_native, uint32_t* pred);
 Workspace* ensure_ws(Graph* g);
+// mg.cu
+Part* part_create(Ctx*, uint64_t n_global, uint32_t lo, uint32_t hi, uint64_t m_local,
+                  const uint32_t* ro, const uint32_t* col, const void* w, int htype, int wtype);
+void part_init(Part*, uint32_t source);
+uint64_t part_advance(Part*, void* out, uint64_t cap, const uint32_t* range_starts, int nparts,
+                      uint32_t* counts_host);
+void part_apply(Part*, const void* in, uint64_t count);
+uint64_t part_pending(Part*);
+void part_read(Part*, void* dist_native, uint64_t* relax, uint64_t* supersteps);
+void part_pred(Part*, const void* gdist, const uint32_t* res, uint32_t* cand, uint32_t round);
 
 }  // namespace gfb

@@ -307,6 +307,12 @@ struct AdvArgs {
   unsigned long long* status;  // zeroed here for the next look-back kernel
   uint32_t status_len;
   unsigned long long* qstatus; // OUT_QUEUE look-back state (zero at launch)
+  // partitioned (multi-GPU) push: destinations in [lo, hi) are local (index
+  // dst - lo); others are min-combined into rbest[dst] = (dist_bits << 32 |
+  // src) and flagged in the remote bitmap rbm (mg.cu)
+  uint32_t lo, hi;
+  unsigned long long* rbest;
+  uint32_t* rbm;
   int op;                    // gfb_op
 };
 
