@@ -197,7 +197,7 @@ def run_ours(args):
     import paper_2212_08200_b200 as gb
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    if world > 1:
+    if world > 1 or args.partitioned:
         import bench_mg
         return bench_mg.run(args, rank, world)
     ctx = gb.Context(0)
@@ -363,6 +363,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--soak", type=float, default=1.5, help="min warm-up seconds (clock samples)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="force the 1-D partitioned NCCL path (default for N > 1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
