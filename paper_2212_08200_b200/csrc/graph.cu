@@ -3,6 +3,7 @@
 // plan, and the device-side synthetic generators (RMAT, grid).
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -121,21 +122,24 @@ __device__ __forceinline__ bool conv_weight<uint32_t>(const void* src, int htype
   return true;
 }
 
+// Interleave one uploaded chunk [e0, e0 + cnt) of col[] / w[] into the
+// device records; validation flags record the first bad global edge index.
 template <class W>
 __global__ void k_interleave(const uint32_t* __restrict__ col, const void* __restrict__ wsrc,
-                             int htype, EdgeRec<W>* adj, uint64_t n, uint64_t m,
-                             unsigned long long* bad_v, unsigned long long* bad_w) {
+                             int htype, EdgeRec<W>* adj, uint64_t e0, uint64_t cnt,
+                             uint64_t bound, unsigned long long* bad_v,
+                             unsigned long long* bad_w) {
   uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
-    uint32_t v = col[e];
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += stride) {
+    uint32_t v = col[i];
     W w{};
-    bool okw = conv_weight<W>(wsrc, htype, e, &w);
-    if (v >= n) atomicMin(bad_v, (unsigned long long)e);
-    if (!okw) atomicMin(bad_w, (unsigned long long)e);
+    bool okw = conv_weight<W>(wsrc, htype, i, &w);
+    if (v >= bound) atomicMin(bad_v, (unsigned long long)(e0 + i));
+    if (!okw) atomicMin(bad_w, (unsigned long long)(e0 + i));
     EdgeRec<W> r{};
     r.v = v;
     r.w = w;
-    adj[e] = r;
+    adj[e0 + i] = r;
   }
 }
 
@@ -151,15 +155,20 @@ __global__ void k_check_ro(const uint32_t* ro, uint64_t n, uint64_t m,
 
 template <class W>
 static void launch_interleave(Graph* g, const uint32_t* dcol, const void* dw, int htype,
-                              unsigned long long* flags) {
+                              uint64_t e0, uint64_t cnt, unsigned long long* flags) {
   Ctx* c = g->ctx;
   k_interleave<W><<<stride_grid(c), 256, 0, c->stream>>>(
-      dcol, dw, htype, g->adj.as<EdgeRec<W>>(), g->col_bound ? g->col_bound : g->n, g->m, flags,
-      flags + 1);
+      dcol, dw, htype, g->adj.as<EdgeRec<W>>(), e0, cnt, g->col_bound ? g->col_bound : g->n,
+      flags, flags + 1);
   GFB_CUDA(cudaGetLastError());
 }
 
 static size_t host_wsize(int htype) { return htype == GFB_W_F64 ? 8 : 4; }
+
+// H2D upload as a two-stream pipeline: chunk b+1 is copied (copy stream,
+// double-buffered staging kept on the graph for refills) while chunk b is
+// validated and interleaved into {dst, w} records (compute stream).
+static constexpr uint64_t UPLOAD_CHUNK = 1ull << 25;  // edges per chunk
 
 static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const void* w,
                        int htype) {
@@ -168,26 +177,52 @@ static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const 
   const uint64_t n = g->n, m = g->m;
   if (htype < GFB_W_U32 || htype > GFB_W_F64) fail(GFB_EINVAL, "graph: bad host weight type");
   if (!ro || (m && (!col || !w))) fail(GFB_EINVAL, "graph: null CSR array");
-  GFB_CUDA(cudaMemcpyAsync(g->ro.p, ro, (n + 1) * 4, cudaMemcpyHostToDevice, s));
-  DBuf dcol, dw, flags;
-  dcol.alloc(m * 4, s);
-  dw.alloc(m * host_wsize(htype), s);
+  if (!c->aux[1]) GFB_CUDA(cudaStreamCreateWithFlags(&c->aux[1], cudaStreamNonBlocking));
+  cudaStream_t cp = c->aux[1];
+  const size_t wsz = host_wsize(htype);
+  const uint64_t chunk = std::min<uint64_t>(UPLOAD_CHUNK, std::max<uint64_t>(m, 1));
+  if (g->stage.bytes < 2 * chunk * (4 + 8)) g->stage.alloc(2 * chunk * (4 + 8), s);
+  DBuf flags;
   flags.alloc(3 * 8, s);
   GFB_CUDA(cudaMemsetAsync(flags.p, 0xFF, 3 * 8, s));
-  if (m) {
-    GFB_CUDA(cudaMemcpyAsync(dcol.p, col, m * 4, cudaMemcpyHostToDevice, s));
-    GFB_CUDA(cudaMemcpyAsync(dw.p, w, m * host_wsize(htype), cudaMemcpyHostToDevice, s));
-  }
   auto* f = flags.as<unsigned long long>();
+  cudaEvent_t ready[2], done[2], start;
+  for (int b = 0; b < 2; ++b) {
+    GFB_CUDA(cudaEventCreateWithFlags(&ready[b], cudaEventDisableTiming));
+    GFB_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
+  }
+  GFB_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  GFB_CUDA(cudaEventRecord(start, s));  // staging / flags ready before any copy
+  GFB_CUDA(cudaStreamWaitEvent(cp, start, 0));
+  GFB_CUDA(cudaMemcpyAsync(g->ro.p, ro, (n + 1) * 4, cudaMemcpyHostToDevice, cp));
+  GFB_CUDA(cudaEventRecord(ready[1], cp));
+  GFB_CUDA(cudaStreamWaitEvent(s, ready[1], 0));
   k_check_ro<<<stride_grid(c), 256, 0, s>>>(g->ro.as<uint32_t>(), n, m, f + 2);
-  if (m) {
-    if (g->wtype == GFB_W_F32) launch_interleave<float>(g, dcol.as<uint32_t>(), dw.p, htype, f);
-    else if (g->wtype == GFB_W_F64) launch_interleave<double>(g, dcol.as<uint32_t>(), dw.p, htype, f);
-    else launch_interleave<uint32_t>(g, dcol.as<uint32_t>(), dw.p, htype, f);
+  for (uint64_t e0 = 0, k = 0; e0 < m; e0 += chunk, ++k) {
+    const int b = (int)(k & 1);
+    const uint64_t cnt = std::min(chunk, m - e0);
+    uint32_t* dcol = reinterpret_cast<uint32_t*>(g->stage.as<char>() + b * chunk * 12);
+    void* dw = g->stage.as<char>() + b * chunk * 12 + chunk * 4;
+    if (k >= 2) GFB_CUDA(cudaStreamWaitEvent(cp, done[b], 0));  // buffer b consumed
+    GFB_CUDA(cudaMemcpyAsync(dcol, col + e0, cnt * 4, cudaMemcpyHostToDevice, cp));
+    GFB_CUDA(cudaMemcpyAsync(dw, static_cast<const char*>(w) + e0 * wsz, cnt * wsz,
+                             cudaMemcpyHostToDevice, cp));
+    GFB_CUDA(cudaEventRecord(ready[b], cp));
+    GFB_CUDA(cudaStreamWaitEvent(s, ready[b], 0));
+    if (g->wtype == GFB_W_F32) launch_interleave<float>(g, dcol, dw, htype, e0, cnt, f);
+    else if (g->wtype == GFB_W_F64) launch_interleave<double>(g, dcol, dw, htype, e0, cnt, f);
+    else launch_interleave<uint32_t>(g, dcol, dw, htype, e0, cnt, f);
+    GFB_CUDA(cudaEventRecord(done[b], s));
   }
   unsigned long long hf[3];
   GFB_CUDA(cudaMemcpyAsync(hf, f, sizeof(hf), cudaMemcpyDeviceToHost, s));
   c->sync();
+  GFB_CUDA(cudaStreamSynchronize(cp));
+  for (int b = 0; b < 2; ++b) {
+    cudaEventDestroy(ready[b]);
+    cudaEventDestroy(done[b]);
+  }
+  cudaEventDestroy(start);
   if (hf[2] != ~0ull)
     fail(GFB_EINVAL, "graph: row_offsets inconsistent at vertex " + std::to_string(hf[2]));
   // graph.hpp:152-160 reports the first offending edge
@@ -300,20 +335,124 @@ static void source_of_edges(Graph* g, DBuf& src_of) {
                                           src_of.as<uint32_t>(), MaxOp(), (int64_t)g->m, s));
 }
 
+// payload for the CSC sort: key = dst, value = the CSC record {src, w} as one
+// 64-bit word (low 32 bits = src, high = weight bits: EdgeRec<W> layout)
+template <class W>
+__global__ void k_csc_payload(const EdgeRec<W>* __restrict__ adj, const uint32_t* __restrict__ src_of,
+                              uint32_t* keys, unsigned long long* vals, uint64_t m) {
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+    EdgeRec<W> r = adj[e];
+    keys[e] = r.v;
+    vals[e] = ((unsigned long long)(*reinterpret_cast<const uint32_t*>(&r.w)) << 32) | src_of[e];
+  }
+}
+
+// CSC slot -> CSR edge id (graph.hpp:206 back-map), for the operator-level
+// record condition only: slots of v are in ascending (src, CSR id) order and
+// parallel edges u->v are contiguous in u's sorted row, so
+// id = ro[u] + lower_bound(row u, v) + (slot - first slot of v with source u).
+template <class W>
+__global__ void k_ceid(const uint32_t* __restrict__ co, const EdgeRec<W>* __restrict__ cadj,
+                       const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ adj,
+                       uint32_t n, uint32_t* ceid) {
+  const int lane = threadIdx.x & 31;
+  uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); v < n; v += warps) {
+    const uint32_t s0 = co[v], s1 = co[v + 1];
+    for (uint32_t sl = s0 + lane; sl < s1; sl += 32) {
+      const uint32_t u = cadj[sl].v;
+      uint32_t lo = s0, hi = sl;  // first slot of v with source u
+      while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (cadj[mid].v < u) lo = mid + 1;
+        else hi = mid;
+      }
+      uint32_t a = ro[u], b = ro[u + 1];  // lower_bound(row u, v)
+      while (a < b) {
+        uint32_t mid = (a + b) >> 1;
+        if (adj[mid].v < v) a = mid + 1;
+        else b = mid;
+      }
+      ceid[sl] = a + (sl - lo);
+    }
+  }
+}
+
+void ensure_ceid(Graph* g) {
+  if (!g->has_csc || g->ceid.p) return;
+  Ctx* c = g->ctx;
+  g->ceid.alloc(g->m * 4, c->stream);
+  if (g->m) {
+    if (g->wtype == GFB_W_F32)
+      k_ceid<float><<<stride_grid(c), 256, 0, c->stream>>>(
+          g->co.as<uint32_t>(), g->cadj.as<EdgeRec<float>>(), g->ro.as<uint32_t>(),
+          g->adj.as<EdgeRec<float>>(), (uint32_t)g->n, g->ceid.as<uint32_t>());
+    else
+      k_ceid<uint32_t><<<stride_grid(c), 256, 0, c->stream>>>(
+          g->co.as<uint32_t>(), g->cadj.as<EdgeRec<uint32_t>>(), g->ro.as<uint32_t>(),
+          g->adj.as<EdgeRec<uint32_t>>(), (uint32_t)g->n, g->ceid.as<uint32_t>());
+    GFB_CUDA(cudaGetLastError());
+  }
+  c->sync();
+}
+
 void build_csc(Graph* g) {
   Ctx* c = g->ctx;
   cudaStream_t s = c->stream;
   const uint64_t n = g->n, m = g->m;
   g->co.alloc((n + 1) * 4, s);
-  g->cadj.alloc(m * g->rec_bytes(), s);
-  g->ceid.alloc(m * 4, s);
+  g->ceid.release();
   if (m == 0) {
+    g->cadj.alloc(16, s);
+    g->ceid.alloc(16, s);
     GFB_CUDA(cudaMemsetAsync(g->co.p, 0, (n + 1) * 4, s));
     g->has_csc = true;
     c->sync();
     return;
   }
-  DBuf keys, ids, keys2, ids2, src_of;
+  DBuf src_of;
+  source_of_edges(g, src_of);
+  if (g->wtype != GFB_W_F64) {
+    // one stable radix sort of {src, w} payloads by dst: the sorted payloads
+    // ARE the CSC records in build_transpose slot order (graph.hpp:198-208)
+    DBuf keys, keys2, vals;
+    keys.alloc(m * 4, s);
+    keys2.alloc(m * 4, s);
+    vals.alloc(m * 8, s);
+    g->cadj.alloc(m * 8, s);
+    if (g->wtype == GFB_W_F32)
+      k_csc_payload<float><<<stride_grid(c), 256, 0, s>>>(
+          g->adj.as<EdgeRec<float>>(), src_of.as<uint32_t>(), keys.as<uint32_t>(),
+          vals.as<unsigned long long>(), m);
+    else
+      k_csc_payload<uint32_t><<<stride_grid(c), 256, 0, s>>>(
+          g->adj.as<EdgeRec<uint32_t>>(), src_of.as<uint32_t>(), keys.as<uint32_t>(),
+          vals.as<unsigned long long>(), m);
+    GFB_CUDA(cudaGetLastError());
+    src_of.release();
+    size_t tb = 0;
+    GFB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<uint32_t>(), keys2.as<uint32_t>(),
+                                             vals.as<unsigned long long>(),
+                                             g->cadj.as<unsigned long long>(), (int64_t)m, 0,
+                                             bits_for(n), s));
+    DBuf tmp;
+    tmp.alloc(tb, s);
+    GFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<uint32_t>(), keys2.as<uint32_t>(),
+                                             vals.as<unsigned long long>(),
+                                             g->cadj.as<unsigned long long>(), (int64_t)m, 0,
+                                             bits_for(n), s));
+    k_offsets_from_sorted<<<stride_grid(c), 256, 0, s>>>(keys2.as<uint32_t>(), m,
+                                                         g->co.as<uint32_t>(), n);
+    GFB_CUDA(cudaGetLastError());
+    c->sync();
+    g->has_csc = true;
+    return;
+  }
+  // f64 (16-byte records): sort CSR ids by dst, then gather records + ids
+  g->cadj.alloc(m * g->rec_bytes(), s);
+  g->ceid.alloc(m * 4, s);
+  DBuf keys, ids, keys2, ids2;
   keys.alloc(m * 4, s);
   ids.alloc(m * 4, s);
   keys2.alloc(m * 4, s);
@@ -334,19 +473,9 @@ void build_csc(Graph* g) {
   ids.release();
   k_offsets_from_sorted<<<stride_grid(c), 256, 0, s>>>(keys2.as<uint32_t>(), m,
                                                        g->co.as<uint32_t>(), n);
-  source_of_edges(g, src_of);
-  if (g->wtype == GFB_W_F32)
-    k_csc_fill<float><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<float>>(), ids2.as<uint32_t>(),
-                                                     src_of.as<uint32_t>(), g->cadj.as<EdgeRec<float>>(),
-                                                     g->ceid.as<uint32_t>(), m);
-  else if (g->wtype == GFB_W_F64)
-    k_csc_fill<double><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<double>>(), ids2.as<uint32_t>(),
-                                                      src_of.as<uint32_t>(), g->cadj.as<EdgeRec<double>>(),
-                                                      g->ceid.as<uint32_t>(), m);
-  else
-    k_csc_fill<uint32_t><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<uint32_t>>(), ids2.as<uint32_t>(),
-                                                        src_of.as<uint32_t>(), g->cadj.as<EdgeRec<uint32_t>>(),
-                                                        g->ceid.as<uint32_t>(), m);
+  k_csc_fill<double><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<double>>(), ids2.as<uint32_t>(),
+                                                    src_of.as<uint32_t>(), g->cadj.as<EdgeRec<double>>(),
+                                                    g->ceid.as<uint32_t>(), m);
   GFB_CUDA(cudaGetLastError());
   c->sync();
   g->has_csc = true;

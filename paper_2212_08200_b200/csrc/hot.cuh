@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(H_BLOCK, 4) k_pull_relax(AdvArgs<W> a, uint32_
       if (best < ld_dist(a.dist + u)) {
         D old = atomic_min_d(a.dist + u, best);
         if (best < old) {
-          a.predrec[u] = make_uint2(ld_rec(a.adj + sl).v, a.ceid[sl]);
+          a.predrec[u] = make_uint2(ld_rec(a.adj + sl).v, sl | PRED_CSC_SLOT);
           atomicOr(a.bm_out + (u >> 5), 1u << (u & 31));
         }
       }

@@ -49,7 +49,8 @@ struct Graph {
   uint64_t col_bound = 0;  // destination ids must be < col_bound (= n, or n_global for a partition)
   int wtype = GFB_W_F32;
   bool has_csc = false;
-  DBuf ro, adj, co, cadj, ceid;
+  DBuf ro, adj, co, cadj, ceid;  // ceid built lazily (ensure_ceid) for the record op
+  DBuf stage;                     // upload staging, kept for refills
   // static pull plan (destinations with in-degree > 0)
   uint32_t pull_k = 0, pull_total = 0;
   DBuf pull_v, pull_off, pull_tseg;
@@ -125,6 +126,7 @@ inline int persist_grid(const Ctx* c, int per_sm) { return c->num_sms * per_sm; 
 
 // graph.cu
 void build_csc(Graph* g);
+void ensure_ceid(Graph* g);
 void build_pull_plan(Graph* g);
 // sssp.cu
 void sssp_run(Ctx* ctx, Graph* g, uint32_t source, const gfb_sssp_opts* o, gfb_sssp_stats* st);

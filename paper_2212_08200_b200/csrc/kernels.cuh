@@ -55,6 +55,8 @@ constexpr int A_BLOCK = 256;
 constexpr int A_VT = 4;
 constexpr int A_TILE = A_BLOCK * A_VT;  // edges per advance tile
 constexpr int PLAN_GRAIN = 256;          // edge granularity of the plan's tile map
+// predrec.y with this bit set holds a CSC slot (pull) instead of a CSR edge id
+constexpr uint32_t PRED_CSC_SLOT = 0x80000000u;
 constexpr int A_RATIO = A_TILE / PLAN_GRAIN;
 
 constexpr int C_WARPS = 8;
@@ -655,7 +657,7 @@ k_advance_pull(AdvArgs<W> a, uint32_t total, uint32_t k) {
           if (best < old) {
             act = true;
             EdgeRec<W> rec = ld_rec(a.adj + slot);
-            a.predrec[u] = make_uint2(rec.v, a.ceid[slot]);
+            a.predrec[u] = make_uint2(rec.v, slot | PRED_CSC_SLOT);
           }
         }
       }
@@ -708,6 +710,7 @@ __global__ void k_init(typename DT<W>::D* dist, uint2* predrec, uint32_t* bm_nex
 template <class W>
 __global__ void __launch_bounds__(256)
 k_pred_verify(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ adj,
+              const uint32_t* __restrict__ co, const EdgeRec<W>* __restrict__ cadj,
               const typename DT<W>::D* __restrict__ dist, const uint2* __restrict__ predrec,
               uint32_t* pred, uint32_t* res, uint32_t* repair_bm, uint32_t* unres_list,
               uint32_t n, uint32_t source, Ctl* ctl) {
@@ -734,9 +737,17 @@ k_pred_verify(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ ad
 #pragma unroll
     for (int r = 0; r < U; ++r) {
       uint32_t v = v0 + r * stride;
-      bool look = v < n && v != source && !(dv[r] == dinf<W>()) && pr[r].x != NIL;
+      bool look = v < n && v != source && !(dv[r] == dinf<W>()) && pr[r].x != NIL &&
+                  pr[r].y != NIL;
       if (look) {
-        rec[r] = adj[pr[r].y];
+        if (pr[r].y & PRED_CSC_SLOT) {  // recorded by a pull step: CSC slot of v
+          const uint32_t sl = pr[r].y & ~PRED_CSC_SLOT;
+          rec[r] = (cadj && sl >= co[v] && sl < co[v + 1]) ? cadj[sl] : EdgeRec<W>{};
+          if (cadj && sl >= co[v] && sl < co[v + 1] && rec[r].v == pr[r].x) rec[r].v = v;
+          else rec[r].v = NIL;
+        } else {
+          rec[r] = adj[pr[r].y];
+        }
         du[r] = dist[pr[r].x];
       }
     }
@@ -751,7 +762,7 @@ k_pred_verify(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ ad
         if (v == source) {
           rr = 1;
         } else {
-          if (pr[r].x != NIL && rec[r].v == v && du[r] < dv[r] &&
+          if (pr[r].x != NIL && pr[r].y != NIL && rec[r].v == v && du[r] < dv[r] &&
               dadd(du[r], rec[r].w, nullptr) == dv[r]) {
             p = pr[r].x;
             rr = 1;

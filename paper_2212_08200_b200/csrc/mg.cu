@@ -251,12 +251,12 @@ static uint64_t part_advance_t(Part* p, void* out, uint64_t cap, const uint32_t*
   k_rscan<<<1, 1024, 0, s>>>(p->ragg.as<uint32_t>(), p->rtiles, p->rtot.as<uint32_t>());
   k_rwrite<<<p->rtiles, 256, 0, s>>>(p->rbm.as<uint32_t>(), p->rbest.as<unsigned long long>(),
                                      rwords, p->ragg.as<uint32_t>(), static_cast<uint4*>(out), cap);
-  DBuf rs;
-  rs.alloc((nparts + 1) * 4, s);
-  GFB_CUDA(cudaMemcpyAsync(rs.p, range_starts, (nparts + 1) * 4, cudaMemcpyHostToDevice, s));
+  // range starts ride in the tail of the counts buffer (no per-call allocation)
+  uint32_t* rs = p->counts.as<uint32_t>() + 4096;
+  GFB_CUDA(cudaMemcpyAsync(rs, range_starts, (nparts + 1) * 4, cudaMemcpyHostToDevice, s));
   k_owner_counts<<<(nparts + 127) / 128, 128, 0, s>>>(static_cast<uint4*>(out),
-                                                      p->rtot.as<uint32_t>(), rs.as<uint32_t>(),
-                                                      nparts, p->counts.as<uint32_t>());
+                                                      p->rtot.as<uint32_t>(), rs, nparts,
+                                                      p->counts.as<uint32_t>());
   GFB_CUDA(cudaGetLastError());
   uint32_t tot = 0;
   GFB_CUDA(cudaMemcpyAsync(&tot, p->rtot.p, 4, cudaMemcpyDeviceToHost, s));
@@ -310,7 +310,7 @@ Part* part_create(Ctx* c, uint64_t n_global, uint32_t lo, uint32_t hi, uint64_t 
   p->rtiles = (uint32_t)std::max<uint64_t>((rwords + 2047) / 2048, 1);
   p->ragg.alloc((size_t)p->rtiles * 4, s);
   p->rtot.alloc(16, s);
-  p->counts.alloc(4096 * 4, s);
+  p->counts.alloc((4096 + 4097) * 4 + 16, s);  // counts | range starts | pending
   return p.release();
 }
 
@@ -336,14 +336,13 @@ void part_apply(Part* p, const void* in, uint64_t count) {
 uint64_t part_pending(Part* p) {
   Ctx* c = p->ctx;
   const uint32_t nwords = (uint32_t)((p->g->n + 31) / 32);
-  DBuf cnt;
-  cnt.alloc(8, c->stream);
-  GFB_CUDA(cudaMemsetAsync(cnt.p, 0, 8, c->stream));
-  k_count_bits<<<stride_grid(c), 256, 0, c->stream>>>(p->bm_next.as<uint32_t>(), nwords,
-                                                      cnt.as<unsigned long long>());
+  unsigned long long* cnt =
+      reinterpret_cast<unsigned long long*>(p->counts.as<uint32_t>() + 4096 + 4098);
+  GFB_CUDA(cudaMemsetAsync(cnt, 0, 8, c->stream));
+  k_count_bits<<<stride_grid(c), 256, 0, c->stream>>>(p->bm_next.as<uint32_t>(), nwords, cnt);
   GFB_CUDA(cudaGetLastError());
   unsigned long long h = 0;
-  GFB_CUDA(cudaMemcpyAsync(&h, cnt.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  GFB_CUDA(cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, c->stream));
   c->sync();
   return h;
 }

@@ -323,6 +323,7 @@ void advance_pull(Ctx* c, const Graph* g, Frontier* in, Frontier* out, int op, v
     fail(GFB_EINVAL, "neighbors_expand_pull: transpose not built");
   if (in->repr != GFB_DENSE || out->repr != GFB_DENSE)  // operators.hpp:301-302
     fail(GFB_EINVAL, "neighbors_expand_pull: dense frontier required");
+  if (op == GFB_OP_RECORD) ensure_ceid(const_cast<Graph*>(g));  // CSR ids of CSC slots
   if (g->wtype == GFB_W_F32) pull_impl<float>(c, g, in, out, op, state);
   else if (g->wtype == GFB_W_F64) pull_impl<double>(c, g, in, out, op, state);
   else pull_impl<uint32_t>(c, g, in, out, op, state);

@@ -305,9 +305,11 @@ struct Runner {
     GFB_CUDA(cudaMemsetAsync(ws->repair_bm.p, 0, (size_t)nwords * 4, s));
     GFB_CUDA(cudaMemsetAsync(&ws->ctl.as<Ctl>()->flag, 0, 4, s));
     k_pred_verify<W><<<c->num_sms * 8, 256, 0, s>>>(
-        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(), ws->dist.as<D>(), ws->predrec.as<uint2>(),
-        ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(), ws->repair_bm.as<uint32_t>(),
-        ws->cand.as<uint32_t>(), n, source, ws->ctl.as<Ctl>());
+        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(),
+        g->has_csc ? g->co.as<uint32_t>() : nullptr,
+        g->has_csc ? g->cadj.as<EdgeRec<W>>() : nullptr, ws->dist.as<D>(),
+        ws->predrec.as<uint2>(), ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(),
+        ws->repair_bm.as<uint32_t>(), ws->cand.as<uint32_t>(), n, source, ws->ctl.as<Ctl>());
     GFB_CUDA(cudaGetLastError());
     ++kernels;
     if (!want) return;
