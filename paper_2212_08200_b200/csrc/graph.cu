@@ -180,7 +180,9 @@ static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const 
   if (!c->aux[1]) GFB_CUDA(cudaStreamCreateWithFlags(&c->aux[1], cudaStreamNonBlocking));
   cudaStream_t cp = c->aux[1];
   const size_t wsz = host_wsize(htype);
-  const uint64_t chunk = std::min<uint64_t>(UPLOAD_CHUNK, std::max<uint64_t>(m, 1));
+  // staging layout per buffer: col[chunk] | w[chunk]; chunk rounded to 64 so
+  // every sub-array stays 16-byte aligned for any weight width
+  const uint64_t chunk = (std::min<uint64_t>(UPLOAD_CHUNK, std::max<uint64_t>(m, 1)) + 63) & ~63ull;
   if (g->stage.bytes < 2 * chunk * (4 + 8)) g->stage.alloc(2 * chunk * (4 + 8), s);
   DBuf flags;
   flags.alloc(3 * 8, s);
