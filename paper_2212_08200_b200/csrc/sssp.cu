@@ -189,8 +189,9 @@ struct Runner {
     GFB_CUDA(cudaStreamEndCapture(s, &tmp));
 
     // loop body
-    if (pullable)  // first iteration expands {source}: default 0 = push
-      GFB_CUDA(cudaGraphConditionalHandleCreate(&hmode, body, 0, cudaGraphCondAssignDefault));
+    if (pullable)  // first iteration expands {source}: push unless pull is forced
+      GFB_CUDA(cudaGraphConditionalHandleCreate(&hmode, body, dir == GFB_DIR_PULL ? 1 : 0,
+                                                cudaGraphCondAssignDefault));
     cudaStream_t b = c->aux[0];
     GFB_CUDA(cudaStreamBeginCaptureToGraph(b, body, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeRelaxed));
