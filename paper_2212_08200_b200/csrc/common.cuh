@@ -134,6 +134,37 @@ __device__ __forceinline__ EdgeRec<double> ld_rec(const EdgeRec<double>* p) {
 template <class D>
 __device__ __forceinline__ D ld_dist(const D* p) { return *p; }
 
+// Explicit fire-and-forget reductions (PTX red.*) with an optional L2
+// eviction-priority hint.
+__device__ __forceinline__ uint64_t evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void red_min_u32(unsigned* p, unsigned v) {
+  asm volatile("red.global.min.u32 [%0], %1;" ::"l"(p), "r"(v));
+}
+__device__ __forceinline__ void red_min_u32_hint(unsigned* p, unsigned v, uint64_t pol) {
+  asm volatile("red.global.L2::cache_hint.min.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol)
+              );
+}
+__device__ __forceinline__ void red_min_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.global.min.u64 [%0], %1;" ::"l"(p), "l"(v));
+}
+__device__ __forceinline__ void red_min_u64_hint(unsigned long long* p, unsigned long long v,
+                                                 uint64_t pol) {
+  asm volatile("red.global.L2::cache_hint.min.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol)
+              );
+}
+__device__ __forceinline__ void red_or_u32(unsigned* p, unsigned v) {
+  asm volatile("red.global.or.b32 [%0], %1;" ::"l"(p), "r"(v));
+}
+__device__ __forceinline__ uint32_t ld_u32_hint(const void* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned r;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));

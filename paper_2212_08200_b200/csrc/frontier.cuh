@@ -31,12 +31,13 @@ struct WarpWords {
   uint32_t deg[F_WPW];
 };
 
+template <bool COH = false>
 __device__ __forceinline__ void load_warp_words(const uint32_t* __restrict__ ro,
                                                 const uint32_t* bm, uint32_t nwords,
                                                 uint32_t wbase, WarpWords& w, uint32_t* raw_word) {
   const int lane = threadIdx.x & 31;
   uint32_t my = 0;
-  if (lane < F_WPW && wbase + lane < nwords) my = bm[wbase + lane];
+  if (lane < F_WPW && wbase + lane < nwords) my = COH ? __ldcg(bm + wbase + lane) : bm[wbase + lane];
   *raw_word = my;
   uint32_t words[F_WPW];
 #pragma unroll
@@ -54,6 +55,35 @@ __device__ __forceinline__ void load_warp_words(const uint32_t* __restrict__ ro,
     bool bit = (words[j] >> lane) & 1u;
     w.deg[j] = bit ? w.deg[j] - w.st[j] : 0u;
     w.keep[j] = __ballot_sync(0xffffffffu, w.deg[j] > 0);
+  }
+}
+
+// Tile-map entries tseg[b] = gi for every b*PLAN_GRAIN in [eoff, eoff+deg)
+// of each lane's segment, written by the whole warp: a hub owns thousands of
+// entries, and one lane looping over them serialises the warp (used by the
+// persistent k_bsp, whose hub CTA owns most of them).
+__device__ __forceinline__ void warp_tile_map(const Plan& plan, uint32_t gi, uint32_t eoff,
+                                              uint32_t deg) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t b0 = (eoff + PLAN_GRAIN - 1) / PLAN_GRAIN;
+  const uint32_t b1 = deg ? (eoff + deg + PLAN_GRAIN - 1) / PLAN_GRAIN : b0;
+  const uint32_t cnt = b1 - b0;
+  const uint32_t cincl = warp_incl_scan(cnt, lane);
+  const uint32_t ctot = __shfl_sync(0xffffffffu, cincl, 31);
+  if (ctot == 0) return;  // warp-uniform
+  const uint32_t cpre = cincl - cnt;
+  for (uint32_t x = lane; x - lane < ctot; x += 32) {
+    int lo = 0;  // owner lane: the first whose inclusive count exceeds x
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1) {
+      const uint32_t p = __shfl_sync(0xffffffffu, cincl, lo + step - 1);
+      if (p <= x) lo += step;
+    }
+    const uint32_t ob0 = __shfl_sync(0xffffffffu, b0, lo);
+    const uint32_t opre = __shfl_sync(0xffffffffu, cpre, lo);
+    const uint32_t ogi = __shfl_sync(0xffffffffu, gi, lo);
+    const uint32_t bb = ob0 + (x - opre);
+    if (x < ctot && bb < plan.tseg_cap) plan.tseg[bb] = ogi;
   }
 }
 
@@ -177,7 +207,7 @@ k_fwrite(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur, u
     if (keep == 0) continue;  // warp-uniform
     const bool mine = (keep >> lane) & 1u;
     const uint32_t incl = warp_incl_scan(w.deg[j], lane);
-    if (mine) {
+    if (mine) {  // per-lane tile map: cheaper here than warp_tile_map (8192 small CTAs)
       const uint32_t gi = gc + __popc(keep & lanemask_lt());
       const uint32_t eoff = ge + incl - w.deg[j];
       plan.v[gi] = (wbase + j) * 32 + lane;

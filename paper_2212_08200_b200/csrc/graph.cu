@@ -172,6 +172,7 @@ static constexpr uint64_t UPLOAD_CHUNK = 1ull << 25;  // edges per chunk
 
 static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const void* w,
                        int htype) {
+  g->nz_valid = false;
   Ctx* c = g->ctx;
   cudaStream_t s = c->stream;
   const uint64_t n = g->n, m = g->m;
@@ -234,6 +235,31 @@ static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const 
     fail(GFB_EINVAL,
          "build_csr: edge " + std::to_string(hf[1]) + " has negative or non-finite weight");
   if (g->ws) g->ws->has_result = false;  // same shape: keep the workspace
+}
+
+// Nonzero-out-degree bitmap (one bit per vertex, the layout of the frontier
+// bitmaps) for the persistent loop's frontier count.
+static __global__ void k_nz(const uint32_t* __restrict__ ro, uint32_t n, uint32_t* nz) {
+  const uint32_t nwords = (n + 31) / 32;
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
+       w += gridDim.x * blockDim.x) {
+    uint32_t bits = 0;
+    for (int b = 0; b < 32; ++b) {
+      const uint32_t v = w * 32 + b;
+      if (v < n && ro[v + 1] > ro[v]) bits |= 1u << b;
+    }
+    nz[w] = bits;
+  }
+}
+
+void ensure_nz(Graph* g) {
+  if (g->nz_valid) return;
+  const uint64_t nwords = (g->n + 31) / 32;
+  if (g->nz.bytes < nwords * 4) g->nz.alloc(nwords * 4, g->ctx->stream);
+  k_nz<<<stride_grid(g->ctx), 256, 0, g->ctx->stream>>>(g->ro.as<uint32_t>(), (uint32_t)g->n,
+                                                        g->nz.as<uint32_t>());
+  GFB_CUDA(cudaGetLastError());
+  g->nz_valid = true;
 }
 
 Graph* graph_upload(Ctx* c, uint64_t n, uint64_t m, const uint32_t* ro, const uint32_t* col,

@@ -19,6 +19,15 @@
 namespace gfb {
 
 constexpr int H_BLOCK = 256;
+
+// Packed predecessor key for 32-bit distances: (dist_bits << 32 | u).  One
+// RED.MIN.64 keeps the pair jointly atomic (see k_push_range).
+__device__ __forceinline__ unsigned long long pred_key(float d, uint32_t u) {
+  return ((unsigned long long)__float_as_uint(d) << 32) | u;
+}
+__device__ __forceinline__ unsigned long long pred_key(uint32_t d, uint32_t u) {
+  return ((unsigned long long)d << 32) | u;
+}
 // edges per thread per tile: 8 for 4-byte weights (2048-edge tiles), 4 for
 // f64 (keeps the f64 kernels under the 48 KB static shared-memory limit)
 template <class W> struct HotCfg {
@@ -133,7 +142,7 @@ __global__ void __launch_bounds__(H_BLOCK, MINB) k_push_relax(AdvArgs<W> a) {
   }
 }
 
-template <class W>
+template <class W, bool KEY = false>
 __global__ void __launch_bounds__(H_BLOCK, 4) k_pull_relax(AdvArgs<W> a, uint32_t total, uint32_t k) {
   using D = typename DT<W>::D;
   using Bits = typename DT<W>::Bits;
@@ -213,6 +222,13 @@ __global__ void __launch_bounds__(H_BLOCK, 4) k_pull_relax(AdvArgs<W> a, uint32_
       D best = *reinterpret_cast<D*>(&b);
       uint32_t u = s_u[j];
       if (best < ld_dist(a.dist + u)) {
+        if constexpr (KEY) {  // fire-and-forget, as in k_push_range
+          red_min_d(a.dist + u, best);
+          atomicMin(reinterpret_cast<unsigned long long*>(a.predrec) + u,
+                    pred_key(best, ld_rec(a.adj + sl).v));
+          atomicOr(a.bm_out + (u >> 5), 1u << (u & 31));
+          continue;
+        }
         D old = atomic_min_d(a.dist + u, best);
         if (best < old) {
           a.predrec[u] = make_uint2(ld_rec(a.adj + sl).v, sl | PRED_CSC_SLOT);
@@ -371,6 +387,186 @@ __global__ void __launch_bounds__(256, MINB) k_push_warp(AdvArgs<W> a) {
       }
       if (c1 >= e1) break;
     }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Range push advance (the default hot kernel for 4-byte distances).
+//
+// Differences from k_push_warp, each removing a dependent memory round trip
+// from the per-warp critical path (ncu of the dense s24 superstep: 66% of
+// warp samples in long-scoreboard stalls, 49% occupancy, profiles/):
+//  1. each warp owns ONE contiguous, equal share of the plan's edges instead
+//     of strided 256-edge tiles, so the tile-map lookup and the segment
+//     window setup (plan loads -> source-distance gather) happen once per 32
+//     segments instead of once per 256 edges, and the next window's plan
+//     entries are prefetched while the current one is expanded;
+//  2. no atomic return values are waited on: a candidate that passes the
+//     test-before-atomic (nd < dist[v]) proves dist[v] drops this superstep,
+//     so it sets v's next-frontier bit itself (RED.OR) and lowers dist[v]
+//     with RED.MIN.  The predecessor is a packed 64-bit key
+//     (dist_bits << 32 | u) lowered with RED.MIN.64: after convergence the
+//     key's high half equals dist[v] and its low half names an in-neighbour
+//     whose final distance makes the edge tight (k_pred_verify<KEY>).
+// ---------------------------------------------------------------------------
+
+// Expand plan edges [e0, e1) with one warp (all lanes converged).
+// COH: every load of data written earlier in the SAME launch (plan, source
+// distances) goes through L2 (ld.cg) -- the persistent k_bsp crosses
+// supersteps inside one kernel and L1 is not coherent across SMs.  The
+// test-before-atomic gather may stay in L1: a stale (larger) value only
+// costs a redundant reduction.
+template <bool COH, class T>
+__device__ __forceinline__ T ldc(const T* p) {
+  if constexpr (COH) return __ldcg(p);
+  else return *p;
+}
+
+// OPT bits (measured alternatives, tools/variants.py):
+//   1: explicit PTX red.* (the compiler emits ATOMG ... RZ for unused atomics)
+//   2: L2 evict_first hint on the predecessor-key reductions (128 MB at s24
+//      that otherwise compete with the 64 MB distance array for L2)
+//   4: L2 evict_last hint on the distance gathers and reductions
+//   8: distance gathers through ld.global.nc
+template <int OPT, class D>
+__device__ __forceinline__ D test_gather(const D* p) {
+  if constexpr ((OPT & 8) != 0) return __ldg(p);
+  else if constexpr ((OPT & 4) != 0) {
+    uint32_t v = ld_u32_hint(p, evict_last_policy());
+    return *reinterpret_cast<D*>(&v);
+  } else return ld_dist(p);
+}
+
+template <int OPT, class D>
+__device__ __forceinline__ void relax_reds(D* dist, unsigned long long* pkey, uint32_t* bm,
+                                           uint32_t v, D nd, uint32_t u) {
+  if constexpr ((OPT & 1) != 0) {
+    const uint32_t bits = *reinterpret_cast<uint32_t*>(&nd);
+    if constexpr ((OPT & 4) != 0)
+      red_min_u32_hint(reinterpret_cast<unsigned*>(dist + v), bits, evict_last_policy());
+    else red_min_u32(reinterpret_cast<unsigned*>(dist + v), bits);
+    if constexpr ((OPT & 2) != 0) red_min_u64_hint(pkey + v, pred_key(nd, u), evict_first_policy());
+    else red_min_u64(pkey + v, pred_key(nd, u));
+    red_or_u32(bm + (v >> 5), 1u << (v & 31));
+  } else {
+    red_min_d(dist + v, nd);
+    atomicMin(pkey + v, pred_key(nd, u));
+    atomicOr(bm + (v >> 5), 1u << (v & 31));
+  }
+}
+
+template <class W, int VT, bool COH = false, int OPT = 0>
+__device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, uint32_t e1,
+                                             uint32_t k, uint32_t total, unsigned* err) {
+  using D = typename DT<W>::D;
+  unsigned long long* pkey = reinterpret_cast<unsigned long long*>(a.predrec);
+  const int lane = threadIdx.x & 31;
+  // segment holding e0: tile-map entry, then a warp-cooperative forward scan
+  uint32_t cs = ldc<COH>(a.plan.tseg + e0 / PLAN_GRAIN);
+  for (;;) {
+    uint32_t cand = cs + lane;
+    uint32_t end = cand < k ? ldc<COH>(a.plan.off + cand + 1) : 0xFFFFFFFFu;
+    unsigned msk = __ballot_sync(0xffffffffu, cand < k && end > e0);
+    if (msk) {
+      cs += __ffs(msk) - 1;
+      break;
+    }
+    cs += 32;
+  }
+  // window = segments [cs, cs+32): lane j holds segment cs+j
+  uint32_t off = 0xFFFFFFFFu, start = 0, u = 0;
+  if (cs + lane < k) {
+    off = ldc<COH>(a.plan.off + cs + lane);
+    start = ldc<COH>(a.plan.start + cs + lane);
+    u = ldc<COH>(a.plan.v + cs + lane);
+  }
+  D du = (cs + lane < k && off < e1) ? ldc<COH>(a.dist + u) : D(0);
+  for (;;) {
+    // prefetch the next window's plan entries (consumed after this window)
+    const uint32_t nj = cs + 32 + lane;
+    uint32_t noff = 0xFFFFFFFFu, nstart = 0, nu = 0;
+    const bool more = __shfl_sync(0xffffffffu, off, 31) < e1 && cs + 32 < k;
+    if (more && nj < k) {
+      noff = ldc<COH>(a.plan.off + nj);
+      nstart = ldc<COH>(a.plan.start + nj);
+      nu = ldc<COH>(a.plan.v + nj);
+    }
+    const uint32_t nxt = cs + 32 < k ? (more ? __shfl_sync(0xffffffffu, noff, 0)
+                                             : ldc<COH>(a.plan.off + cs + 32))
+                                     : total;
+    const uint32_t c0 = max(__shfl_sync(0xffffffffu, off, 0), e0);
+    const uint32_t c1 = min(nxt, e1);
+    for (uint32_t x = c0; x < c1; x += 32 * VT) {
+      uint32_t dst[VT], uu[VT];
+      D nd[VT], cur[VT];
+#pragma unroll
+      for (int r = 0; r < VT; ++r) {  // A: segment search + record stream
+        const uint32_t le = x + r * 32 + lane;
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          uint32_t o = __shfl_sync(0xffffffffu, off, lo + step);
+          if (o <= le) lo += step;
+        }
+        const uint32_t so = __shfl_sync(0xffffffffu, off, lo);
+        const uint32_t ss = __shfl_sync(0xffffffffu, start, lo);
+        const D sd = shfl_d(du, lo);
+        uu[r] = __shfl_sync(0xffffffffu, u, lo);
+        dst[r] = NIL;
+        if (le < c1) {
+          EdgeRec<W> rec = ld_rec(a.adj + (ss + (le - so)));
+          dst[r] = rec.v;
+          nd[r] = dadd(sd, rec.w, err);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < VT; ++r)  // B: distance gathers (test before atomic)
+        if (dst[r] != NIL) cur[r] = test_gather<OPT>(a.dist + dst[r]);
+#pragma unroll
+      for (int r = 0; r < VT; ++r)  // C: fire-and-forget reductions
+        if (dst[r] != NIL && nd[r] < cur[r])
+          relax_reds<OPT>(a.dist, pkey, a.bm_out, dst[r], nd[r], uu[r]);
+    }
+    if (c1 >= e1) break;
+    cs += 32;
+    off = noff;
+    start = nstart;
+    u = nu;
+    du = (nj < k && noff < e1) ? ldc<COH>(a.dist + nu) : D(0);
+  }
+}
+
+// TILE == 0: one contiguous equal share of the plan per warp.  TILE > 0:
+// warps claim TILE-edge tiles round-robin, so the whole grid sweeps the plan
+// in ascending vertex order.  On unpermuted RMAT the low ids are the hubs
+// with the smallest distances: relaxing them first lets their improvements
+// reach later edges of the SAME superstep (measured: contiguous shares do
+// 4.4 relaxations per reached edge at s24, the sweep 3.5).
+template <class W, int VT, int MINB, int TILE, int OPT = 0>
+__global__ void __launch_bounds__(256, MINB) k_push_range(AdvArgs<W> a) {
+  using D = typename DT<W>::D;
+  static_assert(sizeof(D) == 4, "packed predecessor keys need 32-bit distances");
+  static_assert(TILE % 32 == 0, "tiles are whole warp rows");
+  const uint32_t gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t total = a.ctl->total;
+  const uint32_t k = a.ctl->k;
+  unsigned* err = &a.ctl->err;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.ctl->relax += total;
+    a.ctl->supersteps += 1;
+    a.ctl->push_steps += 1;
+  }
+  if constexpr (TILE == 0) {
+    const uint32_t per = (uint32_t)((((uint64_t)total + nwarps - 1) / nwarps + 31) & ~31ull);
+    const uint32_t e0 = (uint32_t)min((uint64_t)gwarp * per, (uint64_t)total);
+    const uint32_t e1 = min(e0 + per, total);
+    if (e0 < e1) range_expand<W, VT, false, OPT>(a, e0, e1, k, total, err);
+  } else {
+    for (uint64_t e0 = (uint64_t)gwarp * TILE; e0 < total; e0 += (uint64_t)nwarps * TILE)
+      range_expand<W, VT, false, OPT>(a, (uint32_t)e0, (uint32_t)min(e0 + TILE, (uint64_t)total),
+                                       k, total, err);
   }
 }
 

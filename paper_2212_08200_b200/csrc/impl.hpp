@@ -51,6 +51,8 @@ struct Graph {
   bool has_csc = false;
   DBuf ro, adj, co, cadj, ceid;  // ceid built lazily (ensure_ceid) for the record op
   DBuf stage;                     // upload staging, kept for refills
+  DBuf nz;                        // bit v: out-degree(v) > 0 (ensure_nz, bsp.cuh)
+  bool nz_valid = false;
   // static pull plan (destinations with in-degree > 0)
   uint32_t pull_k = 0, pull_total = 0;
   DBuf pull_v, pull_off, pull_tseg;
@@ -93,6 +95,8 @@ struct Workspace {
   DBuf ctl;
   DBuf agg;        // per-tile (count, edges) of the frontier compaction
   DBuf src_dev;    // the source vertex (read by k_init)
+  DBuf bar;        // grid barrier of the persistent loop (bsp.cuh)
+  DBuf bsp_agg, bsp_flag, bsp_tot;  // its per-CTA frontier aggregates / totals
   uint32_t ftiles = 0;
   // device loop: one instantiated CUDA graph per (direction, alpha, variant)
   cudaGraphExec_t loop_exec = nullptr;
@@ -128,6 +132,7 @@ inline int persist_grid(const Ctx* c, int per_sm) { return c->num_sms * per_sm; 
 void build_csc(Graph* g);
 void ensure_ceid(Graph* g);
 void build_pull_plan(Graph* g);
+void ensure_nz(Graph* g);
 // sssp.cu
 void sssp_run(Ctx* ctx, Graph* g, uint32_t source, const gfb_sssp_opts* o, gfb_sssp_stats* st);
 void sssp_read(Graph* g, double* dist, void* dist_native, uint32_t* pred);

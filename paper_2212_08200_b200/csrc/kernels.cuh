@@ -707,7 +707,7 @@ __global__ void k_init(typename DT<W>::D* dist, uint2* predrec, uint32_t* bm_nex
 //    algorithms.hpp:506-511).  Smallest u wins (deterministic).
 // Also accumulates n_reach / m_reach for the bench's GTEPS.
 // ---------------------------------------------------------------------------
-template <class W>
+template <class W, bool KEY = false>
 __global__ void __launch_bounds__(256)
 k_pred_verify(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ adj,
               const uint32_t* __restrict__ co, const EdgeRec<W>* __restrict__ cadj,
@@ -739,7 +739,13 @@ k_pred_verify(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ ad
       uint32_t v = v0 + r * stride;
       bool look = v < n && v != source && !(dv[r] == dinf<W>()) && pr[r].x != NIL &&
                   pr[r].y != NIL;
-      if (look) {
+      if (look && KEY) {
+        // packed key (dist_bits << 32 | u), k_push_range: the edge u -> v
+        // that proposed dist[v] is tight at the fixpoint (any later drop of
+        // dist[u] re-expanded u and would have lowered the key)
+        du[r] = dist[pr[r].x];
+        rec[r].v = pr[r].y == *reinterpret_cast<const uint32_t*>(&dv[r]) ? v : NIL;
+      } else if (look) {
         if (pr[r].y & PRED_CSC_SLOT) {  // recorded by a pull step: CSC slot of v
           const uint32_t sl = pr[r].y & ~PRED_CSC_SLOT;
           rec[r] = (cadj && sl >= co[v] && sl < co[v + 1]) ? cadj[sl] : EdgeRec<W>{};
@@ -763,7 +769,7 @@ k_pred_verify(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ ad
           rr = 1;
         } else {
           if (pr[r].x != NIL && pr[r].y != NIL && rec[r].v == v && du[r] < dv[r] &&
-              dadd(du[r], rec[r].w, nullptr) == dv[r]) {
+              (KEY || dadd(du[r], rec[r].w, nullptr) == dv[r])) {
             p = pr[r].x;
             rr = 1;
           }

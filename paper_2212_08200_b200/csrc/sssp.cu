@@ -5,7 +5,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
+#include "bsp.cuh"
 #include "frontier.cuh"
 #include "hot.cuh"
 #include "impl.hpp"
@@ -42,6 +44,9 @@ Workspace* ensure_ws(Graph* g) {
   ws->status_len = ws->compact_tiles + 1;
   ws->status.alloc((size_t)ws->status_len * 8, s);
   ws->ctl.alloc(sizeof(Ctl), s);
+  ws->bar.alloc(BAR_WORDS * 4, s);
+  GFB_CUDA(cudaMemsetAsync(ws->bar.p, 0, BAR_WORDS * 4, s));
+  ws->bsp_tot.alloc(16, s);
   GFB_CUDA(cudaMallocHost(&ws->ctl_host, sizeof(Ctl)));
   g->ws = std::move(ws);
   return g->ws.get();
@@ -123,7 +128,28 @@ struct Runner {
   void pull_launch(cudaStream_t st) {
     uint32_t ntiles = (g->pull_total + HotCfg<W>::TILE - 1) / HotCfg<W>::TILE;
     uint32_t grid = std::min<uint32_t>(std::max<uint32_t>(ntiles, 1), c->num_sms * 4);
-    k_pull_relax<W><<<grid, H_BLOCK, 0, st>>>(args(true), g->pull_total, g->pull_k);
+    if constexpr (sizeof(D) == 4) {
+      if (key_mode()) {
+        k_pull_relax<W, true><<<grid, H_BLOCK, 0, st>>>(args(true), g->pull_total, g->pull_k);
+        return;
+      }
+    }
+    k_pull_relax<W, false><<<grid, H_BLOCK, 0, st>>>(args(true), g->pull_total, g->pull_k);
+  }
+
+  // Packed (dist, pred) keys with fire-and-forget reductions (k_push_range)
+  // for 32-bit distances; the {u, edge} record path for f64 and the legacy
+  // experiment kernels.
+  bool key_mode() const {
+    return sizeof(D) == 4 && variant != 1 && variant != 2 && variant != 4 && variant != 6 &&
+           variant != 10;
+  }
+
+  template <int VT, int MINB, int TILE, int OPT = 0>
+  void range_launch(cudaStream_t st) {
+    if constexpr (sizeof(D) == 4) {
+      k_push_range<W, VT, MINB, TILE, OPT><<<c->num_sms * MINB, 256, 0, st>>>(args(false));
+    }
   }
 
   // total == UINT32_MAX: unknown on the host (device loop) -> full grid
@@ -139,7 +165,112 @@ struct Runner {
         break;
       }
       case 6: warp_launch<4, 8>(st, total, full); break;
-      default: warp_launch<(sizeof(W) == 8 ? 4 : 8), 4>(st, total, full);
+      case 10: warp_launch<(sizeof(W) == 8 ? 4 : 8), 4>(st, total, full); break;
+      case 8: range_launch<4, 8, 0>(st); break;
+      case 9: range_launch<8, 4, 0>(st); break;
+      case 11: range_launch<8, 4, 256>(st); break;
+      case 12: range_launch<8, 4, 512>(st); break;
+      case 13: range_launch<8, 4, 1024>(st); break;
+      case 14: range_launch<4, 8, 512>(st); break;
+      case 15: range_launch<8, 4, 2048>(st); break;
+      case 16: range_launch<4, 8, 256>(st); break;
+      case 17: range_launch<4, 8, 1024>(st); break;
+      case 18: range_launch<2, 8, 512>(st); break;
+      case 19: range_launch<4, 6, 512>(st); break;
+      case 20: range_launch<2, 8, 256>(st); break;
+      case 21: range_launch<6, 5, 768>(st); break;
+      case 22: range_launch<2, 8, 256, 3>(st); break;
+      case 23: range_launch<2, 8, 256, 11>(st); break;
+      case 24: range_launch<2, 8, 128, 1>(st); break;
+      case 25: range_launch<1, 8, 128, 1>(st); break;
+      default:  // measured best at RMAT s24 (profiles/r01_variants_s24.txt)
+        if (key_mode()) range_launch<2, 8, 256, 1>(st);
+        else warp_launch<(sizeof(W) == 8 ? 4 : 8), 4>(st, total, full);
+    }
+  }
+
+  // The persistent single-launch loop (bsp.cuh) for 32-bit distances.
+  template <int VT, int TILE, int OPT = 0>
+  bool bsp_launch(int dir, float alpha) {
+    if constexpr (sizeof(D) == 4) {
+      auto kern = k_bsp<W, VT, TILE, OPT>;
+      int per_sm = 0;
+      GFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, B_THREADS, 0));
+      if (per_sm <= 0) return false;
+      const uint32_t grid = (uint32_t)std::min(per_sm, 2) * c->num_sms;
+      const uint64_t wpc = ((uint64_t)nwords + grid - 1) / grid;
+      if ((wpc + F_WPW - 1) / F_WPW > (uint64_t)B_MAX_GROUPS) return false;  // graph loop instead
+      BspArgs<W> b{};
+      b.push = args(false);
+      b.pull = args(true);
+      ensure_nz(g);
+      if (ws->bsp_agg.bytes < (size_t)grid * 8) {
+        ws->bsp_agg.alloc((size_t)grid * 8, s);
+        ws->bsp_flag.alloc((size_t)grid * 4, s);
+      }
+      b.ro = g->ro.as<uint32_t>();
+      b.nz = g->nz.as<uint32_t>();
+      b.agg_flag = ws->bsp_flag.as<unsigned>();
+      b.totals = ws->bsp_tot.as<uint2>();
+      b.bm_cur = ws->bm_cur.as<uint32_t>();
+      b.n = n;
+      b.nwords = nwords;
+      b.m = (uint32_t)g->m;
+      b.pull_total = g->pull_total;
+      b.pull_k = g->pull_k;
+      b.agg = ws->bsp_agg.as<uint2>();
+      b.bar = ws->bar.as<unsigned>();
+      b.src_ptr = ws->src_dev.as<uint32_t>();
+      b.alpha = alpha;
+      b.can_pull = dir == GFB_DIR_AUTO && g->has_csc ? 1 : 0;
+      b.force_pull = dir == GFB_DIR_PULL ? 1 : 0;
+      const char* tr = getenv("GFB_TRACE");
+      DBuf trace;
+      if (tr && tr[0] == '1') {
+        b.trace_cap = 4096;
+        trace.alloc(b.trace_cap * 8, s);
+        GFB_CUDA(cudaMemsetAsync(trace.p, 0, b.trace_cap * 8, s));
+        b.trace = trace.as<unsigned long long>();
+      }
+      void* params[] = {&b};
+      GFB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, grid, B_THREADS, params, 0, s));
+      kernels += 1;
+      if (b.trace) {  // per-phase device times (instrumentation only)
+        std::vector<unsigned long long> h(b.trace_cap);
+        GFB_CUDA(cudaMemcpyAsync(h.data(), trace.p, b.trace_cap * 8, cudaMemcpyDeviceToHost, s));
+        c->sync();
+        double sum[4] = {0, 0, 0, 0};
+        for (uint32_t i = 1; i < b.trace_cap && h[i]; ++i) {
+          double us = ((h[i] >> 2) - (h[i - 1] >> 2)) * 1e-3;
+          int tag = (int)(h[i] & 3);
+          sum[tag] += us;
+          fprintf(stderr, "[gfb bsp] %s %.1f us\n",
+                  tag == 1 ? "compact" : "advance", us);
+        }
+        fprintf(stderr, "[gfb bsp] grid %u: compact %.1f us, advance %.1f us\n", grid, sum[1],
+                sum[3]);
+      }
+      return true;
+    }
+    return false;
+  }
+
+  // The persistent single-launch loop is kept as an experiment (variants >= 30):
+  // at s24 its compaction/advance latency chains cost more than the graph
+  // loop's launches (tools/variants.py).
+  bool persistent() const { return key_mode() && variant >= 30; }
+
+  bool bsp_run(int dir, float alpha) {
+    switch (variant) {
+      case 31: return bsp_launch<4, 512>(dir, alpha);
+      case 32: return bsp_launch<2, 512>(dir, alpha);
+      case 33: return bsp_launch<4, 256>(dir, alpha);
+      case 34: return bsp_launch<2, 256, 1>(dir, alpha);
+      case 35: return bsp_launch<2, 256, 3>(dir, alpha);
+      case 36: return bsp_launch<2, 256, 7>(dir, alpha);
+      case 37: return bsp_launch<2, 256, 11>(dir, alpha);
+      case 38: return bsp_launch<2, 256, 5>(dir, alpha);
+      default: return bsp_launch<2, 256>(dir, alpha);
     }
   }
 
@@ -239,7 +370,10 @@ struct Runner {
     uint64_t launches = 0;
     float adv_ms = 0;
     GFB_CUDA(cudaEventRecord(c->ev[0], s));
-    if (o->device_loop) {
+    bool done = false;
+    if (o->device_loop && persistent()) done = bsp_run(dir, alpha);
+    if (done) {
+    } else if (o->device_loop) {
       int key[3] = {dir, (int)(alpha * 1000), variant};
       if (!ws->loop_exec || memcmp(key, ws->loop_key, sizeof(key)) != 0) {
         GFB_CUDA(cudaStreamSynchronize(s));
@@ -284,7 +418,7 @@ struct Runner {
     if (h.err & 1u) fail(GFB_ERANGE, "sssp: u32 distance overflow (use f64 weights)");
     float ms = 0;
     GFB_CUDA(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
-    if (o->device_loop) kernels += 4 + 4ull * h.supersteps;
+    if (o->device_loop && !done) kernels += 4 + 4ull * h.supersteps;
     ws->has_result = true;
     ws->source = source;
     if (st) {
@@ -305,7 +439,10 @@ struct Runner {
   void pred_pass(uint32_t source, bool want, uint64_t* fallback) {
     GFB_CUDA(cudaMemsetAsync(ws->repair_bm.p, 0, (size_t)nwords * 4, s));
     GFB_CUDA(cudaMemsetAsync(&ws->ctl.as<Ctl>()->flag, 0, 4, s));
-    k_pred_verify<W><<<c->num_sms * 8, 256, 0, s>>>(
+    auto verify = k_pred_verify<W, false>;
+    if constexpr (sizeof(D) == 4)
+      if (key_mode()) verify = k_pred_verify<W, true>;
+    verify<<<c->num_sms * 8, 256, 0, s>>>(
         g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(),
         g->has_csc ? g->co.as<uint32_t>() : nullptr,
         g->has_csc ? g->cadj.as<EdgeRec<W>>() : nullptr, ws->dist.as<D>(),
