@@ -53,6 +53,11 @@ struct Graph {
   DBuf stage;                     // upload staging, kept for refills
   DBuf nz;                        // bit v: out-degree(v) > 0 (ensure_nz, bsp.cuh)
   bool nz_valid = false;
+  // In-degree-ordered copy of the CSR used inside the SSSP loop (ensure_relabel):
+  // new id i = rank of vertex iperm[i] by descending in-degree, so the hot
+  // destinations share distance cache lines.  4-byte weights only.
+  DBuf rl_ro, rl_adj, rl_perm, rl_iperm;
+  bool rl_valid = false;
   // static pull plan (destinations with in-degree > 0)
   uint32_t pull_k = 0, pull_total = 0;
   DBuf pull_v, pull_off, pull_tseg;
@@ -97,6 +102,8 @@ struct Workspace {
   DBuf src_dev;    // the source vertex (read by k_init)
   DBuf bar;        // grid barrier of the persistent loop (bsp.cuh)
   DBuf bsp_agg, bsp_flag, bsp_tot;  // its per-CTA frontier aggregates / totals
+  DBuf dist_int, pkey_int;          // loop state in relabelled ids (ensure_relabel)
+  DBuf nf_q, nf_bm, nf_cnt;         // near-far queues / bitmaps / counters (nearfar.cuh)
   uint32_t ftiles = 0;
   // device loop: one instantiated CUDA graph per (direction, alpha, variant)
   cudaGraphExec_t loop_exec = nullptr;
@@ -133,6 +140,7 @@ void build_csc(Graph* g);
 void ensure_ceid(Graph* g);
 void build_pull_plan(Graph* g);
 void ensure_nz(Graph* g);
+void ensure_relabel(Graph* g);
 // sssp.cu
 void sssp_run(Ctx* ctx, Graph* g, uint32_t source, const gfb_sssp_opts* o, gfb_sssp_stats* st);
 void sssp_read(Graph* g, double* dist, void* dist_native, uint32_t* pred);

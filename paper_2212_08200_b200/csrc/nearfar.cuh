@@ -1,0 +1,223 @@
+// nearfar.cuh -- SSSP with a near-far filter (delta > 0) as ONE persistent
+// cooperative kernel with queue frontiers: the high-diameter path (BASELINE
+// configs[3], the 4096^2 grid: 8.5K BSP supersteps at ~215 relaxations per
+// edge).
+//
+// Same operators as the BSP loop (algorithms.hpp:586-602): advance + relax
+// over the frontier, a filter on the output, loop until empty.  The filter
+// splits the improved vertices at a distance threshold (the
+// near-far work-efficient variant of Davidson et al.):
+//
+//   near phase   expand the near queue; an improved v goes to the next near
+//                queue when its new distance < thr, else to the far pile
+//                (bitmap dedup + warp-aggregated appends)        | grid sync
+//   split phase  (near queue empty) min over the live far pile   | grid sync
+//                thr = min + delta; far entries below thr move to the near
+//                queue, the rest are compacted; stale entries    | grid sync
+//                (dist < old thr: already expanded) are dropped
+//
+// The fixpoint is the same as the BSP loop's (a label-correcting order
+// change only), so distances are bit-identical; predecessors use the packed
+// (dist, u) keys of k_push_range.  One launch; a phase costs one grid barrier
+// (1.3 us, tools/microbench_barrier.cu) plus its work, instead of four
+// kernel launches per superstep.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "hot.cuh"
+
+namespace gfb {
+
+namespace cgn = cooperative_groups;
+
+constexpr int NF_THREADS = 1024;
+
+template <class W>
+struct NfArgs {
+  using D = typename DT<W>::D;
+  const uint32_t* ro;
+  const EdgeRec<W>* adj;
+  D* dist;
+  unsigned long long* pkey;
+  uint32_t* nq[2];       // near queues (capacity n)
+  uint32_t* fq[2];       // far piles (capacity n)
+  uint32_t* nbm[2];      // near-queue membership bitmaps (parity of the producing phase)
+  uint32_t* fbm;         // far-pile membership bitmap
+  uint32_t* cnt;         // [0..2] near counts (rotating), [3..4] far counts, [5..6] min-far bits
+  Ctl* ctl;
+  const uint32_t* src_ptr;
+  uint32_t n, nwords;
+  D delta;
+};
+
+__device__ __forceinline__ uint32_t dbits(float x) { return __float_as_uint(x); }
+__device__ __forceinline__ uint32_t dbits(uint32_t x) { return x; }
+template <class D> __device__ __forceinline__ D dfrom(uint32_t b);
+template <> __device__ __forceinline__ float dfrom<float>(uint32_t b) { return __uint_as_float(b); }
+template <> __device__ __forceinline__ uint32_t dfrom<uint32_t>(uint32_t b) { return b; }
+
+// Append v to queue q (count *c) if this lane's flag is set: one atomicAdd per
+// warp (ballot + popc), then each lane writes its own slot.
+__device__ __forceinline__ void warp_append(bool flag, uint32_t v, uint32_t* q, uint32_t* c) {
+  const unsigned m = __ballot_sync(0xffffffffu, flag);
+  if (m == 0) return;
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(c, (uint32_t)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (flag) q[base + __popc(m & lanemask_lt())] = v;
+}
+
+// Set v's bit; true when this call set it (first activation).
+__device__ __forceinline__ bool claim_bit(uint32_t* bm, uint32_t v) {
+  const uint32_t bit = 1u << (v & 31);
+  return (atomicOr(bm + (v >> 5), bit) & bit) == 0;
+}
+
+template <class W>
+__global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
+  using D = typename DT<W>::D;
+  static_assert(sizeof(D) == 4, "packed predecessor keys need 32-bit distances");
+  cgn::grid_group grid = cgn::this_grid();
+  const int lane = threadIdx.x & 31;
+  const uint32_t gtid = blockIdx.x * NF_THREADS + threadIdx.x;
+  const uint32_t gthreads = gridDim.x * NF_THREADS;
+  const uint32_t gwarp = gtid >> 5, nwarps = gthreads >> 5;
+  unsigned* err = &a.ctl->err;
+
+  // ---- init (algorithms.hpp:579-583): dist, keys, bitmaps, queues ----
+  const uint32_t source = *a.src_ptr;
+  for (uint32_t i = gtid; i < a.n; i += gthreads) {
+    a.dist[i] = i == source ? D(0) : dinf<W>();
+    a.pkey[i] = ~0ull;
+  }
+  for (uint32_t i = gtid; i < a.nwords; i += gthreads) {
+    a.nbm[0][i] = (source >> 5) == i ? (1u << (source & 31)) : 0u;
+    a.nbm[1][i] = 0;
+    a.fbm[i] = 0;
+  }
+  if (gtid == 0) {
+    Ctl c0 = {};
+    *a.ctl = c0;
+    a.nq[0][0] = source;
+    a.cnt[0] = 1;
+    a.cnt[1] = a.cnt[2] = a.cnt[3] = a.cnt[4] = 0;
+    a.cnt[5] = a.cnt[6] = 0xFFFFFFFFu;
+  }
+  grid.sync();
+
+  D thr = a.delta;  // near: dist < thr
+  uint32_t fp = 0, mp = 0;
+  unsigned long long relax = 0;
+  uint32_t phases = 0;
+  for (uint32_t ph = 0;; ++ph) {
+    const uint32_t cur = ph & 1, nxt = cur ^ 1;
+    const uint32_t K = __ldcg(a.cnt + ph % 3);
+    uint32_t* qin = a.nq[cur];
+    uint32_t* qout = a.nq[nxt];
+    uint32_t* cout = a.cnt + (ph + 1) % 3;
+    if (gtid == 0) a.cnt[(ph + 2) % 3] = 0;  // the count two phases ahead
+    if (K > 0) {
+      // ---------------- near phase: expand the near queue ----------------
+      ++phases;
+      for (uint32_t base = gwarp * 32; base < K; base += nwarps * 32) {
+        // lane j holds queue entry base+j: vertex, row, degree, distance
+        const uint32_t j = base + lane;
+        uint32_t u = 0, st = 0, deg = 0;
+        D du = D(0);
+        if (j < K) {
+          u = __ldcg(qin + j);
+          atomicAnd(a.nbm[cur] + (u >> 5), ~(1u << (u & 31)));  // leaves the queue
+          st = a.ro[u];
+          deg = a.ro[u + 1] - st;
+          du = __ldcg(a.dist + u);
+        }
+        const uint32_t incl = warp_incl_scan(deg, lane);
+        const uint32_t off = incl - deg;  // first chunk edge of this lane's vertex
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        relax += lane == 0 ? tot : 0;
+        for (uint32_t x = 0; x < tot; x += 32) {
+          const uint32_t le = x + lane;
+          int lo = 0;  // owner lane: the first whose inclusive degree exceeds le
+#pragma unroll
+          for (int step = 16; step >= 1; step >>= 1) {
+            const uint32_t p = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+            if (p <= le) lo += step;
+          }
+          const uint32_t ost = __shfl_sync(0xffffffffu, st, lo);
+          const uint32_t ooff = __shfl_sync(0xffffffffu, off, lo);
+          const uint32_t ou = __shfl_sync(0xffffffffu, u, lo);
+          const D odu = shfl_d(du, lo);
+          bool to_near = false, to_far = false;
+          uint32_t v = 0;
+          if (le < tot) {
+            const EdgeRec<W> rec = ld_rec(a.adj + ost + (le - ooff));
+            v = rec.v;
+            const D nd = dadd(odu, rec.w, err);
+            if (nd < __ldcg(a.dist + v)) {
+              red_min_u32(reinterpret_cast<unsigned*>(a.dist + v), dbits(nd));
+              red_min_u64(a.pkey + v, pred_key(nd, ou));
+              if (nd < thr) to_near = claim_bit(a.nbm[nxt], v);
+              else to_far = claim_bit(a.fbm, v);
+            }
+          }
+          warp_append(to_near, v, qout, cout);
+          warp_append(to_far, v, a.fq[fp], a.cnt + 3 + fp);
+        }
+      }
+      grid.sync();
+      continue;
+    }
+    // ---------------- split phase: refill the near queue from the far pile ----
+    const uint32_t F = __ldcg(a.cnt + 3 + fp);
+    uint32_t* fin = a.fq[fp];
+    // pass 1: minimum live far distance (entries below thr are stale)
+    uint32_t mloc = 0xFFFFFFFFu;
+    for (uint32_t i = gtid; i < F; i += gthreads) {
+      const D dv = __ldcg(a.dist + __ldcg(fin + i));
+      if (!(dv < thr)) mloc = min(mloc, dbits(dv));
+    }
+    for (int d = 16; d > 0; d >>= 1) mloc = min(mloc, __shfl_xor_sync(0xffffffffu, mloc, d));
+    if (lane == 0 && mloc != 0xFFFFFFFFu) atomicMin(a.cnt + 5 + mp, mloc);
+    if (gtid == 0) {
+      a.cnt[3 + (fp ^ 1)] = 0;
+      a.cnt[5 + (mp ^ 1)] = 0xFFFFFFFFu;
+    }
+    grid.sync();
+    const uint32_t mbits = __ldcg(a.cnt + 5 + mp);
+    if (mbits == 0xFFFFFFFFu) break;  // far pile empty or all stale: converged
+    const D old_thr = thr;
+    const D mfar = dfrom<D>(mbits);
+    thr = dadd(mfar, a.delta, nullptr);
+    if (!(mfar < thr)) thr = dinf<W>();  // delta absorbed by rounding: take everything
+    // pass 2: split the far pile
+    for (uint32_t b0 = gwarp * 32; b0 < F; b0 += nwarps * 32) {
+      const uint32_t i = b0 + lane;
+      uint32_t v = 0;
+      bool near = false, keep = false;
+      if (i < F) {
+        v = __ldcg(fin + i);
+        const D dv = __ldcg(a.dist + v);
+        if (dv < thr) {
+          atomicAnd(a.fbm + (v >> 5), ~(1u << (v & 31)));
+          near = !(dv < old_thr) && claim_bit(a.nbm[nxt], v);
+        } else {
+          keep = true;
+        }
+      }
+      warp_append(near, v, qout, cout);
+      warp_append(keep, v, a.fq[fp ^ 1], a.cnt + 3 + (fp ^ 1));
+    }
+    fp ^= 1;
+    mp ^= 1;
+    grid.sync();
+  }
+  if (relax) atomicAdd(&a.ctl->relax, relax);
+  if (gtid == 0) {
+    a.ctl->supersteps = phases;
+    a.ctl->push_steps = phases;
+  }
+}
+
+}  // namespace gfb

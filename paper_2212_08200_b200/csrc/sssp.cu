@@ -5,9 +5,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "bsp.cuh"
+#include "nearfar.cuh"
 #include "frontier.cuh"
 #include "hot.cuh"
 #include "impl.hpp"
@@ -52,6 +54,23 @@ Workspace* ensure_ws(Graph* g) {
   return g->ws.get();
 }
 
+// Relabelled loop state -> caller ids: dist[v] = dist_int[perm[v]], and the
+// predecessor key's vertex half mapped back through iperm.
+template <class D>
+__global__ void k_unpermute(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ iperm,
+                            const D* __restrict__ dist_int,
+                            const unsigned long long* __restrict__ key_int, D* dist,
+                            unsigned long long* key, uint32_t n) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint32_t i = perm[v];
+    dist[v] = dist_int[i];
+    unsigned long long k = key_int[i];
+    const uint32_t u = (uint32_t)k;
+    if (u != NIL) k = (k & 0xFFFFFFFF00000000ull) | iperm[u];
+    key[v] = k;
+  }
+}
+
 template <class W>
 struct Runner {
   using D = typename DT<W>::D;
@@ -62,6 +81,11 @@ struct Runner {
   uint32_t n, nwords;
   uint64_t kernels = 0;
   int variant = 0;  // experimental kernel shape (opts.reserved[0])
+  bool rl = false;  // loop runs on the in-degree-relabelled CSR (ensure_relabel)
+
+  const uint32_t* lro() const { return rl ? g->rl_ro.as<uint32_t>() : g->ro.as<uint32_t>(); }
+  D* ldist() const { return rl ? ws->dist_int.as<D>() : ws->dist.as<D>(); }
+  uint2* lpred() const { return rl ? ws->pkey_int.as<uint2>() : ws->predrec.as<uint2>(); }
 
   Plan plan() const {
     return Plan{ws->pv.as<uint32_t>(), ws->pstart.as<uint32_t>(), ws->poff.as<uint32_t>(),
@@ -74,10 +98,11 @@ struct Runner {
 
   AdvArgs<W> args(bool pull) const {
     AdvArgs<W> a{};
-    a.adj = pull ? g->cadj.as<EdgeRec<W>>() : g->adj.as<EdgeRec<W>>();
+    a.adj = pull ? g->cadj.as<EdgeRec<W>>()
+                 : (rl ? g->rl_adj.as<EdgeRec<W>>() : g->adj.as<EdgeRec<W>>());
     a.ceid = g->ceid.as<uint32_t>();
-    a.dist = ws->dist.as<D>();
-    a.predrec = ws->predrec.as<uint2>();
+    a.dist = ldist();
+    a.predrec = lpred();
     a.plan = pull ? pull_plan() : plan();
     a.ctl = ws->ctl.as<Ctl>();
     a.bm_out = ws->bm_next.as<uint32_t>();
@@ -92,14 +117,14 @@ struct Runner {
   void compact(int dir, float alpha, cudaGraphConditionalHandle hloop,
                cudaGraphConditionalHandle hmode, bool set_loop, bool set_mode) {
     const uint32_t tiles = ws->ftiles;
-    k_fcount<<<tiles, F_WARPS * 32, 0, s>>>(g->ro.as<uint32_t>(), ws->bm_next.as<uint32_t>(),
+    k_fcount<<<tiles, F_WARPS * 32, 0, s>>>(lro(), ws->bm_next.as<uint32_t>(),
                                             nwords, ws->agg.as<uint2>());
     k_fscan<<<1, F_SCAN_THREADS, 0, s>>>(ws->agg.as<uint2>(), tiles, plan(), ws->ctl.as<Ctl>(),
                                          (uint32_t)g->m, alpha,
                                          dir == GFB_DIR_AUTO && g->has_csc ? 1 : 0,
                                          dir == GFB_DIR_PULL ? 1 : 0, hloop, hmode,
                                          set_loop ? 1 : 0, set_mode ? 1 : 0);
-    k_fwrite<<<tiles, F_WARPS * 32, 0, s>>>(g->ro.as<uint32_t>(), ws->bm_next.as<uint32_t>(),
+    k_fwrite<<<tiles, F_WARPS * 32, 0, s>>>(lro(), ws->bm_next.as<uint32_t>(),
                                             ws->bm_cur.as<uint32_t>(), nwords,
                                             ws->agg.as<uint2>(), plan());
     GFB_CUDA(cudaGetLastError());
@@ -258,7 +283,7 @@ struct Runner {
   // The persistent single-launch loop is kept as an experiment (variants >= 30):
   // at s24 its compaction/advance latency chains cost more than the graph
   // loop's launches (tools/variants.py).
-  bool persistent() const { return key_mode() && variant >= 30; }
+  bool persistent() const { return key_mode() && variant >= 30 && variant < 40; }
 
   bool bsp_run(int dir, float alpha) {
     switch (variant) {
@@ -274,8 +299,50 @@ struct Runner {
     }
   }
 
+  // Near-far filter (opts.delta > 0): one persistent launch (nearfar.cuh).
+  bool nearfar_launch(double delta) {
+    if constexpr (sizeof(D) == 4) {
+      auto kern = k_nearfar<W>;
+      int per_sm = 0;
+      GFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NF_THREADS, 0));
+      if (per_sm <= 0) return false;
+      const uint32_t grid = (uint32_t)std::min(per_sm, 2) * c->num_sms;
+      if (ws->nf_q.bytes < (size_t)n * 16) {
+        ws->nf_q.alloc((size_t)n * 16, s);
+        ws->nf_bm.alloc((size_t)nwords * 12, s);
+        ws->nf_cnt.alloc(64, s);
+      }
+      NfArgs<W> a{};
+      a.ro = g->ro.as<uint32_t>();
+      a.adj = g->adj.as<EdgeRec<W>>();
+      a.dist = ws->dist.as<D>();
+      a.pkey = ws->predrec.as<unsigned long long>();
+      uint32_t* q = ws->nf_q.as<uint32_t>();
+      a.nq[0] = q;
+      a.nq[1] = q + n;
+      a.fq[0] = q + 2 * (size_t)n;
+      a.fq[1] = q + 3 * (size_t)n;
+      uint32_t* bm = ws->nf_bm.as<uint32_t>();
+      a.nbm[0] = bm;
+      a.nbm[1] = bm + nwords;
+      a.fbm = bm + 2 * (size_t)nwords;
+      a.cnt = ws->nf_cnt.as<uint32_t>();
+      a.ctl = ws->ctl.as<Ctl>();
+      a.src_ptr = ws->src_dev.as<uint32_t>();
+      a.n = n;
+      a.nwords = nwords;
+      if constexpr (std::is_same<D, float>::value) a.delta = (float)delta;
+      else a.delta = (D)std::min(std::max(std::llround(delta), 1ll), 0xFFFFFFFEll);
+      void* params[] = {&a};
+      GFB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, grid, NF_THREADS, params, 0, s));
+      kernels += 1;
+      return true;
+    }
+    return false;
+  }
+
   void init_launch() {
-    k_init<W><<<stride_grid(c), 256, 0, s>>>(ws->dist.as<D>(), ws->predrec.as<uint2>(),
+    k_init<W><<<stride_grid(c), 256, 0, s>>>(ldist(), lpred(),
                                              ws->bm_next.as<uint32_t>(), ws->bm_cur.as<uint32_t>(),
                                              n, nwords, ws->src_dev.as<uint32_t>(),
                                              ws->ctl.as<Ctl>());
@@ -365,13 +432,31 @@ struct Runner {
     variant = o->reserved[0];
     const int dir = o->direction;
     const float alpha = o->pull_alpha > 0 ? o->pull_alpha : 0.25f;
+    // The relabelled CSR has no CSC: only when no superstep can pull (the
+    // AUTO switch needs frontier edges > m / alpha, impossible for alpha <= 1).
+    rl = key_mode() && variant == 41 &&
+         (dir == GFB_DIR_PUSH || (dir == GFB_DIR_AUTO && (alpha <= 1.0f || !g->has_csc)));
+    if (rl) {
+      ensure_relabel(g);
+      if (ws->dist_int.bytes < (size_t)n * sizeof(D)) {
+        ws->dist_int.alloc((size_t)n * sizeof(D), s);
+        ws->pkey_int.alloc((size_t)n * 8, s);
+      }
+    }
     // source -> device (pinned staging in ctl_host's slot)
     GFB_CUDA(cudaMemcpyAsync(ws->src_dev.p, &source, 4, cudaMemcpyHostToDevice, s));
+    if (rl)
+      GFB_CUDA(cudaMemcpyAsync(ws->src_dev.p, g->rl_perm.as<uint32_t>() + source, 4,
+                               cudaMemcpyDeviceToDevice, s));
     uint64_t launches = 0;
     float adv_ms = 0;
     GFB_CUDA(cudaEventRecord(c->ev[0], s));
     bool done = false;
-    if (o->device_loop && persistent()) done = bsp_run(dir, alpha);
+    if (o->delta > 0 && key_mode() && !rl) {
+      if (dir == GFB_DIR_PULL) fail(GFB_EINVAL, "sssp: the near-far filter (delta > 0) is push-only");
+      done = nearfar_launch(o->delta);
+    }
+    if (!done && o->device_loop && persistent()) done = bsp_run(dir, alpha);
     if (done) {
     } else if (o->device_loop) {
       int key[3] = {dir, (int)(alpha * 1000), variant};
@@ -409,6 +494,15 @@ struct Runner {
           fprintf(stderr, "[gfb] superstep %llu %s frontier=%u edges=%u advance=%.3f ms (%.1f G edges/s)\n",
                   (unsigned long long)launches, h.mode ? "pull" : "push", h.k, h.total, ms,
                   (h.mode ? g->pull_total : h.total) / (ms * 1e-3) / 1e9);
+      }
+    }
+    if (rl) {  // back to the caller's vertex ids for the predecessor pass and reads
+      if constexpr (sizeof(D) == 4) {
+        k_unpermute<D><<<stride_grid(c), 256, 0, s>>>(
+            g->rl_perm.as<uint32_t>(), g->rl_iperm.as<uint32_t>(), ws->dist_int.as<D>(),
+            ws->pkey_int.as<unsigned long long>(), ws->dist.as<D>(),
+            ws->predrec.as<unsigned long long>(), n);
+        ++kernels;
       }
     }
     uint64_t fallback = 0;

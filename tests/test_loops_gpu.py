@@ -1,0 +1,119 @@
+"""GPU parity of the alternative loop drivers against the oracle.
+
+Every driver runs the same operators (advance + relax + filter until the
+frontier is empty, algorithms.hpp:586-602) in a different order, so they all
+reach the same unique fixpoint: distances must be bit-identical to the
+oracle (f32 restatement of reference_dijkstra, u32 = the reference's own
+integer arithmetic) and predecessor trees valid.
+
+  delta > 0     near-far filter, one persistent cooperative launch with
+                queue frontiers (nearfar.cuh) -- the high-diameter path
+  variant 41    BSP loop on the in-degree-relabelled CSR (ensure_relabel)
+  variant 3x    BSP loop as one persistent cooperative launch (bsp.cuh)
+  variant 10    the previous warp-tile push kernel with {u, edge} records
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2212_08200_b200 as gb
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(g, dist, pred, source=0, wtype="f32"):
+    ro, col, w = g.csr()
+    if wtype == "f32":
+        want, _ = O.dijkstra(g.num_vertices, ro, col, w, source, "f32")
+        assert np.array_equal(dist.astype(np.float32), want)
+        assert O.check_pred_tree(g.num_vertices, ro, col, w, dist.astype(np.float32), source,
+                                 pred) == -1
+    else:
+        want, _ = O.dijkstra(g.num_vertices, ro, col, w.astype(np.float64), source, "f64")
+        assert np.array_equal(dist, want)
+        assert O.check_pred_tree(g.num_vertices, ro, col, w.astype(np.float64), dist, source,
+                                 pred) == -1
+
+
+@pytest.mark.parametrize("delta", [0.25, 1.0, 8.0])
+def test_nearfar_grid(ctx, delta):
+    g = gb.grid(128, seed=1, transpose=True, ctx=ctx)
+    dist, pred, st = gb.sssp_stats(g, 0, delta=delta)
+    _check(g, dist, pred)
+    assert st.relaxations >= st.m_reach  # every reached edge relaxed at least once
+
+
+@pytest.mark.parametrize("delta", [0.01, 0.1, 1.0])
+def test_nearfar_rmat(ctx, delta):
+    g = gb.rmat(12, 16, seed=1, wtype="f32", transpose=True, ctx=ctx)
+    dist, pred, st = gb.sssp_stats(g, 0, delta=delta)
+    _check(g, dist, pred)
+
+
+def test_nearfar_u32_and_sources(ctx):
+    g = gb.rmat(12, 16, seed=2, wtype="u32", transpose=True, ctx=ctx)
+    for src in (0, 5, 1000):
+        dist, pred, st = gb.sssp_stats(g, src, delta=16)
+        _check(g, dist, pred, source=src, wtype="u32")
+
+
+def test_nearfar_corpus_f32(ctx):
+    """acceptance.cpp:95-122 corpus graphs (G(n, 4/n), 10% zero weights)."""
+    corpus = np.load(os.path.join(os.path.dirname(__file__), "golden", "corpus.npz"))
+    for i in range(0, 200, 7):
+        n, seed = int(corpus["meta"][i][0]), int(corpus["meta"][i][1])
+        s, d, w = O.random_edges(n, seed)
+        g = gb.build_csr((s, d, w), n, wtype="f32", transpose=True, ctx=ctx)
+        dist, pred, st = gb.sssp_stats(g, 0, delta=2.0)
+        _check(g, dist, pred)
+
+
+def test_nearfar_rejects_pull(ctx):
+    g = gb.grid(16, seed=1, transpose=True, ctx=ctx)
+    with pytest.raises(ValueError):
+        gb.sssp_stats(g, 0, delta=1.0, direction="pull")
+
+
+@pytest.mark.parametrize("variant", [10, 30, 34, 41])
+def test_loop_variants_rmat(ctx, variant):
+    g = gb.rmat(14, 16, seed=1, wtype="f32", transpose=True, ctx=ctx)
+    dist, pred, st = gb.sssp_stats(g, 0, variant=variant)
+    _check(g, dist, pred)
+
+
+@pytest.mark.parametrize("variant", [30, 41])
+def test_loop_variants_u32_grid(ctx, variant):
+    g = gb.rmat(12, 16, seed=1, wtype="u32", transpose=True, ctx=ctx)
+    dist, pred, st = gb.sssp_stats(g, 0, variant=variant)
+    _check(g, dist, pred, wtype="u32")
+    g = gb.grid(64, seed=1, transpose=True, ctx=ctx)
+    dist, pred, st = gb.sssp_stats(g, 0, variant=variant)
+    _check(g, dist, pred)
+
+
+def test_relabel_view_is_permuted_csr(ctx):
+    """ensure_relabel: rows keyed by descending in-degree, contents mapped."""
+    import ctypes as C
+    from paper_2212_08200_b200 import _lib
+    g = gb.rmat(10, 16, seed=1, wtype="f32", transpose=True, ctx=ctx)
+    ro, col, w = g.csr()
+    n, m = g.num_vertices, g.num_edges
+    ro2 = np.zeros(n + 1, np.uint32)
+    adj = np.zeros(2 * m, np.uint32)
+    perm = np.zeros(n, np.uint32)
+    assert _lib.load().gfb_debug_relabel(g.h, C.c_void_p(ro2.ctypes.data),
+                                         C.c_void_p(adj.ctypes.data),
+                                         C.c_void_p(perm.ctypes.data)) == 0
+    indeg = np.bincount(col, minlength=n)
+    iperm = np.argsort(-indeg.astype(np.int64), kind="stable")
+    assert np.array_equal(perm[iperm], np.arange(n))
+    deg = np.diff(ro.astype(np.int64))
+    assert np.array_equal(ro2, np.concatenate([[0], np.cumsum(deg[iperm])]))
+    dst, ww = adj[0::2], adj[1::2].view(np.float32)
+    for i in range(0, n, 7):
+        p = iperm[i]
+        a = sorted(zip(perm[col[ro[p]:ro[p + 1]]].tolist(), w[ro[p]:ro[p + 1]].tolist()))
+        b = sorted(zip(dst[ro2[i]:ro2[i + 1]].tolist(), ww[ro2[i]:ro2[i + 1]].tolist()))
+        assert a == b

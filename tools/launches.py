@@ -16,7 +16,7 @@ def load(path):
             d = dict(zip(hdr, r))
             v = float(d["Metric Value"])
             u = d["Metric Unit"]
-            v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3,
+            v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "%": None,
                   "ms": 1e3, "second": 1e6, "s": 1e6}[u]
             data.append((d["Kernel Name"].split("(")[0].replace("void ", ""), v, d.get("Grid Size", "")))
     return data
