@@ -241,12 +241,14 @@ def run_ours(args):
         if tr.get("scale") == args.scale:
             traffic = tr.get("dram_bytes_per_launch")
 
-    # correctness spot-check of the timed configuration (size-independent
-    # property: no edge can still relax; cheap on the device result)
-    dist, pred = gb.sssp_read(g, native=True)
-
     # e2e through the public API with host buffers
     e2e = run_e2e(gb, ctx, g, args, kw)
+
+    # correctness of the timed configuration at full size (size-independent
+    # properties): no edge can still relax, reach counts match
+    check = fixpoint_check(gb, g, st)
+
+    secondary = [] if args.no_secondary else secondary_configs(gb, ctx, args)
 
     cpu = None
     if not args.no_cpu:
@@ -260,7 +262,7 @@ def run_ours(args):
         "e2e": e2e,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None, "traffic": traffic,
-                     "kernel": "k_advance_push/k_advance_pull",
+                     "kernel": "k_push_range (advance, hot.cuh)",
                      "bytes_per_visit": b_alg, "visits_per_step": ist.relaxations,
                      "advance_ms_per_step": ist.advance_ms,
                      "advance_launches_per_step": ist.advance_launches,
@@ -285,12 +287,69 @@ def run_ours(args):
         "relaxations": st.relaxations, "work_inflation": st.relaxations / m_reach,
         "push_steps": st.push_steps, "pull_steps": st.pull_steps,
         "pred_fallback": st.pred_fallback, "wall_s_timed": wall,
+        "fixpoint_check": check,
+        "secondary": secondary,
     }
     if cpu and cpu.get("value"):
         out["speedup_vs_cpu_best"] = gteps / cpu["value"]
         if e2e and e2e.get("value"):
             out["e2e_speedup_vs_cpu_best"] = e2e["value"] / cpu["value"]
     print(json.dumps(out))
+
+
+def fixpoint_check(gb, g, st):
+    """No edge can still relax (f32 arithmetic) and n_reach / m_reach agree."""
+    dist, _ = gb.sssp_read(g, native=True)
+    ro, col, w = g.csr()
+    deg = np.diff(ro.astype(np.int64))
+    bad = 0
+    chunk = 1 << 25
+    srcs = np.repeat(np.arange(len(deg), dtype=np.uint32), deg)
+    for e0 in range(0, len(col), chunk):
+        e1 = min(e0 + chunk, len(col))
+        du = dist[srcs[e0:e1]]
+        nd = (du + w[e0:e1]).astype(np.float32)
+        fin = np.isfinite(du)
+        bad += int(np.count_nonzero(dist[col[e0:e1]][fin] > nd[fin]))
+    reach = np.isfinite(dist)
+    ok = bad == 0 and int(reach.sum()) == st.n_reach and int(deg[reach].sum()) == st.m_reach
+    return {"ok": bool(ok), "edges_still_relaxable": bad,
+            "property": "dist[v] <= dist[u] + w for every edge; n_reach/m_reach recount"}
+
+
+def secondary_configs(gb, ctx, args):
+    """The other BASELINE.json configs as extra measurements (not the headline):
+    configs[1] RMAT s22 push-only, configs[3] 4096^2 grid (near-far filter vs
+    plain BSP, device-side convergence)."""
+    out = []
+
+    def timed(g, runs, **kw):
+        ms = []
+        for i in range(runs + 1):
+            _, _, st = gb.sssp_stats(g, 0, want_result=False, **kw)
+            if i:
+                ms.append(st.device_ms)
+        return statistics.median(ms), st
+
+    g = gb.rmat(22, args.edgefactor, seed=args.seed, wtype="f32", transpose=True, ctx=ctx)
+    ms, st = timed(g, 5, direction="push")
+    out.append({"config": "BASELINE configs[1]: RMAT s22 EF16 fp32, push-only",
+                "gteps": st.m_reach / (ms * 1e-3) / 1e9, "ms": ms, "supersteps": st.supersteps,
+                "work_inflation": st.relaxations / st.m_reach})
+    del g
+    side = args.grid_side
+    g = gb.grid(side, seed=args.seed, transpose=True, ctx=ctx)
+    ms, st = timed(g, 3, delta=args.grid_delta)
+    rec = {"config": f"BASELINE configs[3]: {side}^2 4-neighbour grid fp32 U[0,1), source 0 "
+                     f"(corner), near-far filter delta={args.grid_delta}, one persistent launch",
+           "gteps": st.m_reach / (ms * 1e-3) / 1e9, "ms": ms, "phases": st.supersteps,
+           "work_inflation": st.relaxations / st.m_reach}
+    bms, bst = timed(g, 1)
+    rec["bsp"] = {"ms": bms, "supersteps": bst.supersteps,
+                  "work_inflation": bst.relaxations / bst.m_reach,
+                  "gteps": bst.m_reach / (bms * 1e-3) / 1e9}
+    out.append(rec)
+    return out
 
 
 def run_e2e(gb, ctx, g, args, kw):
@@ -363,6 +422,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--soak", type=float, default=1.5, help="min warm-up seconds (clock samples)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--grid-side", type=int, default=4096)
+    ap.add_argument("--grid-delta", type=float, default=8.0)
     ap.add_argument("--partitioned", action="store_true",
                     help="force the 1-D partitioned NCCL path (default for N > 1)")
     args = ap.parse_args()

@@ -10,15 +10,17 @@
 //
 //   near phase   expand the near queue; an improved v goes to the next near
 //                queue when its new distance < thr, else to the far pile
-//                (bitmap dedup + warp-aggregated appends)        | grid sync
+//                (warp-aggregated appends of (v, dist) entries)  | grid sync
 //   split phase  (near queue empty) min over the live far pile   | grid sync
 //                thr = min + delta; far entries below thr move to the near
 //                queue, the rest are compacted; stale entries    | grid sync
-//                (dist < old thr: already expanded) are dropped
+//                (vertex lowered again since) are dropped
 //
 // The fixpoint is the same as the BSP loop's (a label-correcting order
 // change only), so distances are bit-identical; predecessors use the packed
-// (dist, u) keys of k_push_range.  One launch; a phase costs one grid barrier
+// (dist, u) keys of k_push_range.  A queue overflow (more activations in one
+// phase than the queue holds) flags ctl->err bit 1 and the host reruns the
+// call on the BSP loop.  One launch; a phase costs one grid barrier
 // (1.3 us, tools/microbench_barrier.cu) plus its work, instead of four
 // kernel launches per superstep.
 #pragma once
@@ -40,10 +42,9 @@ struct NfArgs {
   const EdgeRec<W>* adj;
   D* dist;
   unsigned long long* pkey;
-  uint32_t* nq[2];       // near queues (capacity n)
-  uint32_t* fq[2];       // far piles (capacity n)
-  uint32_t* nbm[2];      // near-queue membership bitmaps (parity of the producing phase)
-  uint32_t* fbm;         // far-pile membership bitmap
+  uint2* nq[2];          // near queues: (v, dist bits at activation)
+  uint2* fq[2];          // far piles, same entries
+  uint32_t cap;          // entries per queue; overflow sets ctl->err bit 1
   uint32_t* cnt;         // [0..2] near counts (rotating), [3..4] far counts, [5..6] min-far bits
   Ctl* ctl;
   const uint32_t* src_ptr;
@@ -57,24 +58,27 @@ template <class D> __device__ __forceinline__ D dfrom(uint32_t b);
 template <> __device__ __forceinline__ float dfrom<float>(uint32_t b) { return __uint_as_float(b); }
 template <> __device__ __forceinline__ uint32_t dfrom<uint32_t>(uint32_t b) { return b; }
 
-// Append v to queue q (count *c) if this lane's flag is set: one atomicAdd per
+// Append e to queue q (count *c) if this lane's flag is set: one atomicAdd per
 // warp (ballot + popc), then each lane writes its own slot.
-__device__ __forceinline__ void warp_append(bool flag, uint32_t v, uint32_t* q, uint32_t* c) {
+__device__ __forceinline__ void warp_append(bool flag, uint2 e, uint2* q, uint32_t* c,
+                                            uint32_t cap, unsigned* err) {
   const unsigned m = __ballot_sync(0xffffffffu, flag);
   if (m == 0) return;
   const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
   uint32_t base = 0;
   if (lane == leader) base = atomicAdd(c, (uint32_t)__popc(m));
   base = __shfl_sync(0xffffffffu, base, leader);
-  if (flag) q[base + __popc(m & lanemask_lt())] = v;
+  const uint32_t slot = base + __popc(m & lanemask_lt());
+  if (flag) {
+    if (slot < cap) q[slot] = e;
+    else atomicOr(err, 2u);
+  }
 }
 
-// Set v's bit; true when this call set it (first activation).
-__device__ __forceinline__ bool claim_bit(uint32_t* bm, uint32_t v) {
-  const uint32_t bit = 1u << (v & 31);
-  return (atomicOr(bm + (v >> 5), bit) & bit) == 0;
-}
-
+// Queue entries carry the distance that activated the vertex; an entry whose
+// vertex has since been lowered again is stale (the lowering appended a newer
+// entry) and is skipped -- dedup without a membership bitmap or a returning
+// atomic on the critical path.
 template <class W>
 __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
   using D = typename DT<W>::D;
@@ -86,21 +90,16 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
   const uint32_t gwarp = gtid >> 5, nwarps = gthreads >> 5;
   unsigned* err = &a.ctl->err;
 
-  // ---- init (algorithms.hpp:579-583): dist, keys, bitmaps, queues ----
+  // ---- init (algorithms.hpp:579-583) ----
   const uint32_t source = *a.src_ptr;
   for (uint32_t i = gtid; i < a.n; i += gthreads) {
     a.dist[i] = i == source ? D(0) : dinf<W>();
     a.pkey[i] = ~0ull;
   }
-  for (uint32_t i = gtid; i < a.nwords; i += gthreads) {
-    a.nbm[0][i] = (source >> 5) == i ? (1u << (source & 31)) : 0u;
-    a.nbm[1][i] = 0;
-    a.fbm[i] = 0;
-  }
   if (gtid == 0) {
     Ctl c0 = {};
     *a.ctl = c0;
-    a.nq[0][0] = source;
+    a.nq[0][0] = make_uint2(source, 0u);  // dist bits of +0.0 / 0u
     a.cnt[0] = 1;
     a.cnt[1] = a.cnt[2] = a.cnt[3] = a.cnt[4] = 0;
     a.cnt[5] = a.cnt[6] = 0xFFFFFFFFu;
@@ -113,9 +112,9 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
   uint32_t phases = 0;
   for (uint32_t ph = 0;; ++ph) {
     const uint32_t cur = ph & 1, nxt = cur ^ 1;
-    const uint32_t K = __ldcg(a.cnt + ph % 3);
-    uint32_t* qin = a.nq[cur];
-    uint32_t* qout = a.nq[nxt];
+    const uint32_t K = min(__ldcg(a.cnt + ph % 3), a.cap);
+    const uint2* qin = a.nq[cur];
+    uint2* qout = a.nq[nxt];
     uint32_t* cout = a.cnt + (ph + 1) % 3;
     if (gtid == 0) a.cnt[(ph + 2) % 3] = 0;  // the count two phases ahead
     if (K > 0) {
@@ -127,11 +126,13 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
         uint32_t u = 0, st = 0, deg = 0;
         D du = D(0);
         if (j < K) {
-          u = __ldcg(qin + j);
-          atomicAnd(a.nbm[cur] + (u >> 5), ~(1u << (u & 31)));  // leaves the queue
+          const uint2 e = __ldcg(qin + j);
+          u = e.x;
           st = a.ro[u];
-          deg = a.ro[u + 1] - st;
-          du = __ldcg(a.dist + u);
+          const uint32_t en = a.ro[u + 1];
+          const D cu = __ldcg(a.dist + u);
+          du = dfrom<D>(e.y);
+          deg = dbits(cu) == e.y ? en - st : 0u;  // stale entry: skip
         }
         const uint32_t incl = warp_incl_scan(deg, lane);
         const uint32_t off = incl - deg;  // first chunk edge of this lane's vertex
@@ -150,33 +151,33 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
           const uint32_t ou = __shfl_sync(0xffffffffu, u, lo);
           const D odu = shfl_d(du, lo);
           bool to_near = false, to_far = false;
-          uint32_t v = 0;
+          uint2 ent = make_uint2(0, 0);
           if (le < tot) {
             const EdgeRec<W> rec = ld_rec(a.adj + ost + (le - ooff));
-            v = rec.v;
             const D nd = dadd(odu, rec.w, err);
-            if (nd < __ldcg(a.dist + v)) {
-              red_min_u32(reinterpret_cast<unsigned*>(a.dist + v), dbits(nd));
-              red_min_u64(a.pkey + v, pred_key(nd, ou));
-              if (nd < thr) to_near = claim_bit(a.nbm[nxt], v);
-              else to_far = claim_bit(a.fbm, v);
+            if (nd < __ldcg(a.dist + rec.v)) {
+              red_min_u32(reinterpret_cast<unsigned*>(a.dist + rec.v), dbits(nd));
+              red_min_u64(a.pkey + rec.v, pred_key(nd, ou));
+              ent = make_uint2(rec.v, dbits(nd));
+              to_near = nd < thr;
+              to_far = !to_near;
             }
           }
-          warp_append(to_near, v, qout, cout);
-          warp_append(to_far, v, a.fq[fp], a.cnt + 3 + fp);
+          warp_append(to_near, ent, qout, cout, a.cap, err);
+          warp_append(to_far, ent, a.fq[fp], a.cnt + 3 + fp, a.cap, err);
         }
       }
       grid.sync();
       continue;
     }
     // ---------------- split phase: refill the near queue from the far pile ----
-    const uint32_t F = __ldcg(a.cnt + 3 + fp);
-    uint32_t* fin = a.fq[fp];
-    // pass 1: minimum live far distance (entries below thr are stale)
+    const uint32_t F = min(__ldcg(a.cnt + 3 + fp), a.cap);
+    const uint2* fin = a.fq[fp];
+    // pass 1: minimum live far distance
     uint32_t mloc = 0xFFFFFFFFu;
     for (uint32_t i = gtid; i < F; i += gthreads) {
-      const D dv = __ldcg(a.dist + __ldcg(fin + i));
-      if (!(dv < thr)) mloc = min(mloc, dbits(dv));
+      const uint2 e = __ldcg(fin + i);
+      if (dbits(__ldcg(a.dist + e.x)) == e.y) mloc = min(mloc, e.y);
     }
     for (int d = 16; d > 0; d >>= 1) mloc = min(mloc, __shfl_xor_sync(0xffffffffu, mloc, d));
     if (lane == 0 && mloc != 0xFFFFFFFFu) atomicMin(a.cnt + 5 + mp, mloc);
@@ -186,28 +187,24 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
     }
     grid.sync();
     const uint32_t mbits = __ldcg(a.cnt + 5 + mp);
-    if (mbits == 0xFFFFFFFFu) break;  // far pile empty or all stale: converged
-    const D old_thr = thr;
+    if (mbits == 0xFFFFFFFFu) break;  // no live far entry: converged
     const D mfar = dfrom<D>(mbits);
     thr = dadd(mfar, a.delta, nullptr);
     if (!(mfar < thr)) thr = dinf<W>();  // delta absorbed by rounding: take everything
-    // pass 2: split the far pile
+    // pass 2: live entries below thr -> near queue, the rest stay far
     for (uint32_t b0 = gwarp * 32; b0 < F; b0 += nwarps * 32) {
       const uint32_t i = b0 + lane;
-      uint32_t v = 0;
+      uint2 e = make_uint2(0, 0);
       bool near = false, keep = false;
       if (i < F) {
-        v = __ldcg(fin + i);
-        const D dv = __ldcg(a.dist + v);
-        if (dv < thr) {
-          atomicAnd(a.fbm + (v >> 5), ~(1u << (v & 31)));
-          near = !(dv < old_thr) && claim_bit(a.nbm[nxt], v);
-        } else {
-          keep = true;
+        e = __ldcg(fin + i);
+        if (dbits(__ldcg(a.dist + e.x)) == e.y) {
+          near = dfrom<D>(e.y) < thr;
+          keep = !near;
         }
       }
-      warp_append(near, v, qout, cout);
-      warp_append(keep, v, a.fq[fp ^ 1], a.cnt + 3 + (fp ^ 1));
+      warp_append(near, e, qout, cout, a.cap, err);
+      warp_append(keep, e, a.fq[fp ^ 1], a.cnt + 3 + (fp ^ 1), a.cap, err);
     }
     fp ^= 1;
     mp ^= 1;

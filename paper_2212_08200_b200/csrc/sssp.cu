@@ -307,9 +307,12 @@ struct Runner {
       GFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NF_THREADS, 0));
       if (per_sm <= 0) return false;
       const uint32_t grid = (uint32_t)std::min(per_sm, 2) * c->num_sms;
-      if (ws->nf_q.bytes < (size_t)n * 16) {
-        ws->nf_q.alloc((size_t)n * 16, s);
-        ws->nf_bm.alloc((size_t)nwords * 12, s);
+      // queue capacity: every activation appends one entry; a phase can
+      // activate at most min(m, n x in-degree) vertices -- size for 2n or m/4
+      const uint64_t cap64 = std::min<uint64_t>(std::max<uint64_t>(2ull * n, g->m / 4), 0xFFFFFFF0ull);
+      const uint32_t cap = (uint32_t)cap64;
+      if (ws->nf_q.bytes < (size_t)cap * 32) {
+        ws->nf_q.alloc((size_t)cap * 32, s);
         ws->nf_cnt.alloc(64, s);
       }
       NfArgs<W> a{};
@@ -317,15 +320,12 @@ struct Runner {
       a.adj = g->adj.as<EdgeRec<W>>();
       a.dist = ws->dist.as<D>();
       a.pkey = ws->predrec.as<unsigned long long>();
-      uint32_t* q = ws->nf_q.as<uint32_t>();
+      uint2* q = ws->nf_q.as<uint2>();
       a.nq[0] = q;
-      a.nq[1] = q + n;
-      a.fq[0] = q + 2 * (size_t)n;
-      a.fq[1] = q + 3 * (size_t)n;
-      uint32_t* bm = ws->nf_bm.as<uint32_t>();
-      a.nbm[0] = bm;
-      a.nbm[1] = bm + nwords;
-      a.fbm = bm + 2 * (size_t)nwords;
+      a.nq[1] = q + cap;
+      a.fq[0] = q + 2 * (size_t)cap;
+      a.fq[1] = q + 3 * (size_t)cap;
+      a.cap = cap;
       a.cnt = ws->nf_cnt.as<uint32_t>();
       a.ctl = ws->ctl.as<Ctl>();
       a.src_ptr = ws->src_dev.as<uint32_t>();
@@ -455,6 +455,7 @@ struct Runner {
     if (o->delta > 0 && key_mode() && !rl) {
       if (dir == GFB_DIR_PULL) fail(GFB_EINVAL, "sssp: the near-far filter (delta > 0) is push-only");
       done = nearfar_launch(o->delta);
+      if (done && (c->read_ctl(ws->ctl.as<Ctl>()).err & 2u)) done = false;  // queue overflow: BSP
     }
     if (!done && o->device_loop && persistent()) done = bsp_run(dir, alpha);
     if (done) {
