@@ -1,6 +1,8 @@
 // sssp.cu -- the device SSSP driver: sssp() of algorithms.hpp:569-623 as
 // init -> { advance (push | pull) -> compact } until the frontier is empty
 // -> predecessor pass, all on one CUDA stream.
+#include <cub/cub.cuh>
+
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -68,6 +70,39 @@ __global__ void k_unpermute(const uint32_t* __restrict__ perm, const uint32_t* _
     const uint32_t u = (uint32_t)k;
     if (u != NIL) k = (k & 0xFFFFFFFF00000000ull) | iperm[u];
     key[v] = k;
+  }
+}
+
+// ---- experiment (variant 42/43): reorder the plan by source distance ----
+template <class D>
+__global__ void k_plan_keys(const uint32_t* v, const D* dist, uint32_t* keys, uint32_t* idx,
+                            uint32_t K, int desc) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) {
+    uint32_t b = *reinterpret_cast<const uint32_t*>(dist + v[i]);
+    keys[i] = desc ? ~b : b;
+    idx[i] = i;
+  }
+}
+static __global__ void k_plan_permute(const uint32_t* idx, const uint32_t* v, const uint32_t* st,
+                                      const uint32_t* off, uint32_t* v2, uint32_t* s2,
+                                      uint32_t* deg, uint32_t K) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= K; i += gridDim.x * blockDim.x) {
+    if (i == K) {
+      deg[K] = 0;
+      continue;
+    }
+    const uint32_t j = idx[i];
+    v2[i] = v[j];
+    s2[i] = st[j];
+    deg[i] = off[j + 1] - off[j];
+  }
+}
+static __global__ void k_plan_tiles(Plan p, const uint32_t* deg, uint32_t K, uint32_t T) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x)
+    tile_map_entries(p, i, p.off[i], deg[i]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    uint32_t sb = (T + PLAN_GRAIN - 1) / PLAN_GRAIN;
+    if (sb < p.tseg_cap) p.tseg[sb] = K;
   }
 }
 
@@ -341,6 +376,34 @@ struct Runner {
     return false;
   }
 
+  void sort_plan(uint32_t K, uint32_t T, bool desc) {
+    if (K < 2) return;
+    DBuf keys, keys2, idx, idx2, v2, s2, deg, tmp;
+    keys.alloc((size_t)K * 4, s); keys2.alloc((size_t)K * 4, s);
+    idx.alloc((size_t)K * 4, s); idx2.alloc((size_t)K * 4, s);
+    v2.alloc((size_t)K * 4, s); s2.alloc((size_t)K * 4, s); deg.alloc((size_t)(K + 1) * 4, s);
+    Plan p = plan();
+    k_plan_keys<D><<<stride_grid(c), 256, 0, s>>>(p.v, ldist(), keys.as<uint32_t>(),
+                                                  idx.as<uint32_t>(), K, desc ? 1 : 0);
+    size_t tb = 0, tb2 = 0;
+    GFB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<uint32_t>(), keys2.as<uint32_t>(),
+                                             idx.as<uint32_t>(), idx2.as<uint32_t>(), (int64_t)K, 0,
+                                             32, s));
+    GFB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, deg.as<uint32_t>(), p.off, (int64_t)(K + 1), s));
+    tmp.alloc(std::max(tb, tb2), s);
+    GFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<uint32_t>(), keys2.as<uint32_t>(),
+                                             idx.as<uint32_t>(), idx2.as<uint32_t>(), (int64_t)K, 0,
+                                             32, s));
+    k_plan_permute<<<stride_grid(c), 256, 0, s>>>(idx2.as<uint32_t>(), p.v, p.start, p.off,
+                                                  v2.as<uint32_t>(), s2.as<uint32_t>(),
+                                                  deg.as<uint32_t>(), K);
+    GFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, deg.as<uint32_t>(), p.off, (int64_t)(K + 1), s));
+    GFB_CUDA(cudaMemcpyAsync(p.v, v2.p, (size_t)K * 4, cudaMemcpyDeviceToDevice, s));
+    GFB_CUDA(cudaMemcpyAsync(p.start, s2.p, (size_t)K * 4, cudaMemcpyDeviceToDevice, s));
+    k_plan_tiles<<<stride_grid(c), 256, 0, s>>>(p, deg.as<uint32_t>(), K, T);
+    GFB_CUDA(cudaGetLastError());
+  }
+
   void init_launch() {
     k_init<W><<<stride_grid(c), 256, 0, s>>>(ldist(), lpred(),
                                              ws->bm_next.as<uint32_t>(), ws->bm_cur.as<uint32_t>(),
@@ -479,6 +542,7 @@ struct Runner {
         Ctl h = c->read_ctl(ws->ctl.as<Ctl>());
         if (h.err & 1u) fail(GFB_ERANGE, "sssp: u32 distance overflow (use f64 weights)");
         if (h.k == 0) break;
+        if ((variant == 42 || variant == 43) && h.mode == 0) sort_plan(h.k, h.total, variant == 43);
         GFB_CUDA(cudaEventRecord(c->ev[2], s));
         if (h.mode == 1) pull_launch(s);
         else push(s, h.total);
