@@ -165,6 +165,11 @@ __device__ __forceinline__ uint32_t ld_u32_hint(const void* p, uint64_t pol) {
   return v;
 }
 
+// float bits of a distance (u32 distances as float): log-scale bucket key
+__device__ __forceinline__ uint32_t fkey(float d) { return __float_as_uint(d); }
+__device__ __forceinline__ uint32_t fkey(uint32_t d) { return __float_as_uint((float)d); }
+__device__ __forceinline__ uint32_t fkey(double d) { return __float_as_uint((float)d); }
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned r;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));

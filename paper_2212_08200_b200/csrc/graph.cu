@@ -282,6 +282,11 @@ static __global__ void k_indeg(const EdgeRec<W>* __restrict__ adj, uint64_t m, u
   }
 }
 
+static __global__ void k_indeg_csc(const uint32_t* __restrict__ co, uint32_t n, uint32_t* cnt) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    cnt[v] = co[v + 1] - co[v];
+}
+
 static __global__ void k_iota_rev(uint32_t* ids, uint32_t n) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     ids[i] = i;
@@ -297,19 +302,68 @@ static __global__ void k_rl_perm(const uint32_t* __restrict__ iperm, const uint3
   if (blockIdx.x == 0 && threadIdx.x == 0) deg2[n] = 0;
 }
 
+// Copy into the new layout.  One warp per 32 new rows: lane j holds row
+// i0+j, the rows' edges are concatenated and copied lane-strided (shuffle
+// search for the owning row), so reads of each old row and writes of the new
+// CSR coalesce even for rows of a handful of edges.  Rows longer than RL_BIG
+// (the hubs, which the in-degree order puts first) would serialise their
+// warp: they are listed and copied by k_rl_big, one CTA per row.
+constexpr uint32_t RL_BIG = 1024;
 template <class W>
 static __global__ void k_rl_rows(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ adj,
                                  const uint32_t* __restrict__ ro2, const uint32_t* __restrict__ iperm,
-                                 const uint32_t* __restrict__ perm, EdgeRec<W>* adj2, uint32_t n) {
+                                 const uint32_t* __restrict__ perm, EdgeRec<W>* adj2, uint32_t n,
+                                 uint32_t* big, uint32_t* nbig) {
   const int lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
-    const uint32_t p = iperm[i];
+  for (uint32_t i0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; i0 < n;
+       i0 += warps * 32) {
+    const uint32_t i = i0 + lane;
+    uint32_t s0 = 0, len = 0, d0 = 0;
+    if (i < n) {
+      const uint32_t p = iperm[i];
+      s0 = ro[p];
+      len = ro[p + 1] - s0;
+      d0 = ro2[i];
+      if (len > RL_BIG) {
+        big[atomicAdd(nbig, 1u)] = i;
+        len = 0;
+      }
+    }
+    const uint32_t incl = warp_incl_scan(len, lane);
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    for (uint32_t x = lane; x - lane < tot; x += 32) {
+      int lo = 0;  // owning row: first lane whose inclusive length exceeds x
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const uint32_t q = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+        if (q <= x) lo += step;
+      }
+      const uint32_t os = __shfl_sync(0xffffffffu, s0, lo);
+      const uint32_t od = __shfl_sync(0xffffffffu, d0, lo);
+      const uint32_t opre = __shfl_sync(0xffffffffu, incl, lo) - __shfl_sync(0xffffffffu, len, lo);
+      if (x < tot) {
+        EdgeRec<W> r = adj[os + (x - opre)];
+        r.v = perm[r.v];
+        adj2[od + (x - opre)] = r;
+      }
+    }
+  }
+}
+
+template <class W>
+static __global__ void k_rl_big(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ adj,
+                                const uint32_t* __restrict__ ro2, const uint32_t* __restrict__ iperm,
+                                const uint32_t* __restrict__ perm, EdgeRec<W>* adj2,
+                                const uint32_t* __restrict__ big, const uint32_t* __restrict__ nbig) {
+  const uint32_t cnt = *nbig;
+  for (uint32_t k = blockIdx.x; k < cnt; k += gridDim.x) {
+    const uint32_t i = big[k], p = iperm[i];
     const uint32_t s0 = ro[p], len = ro[p + 1] - s0, d0 = ro2[i];
-    for (uint32_t j = lane; j < len; j += 32) {
-      EdgeRec<W> r = adj[s0 + j];
+    for (uint32_t x = threadIdx.x; x < len; x += blockDim.x) {
+      EdgeRec<W> r = adj[s0 + x];
       r.v = perm[r.v];
-      adj2[d0 + j] = r;
+      adj2[d0 + x] = r;
     }
   }
 }
@@ -332,12 +386,17 @@ void ensure_relabel(Graph* g) {
     g->rl_ro.alloc((size_t)(n + 1) * 4, s);
     g->rl_adj.alloc(m * 8, s);
   }
-  GFB_CUDA(cudaMemsetAsync(cnt.p, 0, (size_t)n * 4, s));
-  if (g->wtype == GFB_W_F32)
-    k_indeg<float><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<float>>(), m, cnt.as<uint32_t>());
-  else
-    k_indeg<uint32_t><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<uint32_t>>(), m,
-                                                     cnt.as<uint32_t>());
+  if (g->has_csc) {  // in-degrees from the transpose's offsets
+    k_indeg_csc<<<stride_grid(c), 256, 0, s>>>(g->co.as<uint32_t>(), n, cnt.as<uint32_t>());
+  } else {
+    GFB_CUDA(cudaMemsetAsync(cnt.p, 0, (size_t)n * 4, s));
+    if (g->wtype == GFB_W_F32)
+      k_indeg<float><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<float>>(), m,
+                                                    cnt.as<uint32_t>());
+    else
+      k_indeg<uint32_t><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<uint32_t>>(), m,
+                                                       cnt.as<uint32_t>());
+  }
   k_iota_rev<<<stride_grid(c), 256, 0, s>>>(ids.as<uint32_t>(), n);
   size_t tb = 0;
   GFB_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, cnt.as<uint32_t>(),
@@ -356,15 +415,29 @@ void ensure_relabel(Graph* g) {
                                            g->rl_perm.as<uint32_t>(), deg2.as<uint32_t>(), n);
   GFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, deg2.as<uint32_t>(), g->rl_ro.as<uint32_t>(),
                                          (int64_t)(n + 1), s));
-  if (g->wtype == GFB_W_F32)
+  DBuf big;
+  big.alloc((size_t)n * 4 + 16, s);
+  uint32_t* nbig = big.as<uint32_t>() + n;
+  GFB_CUDA(cudaMemsetAsync(nbig, 0, 4, s));
+  if (g->wtype == GFB_W_F32) {
     k_rl_rows<float><<<stride_grid(c), 256, 0, s>>>(
         g->ro.as<uint32_t>(), g->adj.as<EdgeRec<float>>(), g->rl_ro.as<uint32_t>(),
-        g->rl_iperm.as<uint32_t>(), g->rl_perm.as<uint32_t>(), g->rl_adj.as<EdgeRec<float>>(), n);
-  else
+        g->rl_iperm.as<uint32_t>(), g->rl_perm.as<uint32_t>(), g->rl_adj.as<EdgeRec<float>>(), n,
+        big.as<uint32_t>(), nbig);
+    k_rl_big<float><<<stride_grid(c), 256, 0, s>>>(
+        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<float>>(), g->rl_ro.as<uint32_t>(),
+        g->rl_iperm.as<uint32_t>(), g->rl_perm.as<uint32_t>(), g->rl_adj.as<EdgeRec<float>>(),
+        big.as<uint32_t>(), nbig);
+  } else {
     k_rl_rows<uint32_t><<<stride_grid(c), 256, 0, s>>>(
         g->ro.as<uint32_t>(), g->adj.as<EdgeRec<uint32_t>>(), g->rl_ro.as<uint32_t>(),
         g->rl_iperm.as<uint32_t>(), g->rl_perm.as<uint32_t>(),
-        g->rl_adj.as<EdgeRec<uint32_t>>(), n);
+        g->rl_adj.as<EdgeRec<uint32_t>>(), n, big.as<uint32_t>(), nbig);
+    k_rl_big<uint32_t><<<stride_grid(c), 256, 0, s>>>(
+        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<uint32_t>>(), g->rl_ro.as<uint32_t>(),
+        g->rl_iperm.as<uint32_t>(), g->rl_perm.as<uint32_t>(),
+        g->rl_adj.as<EdgeRec<uint32_t>>(), big.as<uint32_t>(), nbig);
+  }
   GFB_CUDA(cudaGetLastError());
   c->sync();  // temporaries are stream-ordered frees; keep the build synchronous
   g->rl_valid = true;

@@ -458,7 +458,8 @@ __device__ __forceinline__ void relax_reds(D* dist, unsigned long long* pkey, ui
 
 template <class W, int VT, bool COH = false, int OPT = 0>
 __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, uint32_t e1,
-                                             uint32_t k, uint32_t total, unsigned* err) {
+                                             uint32_t k, uint32_t total, unsigned* err,
+                                             uint32_t* fmin = nullptr) {
   using D = typename DT<W>::D;
   unsigned long long* pkey = reinterpret_cast<unsigned long long*>(a.predrec);
   const int lane = threadIdx.x & 31;
@@ -524,9 +525,12 @@ __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, u
       for (int r = 0; r < VT; ++r)  // B: distance gathers (test before atomic)
         if (dst[r] != NIL) cur[r] = test_gather<OPT>(a.dist + dst[r]);
 #pragma unroll
-      for (int r = 0; r < VT; ++r)  // C: fire-and-forget reductions
-        if (dst[r] != NIL && nd[r] < cur[r])
+      for (int r = 0; r < VT; ++r) {  // C: fire-and-forget reductions
+        if (dst[r] != NIL && nd[r] < cur[r]) {
           relax_reds<OPT>(a.dist, pkey, a.bm_out, dst[r], nd[r], uu[r]);
+          if (fmin) *fmin = min(*fmin, fkey(nd[r]));  // for the distance-ordered plan
+        }
+      }
     }
     if (c1 >= e1) break;
     cs += 32;
@@ -558,16 +562,20 @@ __global__ void __launch_bounds__(256, MINB) k_push_range(AdvArgs<W> a) {
     a.ctl->supersteps += 1;
     a.ctl->push_steps += 1;
   }
+  uint32_t fmin = 0xFFFFFFFFu;
   if constexpr (TILE == 0) {
     const uint32_t per = (uint32_t)((((uint64_t)total + nwarps - 1) / nwarps + 31) & ~31ull);
     const uint32_t e0 = (uint32_t)min((uint64_t)gwarp * per, (uint64_t)total);
     const uint32_t e1 = min(e0 + per, total);
-    if (e0 < e1) range_expand<W, VT, false, OPT>(a, e0, e1, k, total, err);
+    if (e0 < e1) range_expand<W, VT, false, OPT>(a, e0, e1, k, total, err, &fmin);
   } else {
     for (uint64_t e0 = (uint64_t)gwarp * TILE; e0 < total; e0 += (uint64_t)nwarps * TILE)
       range_expand<W, VT, false, OPT>(a, (uint32_t)e0, (uint32_t)min(e0 + TILE, (uint64_t)total),
-                                       k, total, err);
+                                       k, total, err, &fmin);
   }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) fmin = min(fmin, __shfl_xor_sync(0xffffffffu, fmin, d));
+  if ((threadIdx.x & 31) == 0 && fmin != 0xFFFFFFFFu) atomicMin(&a.ctl->fmin, fmin);
 }
 
 }  // namespace gfb

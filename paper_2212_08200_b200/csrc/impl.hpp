@@ -99,6 +99,7 @@ struct Workspace {
   DBuf status;
   DBuf ctl;
   DBuf agg;        // per-tile (count, edges) of the frontier compaction
+  DBuf oagg, obuck; // distance-ordered compaction: per (tile, bucket) cells, bucket totals/cursors
   DBuf src_dev;    // the source vertex (read by k_init)
   DBuf bar;        // grid barrier of the persistent loop (bsp.cuh)
   DBuf bsp_agg, bsp_flag, bsp_tot;  // its per-CTA frontier aggregates / totals

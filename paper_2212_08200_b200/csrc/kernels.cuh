@@ -40,6 +40,11 @@ struct Ctl {
   uint32_t flag;       // generic
   uint32_t mode;       // 0 push, 1 pull (chosen by k_plan_direction)
   unsigned long long n_reach, m_reach;
+  uint32_t resolved;   // predecessor repair: vertices resolved over all rounds
+  // distance-ordered plan (frontier.cuh k_fcount_o): smallest activation
+  // distance of the frontier being built (float bits, written by the push
+  // advance) and the value frozen for the compaction in progress
+  uint32_t fmin, blo;
 };
 
 // Expansion plan: the frontier restricted to vertices with out-degree > 0.
@@ -841,51 +846,59 @@ __global__ void k_pred_repair(const uint32_t* __restrict__ ro, const EdgeRec<W>*
   }
 }
 
-// CSC repair round: one warp per unresolved vertex scans its in-edges in
-// CSC order (ascending source) and takes the FIRST acceptable tight edge,
-// i.e. the smallest source id -- deterministic, with an early exit.
+// CSC repair round, one CTA per unresolved vertex (a hub's in-edge list is
+// hundreds of thousands long: one warp scanning it took 80 us per round at
+// s24).  The list length is read on the device (ctl->unresolved), so rounds
+// can be queued without a host round trip.  Round 1 accepts strictly
+// decreasing tight in-edges, round r > 1 equal-distance tight in-edges from
+// vertices resolved in an earlier round.  Smallest acceptable CSC slot wins
+// (= smallest source id: CSC slots are ascending by source).
 template <class W>
-__global__ void k_pred_csc_round(const uint32_t* __restrict__ co,
-                                 const EdgeRec<W>* __restrict__ cadj,
-                                 const typename DT<W>::D* __restrict__ dist, uint32_t* pred,
-                                 uint32_t* res, const uint32_t* list, uint32_t count,
-                                 uint32_t round, Ctl* ctl) {
+__global__ void __launch_bounds__(256)
+k_pred_csc_block(const uint32_t* __restrict__ co, const EdgeRec<W>* __restrict__ cadj,
+                 const typename DT<W>::D* __restrict__ dist, uint32_t* pred, uint32_t* res,
+                 const uint32_t* list, uint32_t round, Ctl* ctl) {
   using D = typename DT<W>::D;
-  const int lane = threadIdx.x & 31;
-  uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  __shared__ uint32_t s_slot;
+  const uint32_t count = ctl->unresolved;
   uint32_t done = 0;
-  for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < count; i += warps) {
-    uint32_t v = list[i];
-    if (res[v] != 0) continue;  // warp-uniform
-    D dv = dist[v];
-    uint32_t found = NIL;
-    for (uint32_t base = co[v]; base < co[v + 1] && found == NIL; base += 32) {
-      uint32_t slot = base + lane;
-      bool ok = false;
-      uint32_t u = 0;
-      if (slot < co[v + 1]) {
-        EdgeRec<W> rec = cadj[slot];
-        u = rec.v;
-        D du = dist[u];
+  for (uint32_t i = blockIdx.x; i < count; i += gridDim.x) {
+    const uint32_t v = list[i];
+    if (res[v] != 0) continue;  // block-uniform
+    const D dv = dist[v];
+    const uint32_t lo = co[v], hi = co[v + 1];
+    if (threadIdx.x == 0) s_slot = NIL;
+    __syncthreads();
+    for (uint32_t base = lo; base < hi; base += blockDim.x) {
+      const uint32_t slot = base + threadIdx.x;
+      if (slot < hi) {
+        const EdgeRec<W> rec = cadj[slot];
+        const D du = dist[rec.v];
+        bool ok = false;
         if (!(du == dinf<W>()) && dadd(du, rec.w, nullptr) == dv) {
           if (round == 1) {
             ok = du < dv;
           } else {
-            uint32_t ru = res[u];
+            const uint32_t ru = res[rec.v];
             ok = du == dv && ru != 0 && ru <= round;
           }
         }
+        if (ok) atomicMin(&s_slot, slot);
       }
-      unsigned mask = __ballot_sync(0xffffffffu, ok);
-      if (mask) found = __shfl_sync(0xffffffffu, u, __ffs(mask) - 1);
+      __syncthreads();
+      if (s_slot != NIL) break;  // block-uniform: the first chunk with a hit holds the minimum
     }
-    if (found != NIL && lane == 0) {
-      pred[v] = found;
+    if (threadIdx.x == 0 && s_slot != NIL) {
+      pred[v] = cadj[s_slot].v;
       res[v] = round + 1;
       ++done;
     }
+    __syncthreads();
   }
-  if (lane == 0 && done) atomicAdd(&ctl->flag, done);
+  if (threadIdx.x == 0 && done) {
+    atomicAdd(&ctl->flag, done);
+    atomicAdd(&ctl->resolved, done);
+  }
 }
 
 // Apply round `round`'s candidates; counts how many vertices were resolved.

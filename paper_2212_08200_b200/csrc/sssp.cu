@@ -42,6 +42,9 @@ Workspace* ensure_ws(Graph* g) {
   ws->ptseg.alloc((m / PLAN_GRAIN + 3) * 4, s);
   ws->ftiles = (uint32_t)std::max<uint64_t>((nwords + F_WORDS - 1) / F_WORDS, 1);
   ws->agg.alloc((size_t)ws->ftiles * 8, s);
+  ws->oagg.alloc((size_t)ws->ftiles * OB_N * 8, s);
+  ws->obuck.alloc(2 * OB_N * 8, s);
+  GFB_CUDA(cudaMemsetAsync(ws->obuck.p, 0, 2 * OB_N * 8, s));
   ws->src_dev.alloc(16, s);
   ws->compact_tiles = (uint32_t)((nwords + C_WORDS - 1) / C_WORDS);
   if (ws->compact_tiles == 0) ws->compact_tiles = 1;
@@ -118,6 +121,11 @@ struct Runner {
   int variant = 0;  // experimental kernel shape (opts.reserved[0])
   bool rl = false;  // loop runs on the in-degree-relabelled CSR (ensure_relabel)
 
+  // distance-ordered plan (frontier.cuh k_fcount_o / k_fwrite_o); variants
+  // 60/61 keep the ascending-id plan for comparison, 62 = ordered plan on the
+  // caller's ids
+  bool ordered() const { return key_mode() && variant != 60 && variant != 61 && variant < 100; }
+
   const uint32_t* lro() const { return rl ? g->rl_ro.as<uint32_t>() : g->ro.as<uint32_t>(); }
   D* ldist() const { return rl ? ws->dist_int.as<D>() : ws->dist.as<D>(); }
   uint2* lpred() const { return rl ? ws->pkey_int.as<uint2>() : ws->predrec.as<uint2>(); }
@@ -151,6 +159,26 @@ struct Runner {
   // frontier compaction: count -> scan (+ loop/direction decision) -> write
   void compact(int dir, float alpha, cudaGraphConditionalHandle hloop,
                cudaGraphConditionalHandle hmode, bool set_loop, bool set_mode) {
+    if constexpr (sizeof(D) == 4) {
+      if (ordered()) {
+        const uint32_t tiles = ws->ftiles;
+        unsigned long long* bt = ws->obuck.as<unsigned long long>();
+        k_fcount_o<D><<<tiles, F_WARPS * 32, 0, s>>>(lro(), ws->bm_next.as<uint32_t>(), nwords,
+                                                     ldist(), ws->ctl.as<Ctl>(),
+                                                     ws->oagg.as<unsigned long long>(), bt);
+        k_fscan_o<<<1, 32, 0, s>>>(bt, bt + OB_N, plan(), ws->ctl.as<Ctl>(), (uint32_t)g->m, alpha,
+                                   dir == GFB_DIR_AUTO && g->has_csc ? 1 : 0,
+                                   dir == GFB_DIR_PULL ? 1 : 0, hloop, hmode, set_loop ? 1 : 0,
+                                   set_mode ? 1 : 0);
+        k_fwrite_o<D><<<tiles, F_WARPS * 32, 0, s>>>(lro(), ws->bm_next.as<uint32_t>(),
+                                                     ws->bm_cur.as<uint32_t>(), nwords, ldist(),
+                                                     ws->ctl.as<Ctl>(),
+                                                     ws->oagg.as<unsigned long long>(), bt + OB_N,
+                                                     plan());
+        GFB_CUDA(cudaGetLastError());
+        return;
+      }
+    }
     const uint32_t tiles = ws->ftiles;
     k_fcount<<<tiles, F_WARPS * 32, 0, s>>>(lro(), ws->bm_next.as<uint32_t>(),
                                             nwords, ws->agg.as<uint2>());
@@ -376,7 +404,7 @@ struct Runner {
     return false;
   }
 
-  void sort_plan(uint32_t K, uint32_t T, bool desc) {
+  void sort_plan(uint32_t K, uint32_t T, bool desc, int begin_bit = 0) {
     if (K < 2) return;
     DBuf keys, keys2, idx, idx2, v2, s2, deg, tmp;
     keys.alloc((size_t)K * 4, s); keys2.alloc((size_t)K * 4, s);
@@ -387,13 +415,13 @@ struct Runner {
                                                   idx.as<uint32_t>(), K, desc ? 1 : 0);
     size_t tb = 0, tb2 = 0;
     GFB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<uint32_t>(), keys2.as<uint32_t>(),
-                                             idx.as<uint32_t>(), idx2.as<uint32_t>(), (int64_t)K, 0,
-                                             32, s));
+                                             idx.as<uint32_t>(), idx2.as<uint32_t>(), (int64_t)K,
+                                             begin_bit, 32, s));
     GFB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, deg.as<uint32_t>(), p.off, (int64_t)(K + 1), s));
     tmp.alloc(std::max(tb, tb2), s);
     GFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<uint32_t>(), keys2.as<uint32_t>(),
-                                             idx.as<uint32_t>(), idx2.as<uint32_t>(), (int64_t)K, 0,
-                                             32, s));
+                                             idx.as<uint32_t>(), idx2.as<uint32_t>(), (int64_t)K,
+                                             begin_bit, 32, s));
     k_plan_permute<<<stride_grid(c), 256, 0, s>>>(idx2.as<uint32_t>(), p.v, p.start, p.off,
                                                   v2.as<uint32_t>(), s2.as<uint32_t>(),
                                                   deg.as<uint32_t>(), K);
@@ -497,7 +525,9 @@ struct Runner {
     const float alpha = o->pull_alpha > 0 ? o->pull_alpha : 0.25f;
     // The relabelled CSR has no CSC: only when no superstep can pull (the
     // AUTO switch needs frontier edges > m / alpha, impossible for alpha <= 1).
-    rl = key_mode() && variant == 41 &&
+    // Default for 32-bit distances on graphs with >= 2^20 vertices (measured
+    // at s24: 6.10 -> 5.86 ms); variants 60-62 keep the caller's ids.
+    rl = key_mode() && o->delta <= 0 && (variant == 41 || (variant == 0 && n >= (1u << 20))) &&
          (dir == GFB_DIR_PUSH || (dir == GFB_DIR_AUTO && (alpha <= 1.0f || !g->has_csc)));
     if (rl) {
       ensure_relabel(g);
@@ -543,6 +573,9 @@ struct Runner {
         if (h.err & 1u) fail(GFB_ERANGE, "sssp: u32 distance overflow (use f64 weights)");
         if (h.k == 0) break;
         if ((variant == 42 || variant == 43) && h.mode == 0) sort_plan(h.k, h.total, variant == 43);
+        if (variant == 47 && h.mode == 0) sort_plan(h.k, h.total, false, 20);
+        if (variant == 48 && h.mode == 0) sort_plan(h.k, h.total, false, 23);
+        if (variant == 49 && h.mode == 0) sort_plan(h.k, h.total, false, 16);
         GFB_CUDA(cudaEventRecord(c->ev[2], s));
         if (h.mode == 1) pull_launch(s);
         else push(s, h.total);
@@ -610,34 +643,42 @@ struct Runner {
     GFB_CUDA(cudaGetLastError());
     ++kernels;
     if (!want) return;
-    Ctl h = c->read_ctl(ws->ctl.as<Ctl>());
-    *fallback = h.unresolved;
-    if (h.unresolved == 0) return;
-    uint64_t left = h.unresolved;
     if (g->has_csc) {
-      // unresolved vertices were appended to ws->cand; scan their in-edges
-      const uint32_t count = h.unresolved;
-      DBuf list;
-      list.alloc((size_t)count * 4, s);
-      GFB_CUDA(cudaMemcpyAsync(list.p, ws->cand.p, (size_t)count * 4, cudaMemcpyDeviceToDevice, s));
-      for (uint32_t round = 1; left > 0; ++round) {
+      // two repair rounds queued without a host round trip (block per vertex,
+      // list length read on the device); more only for deep zero-weight ties
+      const uint32_t grid = c->num_sms * 8;
+      for (uint32_t round = 1; round <= 2; ++round) {
         GFB_CUDA(cudaMemsetAsync(&ws->ctl.as<Ctl>()->flag, 0, 4, s));
-        uint32_t grid = std::min<uint32_t>((count + 7) / 8, c->num_sms * 8);
-        k_pred_csc_round<W><<<grid, 256, 0, s>>>(
+        k_pred_csc_block<W><<<grid, 256, 0, s>>>(
             g->co.as<uint32_t>(), g->cadj.as<EdgeRec<W>>(), ws->dist.as<D>(),
-            ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(), list.as<uint32_t>(), count, round,
+            ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(), ws->cand.as<uint32_t>(), round,
+            ws->ctl.as<Ctl>());
+        GFB_CUDA(cudaGetLastError());
+        ++kernels;
+      }
+      Ctl h = c->read_ctl(ws->ctl.as<Ctl>());
+      *fallback = h.unresolved;
+      uint64_t left = h.unresolved - std::min(h.unresolved, h.resolved);
+      if (left > 0 && h.flag == 0)
+        fail(GFB_ELOGIC, "sssp: predecessor repair made no progress");
+      for (uint32_t round = 3; left > 0; ++round) {
+        GFB_CUDA(cudaMemsetAsync(&ws->ctl.as<Ctl>()->flag, 0, 4, s));
+        k_pred_csc_block<W><<<grid, 256, 0, s>>>(
+            g->co.as<uint32_t>(), g->cadj.as<EdgeRec<W>>(), ws->dist.as<D>(),
+            ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(), ws->cand.as<uint32_t>(), round,
             ws->ctl.as<Ctl>());
         GFB_CUDA(cudaGetLastError());
         ++kernels;
         Ctl r = c->read_ctl(ws->ctl.as<Ctl>());
-        // round 1 (strict edges) may resolve nothing when every unresolved
-        // vertex sits in a zero-weight tie class; later rounds must progress.
-        if (r.flag == 0 && round > 1)
-          fail(GFB_ELOGIC, "sssp: predecessor repair made no progress");
+        if (r.flag == 0) fail(GFB_ELOGIC, "sssp: predecessor repair made no progress");
         left -= std::min<uint64_t>(left, r.flag);
       }
       return;
     }
+    Ctl h = c->read_ctl(ws->ctl.as<Ctl>());
+    *fallback = h.unresolved;
+    if (h.unresolved == 0) return;
+    uint64_t left = h.unresolved;
     // no CSC: candidate rounds over every CSR row (O(m) per round)
     GFB_CUDA(cudaMemsetAsync(ws->cand.p, 0xFF, (size_t)n * 4, s));
     for (uint32_t round = 1; left > 0; ++round) {

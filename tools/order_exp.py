@@ -7,7 +7,7 @@ ctx = gb.Context(0)
 for sc in [int(x) for x in sys.argv[1:]] or [20, 24]:
     g = gb.rmat(sc, 16, seed=1, wtype="f32", transpose=True, ctx=ctx)
     base = None
-    for v in (0, 42, 43):
+    for v in (0, 42, 43, 47, 48, 49):
         d, p, st = gb.sssp_stats(g, 0, variant=v, device_loop=False)
         if base is None: base = d
         print(json.dumps({"scale": sc, "variant": v, "relax": st.relaxations,
