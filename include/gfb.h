@@ -166,9 +166,13 @@ typedef struct gfb_sssp_opts {
   int32_t direction;     /* gfb_direction; AUTO default */
   float pull_alpha;      /* AUTO: pull when frontier edges > m / pull_alpha */
   int32_t device_loop;   /* 1: device-side convergence (CUDA graph) */
-  double delta;          /* >0: near-far filter with this width; 0: plain BSP */
+  double delta;          /* >0: near-far filter of this width (push only; one
+                            persistent launch with queue frontiers, for
+                            high-diameter graphs); 0: BSP loop.  u32/f32
+                            arithmetic (f64 ignores it).  Same distances. */
   int32_t compute_pred;  /* 1: fill pred (tight-edge tree) */
-  int32_t reserved[7];
+  int32_t reserved[7];   /* reserved[0]: kernel-shape experiment id (0 = the
+                            measured default; see sssp.cu Runner::variant) */
 } gfb_sssp_opts;
 
 void gfb_sssp_opts_default(gfb_sssp_opts* o);
@@ -198,6 +202,14 @@ int gfb_sssp(gfb_ctx* ctx, gfb_graph* g, uint32_t source,
 /* Result of the last gfb_sssp on g: dist widened to double and/or in the
  * graph's native type (u32 / f32 / f64 bytes). */
 int gfb_sssp_read(gfb_graph* g, double* dist, void* dist_native, uint32_t* pred);
+
+/* ---- inspection (tests / tools; no reference counterpart) ----------------
+ * The in-degree-relabelled CSR the BSP loop runs on for 32-bit weights
+ * (built on first use, cached until a refill): row offsets (n+1), records as
+ * {dst, weight bits} u32 pairs (2m), perm old->new id (n).  Any pointer may
+ * be 0.  4-byte weights only (else GFB_EINVAL). */
+int gfb_debug_relabel(gfb_graph* g, uint32_t* row_offsets, uint32_t* adj_pairs,
+                      uint32_t* perm);
 
 /* ---- 1-D partitioned SSSP: one rank's share (multi-GPU) ----
  * No reference counterpart (the reference is single-host); mg.py drives one

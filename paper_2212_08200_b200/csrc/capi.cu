@@ -447,13 +447,13 @@ int gfb_sssp_read(gfb_graph* g, double* dist, void* dist_native, uint32_t* pred)
 
 }  // extern "C"
 
-// Debug/inspection: the in-degree-relabelled loop CSR (row offsets, records
-// as {dst, weight bits} pairs, perm old->new).  Not part of the reference API.
-extern "C" int gfb_debug_relabel(gfb_graph* g, uint32_t* ro, uint32_t* adj_pairs, uint32_t* perm) {
+// Inspection: the in-degree-relabelled loop CSR (include/gfb.h).
+int gfb_debug_relabel(gfb_graph* g, uint32_t* ro, uint32_t* adj_pairs, uint32_t* perm) {
   return guard([&] {
     NEED(g);
     set_device(g->ctx);
     gfb::ensure_relabel(g);
+    if (g->rl_skip) gfb::fail(GFB_ELOGIC, "relabel: in-degrees not skewed, no relabelled view");
     cudaStream_t s = g->ctx->stream;
     if (ro) GFB_CUDA(cudaMemcpyAsync(ro, g->rl_ro.p, (g->n + 1) * 4, cudaMemcpyDeviceToHost, s));
     if (adj_pairs) GFB_CUDA(cudaMemcpyAsync(adj_pairs, g->rl_adj.p, g->m * 8, cudaMemcpyDeviceToHost, s));

@@ -397,6 +397,22 @@ void ensure_relabel(Graph* g) {
       k_indeg<uint32_t><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<uint32_t>>(), m,
                                                        cnt.as<uint32_t>());
   }
+  {  // only skewed in-degrees profit (grids lose their locality): max >= 32x mean
+    DBuf mx, tmpr;
+    mx.alloc(8, s);
+    size_t tr = 0;
+    GFB_CUDA(cub::DeviceReduce::Max(nullptr, tr, cnt.as<uint32_t>(), mx.as<uint32_t>(), (int64_t)n, s));
+    tmpr.alloc(tr, s);
+    GFB_CUDA(cub::DeviceReduce::Max(tmpr.p, tr, cnt.as<uint32_t>(), mx.as<uint32_t>(), (int64_t)n, s));
+    uint32_t hmax = 0;
+    GFB_CUDA(cudaMemcpyAsync(&hmax, mx.p, 4, cudaMemcpyDeviceToHost, s));
+    c->sync();
+    g->rl_skip = (double)hmax < 32.0 * (double)m / (double)std::max<uint32_t>(n, 1);
+    if (g->rl_skip) {
+      g->rl_valid = true;
+      return;
+    }
+  }
   k_iota_rev<<<stride_grid(c), 256, 0, s>>>(ids.as<uint32_t>(), n);
   size_t tb = 0;
   GFB_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, cnt.as<uint32_t>(),

@@ -58,6 +58,7 @@ struct Graph {
   // destinations share distance cache lines.  4-byte weights only.
   DBuf rl_ro, rl_adj, rl_perm, rl_iperm;
   bool rl_valid = false;
+  bool rl_skip = false;  // in-degrees not skewed enough to pay (no arrays built)
   // static pull plan (destinations with in-degree > 0)
   uint32_t pull_k = 0, pull_total = 0;
   DBuf pull_v, pull_off, pull_tseg;

@@ -531,6 +531,9 @@ struct Runner {
          (dir == GFB_DIR_PUSH || (dir == GFB_DIR_AUTO && (alpha <= 1.0f || !g->has_csc)));
     if (rl) {
       ensure_relabel(g);
+      rl = !g->rl_skip;
+    }
+    if (rl) {
       if (ws->dist_int.bytes < (size_t)n * sizeof(D)) {
         ws->dist_int.alloc((size_t)n * sizeof(D), s);
         ws->pkey_int.alloc((size_t)n * 8, s);

@@ -1,0 +1,47 @@
+"""Summarise an ncu --set full report (one kernel launch) into the metrics the
+DESIGN.md roofline discussion cites.  usage: python tools/ncu_summary.py x.ncu-rep"""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of peak"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput % of peak"),
+    ("lts__t_sector_hit_rate.pct", "L2 sector hit rate %"),
+    ("l1tex__t_sector_hit_rate.pct", "L1 sector hit rate %"),
+    ("l1tex__t_sector_pipe_lsu_mem_global_op_ld_hit_rate.pct", "L1 global-load hit rate %"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput % of peak"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
+    ("launch__registers_per_thread", "registers/thread"),
+    ("launch__grid_size", "grid"),
+    ("launch__block_size", "block"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+    ("lts__t_sectors_srcunit_tex_op_read.sum", "L2 read sectors (from SMs)"),
+    ("lts__t_sectors_srcunit_tex_op_red.sum", "L2 RED sectors"),
+    ("lts__t_sectors_srcunit_tex_op_atom.sum", "L2 ATOM sectors"),
+]
+raw = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True,
+                     text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr, units, val = rows[0], rows[1], rows[2]
+name = val[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"
+print(f"kernel: {name}")
+for k, label in KEYS:
+    if k in hdr:
+        i = hdr.index(k)
+        print(f"  {label:32s} {val[i]:>16s} {units[i]}")
+stalls = []
+for i, h in enumerate(hdr):
+    if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued"):
+        try:
+            stalls.append((float(val[i]), h.replace("smsp__pcsamp_warps_issue_stalled_", "")))
+        except ValueError:
+            pass
+tot = sum(v for v, _ in stalls) or 1
+print("  warp-state samples (top 5):")
+for v, h in sorted(stalls, reverse=True)[:5]:
+    print(f"    {h:28s} {100 * v / tot:5.1f}%")
