@@ -382,7 +382,7 @@ def run_e2e(gb, ctx, g, args, kw):
     d2h = dist.nbytes + pred.nbytes
     return {"value": st.m_reach / t / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": t * 1e3, "steps": steps,
-            "path": "gfb_graph_refill(pinned CSR, build CSC) + gfb_sssp(dist f64, pred)"}
+            "path": "gfb_graph_refill(pinned CSR; device CSR build, transpose built on first use) + gfb_sssp(dist f64, pred)"}
 
 
 def cpu_baseline(gb, ctx, args):

@@ -96,6 +96,11 @@ int gfb_ctx_create(int device, gfb_ctx** out) {
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
     try {
+      // keep freed pool memory reserved (DBuf allocates stream-ordered)
+      cudaMemPool_t pool;
+      GFB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+      uint64_t keep = ~0ull;
+      GFB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
       GFB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       for (auto& e : c->ev) GFB_CUDA(cudaEventCreate(&e));
       GFB_CUDA(cudaMallocHost(&c->ctl_host, sizeof(Ctl)));
@@ -159,7 +164,7 @@ int gfb_graph_info(const gfb_graph* g, uint64_t* n, uint64_t* m, int* wtype, int
     if (n) *n = g->n;
     if (m) *m = g->m;
     if (wtype) *wtype = g->wtype;
-    if (has_csc) *has_csc = g->has_csc ? 1 : 0;
+    if (has_csc) *has_csc = g->csc_wanted ? 1 : 0;
   });
 }
 

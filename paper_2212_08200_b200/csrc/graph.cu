@@ -13,21 +13,36 @@
 
 namespace gfb {
 
+// Stream-ordered allocations from the device's default pool (its release
+// threshold is raised at context creation, so memory stays reserved and a
+// temporary costs no page mapping and no device-wide synchronisation -- a
+// plain cudaFree synchronises the whole device).  Every buffer is used on the
+// stream it was allocated on, or on helper streams the owner synchronises
+// before returning (fill_graph).
 void DBuf::alloc(size_t b, cudaStream_t stream) {
   release();
   s = stream;
   if (b == 0) b = 16;
-  cudaError_t e = cudaMalloc(&p, b);
+  cudaError_t e = cudaMallocAsync(&p, b, stream);
   if (e == cudaErrorMemoryAllocation) {
     cudaGetLastError();
     p = nullptr;
     fail(GFB_ENOMEM, "device allocation of " + std::to_string(b) + " bytes failed");
   }
-  check_cuda(e, "cudaMalloc");
+  check_cuda(e, "cudaMallocAsync");
   bytes = b;
 }
 
 void DBuf::release() {
+  if (p && cudaFreeAsync(p, s) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(p);
+  }
+  p = nullptr;
+  bytes = 0;
+}
+
+void DBuf::release_sync() {
   if (p) cudaFree(p);
   p = nullptr;
   bytes = 0;
@@ -66,7 +81,7 @@ Workspace::~Workspace() {
 
 void Frontier::reserve(uint64_t c) {
   if (c <= cap) return;
-  DBuf nb;
+  TBuf nb;
   nb.alloc(c * 4, ctx->stream);
   if (len) GFB_CUDA(cudaMemcpyAsync(nb.p, list.p, len * 4, cudaMemcpyDeviceToDevice, ctx->stream));
   std::swap(list.p, nb.p);
@@ -186,7 +201,7 @@ static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const 
   // every sub-array stays 16-byte aligned for any weight width
   const uint64_t chunk = (std::min<uint64_t>(UPLOAD_CHUNK, std::max<uint64_t>(m, 1)) + 63) & ~63ull;
   if (g->stage.bytes < 2 * chunk * (4 + 8)) g->stage.alloc(2 * chunk * (4 + 8), s);
-  DBuf flags;
+  TBuf flags;
   flags.alloc(3 * 8, s);
   GFB_CUDA(cudaMemsetAsync(flags.p, 0xFF, 3 * 8, s));
   auto* f = flags.as<unsigned long long>();
@@ -375,7 +390,7 @@ void ensure_relabel(Graph* g) {
   cudaStream_t s = c->stream;
   const uint32_t n = (uint32_t)g->n;
   const uint64_t m = g->m;
-  DBuf cnt, cnt2, ids, deg2, tmp;
+  TBuf cnt, cnt2, ids, deg2, tmp;
   cnt.alloc((size_t)n * 4, s);
   cnt2.alloc((size_t)n * 4, s);
   ids.alloc((size_t)n * 4, s);
@@ -398,7 +413,7 @@ void ensure_relabel(Graph* g) {
                                                        cnt.as<uint32_t>());
   }
   {  // only skewed in-degrees profit (grids lose their locality): max >= 32x mean
-    DBuf mx, tmpr;
+    TBuf mx, tmpr;
     mx.alloc(8, s);
     size_t tr = 0;
     GFB_CUDA(cub::DeviceReduce::Max(nullptr, tr, cnt.as<uint32_t>(), mx.as<uint32_t>(), (int64_t)n, s));
@@ -431,7 +446,7 @@ void ensure_relabel(Graph* g) {
                                            g->rl_perm.as<uint32_t>(), deg2.as<uint32_t>(), n);
   GFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, deg2.as<uint32_t>(), g->rl_ro.as<uint32_t>(),
                                          (int64_t)(n + 1), s));
-  DBuf big;
+  TBuf big;
   big.alloc((size_t)n * 4 + 16, s);
   uint32_t* nbig = big.as<uint32_t>() + n;
   GFB_CUDA(cudaMemsetAsync(nbig, 0, 4, s));
@@ -473,19 +488,23 @@ Graph* graph_upload(Ctx* c, uint64_t n, uint64_t m, const uint32_t* ro, const ui
   g->ro.alloc((n + 1) * 4, c->stream);
   g->adj.alloc(m * g->rec_bytes(), c->stream);
   fill_graph(g.get(), ro, col, w, htype);
-  if (build_csc_flag) {
-    build_csc(g.get());
-    build_pull_plan(g.get());
-  }
+  g->csc_wanted = build_csc_flag != 0;  // built on first use (ensure_csc)
   return g.release();
 }
 
 void graph_refill(Graph* g, const uint32_t* ro, const uint32_t* col, const void* w, int htype) {
   fill_graph(g, ro, col, w, htype);
-  if (g->has_csc) {
-    build_csc(g);
-    build_pull_plan(g);
-  }
+  g->has_csc = false;  // stale: rebuilt on first use
+  g->ceid.release();
+}
+
+// The transpose is built lazily: a push-only or AUTO (alpha <= 1) sssp and
+// the transpose-free predecessor repair never need it, and its radix sort is
+// the largest part of an upload after the H2D copy (~25 ms at s24).
+void ensure_csc(Graph* g) {
+  if (!g->csc_wanted || g->has_csc) return;
+  build_csc(g);
+  build_pull_plan(g);
 }
 
 // ---------------------------------------------------------------------------
@@ -554,7 +573,7 @@ static void source_of_edges(Graph* g, DBuf& src_of) {
   size_t tb = 0;
   GFB_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb, src_of.as<uint32_t>(),
                                           src_of.as<uint32_t>(), MaxOp(), (int64_t)g->m, s));
-  DBuf tmp;
+  TBuf tmp;
   tmp.alloc(tb, s);
   GFB_CUDA(cub::DeviceScan::InclusiveScan(tmp.p, tb, src_of.as<uint32_t>(),
                                           src_of.as<uint32_t>(), MaxOp(), (int64_t)g->m, s));
@@ -605,6 +624,7 @@ __global__ void k_ceid(const uint32_t* __restrict__ co, const EdgeRec<W>* __rest
 }
 
 void ensure_ceid(Graph* g) {
+  ensure_csc(g);
   if (!g->has_csc || g->ceid.p) return;
   Ctx* c = g->ctx;
   g->ceid.alloc(g->m * 4, c->stream);
@@ -636,12 +656,12 @@ void build_csc(Graph* g) {
     c->sync();
     return;
   }
-  DBuf src_of;
+  TBuf src_of;
   source_of_edges(g, src_of);
   if (g->wtype != GFB_W_F64) {
     // one stable radix sort of {src, w} payloads by dst: the sorted payloads
     // ARE the CSC records in build_transpose slot order (graph.hpp:198-208)
-    DBuf keys, keys2, vals;
+    TBuf keys, keys2, vals;
     keys.alloc(m * 4, s);
     keys2.alloc(m * 4, s);
     vals.alloc(m * 8, s);
@@ -661,7 +681,7 @@ void build_csc(Graph* g) {
                                              vals.as<unsigned long long>(),
                                              g->cadj.as<unsigned long long>(), (int64_t)m, 0,
                                              bits_for(n), s));
-    DBuf tmp;
+    TBuf tmp;
     tmp.alloc(tb, s);
     GFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<uint32_t>(), keys2.as<uint32_t>(),
                                              vals.as<unsigned long long>(),
@@ -677,7 +697,7 @@ void build_csc(Graph* g) {
   // f64 (16-byte records): sort CSR ids by dst, then gather records + ids
   g->cadj.alloc(m * g->rec_bytes(), s);
   g->ceid.alloc(m * 4, s);
-  DBuf keys, ids, keys2, ids2;
+  TBuf keys, ids, keys2, ids2;
   keys.alloc(m * 4, s);
   ids.alloc(m * 4, s);
   keys2.alloc(m * 4, s);
@@ -688,7 +708,7 @@ void build_csc(Graph* g) {
   GFB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<uint32_t>(), keys2.as<uint32_t>(),
                                            ids.as<uint32_t>(), ids2.as<uint32_t>(), (int64_t)m, 0,
                                            bits_for(n), s));
-  DBuf tmp;
+  TBuf tmp;
   tmp.alloc(tb, s);
   GFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<uint32_t>(), keys2.as<uint32_t>(),
                                            ids.as<uint32_t>(), ids2.as<uint32_t>(), (int64_t)m, 0,
@@ -727,7 +747,7 @@ void build_pull_plan(Graph* g) {
   g->pull_v.alloc((n + 1) * 4, s);
   g->pull_off.alloc((n + 1) * 4, s);
   g->pull_tseg.alloc((m / PLAN_GRAIN + 3) * 4, s);
-  DBuf bm, ctl, status;
+  TBuf bm, ctl, status;
   bm.alloc(nwords * 4, s);
   ctl.alloc(sizeof(Ctl), s);
   status.alloc((size_t)(ntiles + 1) * 8, s);
@@ -741,7 +761,7 @@ void build_pull_plan(Graph* g) {
   }
   k_fill_ones<<<stride_grid(c), 256, 0, s>>>(bm.as<uint32_t>(), nwords, n);
   // start and off coincide for a complete plan: start = co[v] = off
-  DBuf start;
+  TBuf start;
   start.alloc((n + 1) * 4, s);
   Plan p{g->pull_v.as<uint32_t>(), start.as<uint32_t>(), g->pull_off.as<uint32_t>(),
          g->pull_tseg.as<uint32_t>(), (uint32_t)(g->pull_tseg.bytes / 4)};
@@ -797,7 +817,7 @@ Graph* graph_generate_rmat(Ctx* c, int scale, int ef, uint64_t seed, int wtype, 
   g->ro.alloc((n + 1) * 4, s);
   g->adj.alloc(m * 8, s);
   {
-    DBuf key, key2, wb, wb2;
+    TBuf key, key2, wb, wb2;
     key.alloc(m * 8, s);
     key2.alloc(m * 8, s);
     wb.alloc(m * 4, s);
@@ -815,7 +835,7 @@ Graph* graph_generate_rmat(Ctx* c, int scale, int ef, uint64_t seed, int wtype, 
     GFB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, key2.as<unsigned long long>(),
                                              key.as<unsigned long long>(), wb2.as<uint32_t>(),
                                              wb.as<uint32_t>(), (int64_t)m, 0, 32 + scale, s));
-    DBuf tmp;
+    TBuf tmp;
     tmp.alloc(tb1 > tb2 ? tb1 : tb2, s);
     size_t tb = tmp.bytes;
     GFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, wb.as<uint32_t>(), wb2.as<uint32_t>(),
@@ -827,7 +847,7 @@ Graph* graph_generate_rmat(Ctx* c, int scale, int ef, uint64_t seed, int wtype, 
                                              wb.as<uint32_t>(), (int64_t)m, 0, 32 + scale, s));
     tmp.release();
     key2.release();
-    DBuf srcs;
+    TBuf srcs;
     srcs.alloc(m * 4, s);
     k_unpack_sorted<<<stride_grid(c), 256, 0, s>>>(key.as<unsigned long long>(), wb.as<uint32_t>(),
                                                    srcs.as<uint32_t>(),
@@ -837,10 +857,7 @@ Graph* graph_generate_rmat(Ctx* c, int scale, int ef, uint64_t seed, int wtype, 
     GFB_CUDA(cudaGetLastError());
     c->sync();
   }
-  if (csc) {
-    build_csc(g.get());
-    build_pull_plan(g.get());
-  }
+  g->csc_wanted = csc != 0;  // built on first use (ensure_csc)
   return g.release();
 }
 
@@ -881,14 +898,14 @@ Graph* graph_generate_grid(Ctx* c, uint32_t side, uint64_t seed, int csc) {
   g->wtype = GFB_W_F32;
   g->ro.alloc((n + 1) * 4, s);
   g->adj.alloc(m * 8, s);
-  DBuf deg;
+  TBuf deg;
   deg.alloc((n + 1) * 4, s);
   GFB_CUDA(cudaMemsetAsync(deg.p, 0, (n + 1) * 4, s));
   k_grid_deg<<<stride_grid(c), 256, 0, s>>>(side, deg.as<uint32_t>());
   size_t tb = 0;
   GFB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, deg.as<uint32_t>(), g->ro.as<uint32_t>(),
                                          (int64_t)(n + 1), s));
-  DBuf tmp;
+  TBuf tmp;
   tmp.alloc(tb, s);
   GFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, deg.as<uint32_t>(), g->ro.as<uint32_t>(),
                                          (int64_t)(n + 1), s));
@@ -896,10 +913,7 @@ Graph* graph_generate_grid(Ctx* c, uint32_t side, uint64_t seed, int csc) {
                                              g->adj.as<EdgeRec<uint32_t>>());
   GFB_CUDA(cudaGetLastError());
   c->sync();
-  if (csc) {
-    build_csc(g.get());
-    build_pull_plan(g.get());
-  }
+  g->csc_wanted = csc != 0;  // built on first use (ensure_csc)
   return g.release();
 }
 
@@ -920,7 +934,7 @@ void graph_download(Graph* g, uint32_t* ro, uint32_t* col, void* w) {
   if (ro) GFB_CUDA(cudaMemcpyAsync(ro, g->ro.p, (g->n + 1) * 4, cudaMemcpyDeviceToHost, s));
   if ((col || w) && g->m) {
     size_t wb = g->wtype == GFB_W_F64 ? 8 : 4;
-    DBuf dc, dw;
+    TBuf dc, dw;
     dc.alloc(g->m * 4, s);
     dw.alloc(g->m * wb, s);
     if (g->wtype == GFB_W_F32)

@@ -11,7 +11,10 @@
 
 namespace gfb {
 
-// Owning device buffer (cudaMallocAsync on the context stream).
+// Owning device buffer, allocated stream-ordered from the device pool
+// (cudaMallocAsync on the given stream).  Re-allocation frees stream-ordered;
+// destruction frees synchronously (cudaFree), because a long-lived buffer
+// may outlive the stream it was allocated on (objects destroyed at exit).
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -19,10 +22,17 @@ struct DBuf {
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  ~DBuf() { release(); }
+  ~DBuf() { release_sync(); }
   void alloc(size_t b, cudaStream_t stream);
-  void release();
+  void release();       // stream-ordered on s
+  void release_sync();  // cudaFree
   template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+// Function-local temporary: freed stream-ordered at scope exit (its stream
+// is alive for the whole call), so temporaries never synchronise the device.
+struct TBuf : DBuf {
+  ~TBuf() { release(); }
 };
 
 struct Ctx {
@@ -48,7 +58,8 @@ struct Graph {
   uint64_t n = 0, m = 0;
   uint64_t col_bound = 0;  // destination ids must be < col_bound (= n, or n_global for a partition)
   int wtype = GFB_W_F32;
-  bool has_csc = false;
+  bool csc_wanted = false;  // the caller asked for the transpose (build_transpose)
+  bool has_csc = false;     // ... and it is built for the current contents (ensure_csc)
   DBuf ro, adj, co, cadj, ceid;  // ceid built lazily (ensure_ceid) for the record op
   DBuf stage;                     // upload staging, kept for refills
   DBuf nz;                        // bit v: out-degree(v) > 0 (ensure_nz, bsp.cuh)
@@ -139,6 +150,7 @@ inline int persist_grid(const Ctx* c, int per_sm) { return c->num_sms * per_sm; 
 
 // graph.cu
 void build_csc(Graph* g);
+void ensure_csc(Graph* g);
 void ensure_ceid(Graph* g);
 void build_pull_plan(Graph* g);
 void ensure_nz(Graph* g);

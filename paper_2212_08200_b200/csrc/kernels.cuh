@@ -705,11 +705,11 @@ __global__ void k_init(typename DT<W>::D* dist, uint2* predrec, uint32_t* bm_nex
 //  k_pred_verify: pred[v] = u of the recorded improving relax when that edge
 //    is still tight and strictly decreasing (dist[u] < dist[v]); else v goes
 //    to the repair set.  Strictly decreasing chains are acyclic.
-//  k_pred_repair: one pass over the CSR edges into repair-set vertices,
-//    round r accepts a tight edge u->v when u was resolved in an earlier
-//    round (round 1: dist[u] < dist[v]; later rounds: equal distances, the
-//    zero-weight tie classes that make a plain argmin cycle, cf.
-//    algorithms.hpp:506-511).  Smallest u wins (deterministic).
+//  repair rounds (k_pred_csc_block with a transpose, k_pred_list_round over
+//    the collected in-edges without one): round r accepts a tight edge u->v
+//    when u was resolved in an earlier round (round 1: dist[u] < dist[v];
+//    later rounds: equal distances, the zero-weight tie classes that make a
+//    plain argmin cycle, cf. algorithms.hpp:506-511).  Smallest u wins.
 // Also accumulates n_reach / m_reach for the bench's GTEPS.
 // ---------------------------------------------------------------------------
 template <class W, bool KEY = false>
@@ -816,36 +816,6 @@ k_pred_verify(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ ad
   }
 }
 
-// One repair round over ALL CSR rows of reached vertices (vertex-parallel,
-// warp per row).  Only runs when the verify pass left vertices unresolved.
-template <class W>
-__global__ void k_pred_repair(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ adj,
-                              const typename DT<W>::D* __restrict__ dist, uint32_t* cand,
-                              const uint32_t* res, const uint32_t* repair_bm, uint32_t n,
-                              uint32_t round) {
-  using D = typename DT<W>::D;
-  const int lane = threadIdx.x & 31;
-  uint32_t warps = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < n; u += warps) {
-    D du = dist[u];
-    if (du == dinf<W>()) continue;
-    // round 1: strictly decreasing tight edges from any reached u;
-    // round r > 1: equal-distance tight edges from u resolved before round r
-    uint32_t ru = res[u];
-    if (round > 1 && (ru == 0 || ru > round)) continue;
-    for (uint32_t e = ro[u] + lane; e < ro[u + 1]; e += 32) {
-      EdgeRec<W> rec = adj[e];
-      uint32_t v = rec.v;
-      if (!((repair_bm[v >> 5] >> (v & 31)) & 1u)) continue;
-      if (res[v] != 0) continue;
-      D dv = dist[v];
-      bool ok = round == 1 ? du < dv : du == dv;
-      if (!ok) continue;
-      if (dadd(du, rec.w, nullptr) == dv) atomicMin(cand + v, u);
-    }
-  }
-}
-
 // CSC repair round, one CTA per unresolved vertex (a hub's in-edge list is
 // hundreds of thousands long: one warp scanning it took 80 us per round at
 // s24).  The list length is read on the device (ctl->unresolved), so rounds
@@ -857,7 +827,7 @@ template <class W>
 __global__ void __launch_bounds__(256)
 k_pred_csc_block(const uint32_t* __restrict__ co, const EdgeRec<W>* __restrict__ cadj,
                  const typename DT<W>::D* __restrict__ dist, uint32_t* pred, uint32_t* res,
-                 const uint32_t* list, uint32_t round, Ctl* ctl) {
+                 const uint32_t* list, uint32_t round, Ctl* ctl, uint32_t base = 0) {
   using D = typename DT<W>::D;
   __shared__ uint32_t s_slot;
   const uint32_t count = ctl->unresolved;
@@ -880,7 +850,7 @@ k_pred_csc_block(const uint32_t* __restrict__ co, const EdgeRec<W>* __restrict__
             ok = du < dv;
           } else {
             const uint32_t ru = res[rec.v];
-            ok = du == dv && ru != 0 && ru <= round;
+            ok = du == dv && ru != 0 && ru <= base + round;
           }
         }
         if (ok) atomicMin(&s_slot, slot);
@@ -890,7 +860,7 @@ k_pred_csc_block(const uint32_t* __restrict__ co, const EdgeRec<W>* __restrict__
     }
     if (threadIdx.x == 0 && s_slot != NIL) {
       pred[v] = cadj[s_slot].v;
-      res[v] = round + 1;
+      res[v] = base + round + 1;
       ++done;
     }
     __syncthreads();
@@ -901,16 +871,143 @@ k_pred_csc_block(const uint32_t* __restrict__ co, const EdgeRec<W>* __restrict__
   }
 }
 
+// Key rounds (32-bit distances, before any in-edge scan): an unresolved v
+// failed verification only because its key's source u0 has dist[u0] ==
+// dist[v] (zero or absorbed weight) -- the edge is still tight.  Round k
+// accepts u0 once u0 is resolved with res[u0] <= k (verify resolves with 1)
+// and assigns k + 1, the equal-distance rule of the repair rounds, so chains
+// stay acyclic.  Only keys that point around a zero-weight cycle are left
+// for the in-edge rounds.
+template <class W>
+__global__ void k_pred_key_round(const uint32_t* __restrict__ list,
+                                 const unsigned long long* __restrict__ key,
+                                 const typename DT<W>::D* __restrict__ dist, uint32_t* pred,
+                                 uint32_t* res, uint32_t k, Ctl* ctl) {
+  const uint32_t count = ctl->unresolved;
+  uint32_t done = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+    const uint32_t v = list[i];
+    if (res[v] != 0) continue;
+    const uint32_t u = (uint32_t)key[v];
+    if (u == NIL || !(dist[u] == dist[v])) continue;
+    const uint32_t ru = res[u];
+    if (ru != 0 && ru <= k) {
+      pred[v] = u;
+      res[v] = k + 1;
+      ++done;
+    }
+  }
+  done = warp_sum(done);
+  if ((threadIdx.x & 31) == 0 && done) atomicAdd(&ctl->resolved, done);
+}
+
+// Repair without a transpose: one pass over the CSR collects the in-edges of
+// the (few) unresolved vertices into a list, then every round only scans the
+// list.  Rows are walked warp-per-32-rows (shuffle search for the owning row)
+// and rows longer than PR_BIG one CTA per row, so hubs do not serialise a
+// warp.  Overflow of the list (cap entries) sets ctl->err bit 2.
+constexpr uint32_t PR_BIG = 1024;
+template <class W>
+__device__ __forceinline__ void pr_emit(uint32_t u, const EdgeRec<W>& r, const uint32_t* repair_bm,
+                                        uint4* list, uint32_t cap, Ctl* ctl) {
+  if ((repair_bm[r.v >> 5] >> (r.v & 31)) & 1u) {
+    const uint32_t i = atomicAdd(&ctl->out_count, 1u);
+    if (i < cap) list[i] = make_uint4(u, r.v, *reinterpret_cast<const uint32_t*>(&r.w),
+                                      sizeof(W) == 8 ? reinterpret_cast<const uint32_t*>(&r.w)[1] : 0u);
+    else atomicOr(&ctl->err, 4u);
+  }
+}
+
+template <class W>
+__global__ void k_pred_inedges(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ adj,
+                               const uint32_t* __restrict__ repair_bm, uint32_t n, uint4* list,
+                               uint32_t cap, uint32_t* big, Ctl* ctl) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t i0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; i0 < n;
+       i0 += warps * 32) {
+    const uint32_t u = i0 + lane;
+    uint32_t s0 = 0, len = 0;
+    if (u < n) {
+      s0 = ro[u];
+      len = ro[u + 1] - s0;
+      if (len > PR_BIG) {
+        big[atomicAdd(&ctl->rec_count, 1u)] = u;
+        len = 0;
+      }
+    }
+    const uint32_t incl = warp_incl_scan(len, lane);
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    for (uint32_t x = lane; x - lane < tot; x += 32) {
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const uint32_t q = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+        if (q <= x) lo += step;
+      }
+      const uint32_t os = __shfl_sync(0xffffffffu, s0, lo);
+      const uint32_t opre = __shfl_sync(0xffffffffu, incl, lo) - __shfl_sync(0xffffffffu, len, lo);
+      if (x < tot) pr_emit<W>(i0 + lo, adj[os + (x - opre)], repair_bm, list, cap, ctl);
+    }
+  }
+}
+
+template <class W>
+__global__ void k_pred_inedges_big(const uint32_t* __restrict__ ro,
+                                   const EdgeRec<W>* __restrict__ adj,
+                                   const uint32_t* __restrict__ repair_bm, uint4* list,
+                                   uint32_t cap, const uint32_t* big, Ctl* ctl) {
+  const uint32_t cnt = ctl->rec_count;
+  for (uint32_t k = blockIdx.x; k < cnt; k += gridDim.x) {
+    const uint32_t u = big[k], s0 = ro[u], len = ro[u + 1] - s0;
+    for (uint32_t x = threadIdx.x; x < len; x += blockDim.x)
+      pr_emit<W>(u, adj[s0 + x], repair_bm, list, cap, ctl);
+  }
+}
+
+// One repair round over the collected in-edges (same acceptance rule as
+// k_pred_csc_block; smallest source wins through atomicMin on cand[v]).
+template <class W>
+__global__ void k_pred_list_round(const uint4* __restrict__ list, const Ctl* __restrict__ ctl,
+                                  uint32_t cap, const typename DT<W>::D* __restrict__ dist,
+                                  const uint32_t* __restrict__ res, uint32_t* cand,
+                                  uint32_t round, uint32_t base = 0) {
+  using D = typename DT<W>::D;
+  const uint32_t cnt = min(ctl->out_count, cap);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    const uint4 e = list[i];
+    if (res[e.y] != 0) continue;
+    W w;
+    if constexpr (sizeof(W) == 8) {
+      const unsigned long long b = ((unsigned long long)e.w << 32) | e.z;
+      w = *reinterpret_cast<const W*>(&b);
+    } else {
+      w = *reinterpret_cast<const W*>(&e.z);
+    }
+    const D du = dist[e.x], dv = dist[e.y];
+    if (du == dinf<W>() || !(dadd(du, w, nullptr) == dv)) continue;
+    bool ok;
+    if (round == 1) {
+      ok = du < dv;
+    } else {
+      const uint32_t ru = res[e.x];
+      ok = du == dv && ru != 0 && ru <= base + round;
+    }
+    if (ok) atomicMin(cand + e.y, e.x);
+  }
+}
+
 // Apply round `round`'s candidates; counts how many vertices were resolved.
 static __global__ void k_pred_apply(uint32_t* cand, uint32_t* pred, uint32_t* res,
-                             uint32_t* repair_bm, uint32_t n, uint32_t round, Ctl* ctl) {
+                             uint32_t* repair_bm, uint32_t n, uint32_t round, Ctl* ctl,
+                             uint32_t base = 0) {
   uint32_t stride = gridDim.x * blockDim.x;
   uint32_t done = 0;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
     uint32_t c = cand[v];
     if (c != NIL && res[v] == 0) {
       pred[v] = c;
-      res[v] = round + 1;
+      res[v] = base + round + 1;
       cand[v] = NIL;
       atomicAnd(repair_bm + (v >> 5), ~(1u << (v & 31)));
       ++done;

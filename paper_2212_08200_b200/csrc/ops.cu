@@ -50,7 +50,7 @@ static uint64_t bitmap_to_list(Ctx* c, const uint32_t* bits, uint64_t n, DBuf& o
   ensure_ctx_ctl(c);
   c->ensure_status(tiles + 1);
   cudaStream_t s = c->stream;
-  DBuf start, off, tseg;
+  TBuf start, off, tseg;
   if (*cap < n + 1) {
     out_list.alloc((n + 1) * 4, s);
     *cap = n + 1;
@@ -85,7 +85,7 @@ Frontier* frontier_create(Ctx* c, uint64_t n, int repr) {
 void frontier_assign(Frontier* f, const uint32_t* list, uint64_t k) {
   Ctx* c = f->ctx;
   cudaStream_t s = c->stream;
-  DBuf tmp, bad;
+  TBuf tmp, bad;
   tmp.alloc(k * 4, s);
   bad.alloc(8, s);
   if (k) GFB_CUDA(cudaMemcpyAsync(tmp.p, list, k * 4, cudaMemcpyHostToDevice, s));
@@ -112,7 +112,7 @@ void frontier_assign(Frontier* f, const uint32_t* list, uint64_t k) {
 uint64_t frontier_size(Frontier* f) {
   if (f->repr == GFB_SPARSE) return f->len;
   Ctx* c = f->ctx;
-  DBuf cnt;
+  TBuf cnt;
   cnt.alloc(8, c->stream);
   GFB_CUDA(cudaMemsetAsync(cnt.p, 0, 8, c->stream));
   k_popcount<<<stride_grid(c), 256, 0, c->stream>>>(f->bits.as<uint32_t>(), f->nwords(),
@@ -133,7 +133,7 @@ void frontier_read(Frontier* f, uint32_t* out, uint64_t cap, uint64_t* k) {
     c->sync();
     return;
   }
-  DBuf lst;
+  TBuf lst;
   uint64_t lcap = 0;
   uint64_t len = bitmap_to_list(c, f->bits.as<uint32_t>(), f->n, lst, &lcap);
   *k = len;
@@ -146,7 +146,7 @@ void frontier_read(Frontier* f, uint32_t* out, uint64_t cap, uint64_t* k) {
 // Operator calls
 // ---------------------------------------------------------------------------
 struct OpPlan {
-  DBuf v, start, off, tseg;
+  TBuf v, start, off, tseg;
 };
 
 // Plan of the input frontier (vertices with out-degree > 0, order kept).
@@ -319,10 +319,11 @@ void advance_push(Ctx* c, const Graph* g, Frontier* in, Frontier* out, int op, v
 
 void advance_pull(Ctx* c, const Graph* g, Frontier* in, Frontier* out, int op, void* state) {
   check_op(g, in, out, op, state);
-  if (!g->has_csc)  // operators.hpp:299-300
+  if (!g->csc_wanted)  // operators.hpp:299-300
     fail(GFB_EINVAL, "neighbors_expand_pull: transpose not built");
   if (in->repr != GFB_DENSE || out->repr != GFB_DENSE)  // operators.hpp:301-302
     fail(GFB_EINVAL, "neighbors_expand_pull: dense frontier required");
+  ensure_csc(const_cast<Graph*>(g));
   if (op == GFB_OP_RECORD) ensure_ceid(const_cast<Graph*>(g));  // CSR ids of CSC slots
   if (g->wtype == GFB_W_F32) pull_impl<float>(c, g, in, out, op, state);
   else if (g->wtype == GFB_W_F64) pull_impl<double>(c, g, in, out, op, state);
@@ -336,13 +337,13 @@ void filter_unique(Ctx* c, Frontier* in, Frontier* out) {
   if (in->n != out->n) fail(GFB_EINVAL, "uniquify: frontier sizes differ");
   cudaStream_t s = c->stream;
   const uint64_t nwords = in->nwords();
-  DBuf bits;
+  TBuf bits;
   bits.alloc(nwords * 4, s);
   GFB_CUDA(cudaMemsetAsync(bits.p, 0, nwords * 4, s));
   if (in->len)
     k_set_bits<<<stride_grid(c), 256, 0, s>>>(in->list.as<uint32_t>(), in->len, bits.as<uint32_t>());
   GFB_CUDA(cudaGetLastError());
-  DBuf lst;
+  TBuf lst;
   uint64_t lcap = 0;
   uint64_t len = bitmap_to_list(c, bits.as<uint32_t>(), in->n, lst, &lcap);
   out->reserve(std::max<uint64_t>(len, 1));
@@ -397,7 +398,7 @@ void dist_read(Dist* d, double* out, uint64_t* relax) {
   const Graph* g = d->g;
   uint32_t n = (uint32_t)g->n;
   if (out) {
-    DBuf tmp;
+    TBuf tmp;
     tmp.alloc((size_t)n * 8, c->stream);
     if (g->wtype == GFB_W_F32) k_widen2<float><<<stride_grid(c), 256, 0, c->stream>>>(d->dist.as<float>(), tmp.as<double>(), n);
     else if (g->wtype == GFB_W_F64) k_widen2<double><<<stride_grid(c), 256, 0, c->stream>>>(d->dist.as<double>(), tmp.as<double>(), n);

@@ -109,6 +109,8 @@ static __global__ void k_plan_tiles(Plan p, const uint32_t* deg, uint32_t K, uin
   }
 }
 
+constexpr uint32_t PRED_KEY_ROUNDS = 4;
+
 template <class W>
 struct Runner {
   using D = typename DT<W>::D;
@@ -313,7 +315,7 @@ struct Runner {
       b.can_pull = dir == GFB_DIR_AUTO && g->has_csc ? 1 : 0;
       b.force_pull = dir == GFB_DIR_PULL ? 1 : 0;
       const char* tr = getenv("GFB_TRACE");
-      DBuf trace;
+      TBuf trace;
       if (tr && tr[0] == '1') {
         b.trace_cap = 4096;
         trace.alloc(b.trace_cap * 8, s);
@@ -406,7 +408,7 @@ struct Runner {
 
   void sort_plan(uint32_t K, uint32_t T, bool desc, int begin_bit = 0) {
     if (K < 2) return;
-    DBuf keys, keys2, idx, idx2, v2, s2, deg, tmp;
+    TBuf keys, keys2, idx, idx2, v2, s2, deg, tmp;
     keys.alloc((size_t)K * 4, s); keys2.alloc((size_t)K * 4, s);
     idx.alloc((size_t)K * 4, s); idx2.alloc((size_t)K * 4, s);
     v2.alloc((size_t)K * 4, s); s2.alloc((size_t)K * 4, s); deg.alloc((size_t)(K + 1) * 4, s);
@@ -646,56 +648,71 @@ struct Runner {
     GFB_CUDA(cudaGetLastError());
     ++kernels;
     if (!want) return;
-    if (g->has_csc) {
-      // two repair rounds queued without a host round trip (block per vertex,
-      // list length read on the device); more only for deep zero-weight ties
-      const uint32_t grid = c->num_sms * 8;
-      for (uint32_t round = 1; round <= 2; ++round) {
-        GFB_CUDA(cudaMemsetAsync(&ws->ctl.as<Ctl>()->flag, 0, 4, s));
-        k_pred_csc_block<W><<<grid, 256, 0, s>>>(
-            g->co.as<uint32_t>(), g->cadj.as<EdgeRec<W>>(), ws->dist.as<D>(),
-            ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(), ws->cand.as<uint32_t>(), round,
-            ws->ctl.as<Ctl>());
+    Ctl* dctl = ws->ctl.as<Ctl>();
+    // key rounds first (no in-edge scan): queued, one host read afterwards
+    uint32_t base = 0;
+    if (key_mode()) {
+      if constexpr (sizeof(D) == 4) {
+        for (uint32_t k = 1; k <= PRED_KEY_ROUNDS; ++k)
+          k_pred_key_round<W><<<c->num_sms, 256, 0, s>>>(
+              ws->cand.as<uint32_t>(), ws->predrec.as<unsigned long long>(), ws->dist.as<D>(),
+              ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(), k, dctl);
         GFB_CUDA(cudaGetLastError());
-        ++kernels;
+        kernels += PRED_KEY_ROUNDS;
+        base = PRED_KEY_ROUNDS;
       }
-      Ctl h = c->read_ctl(ws->ctl.as<Ctl>());
-      *fallback = h.unresolved;
-      uint64_t left = h.unresolved - std::min(h.unresolved, h.resolved);
-      if (left > 0 && h.flag == 0)
-        fail(GFB_ELOGIC, "sssp: predecessor repair made no progress");
-      for (uint32_t round = 3; left > 0; ++round) {
-        GFB_CUDA(cudaMemsetAsync(&ws->ctl.as<Ctl>()->flag, 0, 4, s));
+    }
+    Ctl h = c->read_ctl(dctl);
+    *fallback = h.unresolved;
+    uint64_t left = h.unresolved - std::min(h.unresolved, h.resolved);
+    if (left == 0) return;
+    // in-edge rounds: res values continue above the key rounds' (base)
+    if (g->has_csc) {
+      const uint32_t grid = c->num_sms * 8;
+      for (uint32_t round = 1; left > 0; ++round) {
+        GFB_CUDA(cudaMemsetAsync(&dctl->flag, 0, 4, s));
         k_pred_csc_block<W><<<grid, 256, 0, s>>>(
             g->co.as<uint32_t>(), g->cadj.as<EdgeRec<W>>(), ws->dist.as<D>(),
-            ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(), ws->cand.as<uint32_t>(), round,
-            ws->ctl.as<Ctl>());
+            ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(), ws->cand.as<uint32_t>(), round, dctl,
+            base);
         GFB_CUDA(cudaGetLastError());
         ++kernels;
-        Ctl r = c->read_ctl(ws->ctl.as<Ctl>());
-        if (r.flag == 0) fail(GFB_ELOGIC, "sssp: predecessor repair made no progress");
+        Ctl r = c->read_ctl(dctl);
+        // round 1 (strict edges) may resolve nothing when every unresolved
+        // vertex sits in a zero-weight tie class; later rounds must progress
+        if (r.flag == 0 && round > 1) fail(GFB_ELOGIC, "sssp: predecessor repair made no progress");
         left -= std::min<uint64_t>(left, r.flag);
       }
       return;
     }
-    Ctl h = c->read_ctl(ws->ctl.as<Ctl>());
-    *fallback = h.unresolved;
-    if (h.unresolved == 0) return;
-    uint64_t left = h.unresolved;
-    // no CSC: candidate rounds over every CSR row (O(m) per round)
+    // no transpose: collect the unresolved vertices' in-edges in one CSR pass,
+    // then run the rounds over that list
+    const uint32_t cap = (uint32_t)std::min<uint64_t>(g->m + 1, 1u << 22);
+    TBuf list, big;
+    list.alloc((size_t)cap * 16, s);
+    big.alloc((size_t)n * 4 + 4, s);
+    GFB_CUDA(cudaMemsetAsync(&dctl->out_count, 0, 8, s));  // out_count, rec_count
+    k_pred_inedges<W><<<stride_grid(c), 256, 0, s>>>(g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(),
+                                                     ws->repair_bm.as<uint32_t>(), n,
+                                                     list.as<uint4>(), cap, big.as<uint32_t>(), dctl);
+    k_pred_inedges_big<W><<<stride_grid(c), 256, 0, s>>>(
+        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(), ws->repair_bm.as<uint32_t>(),
+        list.as<uint4>(), cap, big.as<uint32_t>(), dctl);
     GFB_CUDA(cudaMemsetAsync(ws->cand.p, 0xFF, (size_t)n * 4, s));
+    kernels += 2;
     for (uint32_t round = 1; left > 0; ++round) {
-      GFB_CUDA(cudaMemsetAsync(&ws->ctl.as<Ctl>()->flag, 0, 4, s));
-      k_pred_repair<W><<<stride_grid(c), 256, 0, s>>>(
-          g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(), ws->dist.as<D>(), ws->cand.as<uint32_t>(),
-          ws->res.as<uint32_t>(), ws->repair_bm.as<uint32_t>(), n, round);
+      GFB_CUDA(cudaMemsetAsync(&dctl->flag, 0, 4, s));
+      k_pred_list_round<W><<<stride_grid(c), 256, 0, s>>>(list.as<uint4>(), dctl, cap,
+                                                          ws->dist.as<D>(), ws->res.as<uint32_t>(),
+                                                          ws->cand.as<uint32_t>(), round, base);
       k_pred_apply<<<stride_grid(c), 256, 0, s>>>(ws->cand.as<uint32_t>(), ws->pred.as<uint32_t>(),
                                                   ws->res.as<uint32_t>(),
-                                                  ws->repair_bm.as<uint32_t>(), n, round,
-                                                  ws->ctl.as<Ctl>());
+                                                  ws->repair_bm.as<uint32_t>(), n, round, dctl,
+                                                  base);
       GFB_CUDA(cudaGetLastError());
       kernels += 2;
-      Ctl r = c->read_ctl(ws->ctl.as<Ctl>());
+      Ctl r = c->read_ctl(dctl);
+      if (r.err & 4u) fail(GFB_ELOGIC, "sssp: predecessor repair list overflow");
       if (r.flag == 0 && round > 1)
         fail(GFB_ELOGIC, "sssp: predecessor repair made no progress");
       left -= std::min<uint64_t>(left, r.flag);
@@ -705,8 +722,14 @@ struct Runner {
 
 void sssp_run(Ctx* c, Graph* g, uint32_t source, const gfb_sssp_opts* o, gfb_sssp_stats* st) {
   if (source >= g->n) fail(GFB_ERANGE, "sssp: source out of range");  // algorithms.hpp:572
-  if (o->direction == GFB_DIR_PULL && !g->has_csc)                     // algorithms.hpp:573-574
+  if (o->direction == GFB_DIR_PULL && !g->csc_wanted)                  // algorithms.hpp:573-574
     fail(GFB_EINVAL, "sssp: pull direction requires a built transpose");
+  // the transpose only when a superstep can pull (AUTO pulls when frontier
+  // edges exceed m / alpha: impossible for alpha <= 1)
+  const float alpha = o->pull_alpha > 0 ? o->pull_alpha : 0.25f;
+  if (o->direction == GFB_DIR_PULL || (o->direction == GFB_DIR_AUTO && alpha > 1.0f &&
+                                       o->delta <= 0))
+    ensure_csc(g);
   if (o->direction < GFB_DIR_PUSH || o->direction > GFB_DIR_AUTO)
     fail(GFB_EINVAL, "sssp: bad direction");
   Workspace* ws = ensure_ws(g);
@@ -732,7 +755,7 @@ void sssp_read(Graph* g, double* dist, void* dist_native, uint32_t* pred) {
   cudaStream_t s = c->stream;
   const uint32_t n = (uint32_t)g->n;
   if (dist) {
-    DBuf tmp;
+    TBuf tmp;
     tmp.alloc((size_t)n * 8, s);
     if (g->wtype == GFB_W_F32) k_widen<float><<<stride_grid(c), 256, 0, s>>>(ws->dist.as<float>(), tmp.as<double>(), n);
     else if (g->wtype == GFB_W_F64) k_widen<double><<<stride_grid(c), 256, 0, s>>>(ws->dist.as<double>(), tmp.as<double>(), n);
