@@ -34,6 +34,11 @@ namespace gfb {
 namespace cgn = cooperative_groups;
 
 constexpr int NF_THREADS = 1024;
+// LH > 0: a warp chases up to LH rounds of its own near activations from a
+// warp-local queue of NF_LQ entries before the grid barrier -- chaotic
+// relaxation inside a phase (still the same fixpoint), fewer phases on
+// high-diameter graphs.
+constexpr uint32_t NF_LQ = 128;
 
 template <class W>
 struct NfArgs {
@@ -79,7 +84,7 @@ __device__ __forceinline__ void warp_append(bool flag, uint2 e, uint2* q, uint32
 // vertex has since been lowered again is stale (the lowering appended a newer
 // entry) and is skipped -- dedup without a membership bitmap or a returning
 // atomic on the critical path.
-template <class W>
+template <class W, int LH = 0>
 __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
   using D = typename DT<W>::D;
   static_assert(sizeof(D) == 4, "packed predecessor keys need 32-bit distances");
@@ -88,7 +93,9 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
   const uint32_t gtid = blockIdx.x * NF_THREADS + threadIdx.x;
   const uint32_t gthreads = gridDim.x * NF_THREADS;
   const uint32_t gwarp = gtid >> 5, nwarps = gthreads >> 5;
+  const int warp = threadIdx.x >> 5;
   unsigned* err = &a.ctl->err;
+  __shared__ uint2 s_lq[NF_THREADS / 32][LH > 0 ? NF_LQ : 1];  // warp-local near queues
 
   // ---- init (algorithms.hpp:579-583) ----
   const uint32_t source = *a.src_ptr;
@@ -120,13 +127,13 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
     if (K > 0) {
       // ---------------- near phase: expand the near queue ----------------
       ++phases;
-      for (uint32_t base = gwarp * 32; base < K; base += nwarps * 32) {
-        // lane j holds queue entry base+j: vertex, row, degree, distance
-        const uint32_t j = base + lane;
+      uint32_t lq_n = 0;  // warp-local queue fill (warp-uniform)
+      // Expand one queue entry per lane (valid lanes only); near activations go
+      // to the warp-local queue while it has room (LH > 0), else global.
+      auto expand = [&](bool valid, uint2 e) {
         uint32_t u = 0, st = 0, deg = 0;
         D du = D(0);
-        if (j < K) {
-          const uint2 e = __ldcg(qin + j);
+        if (valid) {
           u = e.x;
           st = a.ro[u];
           const uint32_t en = a.ro[u + 1];
@@ -163,9 +170,43 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
               to_far = !to_near;
             }
           }
-          warp_append(to_near, ent, qout, cout, a.cap, err);
+          if constexpr (LH > 0) {
+            const unsigned m = __ballot_sync(0xffffffffu, to_near);
+            const uint32_t room = NF_LQ - lq_n;
+            const uint32_t rank = __popc(m & lanemask_lt());
+            const bool loc = to_near && rank < room;
+            if (loc) s_lq[warp][lq_n + rank] = ent;
+            lq_n += min((uint32_t)__popc(m), room);
+            __syncwarp();
+            warp_append(to_near && !loc, ent, qout, cout, a.cap, err);
+          } else {
+            warp_append(to_near, ent, qout, cout, a.cap, err);
+          }
           warp_append(to_far, ent, a.fq[fp], a.cnt + 3 + fp, a.cap, err);
         }
+      };
+      for (uint32_t base = gwarp * 32; base < K; base += nwarps * 32) {
+        const uint32_t j = base + lane;
+        expand(j < K, j < K ? __ldcg(qin + j) : make_uint2(0, 0));
+        if constexpr (LH > 0) {
+          // chase this warp's own near activations without a grid barrier
+          for (int hop = 0; hop < LH && lq_n > 0; ++hop) {
+            const uint32_t take = min(lq_n, 32u);
+            const bool v = (uint32_t)lane < take;
+            const uint2 e = v ? s_lq[warp][lq_n - take + lane] : make_uint2(0, 0);
+            lq_n -= take;
+            __syncwarp();
+            expand(v, e);
+          }
+        }
+      }
+      if constexpr (LH > 0) {  // hand the rest to the next phase
+        for (uint32_t b0 = 0; b0 < lq_n; b0 += 32) {
+          const bool v = b0 + lane < lq_n;
+          warp_append(v, v ? s_lq[warp][b0 + lane] : make_uint2(0, 0), qout, cout, a.cap, err);
+        }
+        lq_n = 0;
+        __syncwarp();
       }
       grid.sync();
       continue;

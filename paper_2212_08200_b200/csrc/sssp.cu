@@ -367,7 +367,13 @@ struct Runner {
   // Near-far filter (opts.delta > 0): one persistent launch (nearfar.cuh).
   bool nearfar_launch(double delta) {
     if constexpr (sizeof(D) == 4) {
-      auto kern = k_nearfar<W>;
+      // warp-local chasing of 4 rounds (measured on the 4096^2 grid: no
+      // chasing 110 ms, LH 2/4/8/16 at delta 8: 72/67/70/84 ms; LH 4 with
+      // delta 32: 56 ms); variants 90-92: LH 0 / 8 / 16
+      auto kern = k_nearfar<W, 4>;
+      if (variant == 90) kern = k_nearfar<W, 0>;
+      else if (variant == 91) kern = k_nearfar<W, 8>;
+      else if (variant == 92) kern = k_nearfar<W, 16>;
       int per_sm = 0;
       GFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NF_THREADS, 0));
       if (per_sm <= 0) return false;
