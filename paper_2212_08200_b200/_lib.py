@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libgfb.so")
+LIB_PATH = os.environ.get("GFB_LIB") or os.path.join(HERE, "lib", "libgfb.so")
 
 GFB_OK, GFB_EINVAL, GFB_ERANGE, GFB_ELOGIC, GFB_ECUDA, GFB_ENOMEM, GFB_ENCCL = range(7)
 W_U32, W_F32, W_F64 = 0, 1, 2
