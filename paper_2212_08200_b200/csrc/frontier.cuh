@@ -293,11 +293,15 @@ k_fcount_o(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uin
 
 // Bucket totals -> bucket cursors (exclusive scan), plan totals, bookkeeping.
 // One warp.  btot is cleared for the next superstep.
+// defer_pct < 100: buckets past the one where the cumulative frontier edges
+// reach defer_pct% stay pending in the bitmap for the next superstep (a soft
+// near-far split inside BSP), when the frontier has >= defer_min edges.
 static __global__ void k_fscan_o(unsigned long long* btot, unsigned long long* bcur, Plan plan,
                                  Ctl* ctl, uint32_t m, float alpha, int can_pull, int force_pull,
                                  cudaGraphConditionalHandle loop_handle,
                                  cudaGraphConditionalHandle mode_handle, int set_loop,
-                                 int set_mode) {
+                                 int set_mode, uint32_t defer_pct = 100,
+                                 uint32_t defer_min = 0, uint32_t defer_floor = 0) {
   const int lane = threadIdx.x;
   static_assert(OB_N <= 32, "one warp scans the bucket totals");
   const unsigned long long x = lane < OB_N ? btot[lane] : 0ull;
@@ -307,13 +311,27 @@ static __global__ void k_fscan_o(unsigned long long* btot, unsigned long long* b
     const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, d);
     if (lane >= d) incl += y;
   }
+  const unsigned long long all = __shfl_sync(0xffffffffu, incl, 31);
+  const uint32_t T_all = (uint32_t)all;
+  uint32_t cut = OB_N - 1;
+  if (defer_pct < 100 && T_all >= defer_min) {
+    // first bucket whose inclusive edge count reaches defer_pct% of all (and
+    // at least defer_floor edges: enough work to fill the GPU)
+    const uint64_t need = max((uint64_t)T_all * defer_pct, (uint64_t)defer_floor * 100);
+    const bool reach = (uint64_t)(uint32_t)incl * 100 >= need;
+    const unsigned bal = __ballot_sync(0xffffffffu, reach && lane < OB_N);
+    if (bal) cut = __ffs(bal) - 1;
+  }
+  const unsigned long long upto = __shfl_sync(0xffffffffu, incl, cut);
   if (lane < OB_N) {
     bcur[lane] = incl - x;
     btot[lane] = 0;
   }
-  if (lane == 31)
-    plan_totals((uint32_t)(incl >> 32), (uint32_t)incl, plan, ctl, m, alpha, can_pull,
+  if (lane == 31) {
+    ctl->bcut = cut;
+    plan_totals((uint32_t)(upto >> 32), (uint32_t)upto, plan, ctl, m, alpha, can_pull,
                 force_pull, loop_handle, mode_handle, set_loop, set_mode);
+  }
 }
 
 // Write: each tile reserves its cell in every bucket (one global atomic per
@@ -328,32 +346,38 @@ k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
            const unsigned long long* __restrict__ agg, unsigned long long* bcur, Plan plan) {
   __shared__ unsigned long long s_cur[OB_N];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t cut = ctl->bcut;
   if (threadIdx.x < OB_N) {
     const unsigned long long x = agg[(size_t)blockIdx.x * OB_N + threadIdx.x];
-    s_cur[threadIdx.x] = x ? atomicAdd(bcur + threadIdx.x, x) : 0ull;
+    s_cur[threadIdx.x] = x && threadIdx.x <= cut ? atomicAdd(bcur + threadIdx.x, x) : 0ull;
   }
   const uint32_t base = ctl->blo >> OB_SHIFT;
   const uint32_t wbase = blockIdx.x * F_WORDS + warp * F_WPW;
   WarpWords w;
   uint32_t raw;
   load_warp_words(ro, bm_next, nwords, wbase, w, &raw);
-  if (lane < F_WPW && wbase + lane < nwords) {
-    if (bm_cur) bm_cur[wbase + lane] = raw;
-    bm_next[wbase + lane] = 0;
-  }
   __syncthreads();
+  uint32_t pend = 0;  // this lane's word (lane < F_WPW): bits deferred to the next superstep
 #pragma unroll
   for (int j = 0; j < F_WPW; ++j) {
-    if ((w.keep[j] >> lane) & 1u) {
-      const uint32_t v = (wbase + j) * 32 + lane;
-      const unsigned long long c =
-          atomicAdd(&s_cur[obucket(dist, v, base)], (1ull << 32) | w.deg[j]);
+    const bool kept = (w.keep[j] >> lane) & 1u;
+    const uint32_t v = (wbase + j) * 32 + lane;
+    const uint32_t b = kept ? obucket(dist, v, base) : 0u;
+    const bool place = kept && b <= cut;
+    const unsigned dm = __ballot_sync(0xffffffffu, kept && !place);
+    if (lane == j) pend = dm;
+    if (place) {
+      const unsigned long long c = atomicAdd(&s_cur[b], (1ull << 32) | w.deg[j]);
       const uint32_t gi = (uint32_t)(c >> 32), eoff = (uint32_t)c;
       plan.v[gi] = v;
       plan.start[gi] = w.st[j];
       plan.off[gi] = eoff;
       tile_map_entries(plan, gi, eoff, w.deg[j]);
     }
+  }
+  if (lane < F_WPW && wbase + lane < nwords) {
+    if (bm_cur) bm_cur[wbase + lane] = raw & ~pend;
+    bm_next[wbase + lane] = pend;
   }
 }
 

@@ -45,6 +45,7 @@ struct Ctl {
   // distance of the frontier being built (float bits, written by the push
   // advance) and the value frozen for the compaction in progress
   uint32_t fmin, blo;
+  uint32_t bcut;       // ordered compaction: buckets above bcut stay pending
 };
 
 // Expansion plan: the frontier restricted to vertices with out-degree > 0.
