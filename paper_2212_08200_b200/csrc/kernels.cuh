@@ -883,7 +883,7 @@ template <class W>
 __global__ void k_pred_key_round(const uint32_t* __restrict__ list,
                                  const unsigned long long* __restrict__ key,
                                  const typename DT<W>::D* __restrict__ dist, uint32_t* pred,
-                                 uint32_t* res, uint32_t k, Ctl* ctl) {
+                                 uint32_t* res, uint32_t* repair_bm, uint32_t k, Ctl* ctl) {
   const uint32_t count = ctl->unresolved;
   uint32_t done = 0;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
@@ -895,6 +895,7 @@ __global__ void k_pred_key_round(const uint32_t* __restrict__ list,
     if (ru != 0 && ru <= k) {
       pred[v] = u;
       res[v] = k + 1;
+      atomicAnd(repair_bm + (v >> 5), ~(1u << (v & 31)));  // off the in-edge scan
       ++done;
     }
   }

@@ -690,22 +690,31 @@ struct Runner {
     ++kernels;
     if (!want) return;
     Ctl* dctl = ws->ctl.as<Ctl>();
-    // key rounds first (no in-edge scan): queued, one host read afterwards
+    // key rounds first (no in-edge scan), queued in batches of
+    // PRED_KEY_ROUNDS with one host read per batch; long zero-weight tie
+    // chains (u32 weights) take more batches while they make progress
     uint32_t base = 0;
-    if (key_mode()) {
-      if constexpr (sizeof(D) == 4) {
-        for (uint32_t k = 1; k <= PRED_KEY_ROUNDS; ++k)
-          k_pred_key_round<W><<<c->num_sms, 256, 0, s>>>(
-              ws->cand.as<uint32_t>(), ws->predrec.as<unsigned long long>(), ws->dist.as<D>(),
-              ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(), k, dctl);
-        GFB_CUDA(cudaGetLastError());
-        kernels += PRED_KEY_ROUNDS;
-        base = PRED_KEY_ROUNDS;
+    Ctl h = {};
+    uint64_t left = 0;
+    for (uint32_t done_before = 0;;) {
+      if (key_mode()) {
+        if constexpr (sizeof(D) == 4) {
+          for (uint32_t k = base + 1; k <= base + PRED_KEY_ROUNDS; ++k)
+            k_pred_key_round<W><<<c->num_sms, 256, 0, s>>>(
+                ws->cand.as<uint32_t>(), ws->predrec.as<unsigned long long>(), ws->dist.as<D>(),
+                ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(), ws->repair_bm.as<uint32_t>(), k,
+                dctl);
+          GFB_CUDA(cudaGetLastError());
+          kernels += PRED_KEY_ROUNDS;
+          base += PRED_KEY_ROUNDS;
+        }
       }
+      h = c->read_ctl(dctl);
+      *fallback = h.unresolved;
+      left = h.unresolved - std::min(h.unresolved, h.resolved);
+      if (left == 0 || !key_mode() || h.resolved == done_before || base >= 64) break;
+      done_before = h.resolved;
     }
-    Ctl h = c->read_ctl(dctl);
-    *fallback = h.unresolved;
-    uint64_t left = h.unresolved - std::min(h.unresolved, h.resolved);
     if (left == 0) return;
     // in-edge rounds: res values continue above the key rounds' (base)
     if (g->has_csc) {
@@ -728,19 +737,26 @@ struct Runner {
     }
     // no transpose: collect the unresolved vertices' in-edges in one CSR pass,
     // then run the rounds over that list
-    const uint32_t cap = (uint32_t)std::min<uint64_t>(g->m + 1, 1u << 22);
+    uint32_t cap = (uint32_t)std::min<uint64_t>(g->m + 1, 1u << 22);
     TBuf list, big;
-    list.alloc((size_t)cap * 16, s);
     big.alloc((size_t)n * 4 + 4, s);
-    GFB_CUDA(cudaMemsetAsync(&dctl->out_count, 0, 8, s));  // out_count, rec_count
-    k_pred_inedges<W><<<stride_grid(c), 256, 0, s>>>(g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(),
-                                                     ws->repair_bm.as<uint32_t>(), n,
-                                                     list.as<uint4>(), cap, big.as<uint32_t>(), dctl);
-    k_pred_inedges_big<W><<<stride_grid(c), 256, 0, s>>>(
-        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(), ws->repair_bm.as<uint32_t>(),
-        list.as<uint4>(), cap, big.as<uint32_t>(), dctl);
+    for (int attempt = 0;; ++attempt) {  // a second pass with the exact size on overflow
+      list.alloc((size_t)cap * 16, s);
+      GFB_CUDA(cudaMemsetAsync(&dctl->out_count, 0, 8, s));  // out_count, rec_count
+      GFB_CUDA(cudaMemsetAsync(&dctl->err, 0, 4, s));
+      k_pred_inedges<W><<<stride_grid(c), 256, 0, s>>>(
+          g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(), ws->repair_bm.as<uint32_t>(), n,
+          list.as<uint4>(), cap, big.as<uint32_t>(), dctl);
+      k_pred_inedges_big<W><<<stride_grid(c), 256, 0, s>>>(
+          g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(), ws->repair_bm.as<uint32_t>(),
+          list.as<uint4>(), cap, big.as<uint32_t>(), dctl);
+      kernels += 2;
+      const Ctl r = c->read_ctl(dctl);
+      if (!(r.err & 4u)) break;
+      if (attempt > 0) fail(GFB_ELOGIC, "sssp: predecessor repair list overflow");
+      cap = r.out_count;  // every in-edge was counted, stored or not
+    }
     GFB_CUDA(cudaMemsetAsync(ws->cand.p, 0xFF, (size_t)n * 4, s));
-    kernels += 2;
     for (uint32_t round = 1; left > 0; ++round) {
       GFB_CUDA(cudaMemsetAsync(&dctl->flag, 0, 4, s));
       k_pred_list_round<W><<<stride_grid(c), 256, 0, s>>>(list.as<uint4>(), dctl, cap,

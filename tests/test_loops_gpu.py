@@ -117,3 +117,22 @@ def test_relabel_view_is_permuted_csr(ctx):
         a = sorted(zip(perm[col[ro[p]:ro[p + 1]]].tolist(), w[ro[p]:ro[p + 1]].tolist()))
         b = sorted(zip(dst[ro2[i]:ro2[i + 1]].tolist(), ww[ro2[i]:ro2[i + 1]].tolist()))
         assert a == b
+
+
+def test_default_path_rmat20_bit_exact(ctx):
+    """The default BSP path at a size where every optimisation is active:
+    relabelled CSR (n >= 2^20), distance-ordered compaction and the deferral
+    of far buckets (frontiers with >= m/4 edges) -- bit-exact vs the oracle,
+    valid predecessor tree, and the deferral actually cut the work."""
+    g = gb.rmat(20, 16, seed=1, wtype="f32", transpose=True, ctx=ctx)
+    dist, pred, st = gb.sssp_stats(g, 0)
+    _check(g, dist, pred)
+    _, _, plain = gb.sssp_stats(g, 0, want_result=False, variant=99)  # deferral off
+    assert st.relaxations < 0.8 * plain.relaxations
+
+
+@pytest.mark.parametrize("src", [1, 12345])
+def test_default_path_rmat20_other_sources_u32(ctx, src):
+    g = gb.rmat(20, 16, seed=5, wtype="u32", transpose=False, ctx=ctx)
+    dist, pred, st = gb.sssp_stats(g, src, direction="push")
+    _check(g, dist, pred, source=src, wtype="u32")
