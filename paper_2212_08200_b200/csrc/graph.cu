@@ -189,6 +189,7 @@ static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const 
                        int htype) {
   g->nz_valid = false;
   g->rl_valid = false;
+  g->runs_since_fill = 0;
   Ctx* c = g->ctx;
   cudaStream_t s = c->stream;
   const uint64_t n = g->n, m = g->m;

@@ -69,6 +69,7 @@ struct Graph {
   // destinations share distance cache lines.  4-byte weights only.
   DBuf rl_ro, rl_adj, rl_perm, rl_iperm;
   bool rl_valid = false;
+  uint32_t runs_since_fill = 0;  // sssp calls on the current contents (relabel pays on reuse)
   bool rl_skip = false;  // in-degrees not skewed enough to pay (no arrays built)
   // static pull plan (destinations with in-degree > 0)
   uint32_t pull_k = 0, pull_total = 0;
@@ -121,7 +122,7 @@ struct Workspace {
   // device loop: one instantiated CUDA graph per (direction, alpha, variant)
   cudaGraphExec_t loop_exec = nullptr;
   cudaGraph_t loop_graph = nullptr;
-  int loop_key[3] = {-1, -1, -1};
+  int loop_key[4] = {-1, -1, -1, -1};
   Ctl* ctl_host = nullptr;  // pinned
   uint32_t compact_tiles = 0;
   uint32_t status_len = 0;

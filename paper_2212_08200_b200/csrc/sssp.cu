@@ -567,10 +567,13 @@ struct Runner {
     const float alpha = o->pull_alpha > 0 ? o->pull_alpha : 0.25f;
     // The relabelled CSR has no CSC: only when no superstep can pull (the
     // AUTO switch needs frontier edges > m / alpha, impossible for alpha <= 1).
-    // Default for 32-bit distances on graphs with >= 2^20 vertices (measured
-    // at s24: 6.10 -> 5.86 ms); variants 60-62 keep the caller's ids.
+    // Default for 32-bit distances on graphs with >= 2^20 vertices from the
+    // second SSSP on the same contents on (the copy costs ~6 ms at s24 and
+    // saves ~0.3 ms per call, so it pays on reuse, not for a one-shot
+    // upload + SSSP); variant 41 forces it, 60-62 keep the caller's ids.
+    const bool reuse = g->runs_since_fill++ > 0 || g->rl_valid;
     rl = key_mode() && o->delta <= 0 &&
-         (variant == 41 || ((variant == 0 || variant >= 99) && n >= (1u << 20))) &&
+         (variant == 41 || ((variant == 0 || variant >= 99) && n >= (1u << 20) && reuse)) &&
          (dir == GFB_DIR_PUSH || (dir == GFB_DIR_AUTO && (alpha <= 1.0f || !g->has_csc)));
     if (rl) {
       ensure_relabel(g);
@@ -599,7 +602,7 @@ struct Runner {
     if (!done && o->device_loop && persistent()) done = bsp_run(dir, alpha);
     if (done) {
     } else if (o->device_loop) {
-      int key[3] = {dir, (int)(alpha * 1000), variant};
+      int key[4] = {dir, (int)(alpha * 1000), variant, rl ? 1 : 0};  // graph holds the loop's arrays
       if (!ws->loop_exec || memcmp(key, ws->loop_key, sizeof(key)) != 0) {
         GFB_CUDA(cudaStreamSynchronize(s));
         build_loop_graph(dir, alpha);

@@ -136,3 +136,25 @@ def test_default_path_rmat20_other_sources_u32(ctx, src):
     g = gb.rmat(20, 16, seed=5, wtype="u32", transpose=False, ctx=ctx)
     dist, pred, st = gb.sssp_stats(g, src, direction="push")
     _check(g, dist, pred, source=src, wtype="u32")
+
+
+def test_relabel_on_reuse_same_result(ctx):
+    """The relabelled copy is built from the second SSSP on the same contents
+    on (and dropped by a refill): every call returns identical results."""
+    g = gb.rmat(20, 16, seed=3, wtype="f32", transpose=False, ctx=ctx)
+    first = gb.sssp_stats(g, 0)
+    _check(g, first[0], first[1])
+    for _ in range(2):
+        d, p, st = gb.sssp_stats(g, 0)
+        assert np.array_equal(d, first[0])
+        _check(g, d, p)
+    ro, col, w = g.csr()
+    g2 = gb.Graph.from_csr(g.num_vertices, ro, col, w.astype(np.float64), wtype="f32", ctx=ctx)
+    import ctypes as C
+    from paper_2212_08200_b200 import _lib
+    assert _lib.load().gfb_graph_refill(g.h, C.c_void_p(ro.ctypes.data),
+                                        C.c_void_p(col.ctypes.data),
+                                        C.c_void_p(w.ctypes.data), gb.W_F32) == 0
+    d, p, st = gb.sssp_stats(g, 0)  # first call after the refill: no relabel
+    assert np.array_equal(d, first[0])
+    assert np.array_equal(gb.sssp_stats(g2, 0)[0], first[0])
