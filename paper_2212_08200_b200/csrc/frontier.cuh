@@ -265,7 +265,7 @@ template <class D>
 __global__ void __launch_bounds__(F_WARPS * 32)
 k_fcount_o(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uint32_t nwords,
            const D* __restrict__ dist, const Ctl* __restrict__ ctl,
-           unsigned long long* agg, unsigned long long* btot) {
+           unsigned long long* agg, unsigned long long* btot, uint32_t* tflag) {
   __shared__ uint32_t s_c[OB_N], s_e[OB_N];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x < OB_N) s_c[threadIdx.x] = s_e[threadIdx.x] = 0;
@@ -283,7 +283,9 @@ k_fcount_o(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uin
       atomicAdd(&s_e[b], w.deg[j]);
     }
   }
-  __syncthreads();
+  // any bit in this tile at all: k_fwrite_o skips tiles without one
+  const int any = __syncthreads_or(raw != 0);
+  if (threadIdx.x == 0) tflag[blockIdx.x] = any;
   if (threadIdx.x < OB_N) {
     const unsigned long long x = ((unsigned long long)s_c[threadIdx.x] << 32) | s_e[threadIdx.x];
     agg[(size_t)blockIdx.x * OB_N + threadIdx.x] = x;
@@ -343,9 +345,11 @@ template <class D>
 __global__ void __launch_bounds__(F_WARPS * 32)
 k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur, uint32_t nwords,
            const D* __restrict__ dist, const Ctl* __restrict__ ctl,
-           const unsigned long long* __restrict__ agg, unsigned long long* bcur, Plan plan) {
+           const unsigned long long* __restrict__ agg, unsigned long long* bcur, Plan plan,
+           const uint32_t* __restrict__ tflag) {
   __shared__ unsigned long long s_cur[OB_N];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (!tflag[blockIdx.x]) return;  // empty tile: nothing to place or clear
   const uint32_t cut = ctl->bcut;
   if (threadIdx.x < OB_N) {
     const unsigned long long x = agg[(size_t)blockIdx.x * OB_N + threadIdx.x];

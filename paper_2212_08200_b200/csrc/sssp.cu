@@ -42,7 +42,7 @@ Workspace* ensure_ws(Graph* g) {
   ws->ptseg.alloc((m / PLAN_GRAIN + 3) * 4, s);
   ws->ftiles = (uint32_t)std::max<uint64_t>((nwords + F_WORDS - 1) / F_WORDS, 1);
   ws->agg.alloc((size_t)ws->ftiles * 8, s);
-  ws->oagg.alloc((size_t)ws->ftiles * OB_N * 8, s);
+  ws->oagg.alloc((size_t)ws->ftiles * (OB_N * 8 + 4), s);  // cells + per-tile nonempty flags
   ws->obuck.alloc(2 * OB_N * 8, s);
   GFB_CUDA(cudaMemsetAsync(ws->obuck.p, 0, 2 * OB_N * 8, s));
   ws->src_dev.alloc(16, s);
@@ -199,9 +199,11 @@ struct Runner {
       if (ordered()) {
         const uint32_t tiles = ws->ftiles;
         unsigned long long* bt = ws->obuck.as<unsigned long long>();
+        uint32_t* tflag =
+            reinterpret_cast<uint32_t*>(ws->oagg.as<unsigned long long>() + (size_t)tiles * OB_N);
         k_fcount_o<D><<<tiles, F_WARPS * 32, 0, s>>>(lro(), ws->bm_next.as<uint32_t>(), nwords,
                                                      ldist(), ws->ctl.as<Ctl>(),
-                                                     ws->oagg.as<unsigned long long>(), bt);
+                                                     ws->oagg.as<unsigned long long>(), bt, tflag);
         k_fscan_o<<<1, 32, 0, s>>>(bt, bt + OB_N, plan(), ws->ctl.as<Ctl>(), (uint32_t)g->m, alpha,
                                    dir == GFB_DIR_AUTO && g->has_csc ? 1 : 0,
                                    dir == GFB_DIR_PULL ? 1 : 0, hloop, hmode, set_loop ? 1 : 0,
@@ -210,7 +212,7 @@ struct Runner {
                                                      ws->bm_cur.as<uint32_t>(), nwords, ldist(),
                                                      ws->ctl.as<Ctl>(),
                                                      ws->oagg.as<unsigned long long>(), bt + OB_N,
-                                                     plan());
+                                                     plan(), tflag);
         GFB_CUDA(cudaGetLastError());
         return;
       }
