@@ -28,6 +28,9 @@ def run(args, rank, world):
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if world == 1:  # --partitioned without torchrun: a single-rank group
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
     ctx = gb.Context(local)
     t0 = time.time()
