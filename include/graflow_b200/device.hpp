@@ -87,11 +87,14 @@ struct DevicePolicy {
   gfb_wtype arithmetic = GFB_W_F64;
   bool auto_direction = true;  // push<->pull switch on the device
   float pull_alpha = 0.25f;    // pull when frontier edges > m / pull_alpha
+  double delta = 0.0;          // > 0: near-far filter (push only; high-diameter
+                               // graphs, u32/f32 arithmetic) -- same distances
 
   void validate() const {
     if (device < 0) throw std::invalid_argument("device policy: device must be >= 0");
     if (arithmetic < GFB_W_U32 || arithmetic > GFB_W_F64)
       throw std::invalid_argument("device policy: bad arithmetic");
+    if (!(delta >= 0.0)) throw std::invalid_argument("device policy: delta must be >= 0");
   }
 };
 
@@ -195,6 +198,10 @@ inline SsspResult sssp(const Graph& g, vertex_t source, const DeviceSsspConfig& 
                     ? GFB_DIR_PULL
                     : (cfg.policy.auto_direction && want_csc ? GFB_DIR_AUTO : GFB_DIR_PUSH);
   o.pull_alpha = cfg.policy.pull_alpha;
+  if (cfg.policy.delta > 0 && cfg.direction != Direction::pull) {
+    o.delta = cfg.policy.delta;
+    o.direction = GFB_DIR_PUSH;  // the near-far loop is push-only
+  }
   SsspResult r;
   r.dist.resize(n);
   r.pred.resize(n);

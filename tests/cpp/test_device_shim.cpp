@@ -157,6 +157,14 @@ int main() {
     auto r = sssp(g, 0, cfg);
     CHECK(r.dist == reference_dijkstra(g, 0).first);
     CHECK(valid_pred_tree(g, 0, r.dist, r.pred));
+    // the near-far loop (policy.delta) reaches the same fixpoint
+    for (double delta : {1.0, 16.0, 200.0}) {
+      DeviceSsspConfig nf = cfg;
+      nf.policy.delta = delta;
+      auto rn = sssp(g, 0, nf);
+      CHECK(rn.dist == r.dist);
+      CHECK(valid_pred_tree(g, 0, rn.dist, rn.pred));
+    }
   }
   // --- acceptance.cpp:157-177 (C3): 20 repeated runs, identical distances
   {
