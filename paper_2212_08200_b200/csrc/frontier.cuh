@@ -336,24 +336,41 @@ static __global__ void k_fscan_o(unsigned long long* btot, unsigned long long* b
   }
 }
 
-// Write: each tile reserves its cell in every bucket (one global atomic per
-// nonzero cell); inside the tile one shared 64-bit cursor per bucket hands
-// out consistent (slot, edge offset) pairs.  (Measured alternatives: staging
-// the tile bucket-major in shared memory and scanning it, or one warp-
-// aggregated atomic per distinct bucket of a word, were 1.2x / 2.1x slower.)
+// Write: each tile reserves its cell in every bucket up to the cut (one
+// global atomic per nonzero cell); a lane's rank in its cell comes from a
+// native 32-bit shared atomic, v/start go straight to their slots, and the
+// edge offsets come from one block scan over the tile's degrees staged
+// bucket-major in shared memory.  Deferred vertices keep their bitmap bit.
+// (Measured alternatives: per-lane 64-bit shared cursors -- a CAS loop --
+// 1-5% slower; full staging of v/start/deg 1.2x; a warp-aggregated atomic per
+// distinct bucket of a word 2.1x.)
 template <class D>
 __global__ void __launch_bounds__(F_WARPS * 32)
 k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur, uint32_t nwords,
-           const D* __restrict__ dist, const Ctl* __restrict__ ctl,
-           const unsigned long long* __restrict__ agg, unsigned long long* bcur, Plan plan,
-           const uint32_t* __restrict__ tflag) {
-  __shared__ unsigned long long s_cur[OB_N];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+            const D* __restrict__ dist, const Ctl* __restrict__ ctl,
+            const unsigned long long* __restrict__ agg, unsigned long long* bcur, Plan plan,
+            const uint32_t* __restrict__ tflag) {
+  constexpr int TV = F_WORDS * 32, NT = F_WARPS * 32, VT = TV / NT;
+  __shared__ uint32_t s_cb[OB_N], s_ce[OB_N], s_lb[OB_N], s_rank[OB_N];
+  __shared__ uint32_t s_deg[TV], s_pre[TV];
+  __shared__ uint8_t s_bk[TV];
+  __shared__ uint32_t s_ws[F_WARPS + 1];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (!tflag[blockIdx.x]) return;  // empty tile: nothing to place or clear
   const uint32_t cut = ctl->bcut;
-  if (threadIdx.x < OB_N) {
-    const unsigned long long x = agg[(size_t)blockIdx.x * OB_N + threadIdx.x];
-    s_cur[threadIdx.x] = x && threadIdx.x <= cut ? atomicAdd(bcur + threadIdx.x, x) : 0ull;
+  if (warp == 0) {
+    const unsigned long long x =
+        lane < OB_N && (uint32_t)lane <= cut ? agg[(size_t)blockIdx.x * OB_N + lane] : 0ull;
+    const uint32_t cnt = (uint32_t)(x >> 32);
+    const uint32_t incl = warp_incl_scan(cnt, lane);
+    if (lane < OB_N) {
+      const unsigned long long g = x ? atomicAdd(bcur + lane, x) : 0ull;
+      s_cb[lane] = (uint32_t)(g >> 32);
+      s_ce[lane] = (uint32_t)g;
+      s_lb[lane] = incl - cnt;
+      s_rank[lane] = 0;
+    }
+    if (lane == 31) s_ws[F_WARPS] = incl;  // placed vertices of this tile
   }
   const uint32_t base = ctl->blo >> OB_SHIFT;
   const uint32_t wbase = blockIdx.x * F_WORDS + warp * F_WPW;
@@ -361,7 +378,7 @@ k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
   uint32_t raw;
   load_warp_words(ro, bm_next, nwords, wbase, w, &raw);
   __syncthreads();
-  uint32_t pend = 0;  // this lane's word (lane < F_WPW): bits deferred to the next superstep
+  uint32_t pend = 0;
 #pragma unroll
   for (int j = 0; j < F_WPW; ++j) {
     const bool kept = (w.keep[j] >> lane) & 1u;
@@ -371,17 +388,48 @@ k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
     const unsigned dm = __ballot_sync(0xffffffffu, kept && !place);
     if (lane == j) pend = dm;
     if (place) {
-      const unsigned long long c = atomicAdd(&s_cur[b], (1ull << 32) | w.deg[j]);
-      const uint32_t gi = (uint32_t)(c >> 32), eoff = (uint32_t)c;
+      const uint32_t r = atomicAdd(&s_rank[b], 1u);
+      const uint32_t p = s_lb[b] + r;
+      const uint32_t gi = s_cb[b] + r;
+      s_deg[p] = w.deg[j];
+      s_bk[p] = (uint8_t)b;
       plan.v[gi] = v;
       plan.start[gi] = w.st[j];
-      plan.off[gi] = eoff;
-      tile_map_entries(plan, gi, eoff, w.deg[j]);
     }
   }
   if (lane < F_WPW && wbase + lane < nwords) {
     if (bm_cur) bm_cur[wbase + lane] = raw & ~pend;
     bm_next[wbase + lane] = pend;
+  }
+  __syncthreads();
+  const uint32_t placed = s_ws[F_WARPS];
+  if (placed == 0) return;  // block-uniform
+  // exclusive scan of the staged degrees (VT consecutive positions per thread)
+  uint32_t d[VT], tsum = 0;
+#pragma unroll
+  for (int r = 0; r < VT; ++r) {
+    const uint32_t p = tid * VT + r;
+    d[r] = p < placed ? s_deg[p] : 0u;
+    tsum += d[r];
+  }
+  const uint32_t incl = warp_incl_scan(tsum, lane);
+  if (lane == 31) s_ws[warp] = incl;
+  __syncthreads();
+  uint32_t run = incl - tsum;
+  for (int i = 0; i < warp; ++i) run += s_ws[i];
+#pragma unroll
+  for (int r = 0; r < VT; ++r) {
+    s_pre[tid * VT + r] = run;
+    run += d[r];
+  }
+  __syncthreads();
+  for (uint32_t p = tid; p < placed; p += NT) {  // cells are contiguous slots
+    const uint32_t b = s_bk[p];
+    const uint32_t r = p - s_lb[b];
+    const uint32_t gi = s_cb[b] + r;
+    const uint32_t eoff = s_ce[b] + (s_pre[p] - s_pre[s_lb[b]]);
+    plan.off[gi] = eoff;
+    tile_map_entries(plan, gi, eoff, s_deg[p]);
   }
 }
 
