@@ -1,17 +1,17 @@
-// hot.cuh -- the specialised hot-path advance kernels of gfb_sssp.
+// hot.cuh -- the advance kernels of gfb_sssp (neighbors_expand /
+// neighbors_expand_pull with the SSSP relax, operators.hpp:255-334,
+// algorithms.hpp:586-593).
 //
-// Same edge-tile load balancing as k_advance_push/k_advance_pull
-// (kernels.cuh), specialised for the SSSP relax condition
-// (algorithms.hpp:586-593) with bitmap output, and restructured so every
-// thread keeps H_VT independent memory operations in flight per phase:
-//   A: H_VT streaming record loads  (8-byte {dst, w}, L1 no-allocate,
-//      L2 evict-first)
-//   B: H_VT distance gathers        (test-before-atomic)
-//   C: H_VT atomicMin on improving candidates (returns consumed in D)
-//   D: predecessor records + next-frontier bitmap (RED.OR)
-// The generic kernels issue these one edge at a time (load -> gather ->
-// atomic chained per edge, MLP ~ 1); ncu showed long-scoreboard stalls on
-// exactly that chain (profiles/r01_push_v1.md).
+//   k_push_range  default push advance for 32-bit distances: warps claim
+//                 256-edge tiles of the plan round-robin (merge-path style
+//                 segment search by shuffles over a 32-segment window), 2
+//                 edges per lane, 64 warps per SM; record stream -> distance
+//                 gather (test before atomic) -> fire-and-forget red.* of the
+//                 distance, the packed (dist, pred) key and the frontier bit.
+//   k_push_warp   the same tiling with atomicMin-with-return and {u, edge}
+//                 records (f64 distances; the partitioned multi-GPU advance).
+//   k_pull_relax  pull over the CSC plan (CTA tiles in shared memory).
+// Each step of the design is a measurement: profiles/r01_variants_s24.txt.
 #pragma once
 
 #include "kernels.cuh"
@@ -81,65 +81,6 @@ __device__ __forceinline__ uint32_t hot_stage(const Plan& plan, const D* dist, u
   }
   __syncthreads();
   return cnt;
-}
-
-template <class W, int H_VT = HotCfg<W>::VT, int MINB = 4>
-__global__ void __launch_bounds__(H_BLOCK, MINB) k_push_relax(AdvArgs<W> a) {
-  using D = typename DT<W>::D;
-  constexpr int H_TILE = H_BLOCK * H_VT;
-  __shared__ uint32_t s_off[H_TILE + 2];
-  __shared__ uint32_t s_start[H_TILE + 2];
-  __shared__ uint32_t s_u[H_TILE + 2];
-  __shared__ D s_du[H_TILE + 2];
-  __shared__ uint16_t s_seg[H_TILE];
-
-  for (uint32_t i = blockIdx.x * H_BLOCK + threadIdx.x; i < a.status_len; i += gridDim.x * H_BLOCK)
-    a.status[i] = 0;
-  const uint32_t total = a.ctl->total;
-  const uint32_t k = a.ctl->k;
-  const uint32_t ntiles = (total + H_TILE - 1) / H_TILE;
-  const int tid = threadIdx.x;
-  unsigned* err = &a.ctl->err;
-  if (blockIdx.x == 0 && tid == 0) {
-    a.ctl->relax += total;
-    a.ctl->supersteps += 1;
-    a.ctl->push_steps += 1;
-  }
-  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const uint32_t cnt = hot_stage<H_VT, D>(a.plan, a.dist, t, ntiles, total, k, s_off, s_start,
-                                            s_u, s_du, s_seg, true);
-    uint32_t dst[H_VT];
-    D nd[H_VT], cur[H_VT];
-#pragma unroll
-    for (int r = 0; r < H_VT; ++r) {  // A: record stream (+ candidate distance)
-      uint32_t le = r * H_BLOCK + tid;
-      dst[r] = NIL;
-      if (le < cnt) {
-        uint32_t j = s_seg[le];
-        EdgeRec<W> rec = ld_rec(a.adj + (s_start[j] + (le - s_off[j])));
-        dst[r] = rec.v;
-        nd[r] = dadd(s_du[j], rec.w, err);
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < H_VT; ++r)  // B: distance gathers (test before atomic)
-      if (dst[r] != NIL) cur[r] = ld_dist(a.dist + dst[r]);
-#pragma unroll
-    for (int r = 0; r < H_VT; ++r) {  // C: atomics on candidates
-      if (dst[r] != NIL && nd[r] < cur[r]) cur[r] = atomic_min_d(a.dist + dst[r], nd[r]);
-      else dst[r] = NIL;
-    }
-#pragma unroll
-    for (int r = 0; r < H_VT; ++r) {  // D: winners
-      if (dst[r] != NIL && nd[r] < cur[r]) {
-        uint32_t le = r * H_BLOCK + tid;
-        uint32_t j = s_seg[le];
-        a.predrec[dst[r]] = make_uint2(s_u[j], s_start[j] + (le - s_off[j]));
-        atomicOr(a.bm_out + (dst[r] >> 5), 1u << (dst[r] & 31));
-      }
-    }
-    __syncthreads();
-  }
 }
 
 template <class W, bool KEY = false>

@@ -231,14 +231,6 @@ struct Runner {
     GFB_CUDA(cudaGetLastError());
   }
 
-  template <int VT, int MINB>
-  void push_launch(cudaStream_t st, uint32_t total) {
-    constexpr int TILE = H_BLOCK * VT;
-    uint32_t ntiles = (total + TILE - 1) / TILE;
-    uint32_t grid = std::min<uint32_t>(std::max<uint32_t>(ntiles, 1), c->num_sms * MINB);
-    k_push_relax<W, VT, MINB><<<grid, H_BLOCK, 0, st>>>(args(false));
-  }
-
   // Persistent-grid warp kernel: the grid depends only on the device, so the
   // same launch serves every superstep inside the captured device loop.
   template <int VT, int MINB>
@@ -266,10 +258,7 @@ struct Runner {
   // Packed (dist, pred) keys with fire-and-forget reductions (k_push_range)
   // for 32-bit distances; the {u, edge} record path for f64 and the legacy
   // experiment kernels.
-  bool key_mode() const {
-    return sizeof(D) == 4 && variant != 1 && variant != 2 && variant != 4 && variant != 6 &&
-           variant != 10;
-  }
+  bool key_mode() const { return sizeof(D) == 4 && variant != 10; }
 
   template <int VT, int MINB, int TILE, int OPT = 0>
   void range_launch(cudaStream_t st) {
@@ -281,38 +270,13 @@ struct Runner {
   // total == UINT32_MAX: unknown on the host (device loop) -> full grid
   void push(cudaStream_t st, uint32_t total) {
     const bool full = total == 0xFFFFFFFFu;
-    switch (variant) {
-      case 1: push_launch<4, 8>(st, full ? 1u << 30 : total); break;
-      case 2: push_launch<4, 6>(st, full ? 1u << 30 : total); break;
-      case 4: {  // generic operator kernel (one edge in flight per thread)
-        uint32_t ntiles = full ? 1u << 20 : (total + A_TILE - 1) / A_TILE;
-        uint32_t grid = std::min<uint32_t>(std::max<uint32_t>(ntiles, 1), c->num_sms * 8);
-        k_advance_push<W, OUT_BITMAP><<<grid, A_BLOCK, 0, st>>>(args(false));
-        break;
-      }
-      case 6: warp_launch<4, 8>(st, total, full); break;
-      case 10: warp_launch<(sizeof(W) == 8 ? 4 : 8), 4>(st, total, full); break;
-      case 8: range_launch<4, 8, 0>(st); break;
-      case 9: range_launch<8, 4, 0>(st); break;
-      case 11: range_launch<8, 4, 256>(st); break;
-      case 12: range_launch<8, 4, 512>(st); break;
-      case 13: range_launch<8, 4, 1024>(st); break;
-      case 14: range_launch<4, 8, 512>(st); break;
-      case 15: range_launch<8, 4, 2048>(st); break;
-      case 16: range_launch<4, 8, 256>(st); break;
-      case 17: range_launch<4, 8, 1024>(st); break;
-      case 18: range_launch<2, 8, 512>(st); break;
-      case 19: range_launch<4, 6, 512>(st); break;
-      case 20: range_launch<2, 8, 256>(st); break;
-      case 21: range_launch<6, 5, 768>(st); break;
-      case 22: range_launch<2, 8, 256, 3>(st); break;
-      case 23: range_launch<2, 8, 256, 11>(st); break;
-      case 24: range_launch<2, 8, 128, 1>(st); break;
-      case 25: range_launch<1, 8, 128, 1>(st); break;
-      default:  // measured best at RMAT s24 (profiles/r01_variants_s24.txt)
-        if (key_mode()) range_launch<2, 8, 256, 1>(st);
-        else warp_launch<(sizeof(W) == 8 ? 4 : 8), 4>(st, total, full);
+    if (variant == 10 || !key_mode()) {  // {u, edge} records (f64; legacy experiment)
+      warp_launch<(sizeof(W) == 8 ? 4 : 8), 4>(st, total, full);
+      return;
     }
+    // measured at RMAT s24 (profiles/r01_variants_s24.txt): 2 edges per lane,
+    // 8 x 256-thread CTAs per SM, strided 256-edge tiles, PTX red.*
+    range_launch<2, 8, 256, 1>(st);
   }
 
   // The persistent single-launch loop (bsp.cuh) for 32-bit distances.
