@@ -713,14 +713,30 @@ __global__ void k_init(typename DT<W>::D* dist, uint2* predrec, uint32_t* bm_nex
 //    plain argmin cycle, cf. algorithms.hpp:506-511).  Smallest u wins.
 // Also accumulates n_reach / m_reach for the bench's GTEPS.
 // ---------------------------------------------------------------------------
-template <class W, bool KEY = false>
+// PERM (relabelled loop, 32-bit keys): the loop's state lives in relabelled
+// ids; the pass reads it through perm (dist_int / key_int), maps the key's
+// source back through iperm and writes dist / predrec in the caller's ids --
+// the unpermute pass fused into the verification.
+template <class D>
+struct PermView {
+  const uint32_t* perm;
+  const uint32_t* iperm;
+  const D* dist_int;
+  const unsigned long long* key_int;
+  D* dist_out;
+  unsigned long long* key_out;
+};
+
+template <class W, bool KEY = false, bool PERM = false>
 __global__ void __launch_bounds__(256)
 k_pred_verify(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ adj,
               const uint32_t* __restrict__ co, const EdgeRec<W>* __restrict__ cadj,
               const typename DT<W>::D* __restrict__ dist, const uint2* __restrict__ predrec,
               uint32_t* pred, uint32_t* res, uint32_t* repair_bm, uint32_t* unres_list,
-              uint32_t n, uint32_t source, Ctl* ctl) {
+              uint32_t n, uint32_t source, Ctl* ctl,
+              PermView<typename DT<W>::D> pv = PermView<typename DT<W>::D>{}) {
   using D = typename DT<W>::D;
+  static_assert(!PERM || KEY, "the relabelled loop uses packed keys");
   constexpr int U = 4;  // vertices per thread per round, loads issued together
   __shared__ unsigned long long s_nr[8], s_mr[8];
   __shared__ uint32_t s_un[8];
@@ -731,12 +747,32 @@ k_pred_verify(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ ad
     D dv[U];
     uint2 pr[U];
     uint32_t deg[U];
+    uint32_t uint_[U];
 #pragma unroll
     for (int r = 0; r < U; ++r) {
       uint32_t v = v0 + r * stride;
-      dv[r] = v < n ? dist[v] : dinf<W>();
-      pr[r] = v < n ? predrec[v] : make_uint2(NIL, NIL);
+      if constexpr (PERM) {
+        const uint32_t i = v < n ? pv.perm[v] : 0u;
+        dv[r] = v < n ? pv.dist_int[i] : dinf<W>();
+        const unsigned long long k = v < n ? pv.key_int[i] : ~0ull;
+        pr[r] = make_uint2((uint32_t)k, (uint32_t)(k >> 32));  // .x: relabelled source
+      } else {
+        dv[r] = v < n ? dist[v] : dinf<W>();
+        pr[r] = v < n ? predrec[v] : make_uint2(NIL, NIL);
+      }
       deg[r] = v < n ? ro[v + 1] - ro[v] : 0u;
+    }
+    if constexpr (PERM) {  // the caller's ids of the key sources; write the results back
+#pragma unroll
+      for (int r = 0; r < U; ++r) {
+        const uint32_t v = v0 + r * stride;
+        uint_[r] = pr[r].x;
+        if (pr[r].x != NIL) pr[r].x = pv.iperm[pr[r].x];
+        if (v < n) {
+          pv.dist_out[v] = dv[r];
+          pv.key_out[v] = ((unsigned long long)pr[r].y << 32) | pr[r].x;
+        }
+      }
     }
     EdgeRec<W> rec[U];
     D du[U];
@@ -749,7 +785,8 @@ k_pred_verify(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ ad
         // packed key (dist_bits << 32 | u), k_push_range: the edge u -> v
         // that proposed dist[v] is tight at the fixpoint (any later drop of
         // dist[u] re-expanded u and would have lowered the key)
-        du[r] = dist[pr[r].x];
+        if constexpr (PERM) du[r] = pv.dist_int[uint_[r]];
+        else du[r] = dist[pr[r].x];
         rec[r].v = pr[r].y == *reinterpret_cast<const uint32_t*>(&dv[r]) ? v : NIL;
       } else if (look) {
         if (pr[r].y & PRED_CSC_SLOT) {  // recorded by a pull step: CSC slot of v

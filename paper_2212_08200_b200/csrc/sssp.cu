@@ -59,23 +59,6 @@ Workspace* ensure_ws(Graph* g) {
   return g->ws.get();
 }
 
-// Relabelled loop state -> caller ids: dist[v] = dist_int[perm[v]], and the
-// predecessor key's vertex half mapped back through iperm.
-template <class D>
-__global__ void k_unpermute(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ iperm,
-                            const D* __restrict__ dist_int,
-                            const unsigned long long* __restrict__ key_int, D* dist,
-                            unsigned long long* key, uint32_t n) {
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    const uint32_t i = perm[v];
-    dist[v] = dist_int[i];
-    unsigned long long k = key_int[i];
-    const uint32_t u = (uint32_t)k;
-    if (u != NIL) k = (k & 0xFFFFFFFF00000000ull) | iperm[u];
-    key[v] = k;
-  }
-}
-
 // ---- experiment (variant 42/43): reorder the plan by source distance ----
 template <class D>
 __global__ void k_plan_keys(const uint32_t* v, const D* dist, uint32_t* keys, uint32_t* idx,
@@ -609,15 +592,6 @@ struct Runner {
                   (h.mode ? g->pull_total : h.total) / (ms * 1e-3) / 1e9);
       }
     }
-    if (rl) {  // back to the caller's vertex ids for the predecessor pass and reads
-      if constexpr (sizeof(D) == 4) {
-        k_unpermute<D><<<stride_grid(c), 256, 0, s>>>(
-            g->rl_perm.as<uint32_t>(), g->rl_iperm.as<uint32_t>(), ws->dist_int.as<D>(),
-            ws->pkey_int.as<unsigned long long>(), ws->dist.as<D>(),
-            ws->predrec.as<unsigned long long>(), n);
-        ++kernels;
-      }
-    }
     uint64_t fallback = 0;
     pred_pass(source, o->compute_pred != 0, &fallback);
     GFB_CUDA(cudaEventRecord(c->ev[1], s));
@@ -646,15 +620,23 @@ struct Runner {
   void pred_pass(uint32_t source, bool want, uint64_t* fallback) {
     GFB_CUDA(cudaMemsetAsync(ws->repair_bm.p, 0, (size_t)nwords * 4, s));
     GFB_CUDA(cudaMemsetAsync(&ws->ctl.as<Ctl>()->flag, 0, 4, s));
-    auto verify = k_pred_verify<W, false>;
-    if constexpr (sizeof(D) == 4)
-      if (key_mode()) verify = k_pred_verify<W, true>;
+    auto verify = k_pred_verify<W, false, false>;
+    PermView<D> pv{};
+    if constexpr (sizeof(D) == 4) {
+      if (key_mode()) verify = k_pred_verify<W, true, false>;
+      if (rl) {  // back to the caller's ids, fused into the verification
+        verify = k_pred_verify<W, true, true>;
+        pv = PermView<D>{g->rl_perm.as<uint32_t>(), g->rl_iperm.as<uint32_t>(),
+                         ws->dist_int.as<D>(), ws->pkey_int.as<unsigned long long>(),
+                         ws->dist.as<D>(), ws->predrec.as<unsigned long long>()};
+      }
+    }
     verify<<<c->num_sms * 8, 256, 0, s>>>(
         g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(),
         g->has_csc ? g->co.as<uint32_t>() : nullptr,
         g->has_csc ? g->cadj.as<EdgeRec<W>>() : nullptr, ws->dist.as<D>(),
         ws->predrec.as<uint2>(), ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(),
-        ws->repair_bm.as<uint32_t>(), ws->cand.as<uint32_t>(), n, source, ws->ctl.as<Ctl>());
+        ws->repair_bm.as<uint32_t>(), ws->cand.as<uint32_t>(), n, source, ws->ctl.as<Ctl>(), pv);
     GFB_CUDA(cudaGetLastError());
     ++kernels;
     if (!want) return;
