@@ -55,6 +55,8 @@ struct NfArgs {
   const uint32_t* src_ptr;
   uint32_t n, nwords;
   D delta;
+  unsigned long long* trace;  // optional (GFB_TRACE=1): per phase (time << 24 | K)
+  uint32_t trace_cap;
 };
 
 __device__ __forceinline__ uint32_t dbits(float x) { return __float_as_uint(x); }
@@ -124,6 +126,11 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
     uint2* qout = a.nq[nxt];
     uint32_t* cout = a.cnt + (ph + 1) % 3;
     if (gtid == 0) a.cnt[(ph + 2) % 3] = 0;  // the count two phases ahead
+    if (a.trace && gtid == 0 && ph < a.trace_cap) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.trace[ph] = (t << 24) | min(K, 0xFFFFFFu);
+    }
     if (K > 0) {
       // ---------------- near phase: expand the near queue ----------------
       ++phases;

@@ -387,9 +387,37 @@ struct Runner {
       a.nwords = nwords;
       if constexpr (std::is_same<D, float>::value) a.delta = (float)delta;
       else a.delta = (D)std::min(std::max(std::llround(delta), 1ll), 0xFFFFFFFEll);
+      const char* tr = getenv("GFB_TRACE");
+      TBuf trace;
+      if (tr && tr[0] == '1') {
+        a.trace_cap = 1u << 16;
+        trace.alloc((size_t)a.trace_cap * 8, s);
+        GFB_CUDA(cudaMemsetAsync(trace.p, 0, (size_t)a.trace_cap * 8, s));
+        a.trace = trace.as<unsigned long long>();
+      }
       void* params[] = {&a};
       GFB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, grid, NF_THREADS, params, 0, s));
       kernels += 1;
+      if (a.trace) {  // phase histogram (instrumentation only)
+        std::vector<unsigned long long> h(a.trace_cap);
+        GFB_CUDA(cudaMemcpyAsync(h.data(), trace.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
+        c->sync();
+        uint32_t np = 0;
+        while (np + 1 < a.trace_cap && h[np + 1]) ++np;
+        double buck_us[8] = {0}, buck_n[8] = {0};
+        for (uint32_t i = 0; i + 1 <= np; ++i) {
+          const double us = ((h[i + 1] >> 24) - (h[i] >> 24)) * 1e-3;
+          const uint32_t K = (uint32_t)(h[i] & 0xFFFFFF);
+          int b = 0;
+          for (uint32_t x = K; x >= 16 && b < 7; x >>= 3) ++b;  // 0:<16 1:<128 2:<1K ...
+          buck_us[b] += us;
+          buck_n[b] += 1;
+        }
+        for (int b = 0; b < 8; ++b)
+          if (buck_n[b] > 0)
+            fprintf(stderr, "[gfb nearfar] K < %8u: %6.0f phases, %8.1f us total, %6.2f us/phase\n",
+                    16u << (3 * b), buck_n[b], buck_us[b], buck_us[b] / buck_n[b]);
+      }
       return true;
     }
     return false;
