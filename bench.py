@@ -439,7 +439,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--grid-side", type=int, default=4096)
-    ap.add_argument("--grid-delta", type=float, default=32.0)
+    ap.add_argument("--grid-delta", type=float, default=16.0)
     ap.add_argument("--partitioned", action="store_true",
                     help="force the 1-D partitioned NCCL path (default for N > 1)")
     args = ap.parse_args()

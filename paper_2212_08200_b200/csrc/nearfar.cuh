@@ -86,7 +86,7 @@ __device__ __forceinline__ void warp_append(bool flag, uint2 e, uint2* q, uint32
 // vertex has since been lowered again is stale (the lowering appended a newer
 // entry) and is skipped -- dedup without a membership bitmap or a returning
 // atomic on the critical path.
-template <class W, int LH = 0>
+template <class W, int LH = 0, uint32_t CH = 32>
 __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
   using D = typename DT<W>::D;
   static_assert(sizeof(D) == 4, "packed predecessor keys need 32-bit distances");
@@ -192,9 +192,12 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
           warp_append(to_far, ent, a.fq[fp], a.cnt + 3 + fp, a.cap, err);
         }
       };
-      for (uint32_t base = gwarp * 32; base < K; base += nwarps * 32) {
+      // CH queue entries per warp: fewer than 32 spreads a small near queue
+      // (and the chasing of its activations) over more warps
+      for (uint32_t base = gwarp * CH; base < K; base += nwarps * CH) {
         const uint32_t j = base + lane;
-        expand(j < K, j < K ? __ldcg(qin + j) : make_uint2(0, 0));
+        const bool ok = (uint32_t)lane < CH && j < K;
+        expand(ok, ok ? __ldcg(qin + j) : make_uint2(0, 0));
         if constexpr (LH > 0) {
           // chase this warp's own near activations without a grid barrier
           for (int hop = 0; hop < LH && lq_n > 0; ++hop) {

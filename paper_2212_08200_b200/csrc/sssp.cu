@@ -350,13 +350,20 @@ struct Runner {
   // Near-far filter (opts.delta > 0): one persistent launch (nearfar.cuh).
   bool nearfar_launch(double delta) {
     if constexpr (sizeof(D) == 4) {
-      // warp-local chasing of 4 rounds (measured on the 4096^2 grid: no
-      // chasing 110 ms, LH 2/4/8/16 at delta 8: 72/67/70/84 ms; LH 4 with
-      // delta 32: 56 ms); variants 90-92: LH 0 / 8 / 16
-      auto kern = k_nearfar<W, 4>;
+      // 8 queue entries per warp (one edge per lane on degree-4 meshes) and
+      // warp-local chasing of 8 rounds.  4096^2 grid: 32 entries/warp, LH 4,
+      // delta 32 = 55 ms; CH 8: LH 4 33.5, LH 8 32.7, LH 16 36.9 ms; CH 4 LH 8
+      // delta 16 32.5 ms (profiles/r01_nearfar_chunk.txt).  Variants keep the
+      // other settings measurable.
+      auto kern = k_nearfar<W, 8, 8>;
       if (variant == 90) kern = k_nearfar<W, 0>;
-      else if (variant == 91) kern = k_nearfar<W, 8>;
+      else if (variant == 91) kern = k_nearfar<W, 4>;
       else if (variant == 92) kern = k_nearfar<W, 16>;
+      else if (variant == 93) kern = k_nearfar<W, 4, 8>;
+      else if (variant == 94) kern = k_nearfar<W, 4, 16>;
+      else if (variant == 96) kern = k_nearfar<W, 8, 4>;
+      else if (variant == 97) kern = k_nearfar<W, 16, 8>;
+      else if (variant == 98) kern = k_nearfar<W, 16, 4>;
       int per_sm = 0;
       GFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NF_THREADS, 0));
       if (per_sm <= 0) return false;

@@ -70,6 +70,17 @@ def test_nearfar_corpus_f32(ctx):
         _check(g, dist, pred)
 
 
+@pytest.mark.parametrize("variant", [90, 91, 93, 96, 98])
+def test_nearfar_chunk_variants(ctx, variant):
+    """Other (chase rounds, entries per warp) settings of k_nearfar."""
+    g = gb.grid(128, seed=3, transpose=True, ctx=ctx)
+    dist, pred, st = gb.sssp_stats(g, 0, delta=4.0, variant=variant)
+    _check(g, dist, pred)
+    g = gb.rmat(12, 16, seed=3, wtype="u32", transpose=True, ctx=ctx)
+    dist, pred, st = gb.sssp_stats(g, 7, delta=32, variant=variant)
+    _check(g, dist, pred, source=7, wtype="u32")
+
+
 def test_nearfar_rejects_pull(ctx):
     g = gb.grid(16, seed=1, transpose=True, ctx=ctx)
     with pytest.raises(ValueError):
