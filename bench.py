@@ -198,8 +198,11 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if world > 1 or args.partitioned:
-        import bench_mg
-        return bench_mg.run(args, rank, world)
+        if args.exchange == "nccl":  # host-driven message exchange (mg.py)
+            import bench_mg
+            return bench_mg.run(args, rank, world)
+        import bench_peer  # device-initiated exchange over peer memory (peer.py)
+        return bench_peer.run(args, rank, world)
     ctx = gb.Context(0)
     t0 = time.time()
     g = gb.rmat(args.scale, args.edgefactor, seed=args.seed, wtype="f32", transpose=True, ctx=ctx)
@@ -441,7 +444,10 @@ def main():
     ap.add_argument("--grid-side", type=int, default=4096)
     ap.add_argument("--grid-delta", type=float, default=16.0)
     ap.add_argument("--partitioned", action="store_true",
-                    help="force the 1-D partitioned NCCL path (default for N > 1)")
+                    help="force the 1-D partitioned path (default for N > 1)")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="partitioned path: device-initiated peer-memory exchange (default) "
+                         "or the host-driven NCCL all-to-all")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

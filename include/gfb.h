@@ -246,6 +246,38 @@ int gfb_part_read(gfb_part* p, void* dist_native, uint64_t* relaxations,
 int gfb_part_pred(gfb_part* p, const void* gdist_dev, const uint32_t* res_dev,
                   uint32_t* cand_dev, uint32_t round);
 
+/* ---- 1-D partitioned SSSP over peer memory (multi-GPU) --
+ * No reference counterpart (the reference is single-host); replaces the
+ * per-superstep host exchange of the gfb_part_* path with a device-initiated
+ * one.  One gfb_peer per rank (one process per GPU); rank r holds CSR rows
+ * [range_starts[r], range_starts[r+1]) with GLOBAL column ids (ro_local
+ * rebased to 0).  range_starts: nparts+1 ascending vertex ids, 0 first,
+ * interior cuts multiples of 32; nparts <= 8.  The loop state lives in one
+ * device allocation per rank, exported as a GFB_PEER_HANDLE_BYTES CUDA IPC
+ * handle; after every rank has called gfb_peer_link with all nparts handles
+ * (rank order; its own entry is ignored), gfb_peer_sssp relaxes remote
+ * destinations directly in their owner's memory (NVLink peer access) and
+ * synchronises the ranks with device-side barriers: every rank must call it
+ * with the same source and options.  Distances / predecessors come back per
+ * rank for its own range (predecessors as global ids); stats are this
+ * rank's share (relaxations, n_reach, m_reach sum over ranks; supersteps are
+ * equal).  f32 / u32 weights, push only, no near-far (delta must be 0).  A
+ * rank that does not arrive at a barrier within GFB_PEER_TIMEOUT_S seconds
+ * (default 30) makes every waiting rank fail with GFB_ECUDA. */
+#define GFB_PEER_HANDLE_BYTES 64
+typedef struct gfb_peer gfb_peer;
+int gfb_peer_create(gfb_ctx* ctx, int rank, int nparts, const uint32_t* range_starts,
+                    uint64_t m_local, const uint32_t* ro_local, const uint32_t* col,
+                    const void* w, int w_host_type, int wtype, gfb_peer** out);
+int gfb_peer_export(gfb_peer* p, void* handle /* GFB_PEER_HANDLE_BYTES */);
+int gfb_peer_link(gfb_peer* p, const void* handles /* nparts x GFB_PEER_HANDLE_BYTES */);
+int gfb_peer_sssp(gfb_peer* p, uint32_t source, const gfb_sssp_opts* opts,
+                  gfb_sssp_stats* stats);
+/* local range: dist widened to double and/or native 4-byte bits, pred global ids */
+int gfb_peer_read(gfb_peer* p, double* dist, void* dist_native, uint32_t* pred);
+/* every rank must be done with all peers' calls before any frees */
+int gfb_peer_free(gfb_peer* p);
+
 #ifdef __cplusplus
 }
 #endif

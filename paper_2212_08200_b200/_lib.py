@@ -83,7 +83,16 @@ SIGNATURES = {
     "gfb_part_pending": ([_vp, _pu64], _int),
     "gfb_part_read": ([_vp, _vp, _pu64, _pu64], _int),
     "gfb_part_pred": ([_vp, _vp, _vp, _vp, _u32], _int),
+    "gfb_peer_create": ([_vp, _int, _int, _vp, _u64, _vp, _vp, _vp, _int, _int, C.POINTER(_vp)],
+                        _int),
+    "gfb_peer_export": ([_vp, _vp], _int),
+    "gfb_peer_link": ([_vp, _vp], _int),
+    "gfb_peer_sssp": ([_vp, _u32, C.POINTER(SsspOpts), C.POINTER(SsspStats)], _int),
+    "gfb_peer_read": ([_vp, _vp, _vp, _vp], _int),
+    "gfb_peer_free": ([_vp], _int),
 }
+
+PEER_HANDLE_BYTES = 64
 
 _LIB = None
 

@@ -466,3 +466,71 @@ int gfb_debug_relabel(gfb_graph* g, uint32_t* ro, uint32_t* adj_pairs, uint32_t*
     g->ctx->sync();
   });
 }
+
+// ---- peer-memory partitioned SSSP (include/gfb.h) ----
+static gfb::Peer* P(gfb_peer* p) { return reinterpret_cast<gfb::Peer*>(p); }
+
+int gfb_peer_create(gfb_ctx* ctx, int rank, int nparts, const uint32_t* range_starts,
+                    uint64_t m_local, const uint32_t* ro_local, const uint32_t* col, const void* w,
+                    int w_host_type, int wtype, gfb_peer** out) {
+  return guard([&] {
+    NEED(ctx);
+    NEED(range_starts);
+    NEED(ro_local);
+    NEED(out);
+    if (m_local && (!col || !w)) gfb::fail(GFB_EINVAL, "peer: null edge arrays");
+    set_device(ctx);
+    *out = reinterpret_cast<gfb_peer*>(gfb::peer_create(ctx, rank, nparts, range_starts, m_local,
+                                                        ro_local, col, w, w_host_type, wtype));
+  });
+}
+
+int gfb_peer_export(gfb_peer* p, void* handle) {
+  return guard([&] {
+    NEED(p);
+    NEED(handle);
+    set_device(gfb::peer_ctx(P(p)));
+    gfb::peer_export(P(p), handle);
+  });
+}
+
+int gfb_peer_link(gfb_peer* p, const void* handles) {
+  return guard([&] {
+    NEED(p);
+    NEED(handles);
+    set_device(gfb::peer_ctx(P(p)));
+    gfb::peer_link(P(p), handles);
+  });
+}
+
+int gfb_peer_sssp(gfb_peer* p, uint32_t source, const gfb_sssp_opts* opts,
+                  gfb_sssp_stats* stats) {
+  return guard([&] {
+    NEED(p);
+    set_device(gfb::peer_ctx(P(p)));
+    gfb_sssp_opts o;
+    gfb_sssp_opts_default(&o);
+    if (opts) {
+      if (opts->struct_size != sizeof(gfb_sssp_opts)) gfb::fail(GFB_EINVAL, "sssp: opts struct_size mismatch");
+      o = *opts;
+    }
+    gfb::peer_sssp(P(p), source, &o, stats);
+  });
+}
+
+int gfb_peer_read(gfb_peer* p, double* dist, void* dist_native, uint32_t* pred) {
+  return guard([&] {
+    NEED(p);
+    set_device(gfb::peer_ctx(P(p)));
+    gfb::peer_read(P(p), dist, dist_native, pred);
+  });
+}
+
+int gfb_peer_free(gfb_peer* p) {
+  return guard([&] {
+    if (!p) return;
+    set_device(gfb::peer_ctx(P(p)));
+    gfb::peer_ctx(P(p))->sync();
+    gfb::peer_free(P(p));
+  });
+}

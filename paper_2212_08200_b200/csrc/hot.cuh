@@ -397,10 +397,15 @@ __device__ __forceinline__ void relax_reds(D* dist, unsigned long long* pkey, ui
   }
 }
 
-template <class W, int VT, bool COH = false, int OPT = 0>
+// PEER: destinations are global ids owned by the ranks of the peer table
+// (shared-memory copy `pt`): the test gather and the reductions go to the
+// owner's slab (NVLink peer memory for remote owners), the packed key names
+// the source by its global id.
+template <class W, int VT, bool COH = false, int OPT = 0, bool PEER = false>
 __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, uint32_t e1,
                                              uint32_t k, uint32_t total, unsigned* err,
-                                             uint32_t* fmin = nullptr) {
+                                             uint32_t* fmin = nullptr,
+                                             const PeerTab* pt = nullptr) {
   using D = typename DT<W>::D;
   unsigned long long* pkey = reinterpret_cast<unsigned long long*>(a.predrec);
   const int lane = threadIdx.x & 31;
@@ -462,6 +467,26 @@ __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, u
           nd[r] = dadd(sd, rec.w, err);
         }
       }
+      if constexpr (PEER) {
+        uint32_t q[VT];
+#pragma unroll
+        for (int r = 0; r < VT; ++r) {  // B: owner; local test (own dist or proposal cache)
+          if (dst[r] == NIL) continue;
+          q[r] = peer_owner(*pt, dst[r]);
+          const uint32_t* tp = q[r] == pt->self ? pt->dist[q[r]] : pt->rc;
+          cur[r] = test_gather<OPT>(reinterpret_cast<const D*>(tp) + dst[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < VT; ++r) {  // C: reductions into the owner's slab
+          if (dst[r] != NIL && nd[r] < cur[r]) {
+            if (q[r] != pt->self)
+              red_min_u32(reinterpret_cast<unsigned*>(pt->rc + dst[r]), dbits(nd[r]));
+            relax_reds<OPT>(reinterpret_cast<D*>(pt->dist[q[r]]), pt->pkey[q[r]], pt->bm[q[r]],
+                            dst[r], nd[r], uu[r] + pt->self_lo);
+            if (fmin) *fmin = min(*fmin, fkey(nd[r]));
+          }
+        }
+      } else {
 #pragma unroll
       for (int r = 0; r < VT; ++r)  // B: distance gathers (test before atomic)
         if (dst[r] != NIL) cur[r] = test_gather<OPT>(a.dist + dst[r]);
@@ -471,6 +496,7 @@ __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, u
           relax_reds<OPT>(a.dist, pkey, a.bm_out, dst[r], nd[r], uu[r]);
           if (fmin) *fmin = min(*fmin, fkey(nd[r]));  // for the distance-ordered plan
         }
+      }
       }
     }
     if (c1 >= e1) break;
@@ -488,11 +514,18 @@ __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, u
 // with the smallest distances: relaxing them first lets their improvements
 // reach later edges of the SAME superstep (measured: contiguous shares do
 // 4.4 relaxations per reached edge at s24, the sweep 3.5).
-template <class W, int VT, int MINB, int TILE, int OPT = 0>
+template <class W, int VT, int MINB, int TILE, int OPT = 0, bool PEER = false>
 __global__ void __launch_bounds__(256, MINB) k_push_range(AdvArgs<W> a) {
   using D = typename DT<W>::D;
   static_assert(sizeof(D) == 4, "packed predecessor keys need 32-bit distances");
   static_assert(TILE % 32 == 0, "tiles are whole warp rows");
+  __shared__ PeerTab s_pt[1];  // (eliminated when !PEER)
+  if constexpr (PEER) {  // the peer table in shared memory (indexed per edge)
+    constexpr int WORDS = sizeof(PeerTab) / 4;
+    for (int i = threadIdx.x; i < WORDS; i += blockDim.x)
+      reinterpret_cast<uint32_t*>(s_pt)[i] = reinterpret_cast<const uint32_t*>(a.peers)[i];
+    __syncthreads();
+  }
   const uint32_t gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const uint32_t total = a.ctl->total;
@@ -508,11 +541,12 @@ __global__ void __launch_bounds__(256, MINB) k_push_range(AdvArgs<W> a) {
     const uint32_t per = (uint32_t)((((uint64_t)total + nwarps - 1) / nwarps + 31) & ~31ull);
     const uint32_t e0 = (uint32_t)min((uint64_t)gwarp * per, (uint64_t)total);
     const uint32_t e1 = min(e0 + per, total);
-    if (e0 < e1) range_expand<W, VT, false, OPT>(a, e0, e1, k, total, err, &fmin);
+    if (e0 < e1) range_expand<W, VT, false, OPT, PEER>(a, e0, e1, k, total, err, &fmin, s_pt);
   } else {
     for (uint64_t e0 = (uint64_t)gwarp * TILE; e0 < total; e0 += (uint64_t)nwarps * TILE)
-      range_expand<W, VT, false, OPT>(a, (uint32_t)e0, (uint32_t)min(e0 + TILE, (uint64_t)total),
-                                       k, total, err, &fmin);
+      range_expand<W, VT, false, OPT, PEER>(a, (uint32_t)e0,
+                                             (uint32_t)min(e0 + TILE, (uint64_t)total), k, total,
+                                             err, &fmin, s_pt);
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) fmin = min(fmin, __shfl_xor_sync(0xffffffffu, fmin, d));

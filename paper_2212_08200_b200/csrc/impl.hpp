@@ -145,6 +145,17 @@ struct Part {
   uint32_t supersteps = 0;
 };
 
+// One rank of the peer-memory partitioned SSSP (peer.cu).
+struct Peer;
+Peer* peer_create(Ctx*, int rank, int nparts, const uint32_t* range_starts, uint64_t m_local,
+                  const uint32_t* ro, const uint32_t* col, const void* w, int htype, int wtype);
+void peer_export(Peer*, void* handle);
+void peer_link(Peer*, const void* handles);
+void peer_sssp(Peer*, uint32_t source, const gfb_sssp_opts*, gfb_sssp_stats*);
+void peer_read(Peer*, double* dist, void* dist_native, uint32_t* pred);
+void peer_free(Peer*);
+Ctx* peer_ctx(Peer*);
+
 // grid sizes
 inline int stride_grid(const Ctx* c) { return c->num_sms * 8; }
 inline int persist_grid(const Ctx* c, int per_sm) { return c->num_sms * per_sm; }

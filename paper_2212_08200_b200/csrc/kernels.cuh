@@ -46,6 +46,9 @@ struct Ctl {
   // advance) and the value frozen for the compaction in progress
   uint32_t fmin, blo;
   uint32_t bcut;       // ordered compaction: buckets above bcut stay pending
+  // peer-memory partition (peer.cu): sums over all ranks from the last
+  // cross-rank barrier (k_xbar) of k / flag / unresolved / resolved
+  uint32_t gk, gflag, gunres, gresolved;
 };
 
 // Expansion plan: the frontier restricted to vertices with out-degree > 0.
@@ -296,6 +299,43 @@ k_plan_list(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ list, 
 // ---------------------------------------------------------------------------
 enum { OUT_BITMAP = 0, OUT_QUEUE = 1 };
 
+// 4-byte distance <-> bits
+__device__ __forceinline__ uint32_t dbits(float x) { return __float_as_uint(x); }
+__device__ __forceinline__ uint32_t dbits(uint32_t x) { return x; }
+template <class D> __device__ __forceinline__ D dfrom(uint32_t b);
+template <> __device__ __forceinline__ float dfrom<float>(uint32_t b) { return __uint_as_float(b); }
+template <> __device__ __forceinline__ uint32_t dfrom<uint32_t>(uint32_t b) { return b; }
+
+// Peer-memory partition (peer.cu): owner q of global vertex v is the last q
+// with start[q] <= v; its distance / packed key / next-frontier bitmap are
+// reached through pointers into q's IPC-mapped slab, pre-offset so that
+// dist[q][v], pkey[q][v] and bm[q][v >> 5] take the GLOBAL id (range starts
+// are multiples of 32).  Local ranks use the same table (q == self).
+constexpr int PEER_MAX = 8;
+struct PeerTab {
+  uint32_t start[PEER_MAX + 1];
+  uint32_t* dist[PEER_MAX];
+  unsigned long long* pkey[PEER_MAX];
+  uint32_t* bm[PEER_MAX];
+  uint32_t* res[PEER_MAX];
+  uint32_t* cand[PEER_MAX];
+  uint32_t* repair[PEER_MAX];
+  // this rank's best proposal so far per REMOTE vertex (local memory, global
+  // ids; null with one rank): the test-before-atomic for remote destinations
+  // reads it instead of the owner's distance, so NVLink carries only
+  // fire-and-forget reductions, once per improvement of this rank's own
+  // proposal (the per-destination combining of a message exchange)
+  uint32_t* rc;
+  uint32_t nparts, self, self_lo, pad;
+};
+
+__device__ __forceinline__ uint32_t peer_owner(const PeerTab& t, uint32_t v) {
+  uint32_t q = 0;
+#pragma unroll
+  for (int i = 1; i < PEER_MAX; ++i) q += (i < (int)t.nparts && v >= t.start[i]) ? 1u : 0u;
+  return q;
+}
+
 template <class W>
 struct AdvArgs {
   using D = typename DT<W>::D;
@@ -322,6 +362,7 @@ struct AdvArgs {
   unsigned long long* rbest;
   uint32_t* rbm;
   int op;                    // gfb_op
+  const PeerTab* peers;      // k_push_range<PEER>: owner-addressed destinations
 };
 
 // Warp-aggregated append of `x` (one atomicAdd per warp).

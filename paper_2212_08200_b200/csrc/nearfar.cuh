@@ -59,11 +59,6 @@ struct NfArgs {
   uint32_t trace_cap;
 };
 
-__device__ __forceinline__ uint32_t dbits(float x) { return __float_as_uint(x); }
-__device__ __forceinline__ uint32_t dbits(uint32_t x) { return x; }
-template <class D> __device__ __forceinline__ D dfrom(uint32_t b);
-template <> __device__ __forceinline__ float dfrom<float>(uint32_t b) { return __uint_as_float(b); }
-template <> __device__ __forceinline__ uint32_t dfrom<uint32_t>(uint32_t b) { return b; }
 
 // Append e to queue q (count *c) if this lane's flag is set: one atomicAdd per
 // warp (ballot + popc), then each lane writes its own slot.

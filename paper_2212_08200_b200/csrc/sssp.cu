@@ -119,6 +119,7 @@ struct Runner {
   uint32_t defer_pct() const {
     if (variant == 0) return 10;
     switch (variant) {
+      case 63: return 10;  // deferral on the caller's ids (no relabel): the peer path's loop
       case 99: return 100;
       case 100: return 50;
       case 101: return 70;

@@ -1,0 +1,136 @@
+"""1-D partitioned SSSP with a device-initiated exchange over peer memory.
+
+The multi-GPU path of SURVEY.md §8e with §8f's "fused device-initiated
+exchange" (peer.cu): the same edge-balanced 1-D partition as ``mg.py`` (cut
+points rounded to multiples of 32), but no per-superstep messages, host
+collectives or host round trips.  Each rank's loop state is one CUDA IPC
+exportable allocation; after the one-time handle exchange below
+(``torch.distributed.all_gather_object``: NCCL or gloo, any backend), the
+push advance of every rank lowers remote distances directly in their owner's
+memory over NVLink, and device-side barriers between ranks decide
+convergence inside each rank's CUDA graph.
+
+One process per GPU (``torchrun``); several processes may also share one GPU
+(CUDA IPC between processes on the same device), which is how the tests
+exercise world sizes 2 and 3 on a single B200.  The reference has no
+partitioned SSSP (it is single-host); results are the same fixpoint as
+``sssp()`` (algorithms.hpp:569-623) on the whole graph.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from . import mg
+
+NIL = 0xFFFFFFFF
+ALIGN = 32  # range starts: whole frontier-bitmap words per owner
+
+
+def aligned_ranges(row_offsets, parts, align=ALIGN):
+    """Edge-balanced cut points (mg.edge_balanced_ranges) rounded down to
+    multiples of ``align``; parts+1 ascending vertex ids, 0 first, n last."""
+    if parts < 1 or parts > 8:
+        raise ValueError("peer: 1 <= parts <= 8")
+    rs = mg.edge_balanced_ranges(row_offsets, parts).astype(np.int64)
+    n = int(rs[-1])
+    cuts = [0] + [(int(c) // align) * align for c in rs[1:-1]] + [n]
+    return np.maximum.accumulate(np.array(cuts, dtype=np.int64)).astype(np.uint32)
+
+
+class PeerSssp:
+    """One rank's share: rows [range_starts[rank], range_starts[rank+1]) with
+    global column ids (``mg.slice_csr``), on ``ctx``'s GPU."""
+
+    def __init__(self, rank, nparts, range_starts, ro_local, col, w, ctx=None):
+        import paper_2212_08200_b200 as gb
+        self.gb = gb
+        self.ctx = ctx or gb.Context.default()
+        self.lib = _lib.load()
+        self.rank, self.nparts = rank, nparts
+        self.range_starts = np.ascontiguousarray(range_starts, np.uint32)
+        if len(self.range_starts) != nparts + 1:
+            raise ValueError("peer: range_starts needs nparts + 1 entries")
+        self.lo = int(self.range_starts[rank])
+        self.hi = int(self.range_starts[rank + 1])
+        w = np.ascontiguousarray(w)
+        if w.dtype == np.float32:
+            wt = _lib.W_F32
+        elif w.dtype == np.uint32:
+            wt = _lib.W_U32
+        else:
+            raise ValueError("peer: f32 or u32 weights")
+        self.wtype = wt
+        ro = np.ascontiguousarray(ro_local, np.uint32)
+        col = np.ascontiguousarray(col, np.uint32)
+        h = C.c_void_p()
+        gb.check(self.lib.gfb_peer_create(
+            self.ctx.h, rank, nparts, C.c_void_p(self.range_starts.ctypes.data), len(col),
+            C.c_void_p(ro.ctypes.data), C.c_void_p(col.ctypes.data) if len(col) else None,
+            C.c_void_p(w.ctypes.data) if len(w) else None, wt, wt, C.byref(h)))
+        self.h = h
+        self.linked = False
+
+    def handle(self) -> bytes:
+        buf = (C.c_char * _lib.PEER_HANDLE_BYTES)()
+        self.gb.check(self.lib.gfb_peer_export(self.h, buf))
+        return bytes(buf)
+
+    def link(self, group=None):
+        """Exchange the IPC handles (collective over ``group``) and map the
+        peers' memory.  Ends with a barrier: nobody relaxes into a peer before
+        it is mapped everywhere."""
+        mine = self.handle()
+        if self.nparts > 1:
+            import torch.distributed as dist
+            handles = [None] * self.nparts
+            dist.all_gather_object(handles, mine, group=group)
+        else:
+            handles = [mine]
+        blob = b"".join(handles)
+        self.gb.check(self.lib.gfb_peer_link(self.h, blob))
+        if self.nparts > 1:
+            import torch.distributed as dist
+            dist.barrier(group=group)
+        self.linked = True
+
+    def sssp(self, source, want_pred=True, variant=0):
+        """Collective: every rank calls it with the same arguments.  Returns
+        this rank's statistics (relaxations / n_reach / m_reach: local share)."""
+        o = self.gb._opts(direction="push", compute_pred=want_pred, variant=variant)
+        st = _lib.SsspStats()
+        self.gb.check(self.lib.gfb_peer_sssp(self.h, int(source), C.byref(o), C.byref(st)))
+        return {k: getattr(st, k) for k, _ in _lib.SsspStats._fields_}
+
+    def read(self, native=False):
+        """(dist, pred) of the local range: dist float64 (or the native 4-byte
+        type), pred as global ids (NIL for the source / unreachable)."""
+        n = self.hi - self.lo
+        pred = np.empty(n, np.uint32)
+        if native:
+            dist = np.empty(n, np.float32 if self.wtype == _lib.W_F32 else np.uint32)
+            self.gb.check(self.lib.gfb_peer_read(self.h, None, C.c_void_p(dist.ctypes.data),
+                                                 C.c_void_p(pred.ctypes.data)))
+        else:
+            dist = np.empty(n, np.float64)
+            self.gb.check(self.lib.gfb_peer_read(self.h, C.c_void_p(dist.ctypes.data), None,
+                                                 C.c_void_p(pred.ctypes.data)))
+        return dist, pred
+
+    def free(self):
+        if self.h:
+            self.gb.check(self.lib.gfb_peer_free(self.h))
+            self.h = None
+
+
+def gather(peer, native=False, group=None):
+    """Whole-graph (dist, pred) on every rank (tests; all_gather_object)."""
+    d, p = peer.read(native=native)
+    if peer.nparts == 1:
+        return d, p
+    import torch.distributed as dist
+    parts = [None] * peer.nparts
+    dist.all_gather_object(parts, (d, p), group=group)
+    return np.concatenate([x[0] for x in parts]), np.concatenate([x[1] for x in parts])

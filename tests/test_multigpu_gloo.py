@@ -102,3 +102,19 @@ def test_gloo_partitioned_sssp_matches_oracle(world):
     assert np.array_equal(dist, want)
     assert O.check_pred_tree(n, ro, col, w, dist, 0, pred) == -1
     assert out[0][2]["messages_sent"] + out[1][2]["messages_sent"] > 0
+
+
+def test_peer_aligned_ranges():
+    """peer.aligned_ranges: 32-aligned interior cuts, ascending, covering [0, n)."""
+    from paper_2212_08200_b200 import peer
+    rng = np.random.default_rng(5)
+    for n in (1, 31, 32, 1000, 4097):
+        deg = rng.integers(0, 50, size=n)
+        ro = np.concatenate([[0], np.cumsum(deg)]).astype(np.uint32)
+        for parts in range(1, 9):
+            rs = peer.aligned_ranges(ro, parts)
+            assert len(rs) == parts + 1 and rs[0] == 0 and rs[-1] == n
+            assert np.all(np.diff(rs.astype(np.int64)) >= 0)
+            assert all(int(c) % 32 == 0 for c in rs[1:-1])
+    with pytest.raises(ValueError):
+        peer.aligned_ranges(np.zeros(2, np.uint32), 9)
