@@ -278,6 +278,22 @@ int gfb_peer_read(gfb_peer* p, double* dist, void* dist_native, uint32_t* pred);
 /* every rank must be done with all peers' calls before any frees */
 int gfb_peer_free(gfb_peer* p);
 
+/* ---- the same partitioned SSSP driven by ONE host thread (SURVEY.md §8b
+ * gfb_mg_*): partition q runs on devices[q] (entries may repeat a device;
+ * distinct devices need peer access, i.e. an NVLink/NVSwitch node).  Upload
+ * takes the whole reference-layout CSR (row_offsets n+1, col m, weights in
+ * w_host_type) and cuts edge-balanced, 32-aligned vertex ranges; gfb_mg_sssp
+ * returns whole-graph dist (double, n) / pred (n) and summed statistics
+ * (device_ms = max over partitions).  f32 / u32 device arithmetic. */
+typedef struct gfb_mg gfb_mg;
+int gfb_mg_create(int ndev, const int* devices, gfb_mg** out);
+int gfb_mg_graph_upload(gfb_mg* mg, uint64_t n, uint64_t m, const uint32_t* row_offsets,
+                        const uint32_t* col, const void* w, int w_host_type, int wtype);
+int gfb_mg_ranges(gfb_mg* mg, uint32_t* range_starts /* ndev + 1 */);
+int gfb_mg_sssp(gfb_mg* mg, uint32_t source, const gfb_sssp_opts* opts, double* dist,
+                uint32_t* pred, gfb_sssp_stats* stats);
+int gfb_mg_destroy(gfb_mg* mg);
+
 #ifdef __cplusplus
 }
 #endif

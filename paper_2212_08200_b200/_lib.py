@@ -90,6 +90,11 @@ SIGNATURES = {
     "gfb_peer_sssp": ([_vp, _u32, C.POINTER(SsspOpts), C.POINTER(SsspStats)], _int),
     "gfb_peer_read": ([_vp, _vp, _vp, _vp], _int),
     "gfb_peer_free": ([_vp], _int),
+    "gfb_mg_create": ([_int, _vp, C.POINTER(_vp)], _int),
+    "gfb_mg_graph_upload": ([_vp, _u64, _u64, _vp, _vp, _vp, _int, _int], _int),
+    "gfb_mg_ranges": ([_vp, _vp], _int),
+    "gfb_mg_sssp": ([_vp, _u32, C.POINTER(SsspOpts), _vp, _vp, C.POINTER(SsspStats)], _int),
+    "gfb_mg_destroy": ([_vp], _int),
 }
 
 PEER_HANDLE_BYTES = 64

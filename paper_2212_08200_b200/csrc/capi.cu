@@ -534,3 +534,68 @@ int gfb_peer_free(gfb_peer* p) {
     gfb::peer_free(P(p));
   });
 }
+
+// ---- one process, several partitions (include/gfb.h) ----
+struct gfb_mg : gfb::Mg {};
+
+int gfb_mg_create(int ndev, const int* devices, gfb_mg** out) {
+  return guard([&] {
+    NEED(devices);
+    NEED(out);
+    if (ndev < 1 || ndev > gfb::PEER_MAX) gfb::fail(GFB_EINVAL, "mg: 1 <= ndev <= 8");
+    auto mg = std::make_unique<gfb_mg>();
+    for (int i = 0; i < ndev; ++i) {
+      gfb_ctx* c = nullptr;
+      const int rc = gfb_ctx_create(devices[i], &c);
+      if (rc != GFB_OK) {
+        for (gfb::Ctx* x : mg->ctx) gfb_ctx_destroy(static_cast<gfb_ctx*>(x));
+        gfb::fail(rc, gfb_last_error());
+      }
+      mg->ctx.push_back(c);
+    }
+    *out = mg.release();
+  });
+}
+
+int gfb_mg_graph_upload(gfb_mg* mg, uint64_t n, uint64_t m, const uint32_t* row_offsets,
+                        const uint32_t* col, const void* w, int w_host_type, int wtype) {
+  return guard([&] {
+    NEED(mg);
+    NEED(row_offsets);
+    if (m && (!col || !w)) gfb::fail(GFB_EINVAL, "mg: null edge arrays");
+    gfb::mg_upload(mg, n, m, row_offsets, col, w, w_host_type, wtype);
+  });
+}
+
+int gfb_mg_ranges(gfb_mg* mg, uint32_t* range_starts) {
+  return guard([&] {
+    NEED(mg);
+    NEED(range_starts);
+    if (mg->starts.empty()) gfb::fail(GFB_ELOGIC, "mg: no graph uploaded");
+    std::memcpy(range_starts, mg->starts.data(), mg->starts.size() * 4);
+  });
+}
+
+int gfb_mg_sssp(gfb_mg* mg, uint32_t source, const gfb_sssp_opts* opts, double* dist,
+                uint32_t* pred, gfb_sssp_stats* stats) {
+  return guard([&] {
+    NEED(mg);
+    gfb_sssp_opts o;
+    gfb_sssp_opts_default(&o);
+    if (opts) {
+      if (opts->struct_size != sizeof(gfb_sssp_opts)) gfb::fail(GFB_EINVAL, "sssp: opts struct_size mismatch");
+      o = *opts;
+    }
+    gfb::mg_sssp(mg, source, &o, dist, pred, stats);
+  });
+}
+
+int gfb_mg_destroy(gfb_mg* mg) {
+  return guard([&] {
+    if (!mg) return;
+    gfb::mg_free(mg);
+    for (gfb::Ctx* x : mg->ctx) gfb_ctx_destroy(static_cast<gfb_ctx*>(x));
+    delete mg;
+  });
+}
+

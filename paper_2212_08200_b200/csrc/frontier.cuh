@@ -258,6 +258,25 @@ __device__ __forceinline__ uint32_t obucket(const D* dist, uint32_t v, uint32_t 
   return k <= base ? 0u : min(k - base, (uint32_t)OB_N - 1);
 }
 
+// Partitioned loop (peer.cu): remote relaxations set the owner's frontier bit
+// without knowing whether they lowered its distance (the sender tested
+// against its own proposal cache).  dexp[v] = distance bits v was last
+// expanded with; a set bit whose distance is unchanged is dropped here.
+// nullptr (single GPU: a bit is only set by a relaxation that lowered v).
+template <class D>
+__device__ __forceinline__ void drop_unchanged(WarpWords& w, const D* dist, const uint32_t* dexp,
+                                               uint32_t wbase) {
+  if (!dexp) return;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < F_WPW; ++j) {
+    const uint32_t v = (wbase + j) * 32 + lane;
+    bool k = (w.keep[j] >> lane) & 1u;
+    if (k) k = dbits(dist[v]) != dexp[v];
+    w.keep[j] = __ballot_sync(0xffffffffu, k);
+  }
+}
+
 // Count: per tile (the F_WORDS-word tiles of k_fcount) and bucket -> agg,
 // and the bucket totals accumulated in btot[OB_N] (64-bit: count << 32 | edges).
 // Native 32-bit shared atomics (a 64-bit shared atomicAdd is a CAS loop).
@@ -265,7 +284,8 @@ template <class D>
 __global__ void __launch_bounds__(F_WARPS * 32)
 k_fcount_o(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uint32_t nwords,
            const D* __restrict__ dist, const Ctl* __restrict__ ctl,
-           unsigned long long* agg, unsigned long long* btot, uint32_t* tflag) {
+           unsigned long long* agg, unsigned long long* btot, uint32_t* tflag,
+           const uint32_t* dexp = nullptr) {
   __shared__ uint32_t s_c[OB_N], s_e[OB_N];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x < OB_N) s_c[threadIdx.x] = s_e[threadIdx.x] = 0;
@@ -275,6 +295,7 @@ k_fcount_o(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uin
   WarpWords w;
   uint32_t raw;
   load_warp_words(ro, bm, nwords, wbase, w, &raw);
+  drop_unchanged(w, dist, dexp, wbase);
 #pragma unroll
   for (int j = 0; j < F_WPW; ++j) {
     if ((w.keep[j] >> lane) & 1u) {
@@ -349,7 +370,7 @@ __global__ void __launch_bounds__(F_WARPS * 32)
 k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur, uint32_t nwords,
             const D* __restrict__ dist, const Ctl* __restrict__ ctl,
             const unsigned long long* __restrict__ agg, unsigned long long* bcur, Plan plan,
-            const uint32_t* __restrict__ tflag) {
+            const uint32_t* __restrict__ tflag, uint32_t* dexp = nullptr) {
   constexpr int TV = F_WORDS * 32, NT = F_WARPS * 32, VT = TV / NT;
   __shared__ uint32_t s_cb[OB_N], s_ce[OB_N], s_lb[OB_N], s_rank[OB_N];
   __shared__ uint32_t s_deg[TV], s_pre[TV];
@@ -377,6 +398,7 @@ k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
   WarpWords w;
   uint32_t raw;
   load_warp_words(ro, bm_next, nwords, wbase, w, &raw);
+  drop_unchanged(w, dist, dexp, wbase);
   __syncthreads();
   uint32_t pend = 0;
 #pragma unroll
@@ -395,6 +417,7 @@ k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
       s_bk[p] = (uint8_t)b;
       plan.v[gi] = v;
       plan.start[gi] = w.st[j];
+      if (dexp) dexp[v] = dbits(dist[v]);
     }
   }
   if (lane < F_WPW && wbase + lane < nwords) {

@@ -155,6 +155,19 @@ void peer_sssp(Peer*, uint32_t source, const gfb_sssp_opts*, gfb_sssp_stats*);
 void peer_read(Peer*, double* dist, void* dist_native, uint32_t* pred);
 void peer_free(Peer*);
 Ctx* peer_ctx(Peer*);
+// One process driving every partition (peer.cu): ctx[q] runs partition q.
+struct Mg {
+  std::vector<Ctx*> ctx;  // owned through the C ABI (gfb_ctx_create / destroy)
+  std::vector<Peer*> peers;
+  std::vector<uint32_t> starts;
+  uint64_t n = 0;
+  int wtype = -1;
+};
+void mg_upload(Mg*, uint64_t n, uint64_t m, const uint32_t* ro, const uint32_t* col,
+               const void* w, int htype, int wtype);
+void mg_sssp(Mg*, uint32_t source, const gfb_sssp_opts*, double* dist, uint32_t* pred,
+             gfb_sssp_stats*);
+void mg_free(Mg*);
 
 // grid sizes
 inline int stride_grid(const Ctx* c) { return c->num_sms * 8; }

@@ -162,7 +162,8 @@ __global__ void __launch_bounds__(32) k_xbar(XBarArgs b) {
 template <class W>
 __global__ void k_peer_init(typename DT<W>::D* dist, unsigned long long* pkey, uint32_t* bm_next,
                             uint32_t* bm_cur, uint32_t* res, uint32_t* cand, uint32_t* repair,
-                            uint32_t n, uint32_t nwords, const uint32_t* src_local, Ctl* ctl) {
+                            uint32_t n, uint32_t nwords, const uint32_t* src_local, Ctl* ctl,
+                            uint32_t* dexp) {
   using D = typename DT<W>::D;
   const uint32_t s = *src_local;  // NIL when the source lives on another rank
   const uint32_t stride = gridDim.x * blockDim.x;
@@ -171,6 +172,7 @@ __global__ void k_peer_init(typename DT<W>::D* dist, unsigned long long* pkey, u
     pkey[i] = ~0ull;
     res[i] = 0;
     cand[i] = NIL;
+    dexp[i] = 0xFFFFFFFFu;  // never expanded (no distance has these bits)
   }
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nwords; i += stride) {
     bm_next[i] = (s != NIL && (s >> 5) == i) ? (1u << (s & 31)) : 0u;
@@ -340,10 +342,14 @@ struct Peer {
   void* slab = nullptr;
   PeerLayout lay{};
   std::vector<void*> opened;  // mapped peer slabs (nullptr for self)
+  std::vector<char*> bases;   // every rank's slab base as seen from this rank
   bool linked = false;
   PeerTab tab{};
   DBuf tab_dev, ctl, epoch, src_dev, bm_cur, pred, list, pv, pstart, poff, ptseg, oagg, obuck;
-  DBuf rc;  // proposal cache for remote destinations (n_global, nparts > 1)
+  DBuf rc;     // proposal cache for remote destinations (n_global, nparts > 1)
+  DBuf rlist;  // predecessor repair: this rank's edges into unresolved vertices
+  DBuf dexp;   // distance bits each local vertex was last expanded with
+  uint64_t call_l0 = 0;
   uint32_t ftiles = 0;
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
@@ -404,6 +410,7 @@ Peer* peer_create(Ctx* c, int rank, int nparts, const uint32_t* range_starts, ui
   p->obuck.alloc(2 * OB_N * 8, s);
   GFB_CUDA(cudaMemsetAsync(p->obuck.p, 0, 2 * OB_N * 8, s));
   p->tab_dev.alloc(sizeof(PeerTab), s);
+  p->dexp.alloc(n1 * 4, s);
   c->sync();
   return p.release();
 }
@@ -414,27 +421,17 @@ void peer_export(Peer* p, void* handle) {
   std::memcpy(handle, &h, sizeof(h));
 }
 
-void peer_link(Peer* p, const void* handles) {
-  if (p->linked) fail(GFB_ELOGIC, "peer: already linked");
+// Peer table from every rank's slab base (own slab included).
+static void peer_link_bases(Peer* p, const std::vector<char*>& bases) {
   PeerTab& t = p->tab;
   t = PeerTab{};
-  p->opened.assign(p->nparts, nullptr);
   for (int q = 0; q <= p->nparts; ++q) t.start[q] = p->starts[q];
   for (int q = p->nparts + 1; q <= PEER_MAX; ++q) t.start[q] = (uint32_t)p->n_global;
+  p->bases = bases;
   for (int q = 0; q < p->nparts; ++q) {
-    char* base;
-    if (q == p->rank) {
-      base = static_cast<char*>(p->slab);
-    } else {
-      cudaIpcMemHandle_t h;
-      std::memcpy(&h, static_cast<const char*>(handles) + (size_t)q * sizeof(h), sizeof(h));
-      void* ptr = nullptr;
-      GFB_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
-      p->opened[q] = ptr;
-      base = static_cast<char*>(ptr);
-    }
     const PeerLayout l = peer_layout(p->starts[q + 1] - p->starts[q]);
     const uint32_t s0 = p->starts[q];
+    char* base = bases[q];
     // pre-offset so that index = global id (s0 is a multiple of 32)
     t.dist[q] = reinterpret_cast<uint32_t*>(base + l.dist) - s0;
     t.pkey[q] = reinterpret_cast<unsigned long long*>(base + l.pkey) - s0;
@@ -453,6 +450,45 @@ void peer_link(Peer* p, const void* handles) {
   GFB_CUDA(cudaMemcpyAsync(p->tab_dev.p, &t, sizeof(t), cudaMemcpyHostToDevice, p->ctx->stream));
   p->ctx->sync();
   p->linked = true;
+}
+
+// Multi-process: open the peers' exported slabs (NVLink peer mappings).
+void peer_link(Peer* p, const void* handles) {
+  if (p->linked) fail(GFB_ELOGIC, "peer: already linked");
+  p->opened.assign(p->nparts, nullptr);
+  std::vector<char*> bases(p->nparts);
+  for (int q = 0; q < p->nparts; ++q) {
+    if (q == p->rank) {
+      bases[q] = static_cast<char*>(p->slab);
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + (size_t)q * sizeof(h), sizeof(h));
+    void* ptr = nullptr;
+    GFB_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    p->opened[q] = ptr;
+    bases[q] = static_cast<char*>(ptr);
+  }
+  peer_link_bases(p, bases);
+}
+
+// One process, all ranks: direct pointers (peer access between devices).
+static void peer_link_local(const std::vector<Peer*>& ps) {
+  std::vector<char*> bases;
+  for (Peer* p : ps) bases.push_back(static_cast<char*>(p->slab));
+  for (Peer* a : ps) {
+    GFB_CUDA(cudaSetDevice(a->ctx->device));
+    for (Peer* b : ps) {
+      if (b->ctx->device == a->ctx->device) continue;
+      int ok = 0;
+      GFB_CUDA(cudaDeviceCanAccessPeer(&ok, a->ctx->device, b->ctx->device));
+      if (!ok) fail(GFB_ECUDA, "mg: no peer access between devices");
+      const cudaError_t e = cudaDeviceEnablePeerAccess(b->ctx->device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else GFB_CUDA(e);
+    }
+    peer_link_bases(a, bases);
+  }
 }
 
 static unsigned long long peer_timeout_ns() {
@@ -484,8 +520,7 @@ struct PeerRun {
     XBarArgs b{};
     for (int q = 0; q < p->nparts; ++q) {
       const PeerLayout l = peer_layout(p->starts[q + 1] - p->starts[q]);
-      char* base = q == p->rank ? static_cast<char*>(p->slab) : static_cast<char*>(p->opened[q]);
-      b.mbox[q] = reinterpret_cast<uint32_t*>(base + l.mbox);
+      b.mbox[q] = reinterpret_cast<uint32_t*>(p->bases[q] + l.mbox);
     }
     b.nparts = (uint32_t)p->nparts;
     b.self = (uint32_t)p->rank;
@@ -508,13 +543,14 @@ struct PeerRun {
     cudaGraphConditionalHandle none{};
     k_fcount_o<D><<<tiles, F_WARPS * 32, 0, st>>>(g->ro.as<uint32_t>(), bm(), p->nwords, dist(),
                                                   ctl(), p->oagg.as<unsigned long long>(), bt,
-                                                  tflag);
+                                                  tflag, p->dexp.as<uint32_t>());
     k_fscan_o<<<1, 32, 0, st>>>(bt, bt + OB_N, plan(), ctl(), (uint32_t)g->m, 1.0f, 0, 0, none,
                                 none, 0, 0, defer_pct, (uint32_t)(g->m >> 2), 0u);
     k_fwrite_o<D><<<tiles, F_WARPS * 32, 0, st>>>(g->ro.as<uint32_t>(), bm(),
                                                   p->bm_cur.as<uint32_t>(), p->nwords, dist(),
                                                   ctl(), p->oagg.as<unsigned long long>(),
-                                                  bt + OB_N, plan(), tflag);
+                                                  bt + OB_N, plan(), tflag,
+                                                  p->dexp.as<uint32_t>());
     p->launches += 3;
   }
 
@@ -551,7 +587,8 @@ struct PeerRun {
     xbar(s, XB_PLAIN);
     k_peer_init<W><<<stride_grid(c), 256, 0, s>>>(dist(), pkey(), bm(), p->bm_cur.as<uint32_t>(),
                                                   res(), cand(), repair(), p->n, p->nwords,
-                                                  p->src_dev.as<uint32_t>(), ctl());
+                                                  p->src_dev.as<uint32_t>(), ctl(),
+                                                  p->dexp.as<uint32_t>());
     if (p->rc.p)  // nothing proposed yet: the unreachable distance's bits
       k_peer_fill<<<stride_grid(c), 256, 0, s>>>(p->rc.as<uint32_t>(),
                                                  std::is_same<D, float>::value ? 0x7F800000u
@@ -586,42 +623,80 @@ struct PeerRun {
     p->graph = G;
   }
 
-  void check_err(const Ctl& h) {
-    if (h.err & 8u) fail(GFB_ECUDA, "peer: cross-rank barrier timed out (a rank did not arrive)");
-    if (h.err & 1u) fail(GFB_ERANGE, "sssp: u32 distance overflow (use f64 weights)");
-  }
+  // ---- one call, split into launch steps: the host runs each step on
+  // every peer before reading any result (peer_call), because a rank's
+  // device barriers only complete when all ranks have launched the step.
+  uint32_t defer = 10;
+  uint32_t src_local = NIL;
 
-  void run(uint32_t source, const gfb_sssp_opts* o, gfb_sssp_stats* st) {
+  void prepare(uint32_t source, const gfb_sssp_opts* o) {
     if (!p->linked) fail(GFB_ELOGIC, "peer: gfb_peer_link first");
     if (source >= p->n_global) fail(GFB_ERANGE, "sssp: source out of range");
     if (o->direction == GFB_DIR_PULL) fail(GFB_EINVAL, "peer: the partitioned SSSP is push-only");
     if (o->delta > 0) fail(GFB_EINVAL, "peer: the near-far filter is single-GPU only");
     p->has_result = false;
-    const int variant = o->reserved[0];
-    const uint32_t defer = variant == 99 ? 100u : 10u;  // as Runner::defer_pct
-    const uint32_t src_local = (source >= p->lo && source < p->lo + p->n) ? source - p->lo : NIL;
-    GFB_CUDA(cudaMemcpyAsync(p->src_dev.p, &src_local, 4, cudaMemcpyHostToDevice, s));
-    GFB_CUDA(cudaEventRecord(c->ev[0], s));
+    defer = o->reserved[0] == 99 ? 100u : 10u;  // as Runner::defer_pct
+    src_local = (source >= p->lo && source < p->lo + p->n) ? source - p->lo : NIL;
     if (!p->exec || p->graph_key != (int)defer) {
       GFB_CUDA(cudaStreamSynchronize(s));
       build(defer);
       p->graph_key = (int)defer;
-      GFB_CUDA(cudaEventRecord(c->ev[0], s));
     }
-    const uint64_t l0 = p->launches;
+    p->call_l0 = p->launches;
+    GFB_CUDA(cudaMemcpyAsync(p->src_dev.p, &src_local, 4, cudaMemcpyHostToDevice, s));
+    GFB_CUDA(cudaEventRecord(c->ev[0], s));
+  }
+  void launch_loop() {
     GFB_CUDA(cudaGraphLaunch(p->exec, s));
-    Ctl h = c->read_ctl(ctl());
-    check_err(h);
-    const uint64_t loop_kernels = (p->rc.p ? 7 : 6) + 6ull * h.supersteps;
-    p->launches = l0 + loop_kernels;
-    uint64_t fallback = 0;
-    pred_pass(src_local, o->compute_pred != 0, &fallback);
+    p->launches += 0;  // counted from the superstep count after the call
+  }
+  void launch_verify() {
+    k_peer_verify<W><<<c->num_sms * 8, 256, 0, s>>>(p->g->ro.as<uint32_t>(),
+                                                    p->tab_dev.as<PeerTab>(), dist(), pkey(),
+                                                    p->pred.as<uint32_t>(), res(), repair(),
+                                                    p->list.as<uint32_t>(), p->n, src_local, ctl());
+    ++p->launches;
+    xbar(s, XB_PLAIN);  // every owner's res / repair state visible
+  }
+  void launch_key_batch(uint32_t base) {
+    for (uint32_t k = base + 1; k <= base + 4; ++k) {
+      k_peer_key_round<W><<<c->num_sms, 256, 0, s>>>(p->list.as<uint32_t>(),
+                                                     p->tab_dev.as<PeerTab>(), pkey(), dist(),
+                                                     p->pred.as<uint32_t>(), res(), repair(), k,
+                                                     ctl());
+      ++p->launches;
+      xbar(s, XB_PLAIN);  // res is read across ranks by the next round
+    }
+  }
+  uint32_t launch_inedges() {
+    Graph* g = p->g.get();
+    const uint32_t cap = (uint32_t)std::min<uint64_t>(g->m + 1, 1u << 24);
+    if (p->rlist.bytes < (size_t)cap * 16) p->rlist.alloc((size_t)cap * 16, s);
+    GFB_CUDA(cudaMemsetAsync(&ctl()->out_count, 0, 4, s));
+    k_peer_inedges<W><<<stride_grid(c), 256, 0, s>>>(g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(),
+                                                     p->tab_dev.as<PeerTab>(), p->n,
+                                                     p->rlist.as<uint4>(), cap, ctl());
+    ++p->launches;
+    return cap;
+  }
+  void launch_round(uint32_t round, uint32_t base, uint32_t cap) {
+    GFB_CUDA(cudaMemsetAsync(&ctl()->flag, 0, 4, s));
+    k_peer_list_round<W><<<stride_grid(c), 256, 0, s>>>(p->rlist.as<uint4>(), ctl(), cap,
+                                                        p->tab_dev.as<PeerTab>(), round, base);
+    xbar(s, XB_PLAIN);  // candidates landed at their owners
+    k_pred_apply<<<stride_grid(c), 256, 0, s>>>(cand(), p->pred.as<uint32_t>(), res(), repair(),
+                                                p->n, round, ctl(), base);
+    xbar(s, XB_PLAIN);  // global count of this round's resolutions
+    p->launches += 2;
+  }
+  void finish(gfb_sssp_stats* st, uint64_t fallback) {
     GFB_CUDA(cudaEventRecord(c->ev[1], s));
-    h = c->read_ctl(ctl());
+    const Ctl h = c->read_ctl(ctl());
     check_err(h);
     float ms = 0;
     GFB_CUDA(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
     p->has_result = true;
+    p->launches += (p->rc.p ? 7 : 6) + 6ull * h.supersteps;  // the loop graph's kernels
     if (st) {
       *st = gfb_sssp_stats{};
       st->supersteps = h.supersteps;
@@ -632,70 +707,91 @@ struct PeerRun {
       st->pred_fallback = fallback;
       st->device_ms = ms;
       st->advance_launches = h.supersteps;
-      st->kernel_launches = p->launches - l0;
+      st->kernel_launches = p->launches - p->call_l0;
     }
   }
-
-  void pred_pass(uint32_t src_local, bool want, uint64_t* fallback) {
-    const PeerTab* tab = p->tab_dev.as<PeerTab>();
-    Graph* g = p->g.get();
-    k_peer_verify<W><<<c->num_sms * 8, 256, 0, s>>>(g->ro.as<uint32_t>(), tab, dist(), pkey(),
-                                                    p->pred.as<uint32_t>(), res(), repair(),
-                                                    p->list.as<uint32_t>(), p->n, src_local, ctl());
-    ++p->launches;
-    xbar(s, XB_PLAIN);  // every owner's res / repair state visible
-    Ctl h = c->read_ctl(ctl());
+  Ctl read() {
+    const Ctl h = c->read_ctl(ctl());
     check_err(h);
-    *fallback = h.gunres;
-    if (!want || h.gunres == 0) return;
-    // key rounds (barrier after each: res is read across ranks)
-    uint32_t base = 0, before = 0;
-    uint64_t left = h.gunres;
-    for (;;) {
-      for (uint32_t k = base + 1; k <= base + 4; ++k) {
-        k_peer_key_round<W><<<c->num_sms, 256, 0, s>>>(p->list.as<uint32_t>(), tab, pkey(), dist(),
-                                                       p->pred.as<uint32_t>(), res(), repair(), k,
-                                                       ctl());
-        xbar(s, XB_PLAIN);
-        p->launches += 1;
-      }
-      base += 4;
-      h = c->read_ctl(ctl());
-      check_err(h);
-      left = h.gunres - std::min(h.gunres, h.gresolved);
-      if (left == 0 || h.gresolved == before || base >= 64) break;
-      before = h.gresolved;
-    }
-    if (left == 0) return;
-    // in-edge rounds over this rank's out-edges into unresolved vertices
-    const uint32_t cap = (uint32_t)std::min<uint64_t>(g->m + 1, 1u << 24);
-    TBuf lst;
-    lst.alloc((size_t)cap * 16, s);
-    GFB_CUDA(cudaMemsetAsync(&ctl()->out_count, 0, 4, s));
-    k_peer_inedges<W><<<stride_grid(c), 256, 0, s>>>(g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(),
-                                                     tab, p->n, lst.as<uint4>(), cap, ctl());
-    ++p->launches;
-    for (uint32_t round = 1; left > 0; ++round) {
-      GFB_CUDA(cudaMemsetAsync(&ctl()->flag, 0, 4, s));
-      k_peer_list_round<W><<<stride_grid(c), 256, 0, s>>>(lst.as<uint4>(), ctl(), cap, tab, round,
-                                                          base);
-      xbar(s, XB_PLAIN);  // candidates landed at their owners
-      k_pred_apply<<<stride_grid(c), 256, 0, s>>>(cand(), p->pred.as<uint32_t>(), res(), repair(),
-                                                  p->n, round, ctl(), base);
-      xbar(s, XB_PLAIN);  // global count of this round's resolutions
-      p->launches += 2;
-      h = c->read_ctl(ctl());
-      check_err(h);
-      if (h.err & 4u) fail(GFB_ELOGIC, "peer: predecessor repair list overflow");
-      if (h.gflag == 0 && round > 1) fail(GFB_ELOGIC, "peer: predecessor repair made no progress");
-      left -= std::min<uint64_t>(left, h.gflag);
-    }
+    return h;
+  }
+
+  static void check_err(const Ctl& h) {
+    if (h.err & 8u) fail(GFB_ECUDA, "peer: cross-rank barrier timed out (a rank did not arrive)");
+    if (h.err & 1u) fail(GFB_ERANGE, "sssp: u32 distance overflow (use f64 weights)");
+    if (h.err & 4u) fail(GFB_ELOGIC, "peer: predecessor repair list overflow");
   }
 };
 
+// One SSSP over the peers this process drives (one per rank in the
+// multi-process case, all of them for gfb_mg): every step is launched on all
+// peers, then every peer's control block is read.  The barrier-published
+// global counters are equal on all ranks, so all hosts take the same
+// decisions without a host collective.
+template <class W>
+static void peer_call_t(const std::vector<Peer*>& ps, uint32_t source, const gfb_sssp_opts* o,
+                        std::vector<gfb_sssp_stats>* st) {
+  std::vector<PeerRun<W>> rs;
+  for (Peer* p : ps) rs.push_back(PeerRun<W>{p, p->ctx, p->ctx->stream});
+  auto each = [&](auto&& f) {
+    for (auto& r : rs) {
+      GFB_CUDA(cudaSetDevice(r.c->device));
+      f(r);
+    }
+  };
+  std::vector<Ctl> h(rs.size());
+  auto read_all = [&] {
+    for (size_t i = 0; i < rs.size(); ++i) {
+      GFB_CUDA(cudaSetDevice(rs[i].c->device));
+      h[i] = rs[i].read();
+    }
+  };
+  each([&](PeerRun<W>& r) { r.prepare(source, o); });
+  each([&](PeerRun<W>& r) { r.launch_loop(); });
+  each([&](PeerRun<W>& r) { r.launch_verify(); });
+  read_all();
+  const uint64_t fallback = h[0].gunres;
+  if (o->compute_pred && h[0].gunres > 0) {
+    uint32_t base = 0, before = 0;
+    uint64_t left = h[0].gunres;
+    for (;;) {  // key rounds in batches of 4 while they make progress
+      each([&](PeerRun<W>& r) { r.launch_key_batch(base); });
+      base += 4;
+      read_all();
+      left = h[0].gunres - std::min(h[0].gunres, h[0].gresolved);
+      if (left == 0 || h[0].gresolved == before || base >= 64) break;
+      before = h[0].gresolved;
+    }
+    if (left > 0) {
+      std::vector<uint32_t> caps;
+      each([&](PeerRun<W>& r) { caps.push_back(r.launch_inedges()); });
+      for (uint32_t round = 1; left > 0; ++round) {
+        size_t i = 0;
+        each([&](PeerRun<W>& r) { r.launch_round(round, base, caps[i++]); });
+        read_all();
+        if (h[0].gflag == 0 && round > 1)
+          fail(GFB_ELOGIC, "peer: predecessor repair made no progress");
+        left -= std::min<uint64_t>(left, h[0].gflag);
+      }
+    }
+  }
+  if (st) st->assign(rs.size(), gfb_sssp_stats{});
+  for (size_t i = 0; i < rs.size(); ++i) {
+    GFB_CUDA(cudaSetDevice(rs[i].c->device));
+    rs[i].finish(st ? &(*st)[i] : nullptr, fallback);
+  }
+}
+
+static void peer_call(const std::vector<Peer*>& ps, uint32_t source, const gfb_sssp_opts* o,
+                      std::vector<gfb_sssp_stats>* st) {
+  if (ps[0]->g->wtype == GFB_W_F32) peer_call_t<float>(ps, source, o, st);
+  else peer_call_t<uint32_t>(ps, source, o, st);
+}
+
 void peer_sssp(Peer* p, uint32_t source, const gfb_sssp_opts* o, gfb_sssp_stats* st) {
-  if (p->g->wtype == GFB_W_F32) PeerRun<float>{p, p->ctx, p->ctx->stream}.run(source, o, st);
-  else PeerRun<uint32_t>{p, p->ctx, p->ctx->stream}.run(source, o, st);
+  std::vector<gfb_sssp_stats> v;
+  peer_call({p}, source, o, &v);
+  if (st) *st = v[0];
 }
 
 // widened distances / native bits / predecessors (global ids) of the local range
@@ -728,6 +824,76 @@ void peer_read(Peer* p, double* dist, void* dist_native, uint32_t* pred) {
 }
 
 void peer_free(Peer* p) { delete p; }
+
+// ---- one process driving every partition (gfb_mg_*) ----------------------
+// Edge-balanced cut points rounded down to multiples of 32.
+static std::vector<uint32_t> mg_ranges(const uint32_t* ro, uint64_t n, int parts) {
+  const uint64_t m = ro[n];
+  std::vector<uint32_t> rs(parts + 1, 0);
+  for (int q = 1; q < parts; ++q) {
+    const uint64_t target = (uint64_t)q * m / parts;
+    const uint64_t v = std::lower_bound(ro, ro + n + 1, (uint32_t)target) - ro;
+    rs[q] = (uint32_t)(std::min<uint64_t>(v, n) & ~31ull);
+    rs[q] = std::max(rs[q], rs[q - 1]);
+  }
+  rs[parts] = (uint32_t)n;
+  return rs;
+}
+
+void mg_upload(Mg* mg, uint64_t n, uint64_t m, const uint32_t* ro, const uint32_t* col,
+               const void* w, int htype, int wtype) {
+  if (n == 0 || n >= 0xFFFFFFFFull) fail(GFB_EINVAL, "mg: bad vertex count");
+  if (ro[0] != 0 || ro[n] != m) fail(GFB_EINVAL, "mg: row_offsets must run from 0 to m");
+  for (Peer* p : mg->peers) delete p;
+  mg->peers.clear();
+  const int P = (int)mg->ctx.size();
+  mg->starts = mg_ranges(ro, n, P);
+  mg->n = n;
+  mg->wtype = wtype;
+  const size_t wsz = htype == GFB_W_F64 ? 8 : 4;
+  for (int q = 0; q < P; ++q) {
+    const uint32_t lo = mg->starts[q], hi = mg->starts[q + 1];
+    std::vector<uint32_t> rl(hi - lo + 1);
+    for (uint32_t i = 0; i <= hi - lo; ++i) rl[i] = ro[lo + i] - ro[lo];
+    GFB_CUDA(cudaSetDevice(mg->ctx[q]->device));
+    mg->peers.push_back(peer_create(mg->ctx[q], q, P, mg->starts.data(), rl[hi - lo], rl.data(),
+                                    col + ro[lo],
+                                    static_cast<const char*>(w) + (size_t)ro[lo] * wsz, htype,
+                                    wtype));
+  }
+  peer_link_local(mg->peers);
+}
+
+void mg_sssp(Mg* mg, uint32_t source, const gfb_sssp_opts* o, double* dist, uint32_t* pred,
+             gfb_sssp_stats* st) {
+  if (mg->peers.empty()) fail(GFB_ELOGIC, "mg: no graph uploaded");
+  std::vector<gfb_sssp_stats> v;
+  peer_call(mg->peers, source, o, &v);
+  for (Peer* p : mg->peers) {
+    GFB_CUDA(cudaSetDevice(p->ctx->device));
+    if (dist || pred)
+      peer_read(p, dist ? dist + p->lo : nullptr, nullptr, pred ? pred + p->lo : nullptr);
+  }
+  if (st) {  // whole-graph view: sums of the shares, max device time
+    *st = v[0];
+    for (size_t i = 1; i < v.size(); ++i) {
+      st->relaxations += v[i].relaxations;
+      st->n_reach += v[i].n_reach;
+      st->m_reach += v[i].m_reach;
+      st->kernel_launches += v[i].kernel_launches;
+      st->device_ms = std::max(st->device_ms, v[i].device_ms);
+    }
+  }
+}
+
+void mg_free(Mg* mg) {
+  for (Peer* p : mg->peers) {
+    GFB_CUDA(cudaSetDevice(p->ctx->device));
+    p->ctx->sync();
+  }
+  for (Peer* p : mg->peers) delete p;
+  mg->peers.clear();
+}
 Ctx* peer_ctx(Peer* p) { return p->ctx; }
 
 }  // namespace gfb

@@ -134,3 +134,50 @@ def gather(peer, native=False, group=None):
     parts = [None] * peer.nparts
     dist.all_gather_object(parts, (d, p), group=group)
     return np.concatenate([x[0] for x in parts]), np.concatenate([x[1] for x in parts])
+
+
+class MgSssp:
+    """The same partitioned SSSP driven by one process (gfb_mg_*): partition q
+    on ``devices[q]`` (entries may repeat a device).  Takes the whole
+    reference-layout CSR; returns whole-graph results."""
+
+    def __init__(self, devices, row_offsets, col, w):
+        import paper_2212_08200_b200 as gb
+        self.gb = gb
+        self.lib = _lib.load()
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        gb.check(self.lib.gfb_mg_create(len(devices), devs, C.byref(h)))
+        self.h = h
+        self.parts = len(devices)
+        ro = np.ascontiguousarray(row_offsets, np.uint32)
+        col = np.ascontiguousarray(col, np.uint32)
+        w = np.ascontiguousarray(w)
+        ht = {np.dtype(np.float32): _lib.W_F32, np.dtype(np.uint32): _lib.W_U32,
+              np.dtype(np.float64): _lib.W_F64}[w.dtype]
+        self.wtype = _lib.W_U32 if ht == _lib.W_U32 else _lib.W_F32
+        self.n, self.m = len(ro) - 1, len(col)
+        gb.check(self.lib.gfb_mg_graph_upload(
+            self.h, self.n, self.m, C.c_void_p(ro.ctypes.data),
+            C.c_void_p(col.ctypes.data) if self.m else None,
+            C.c_void_p(w.ctypes.data) if self.m else None, ht, self.wtype))
+
+    def ranges(self):
+        rs = np.empty(self.parts + 1, np.uint32)
+        self.gb.check(self.lib.gfb_mg_ranges(self.h, C.c_void_p(rs.ctypes.data)))
+        return rs
+
+    def sssp(self, source, want_pred=True, variant=0):
+        o = self.gb._opts(direction="push", compute_pred=want_pred, variant=variant)
+        st = _lib.SsspStats()
+        dist = np.empty(self.n, np.float64)
+        pred = np.empty(self.n, np.uint32)
+        self.gb.check(self.lib.gfb_mg_sssp(self.h, int(source), C.byref(o),
+                                           C.c_void_p(dist.ctypes.data),
+                                           C.c_void_p(pred.ctypes.data), C.byref(st)))
+        return dist, pred, {k: getattr(st, k) for k, _ in _lib.SsspStats._fields_}
+
+    def free(self):
+        if self.h:
+            self.gb.check(self.lib.gfb_mg_destroy(self.h))
+            self.h = None

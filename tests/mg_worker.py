@@ -1,0 +1,41 @@
+"""gfb_mg_* parity in one process (test_peer_gpu.py::test_mg_one_process):
+python tests/mg_worker.py PARTS -- all partitions on device 0."""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+sys.path.insert(0, HERE)
+import peer_worker as W  # noqa: E402
+from paper_2212_08200_b200 import peer  # noqa: E402
+
+
+def main():
+    parts = int(sys.argv[1])
+    for name, (n, ro, col, w), sources in [("rmat13-f32", W.rmat(13, 1, 1), [0, 8000]),
+                                           ("rmat12-u32", W.rmat(12, 0, 2), [0, 77]),
+                                           ("grid48-f32", W.grid(48, 3), [0, 2000]),
+                                           ("corpus-f32", W.corpus(300, 9001), [0, 5])]:
+        mg = peer.MgSssp([0] * parts, ro, col, w)
+        rs = mg.ranges()
+        assert rs[0] == 0 and rs[-1] == n and all(int(c) % 32 == 0 for c in rs[1:-1])
+        for src in sources:
+            for _ in range(2):
+                d, p, st = mg.sssp(src)
+                W.check(name, n, ro, col, w, src, d, p, 0)
+                fin = np.isfinite(d)
+                assert st["n_reach"] == int(fin.sum())
+                assert st["m_reach"] == int(np.diff(ro.astype(np.int64))[fin].sum())
+        try:
+            mg.sssp(n)
+            raise AssertionError("source out of range accepted")
+        except IndexError:
+            pass
+        mg.free()
+    print(f"MG_OK parts {parts}", flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -38,3 +38,18 @@ def test_peer_partitioned_sssp(world):
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert out.count("PEER_OK") == world, out[-4000:]
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 8])
+def test_mg_one_process(parts):
+    """gfb_mg_*: one host thread drives `parts` partitions, all on device 0
+    here (concurrent streams of one context, lock-step host steps).  Same-
+    device partitions need a hardware queue per stream, or a spinning
+    barrier can block a peer's kernels behind it: CUDA_DEVICE_MAX_CONNECTIONS
+    is raised for the child (one device per partition has no such limit)."""
+    env = dict(os.environ, GFB_PEER_TIMEOUT_S="20", CUDA_DEVICE_MAX_CONNECTIONS="32")
+    r = subprocess.run([sys.executable, os.path.join(HERE, "mg_worker.py"), str(parts)],
+                       capture_output=True, text=True, timeout=900, env=env,
+                       cwd=os.path.dirname(HERE))
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and "MG_OK" in out, out[-4000:]
