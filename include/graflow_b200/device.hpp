@@ -89,9 +89,21 @@ struct DevicePolicy {
   float pull_alpha = 0.25f;    // pull when frontier edges > m / pull_alpha
   double delta = 0.0;          // > 0: near-far filter (push only; high-diameter
                                // graphs, u32/f32 arithmetic) -- same distances
+  // More than one entry: the graph is cut into edge-balanced vertex ranges,
+  // partition q runs on devices[q] and relaxes remote vertices directly in
+  // their owner's memory (gfb_mg_*, NVLink peer access; entries may repeat a
+  // device).  u32 / f32 arithmetic, push, no near-far.  `device` is unused.
+  std::vector<int> devices;
 
   void validate() const {
     if (device < 0) throw std::invalid_argument("device policy: device must be >= 0");
+    if (devices.size() > 8) throw std::invalid_argument("device policy: at most 8 devices");
+    for (int d : devices)
+      if (d < 0) throw std::invalid_argument("device policy: device must be >= 0");
+    if (devices.size() > 1 && arithmetic == GFB_W_F64)
+      throw std::invalid_argument("device policy: multi-GPU needs u32 or f32 arithmetic");
+    if (devices.size() > 1 && delta > 0)
+      throw std::invalid_argument("device policy: the near-far filter is single-GPU");
     if (arithmetic < GFB_W_U32 || arithmetic > GFB_W_F64)
       throw std::invalid_argument("device policy: bad arithmetic");
     if (!(delta >= 0.0)) throw std::invalid_argument("device policy: delta must be >= 0");
@@ -180,6 +192,38 @@ class DeviceGraph {
   gfb_ctx* ctx_ = nullptr;
 };
 
+/// The graph partitioned over several devices (gfb_mg_*), cached like
+/// DeviceGraph.
+class DeviceMgGraph {
+ public:
+  DeviceMgGraph(const Graph& g, const DevicePolicy& p) {
+    gfb_mg* h = nullptr;
+    device_detail::check(gfb_mg_create((int)p.devices.size(), p.devices.data(), &h));
+    h_.reset(h);
+    device_detail::check(gfb_mg_graph_upload(h, g.num_vertices(), g.num_edges(),
+                                             g.row_offsets().data(), g.column_indices().data(),
+                                             g.values().data(), GFB_W_F64, p.arithmetic));
+  }
+  gfb_mg* handle() const { return h_.get(); }
+
+  static DeviceMgGraph& of(const Graph& g, const DevicePolicy& p) {
+    using Key = std::tuple<const Graph*, const void*, std::size_t, std::size_t, std::uint64_t,
+                           std::vector<int>, int>;
+    thread_local std::map<Key, std::unique_ptr<DeviceMgGraph>> cache;
+    Key k{&g, g.row_offsets().data(), g.num_vertices(), g.num_edges(),
+          DeviceGraph::fingerprint(g), p.devices, p.arithmetic};
+    auto& slot = cache[k];
+    if (!slot) slot = std::make_unique<DeviceMgGraph>(g, p);
+    return *slot;
+  }
+
+ private:
+  struct Deleter {
+    void operator()(gfb_mg* h) const { gfb_mg_destroy(h); }
+  };
+  std::unique_ptr<gfb_mg, Deleter> h_;
+};
+
 /// Single-source shortest paths on the device (algorithms.hpp:569-623):
 /// same validation order and exception types, same SsspResult layout.
 /// dist is widened from the device arithmetic to double (exact); pred is
@@ -190,6 +234,19 @@ inline SsspResult sssp(const Graph& g, vertex_t source, const DeviceSsspConfig& 
   if (source >= n) throw std::out_of_range("sssp: source out of range");
   if (cfg.direction == Direction::pull && !g.has_transpose())
     throw std::invalid_argument("sssp: pull direction requires a built transpose");
+  if (cfg.policy.devices.size() > 1) {  // partitioned over several devices
+    if (cfg.direction == Direction::pull)
+      throw std::invalid_argument("sssp: the multi-GPU loop is push-only");
+    DeviceMgGraph& mg = DeviceMgGraph::of(g, cfg.policy);
+    SsspResult r;
+    r.dist.resize(n);
+    r.pred.resize(n);
+    gfb_sssp_stats st{};
+    device_detail::check(gfb_mg_sssp(mg.handle(), source, nullptr, r.dist.data(), r.pred.data(), &st));
+    r.supersteps = st.supersteps;
+    r.relaxations = st.relaxations;
+    return r;
+  }
   bool want_csc = g.has_transpose();
   DeviceGraph& dg = DeviceGraph::of(g, cfg.policy, want_csc);
   gfb_sssp_opts o;

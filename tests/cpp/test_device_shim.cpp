@@ -157,6 +157,29 @@ int main() {
     auto r = sssp(g, 0, cfg);
     CHECK(r.dist == reference_dijkstra(g, 0).first);
     CHECK(valid_pred_tree(g, 0, r.dist, r.pred));
+    // the partitioned loop (policy.devices, gfb_mg_*): 2 and 3 partitions
+    // on device 0, same fixpoint; f64 arithmetic is rejected
+    for (int parts : {2, 3}) {
+      DeviceSsspConfig mc = cfg;
+      mc.policy.devices.assign(parts, 0);
+      auto rm = sssp(g, 0, mc);
+      CHECK(rm.dist == r.dist);
+      CHECK(valid_pred_tree(g, 0, rm.dist, rm.pred));
+      auto rm7 = sssp(g, 7, mc);
+      CHECK(rm7.dist == reference_dijkstra(g, 7).first);
+    }
+    {
+      DeviceSsspConfig bad = cfg;
+      bad.policy.devices = {0, 0};
+      bad.policy.arithmetic = GFB_W_F64;
+      bool threw = false;
+      try {
+        sssp(g, 0, bad);
+      } catch (const std::invalid_argument&) {
+        threw = true;
+      }
+      CHECK(threw);
+    }
     // the near-far loop (policy.delta) reaches the same fixpoint
     for (double delta : {1.0, 16.0, 200.0}) {
       DeviceSsspConfig nf = cfg;
