@@ -472,7 +472,8 @@ __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, u
 #pragma unroll
         for (int r = 0; r < VT; ++r) {  // B: owner; local test (own dist or proposal cache)
           if (dst[r] == NIL) continue;
-          q[r] = peer_owner(*pt, dst[r]);
+          q[r] = dst[r] >> PEER_VBITS;  // owner-encoded id (k_peer_encode)
+          dst[r] &= PEER_VMASK;
           const uint32_t* tp = q[r] == pt->self ? pt->dist[q[r]] : pt->rc;
           cur[r] = test_gather<OPT>(reinterpret_cast<const D*>(tp) + dst[r]);
         }

@@ -329,6 +329,10 @@ struct PeerTab {
   uint32_t nparts, self, self_lo, pad;
 };
 
+// The partitioned CSR stores each destination's owner in the top 3 bits of
+// its id (n < 2^29, k_peer_encode): the advance decodes it with a shift.
+constexpr uint32_t PEER_VBITS = 29, PEER_VMASK = (1u << PEER_VBITS) - 1;
+
 __device__ __forceinline__ uint32_t peer_owner(const PeerTab& t, uint32_t v) {
   uint32_t q = 0;
 #pragma unroll

@@ -185,6 +185,22 @@ __global__ void k_peer_init(typename DT<W>::D* dist, unsigned long long* pkey, u
   }
 }
 
+// Owner of every destination into the top bits of its id (PEER_VBITS).
+struct Starts {
+  uint32_t s[PEER_MAX + 1];
+  uint32_t nparts;
+};
+template <class W>
+__global__ void k_peer_encode(EdgeRec<W>* adj, uint64_t m, Starts st) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = adj[e].v;
+    uint32_t q = 0;
+    for (uint32_t i = 1; i < st.nparts; ++i) q += v >= st.s[i] ? 1u : 0u;
+    adj[e].v = v | (q << PEER_VBITS);
+  }
+}
+
 __global__ void k_peer_fill(uint32_t* a, uint32_t v, uint32_t n) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     a[i] = v;
@@ -293,10 +309,10 @@ __global__ void k_peer_inedges(const uint32_t* __restrict__ ro, const EdgeRec<W>
     const uint32_t s0 = ro[u], s1 = ro[u + 1];
     for (uint32_t e = s0 + lane; e < s1; e += 32) {
       const EdgeRec<W> r = adj[e];
-      const uint32_t q = peer_owner(t, r.v);
-      if ((__ldcg(t.repair[q] + (r.v >> 5)) >> (r.v & 31)) & 1u) {
+      const uint32_t q = r.v >> PEER_VBITS, v = r.v & PEER_VMASK;  // owner-encoded
+      if ((__ldcg(t.repair[q] + (v >> 5)) >> (v & 31)) & 1u) {
         const uint32_t i = atomicAdd(&ctl->out_count, 1u);
-        if (i < cap) list[i] = make_uint4(u + t.self_lo, r.v, *reinterpret_cast<const uint32_t*>(&r.w), 0u);
+        if (i < cap) list[i] = make_uint4(u + t.self_lo, v, *reinterpret_cast<const uint32_t*>(&r.w), 0u);
         else atomicOr(&ctl->err, 4u);
       }
     }
@@ -388,7 +404,20 @@ Peer* peer_create(Ctx* c, int rank, int nparts, const uint32_t* range_starts, ui
   p->n = range_starts[rank + 1] - p->lo;
   p->nwords = (p->n + 31) / 32;
   cudaStream_t s = c->stream;
+  if (p->n_global >= (1ull << PEER_VBITS)) fail(GFB_EINVAL, "peer: n must be < 2^29");
   p->g.reset(graph_upload(c, p->n, m_local, ro, col, w, htype, wtype, 0, p->n_global));
+  {  // owner-encoded destination ids (the advance decodes them with a shift)
+    Starts st{};
+    for (int q = 0; q <= nparts; ++q) st.s[q] = range_starts[q];
+    st.nparts = (uint32_t)nparts;
+    if (m_local) {
+      if (wtype == GFB_W_F32)
+        k_peer_encode<float><<<stride_grid(c), 256, 0, s>>>(p->g->adj.as<EdgeRec<float>>(), m_local, st);
+      else
+        k_peer_encode<uint32_t><<<stride_grid(c), 256, 0, s>>>(p->g->adj.as<EdgeRec<uint32_t>>(), m_local, st);
+      GFB_CUDA(cudaGetLastError());
+    }
+  }
   p->lay = peer_layout(p->n);
   GFB_CUDA(cudaMalloc(&p->slab, p->lay.bytes));  // plain cudaMalloc: IPC-exportable
   GFB_CUDA(cudaMemsetAsync(p->at<char>(p->lay.mbox), 0, 2 * PEER_MAX * MBOX_WORDS * 4, s));
@@ -534,7 +563,13 @@ struct PeerRun {
     ++p->launches;
   }
 
-  void compact(cudaStream_t st, uint32_t defer_pct) {
+  static int exp_bits() {
+    const char* e = getenv("GFB_PEER_EXP");
+    return e ? atoi(e) : 0;
+  }
+
+  void compact(cudaStream_t st, uint32_t defer_pct, cudaGraphConditionalHandle hl = {},
+               bool set_loop = false) {
     Graph* g = p->g.get();
     const uint32_t tiles = p->ftiles;
     unsigned long long* bt = p->obuck.as<unsigned long long>();
@@ -544,8 +579,8 @@ struct PeerRun {
     k_fcount_o<D><<<tiles, F_WARPS * 32, 0, st>>>(g->ro.as<uint32_t>(), bm(), p->nwords, dist(),
                                                   ctl(), p->oagg.as<unsigned long long>(), bt,
                                                   tflag, p->dexp.as<uint32_t>());
-    k_fscan_o<<<1, 32, 0, st>>>(bt, bt + OB_N, plan(), ctl(), (uint32_t)g->m, 1.0f, 0, 0, none,
-                                none, 0, 0, defer_pct, (uint32_t)(g->m >> 2), 0u);
+    k_fscan_o<<<1, 32, 0, st>>>(bt, bt + OB_N, plan(), ctl(), (uint32_t)g->m, 1.0f, 0, 0, hl,
+                                none, set_loop ? 1 : 0, 0, defer_pct, (uint32_t)(g->m >> 2), 0u);
     k_fwrite_o<D><<<tiles, F_WARPS * 32, 0, st>>>(g->ro.as<uint32_t>(), bm(),
                                                   p->bm_cur.as<uint32_t>(), p->nwords, dist(),
                                                   ctl(), p->oagg.as<unsigned long long>(),
@@ -564,8 +599,12 @@ struct PeerRun {
     a.bm_out = bm();
     a.op = GFB_OP_RELAX_MIN;
     a.peers = p->tab_dev.as<PeerTab>();
-    if constexpr (sizeof(D) == 4)
-      k_push_range<W, 2, 8, 256, 1, true><<<c->num_sms * 8, 256, 0, st>>>(a);
+    if constexpr (sizeof(D) == 4) {
+      if (p->nparts == 1 && (exp_bits() & 1))  // experiment: plain advance (all owners local)
+        k_push_range<W, 2, 8, 256, 1, false><<<c->num_sms * 8, 256, 0, st>>>(a);
+      else
+        k_push_range<W, 2, 8, 256, 1, true><<<c->num_sms * 8, 256, 0, st>>>(a);
+    }
     ++p->launches;
   }
 
@@ -614,10 +653,15 @@ struct PeerRun {
     GFB_CUDA(cudaStreamEndCapture(s, &tmp));
     cudaStream_t b = c->aux[0];
     GFB_CUDA(cudaStreamBeginCaptureToGraph(b, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    push(b);
-    xbar(b, XB_FMIN);
-    compact(b, defer_pct);
-    xbar(b, XB_LOOP, hloop, true);
+    if (p->nparts == 1 && (exp_bits() & 2)) {  // experiment: no barriers (one rank)
+      push(b);
+      compact(b, defer_pct, hloop, true);
+    } else {
+      push(b);
+      xbar(b, XB_FMIN);
+      compact(b, defer_pct);
+      xbar(b, XB_LOOP, hloop, true);
+    }
     GFB_CUDA(cudaStreamEndCapture(b, &tmp));
     GFB_CUDA(cudaGraphInstantiate(&p->exec, G, 0));
     p->graph = G;
