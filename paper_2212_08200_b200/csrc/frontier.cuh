@@ -263,10 +263,10 @@ __device__ __forceinline__ uint32_t obucket(const D* dist, uint32_t v, uint32_t 
 // against its own proposal cache).  dexp[v] = distance bits v was last
 // expanded with; a set bit whose distance is unchanged is dropped here.
 // nullptr (single GPU: a bit is only set by a relaxation that lowered v).
-template <class D>
+template <bool DEXP, class D>
 __device__ __forceinline__ void drop_unchanged(WarpWords& w, const D* dist, const uint32_t* dexp,
                                                uint32_t wbase) {
-  if (!dexp) return;
+  if constexpr (!DEXP) return;
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int j = 0; j < F_WPW; ++j) {
@@ -280,7 +280,7 @@ __device__ __forceinline__ void drop_unchanged(WarpWords& w, const D* dist, cons
 // Count: per tile (the F_WORDS-word tiles of k_fcount) and bucket -> agg,
 // and the bucket totals accumulated in btot[OB_N] (64-bit: count << 32 | edges).
 // Native 32-bit shared atomics (a 64-bit shared atomicAdd is a CAS loop).
-template <class D>
+template <class D, bool DEXP = false>
 __global__ void __launch_bounds__(F_WARPS * 32)
 k_fcount_o(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uint32_t nwords,
            const D* __restrict__ dist, const Ctl* __restrict__ ctl,
@@ -295,7 +295,7 @@ k_fcount_o(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uin
   WarpWords w;
   uint32_t raw;
   load_warp_words(ro, bm, nwords, wbase, w, &raw);
-  drop_unchanged(w, dist, dexp, wbase);
+  drop_unchanged<DEXP>(w, dist, dexp, wbase);
 #pragma unroll
   for (int j = 0; j < F_WPW; ++j) {
     if ((w.keep[j] >> lane) & 1u) {
@@ -365,7 +365,7 @@ static __global__ void k_fscan_o(unsigned long long* btot, unsigned long long* b
 // (Measured alternatives: per-lane 64-bit shared cursors -- a CAS loop --
 // 1-5% slower; full staging of v/start/deg 1.2x; a warp-aggregated atomic per
 // distinct bucket of a word 2.1x.)
-template <class D>
+template <class D, bool DEXP = false>
 __global__ void __launch_bounds__(F_WARPS * 32)
 k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur, uint32_t nwords,
             const D* __restrict__ dist, const Ctl* __restrict__ ctl,
@@ -398,7 +398,7 @@ k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
   WarpWords w;
   uint32_t raw;
   load_warp_words(ro, bm_next, nwords, wbase, w, &raw);
-  drop_unchanged(w, dist, dexp, wbase);
+  drop_unchanged<DEXP>(w, dist, dexp, wbase);
   __syncthreads();
   uint32_t pend = 0;
 #pragma unroll
@@ -417,7 +417,7 @@ k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
       s_bk[p] = (uint8_t)b;
       plan.v[gi] = v;
       plan.start[gi] = w.st[j];
-      if (dexp) dexp[v] = dbits(dist[v]);
+      if constexpr (DEXP) dexp[v] = dbits(dist[v]);
     }
   }
   if (lane < F_WPW && wbase + lane < nwords) {

@@ -576,12 +576,12 @@ struct PeerRun {
     uint32_t* tflag =
         reinterpret_cast<uint32_t*>(p->oagg.as<unsigned long long>() + (size_t)tiles * OB_N);
     cudaGraphConditionalHandle none{};
-    k_fcount_o<D><<<tiles, F_WARPS * 32, 0, st>>>(g->ro.as<uint32_t>(), bm(), p->nwords, dist(),
+    k_fcount_o<D, true><<<tiles, F_WARPS * 32, 0, st>>>(g->ro.as<uint32_t>(), bm(), p->nwords, dist(),
                                                   ctl(), p->oagg.as<unsigned long long>(), bt,
                                                   tflag, p->dexp.as<uint32_t>());
     k_fscan_o<<<1, 32, 0, st>>>(bt, bt + OB_N, plan(), ctl(), (uint32_t)g->m, 1.0f, 0, 0, hl,
                                 none, set_loop ? 1 : 0, 0, defer_pct, (uint32_t)(g->m >> 2), 0u);
-    k_fwrite_o<D><<<tiles, F_WARPS * 32, 0, st>>>(g->ro.as<uint32_t>(), bm(),
+    k_fwrite_o<D, true><<<tiles, F_WARPS * 32, 0, st>>>(g->ro.as<uint32_t>(), bm(),
                                                   p->bm_cur.as<uint32_t>(), p->nwords, dist(),
                                                   ctl(), p->oagg.as<unsigned long long>(),
                                                   bt + OB_N, plan(), tflag,
