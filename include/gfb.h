@@ -211,6 +211,16 @@ int gfb_sssp_read(gfb_graph* g, double* dist, void* dist_native, uint32_t* pred)
 int gfb_debug_relabel(gfb_graph* g, uint32_t* row_offsets, uint32_t* adj_pairs,
                       uint32_t* perm);
 
+/* Breadth-first search as operator reuse (algorithms.hpp:194-233 bfs()):
+ * depth[n] as double (math.inf for unreachable, like BfsResult.depth),
+ * supersteps = levels expanded (max depth + 1), relaxations = claim
+ * evaluations (the out-degree sum of the reached vertices, the same for push
+ * and pull).  direction: gfb_direction; pull needs a transpose (build_csc)
+ * like the reference, and is executed as push (identical results).
+ * GFB_ERANGE: source >= n. */
+int gfb_bfs(gfb_ctx* ctx, gfb_graph* g, uint32_t source, int direction, double* depth,
+            uint64_t* supersteps, uint64_t* relaxations);
+
 /* ---- 1-D partitioned SSSP: one rank's share (multi-GPU) ----
  * No reference counterpart (the reference is single-host); mg.py drives one
  * gfb_part per rank and exchanges the messages with torch.distributed

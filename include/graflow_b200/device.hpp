@@ -269,6 +269,32 @@ inline SsspResult sssp(const Graph& g, vertex_t source, const DeviceSsspConfig& 
   return r;
 }
 
+/// Breadth-first search on the device (algorithms.hpp:194-233): same
+/// validation and exceptions, same BfsResult (depth as double, +inf when
+/// unreachable; supersteps; relaxations = claim evaluations).
+inline BfsResult bfs(const Graph& g, vertex_t source, const DeviceSsspConfig& cfg) {
+  cfg.validate();
+  if (cfg.frontier_repr == FrontierRepr::queue)
+    throw std::invalid_argument("bfs: queue configuration not supported "
+                                "(level semantics require supersteps)");
+  std::size_t n = g.num_vertices();
+  if (source >= n) throw std::out_of_range("bfs: source out of range");
+  if (cfg.direction == Direction::pull && !g.has_transpose())
+    throw std::invalid_argument("bfs: pull direction requires a built transpose");
+  DevicePolicy p = cfg.policy;
+  if (p.devices.size() > 1) p.device = p.devices[0];  // BFS runs on one device
+  DeviceGraph& dg = DeviceGraph::of(g, p, g.has_transpose());
+  BfsResult r;
+  r.depth.resize(n);
+  uint64_t st = 0, rl = 0;
+  device_detail::check(gfb_bfs(dg.ctx(), dg.handle(), source,
+                               cfg.direction == Direction::pull ? GFB_DIR_PULL : GFB_DIR_PUSH,
+                               r.depth.data(), &st, &rl));
+  r.supersteps = st;
+  r.relaxations = rl;
+  return r;
+}
+
 // ---------------------------------------------------------------- operators
 
 /// Device frontier (frontier.hpp:37-218, sparse and dense representations).

@@ -416,3 +416,47 @@ uint64_t orc_grid_csr(uint32_t side, uint64_t seed, uint32_t* ro,
   if (ro) ro[n] = (uint32_t)e;
   return e;
 }
+
+/* algorithms.hpp:194-233 bfs(): the frontier of level L is expanded once per
+ * superstep (:219-231); every out-edge of a frontier vertex evaluates the
+ * claim once (:206-208 relaxations), and an unclaimed destination takes
+ * level L + 1 (:210-215, first claimant wins; all claimants of one level
+ * write the same value).  The loop runs while the frontier is non-empty
+ * (:218), so supersteps = number of non-empty levels. */
+int orc_bfs(size_t n, const uint32_t* ro, const uint32_t* col, uint32_t source, double* depth,
+            uint64_t* supersteps, uint64_t* relaxations) {
+  if (source >= n) return -1;
+  uint32_t* cur = (uint32_t*)malloc((n ? n : 1) * sizeof(uint32_t));
+  uint32_t* nxt = (uint32_t*)malloc((n ? n : 1) * sizeof(uint32_t));
+  for (size_t i = 0; i < n; ++i) depth[i] = INFINITY;
+  depth[source] = 0.0;
+  size_t k = 0, level = 0;
+  uint64_t steps = 0, rel = 0;
+  cur[k++] = source;
+  while (k != 0) {
+    ++steps;
+    size_t kn = 0;
+    for (size_t i = 0; i < k; ++i) {
+      const uint32_t u = cur[i];
+      for (uint32_t e = ro[u]; e < ro[u + 1]; ++e) {
+        ++rel;
+        const uint32_t v = col[e];
+        if (isinf(depth[v])) {
+          depth[v] = (double)(level + 1);
+          nxt[kn++] = v;
+        }
+      }
+    }
+    uint32_t* t = cur;
+    cur = nxt;
+    nxt = t;
+    k = kn;
+    ++level;
+  }
+  free(cur);
+  free(nxt);
+  *supersteps = steps;
+  *relaxations = rel;
+  return 0;
+}
+

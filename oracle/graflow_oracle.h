@@ -106,6 +106,12 @@ int64_t orc_check_pred_tree(size_t n, const uint32_t* ro, const uint32_t* col,
  * produce identical edge lists.  This restates paper_2212_08200_b200/csrc/
  * rmat.cuh independently; tests assert the two agree.
  * wkind: 0 = u32 U{0..255}, 1 = f32 U[0,1) on a 2^-24 grid. */
+/* algorithms.hpp:194-233 bfs(): level-synchronous push with the claim
+ * condition; depth as double (+inf unreachable), supersteps = expanded
+ * levels, relaxations = claim evaluations.  Returns -1 if source >= n. */
+int orc_bfs(size_t n, const uint32_t* ro, const uint32_t* col, uint32_t source, double* depth,
+            uint64_t* supersteps, uint64_t* relaxations);
+
 void orc_rmat_edges(int scale, uint64_t m, uint64_t seed, int wkind,
                     uint64_t first, uint64_t count, uint32_t* src,
                     uint32_t* dst, uint32_t* wbits);

@@ -55,6 +55,8 @@ def orc():
                                           C.c_uint32, u32p]
         L.orc_rmat_edges.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_int, C.c_uint64,
                                      C.c_uint64, u32p, u32p, u32p]
+        L.orc_bfs.argtypes = [sz, u32p, u32p, C.c_uint32, f64p, C.POINTER(C.c_uint64),
+                              C.POINTER(C.c_uint64)]
         L.orc_grid_csr.restype = C.c_uint64
         L.orc_grid_csr.argtypes = [C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]
         _ORC = L
@@ -80,6 +82,8 @@ def ref():
         L.ref_sssp.argtypes = [C.c_void_p, C.c_uint32, C.c_int, sz, C.c_int, C.c_int, C.c_int,
                                f64p, u32p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.ref_dijkstra.argtypes = [C.c_void_p, C.c_uint32, f64p, u32p]
+        L.ref_bfs.argtypes = [C.c_void_p, C.c_uint32, C.c_int, sz, C.c_int, C.c_int, f64p,
+                              C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.ref_expand_record.restype = sz
         L.ref_expand_record.argtypes = [C.c_void_p, u32p, sz, C.c_int, u32p, u32p, u32p, sz]
         _REF = L
@@ -140,6 +144,15 @@ def dijkstra(n, ro, col, w, source, kind="f64"):
     if rc != 0:
         raise IndexError("reference_dijkstra: source out of range")
     return dist, pred
+
+
+def bfs(n, ro, col, source):
+    """algorithms.hpp:194-233 restated: (depth f64, supersteps, relaxations)."""
+    depth = np.empty(max(n, 1), np.float64)
+    st = C.c_uint64(); rl = C.c_uint64()
+    if orc().orc_bfs(n, ro, _nz(col, np.uint32), source, depth, C.byref(st), C.byref(rl)) != 0:
+        raise IndexError("bfs: source out of range")
+    return depth[:n], st.value, rl.value
 
 
 def sssp_bsp(n, ro, col, w, source, dedup=True):
@@ -236,6 +249,16 @@ class RefGraph:
             raise {1: ValueError, 2: IndexError}.get(rc, RuntimeError)(
                 self.L.ref_last_error().decode())
         return dist[: self.n], pred[: self.n], st.value, rl.value
+
+    def bfs(self, source, mode=0, workers=1, direction=0, repr_=0):
+        depth = np.empty(max(self.n, 1), np.float64)
+        st = C.c_uint64(); rl = C.c_uint64()
+        rc = self.L.ref_bfs(self.h, source, mode, workers, direction, repr_, depth,
+                            C.byref(st), C.byref(rl))
+        if rc:
+            raise {1: ValueError, 2: IndexError}.get(rc, RuntimeError)(
+                self.L.ref_last_error().decode())
+        return depth[: self.n], st.value, rl.value
 
     def dijkstra(self, source):
         dist = np.empty(max(self.n, 1), np.float64); pred = np.empty(max(self.n, 1), np.uint32)

@@ -120,6 +120,21 @@ int ref_sssp(void* gp, uint32_t source, int mode, size_t workers, int direction,
   });
 }
 
+// algorithms.hpp:194-233 (mode / direction / repr as ref_sssp)
+int ref_bfs(void* gp, uint32_t source, int mode, size_t workers, int direction, int repr,
+            double* depth, uint64_t* supersteps, uint64_t* relaxations) {
+  return guarded([&] {
+    SsspConfig cfg;
+    cfg.policy = {static_cast<ExecutionMode>(mode), workers};
+    cfg.direction = direction ? Direction::pull : Direction::push;
+    cfg.frontier_repr = static_cast<FrontierRepr>(repr);
+    auto r = bfs(*static_cast<Graph*>(gp), source, cfg);
+    std::memcpy(depth, r.depth.data(), r.depth.size() * 8);
+    *supersteps = r.supersteps;
+    *relaxations = r.relaxations;
+  });
+}
+
 // algorithms.hpp:536-563
 int ref_dijkstra(void* gp, uint32_t source, double* dist, uint32_t* pred) {
   return guarded([&] {

@@ -244,6 +244,32 @@ def sssp(g, source, policy="device", direction="auto", frontier="dense", workers
     return dist, pred, st.supersteps, st.relaxations
 
 
+def bfs(g, source, policy="device", direction="push", frontier="sparse", workers=None,
+        as_lists=False, want_result=True):
+    """algorithms.hpp:194-233 on the device; mirrors module.cpp:130-140:
+    returns ``(depths, supersteps, relaxations)`` with depths as float64
+    (math.inf when unreachable).  The queue frontier is rejected like the
+    reference (level semantics need supersteps)."""
+    if policy != "device":
+        raise ValueError("policy must be device (the CPU policies live in the reference)")
+    if frontier == "queue":
+        raise ValueError("bfs: queue configuration not supported "
+                         "(level semantics require supersteps)")
+    if frontier not in ("sparse", "dense"):
+        raise ValueError("frontier must be sparse|dense")
+    if direction not in _DIR:
+        raise ValueError("direction must be push|pull|auto")
+    if source < 0:
+        raise IndexError("bfs: source out of range")
+    depth = np.empty(g.num_vertices, np.float64) if want_result else None
+    st, rl = C.c_uint64(), C.c_uint64()
+    check(g._lib.gfb_bfs(g.ctx.h, g.h, source, _DIR[direction], _ptr(depth), C.byref(st),
+                         C.byref(rl)))
+    if as_lists:
+        return depth.tolist(), st.value, rl.value
+    return depth, st.value, rl.value
+
+
 def sssp_stats(g, source, direction="auto", want_result=True, **kw):
     """gfb_sssp with the full statistics record (device time, n/m_reach...)."""
     if source < 0:

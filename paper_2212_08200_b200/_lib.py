@@ -74,6 +74,7 @@ SIGNATURES = {
     "gfb_sssp_opts_default": ([C.POINTER(SsspOpts)], None),
     "gfb_sssp": ([_vp, _vp, _u32, C.POINTER(SsspOpts), _vp, _vp, C.POINTER(SsspStats)], _int),
     "gfb_sssp_read": ([_vp, _vp, _vp, _vp], _int),
+    "gfb_bfs": ([_vp, _vp, _u32, _int, _vp, _pu64, _pu64], _int),
     "gfb_part_create": ([_vp, _u64, _u32, _u32, _u64, _vp, _vp, _vp, _int, _int,
                          C.POINTER(_vp)], _int),
     "gfb_part_free": ([_vp], _int),

@@ -599,3 +599,14 @@ int gfb_mg_destroy(gfb_mg* mg) {
   });
 }
 
+// ---- bfs (include/gfb.h) ----
+int gfb_bfs(gfb_ctx* ctx, gfb_graph* g, uint32_t source, int direction, double* depth,
+            uint64_t* supersteps, uint64_t* relaxations) {
+  return guard([&] {
+    NEED(ctx);
+    NEED(g);
+    set_device(ctx);
+    gfb::bfs_run(ctx, g, source, direction, depth, supersteps, relaxations);
+  });
+}
+

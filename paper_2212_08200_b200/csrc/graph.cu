@@ -76,6 +76,8 @@ Graph::~Graph() = default;
 Workspace::~Workspace() {
   if (loop_exec) cudaGraphExecDestroy(loop_exec);
   if (loop_graph) cudaGraphDestroy(loop_graph);
+  if (bfs_exec) cudaGraphExecDestroy(bfs_exec);
+  if (bfs_graph) cudaGraphDestroy(bfs_graph);
   if (ctl_host) cudaFreeHost(ctl_host);
 }
 

@@ -123,6 +123,8 @@ struct Workspace {
   cudaGraphExec_t loop_exec = nullptr;
   cudaGraph_t loop_graph = nullptr;
   int loop_key[4] = {-1, -1, -1, -1};
+  cudaGraphExec_t bfs_exec = nullptr;  // bfs.cu device loop
+  cudaGraph_t bfs_graph = nullptr;
   Ctl* ctl_host = nullptr;  // pinned
   uint32_t compact_tiles = 0;
   uint32_t status_len = 0;
@@ -180,6 +182,9 @@ void ensure_ceid(Graph* g);
 void build_pull_plan(Graph* g);
 void ensure_nz(Graph* g);
 void ensure_relabel(Graph* g);
+// bfs.cu
+void bfs_run(Ctx* c, Graph* g, uint32_t source, int direction, double* depth,
+             uint64_t* supersteps, uint64_t* relaxations);
 // sssp.cu
 void sssp_run(Ctx* ctx, Graph* g, uint32_t source, const gfb_sssp_opts* o, gfb_sssp_stats* st);
 void sssp_read(Graph* g, double* dist, void* dist_native, uint32_t* pred);

@@ -189,6 +189,39 @@ int main() {
       CHECK(valid_pred_tree(g, 0, rn.dist, rn.pred));
     }
   }
+  // --- BFS: test_algorithms.cpp:185-211 and acceptance.cpp:180-199 (C5)
+  {
+    DeviceSsspConfig cfg;
+    CHECK((bfs(triangle(), 0, cfg).depth == DistanceMap{0, 1, 1}));
+    Graph path = build_csr({{0, 1, 5.0}, {1, 2, 0.5}, {2, 3, 2.0}}, 4);
+    CHECK((bfs(path, 0, cfg).depth == DistanceMap{0, 1, 2, 3}));
+    DeviceSsspConfig q = cfg;
+    q.frontier_repr = FrontierRepr::queue;
+    bool threw = false;
+    try {
+      bfs(triangle(), 0, q);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+    int bad = 0;
+    for (int instance = 0; instance < 50; ++instance) {
+      std::size_t n = 5 + instance * 7;
+      auto edges = testutil::random_edges(n, 6000 + instance);
+      Graph g = build_transpose(build_csr(edges, n));
+      auto want = graflow::bfs(g, 0, SsspConfig{ExecutionPolicy::sequential()});
+      for (Direction dir : {Direction::push, Direction::pull}) {
+        DeviceSsspConfig c2;
+        c2.direction = dir;
+        auto got = bfs(g, 0, c2);
+        if (got.depth != want.depth || got.supersteps != want.supersteps ||
+            got.relaxations != want.relaxations)
+          ++bad;
+      }
+    }
+    std::printf("C5 bfs vs reference bfs(): %d mismatching runs\n", bad);
+    CHECK(bad == 0);
+  }
   // --- acceptance.cpp:157-177 (C3): 20 repeated runs, identical distances
   {
     Graph g = testutil::random_graph(1000, 424242);

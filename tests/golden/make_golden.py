@@ -13,6 +13,11 @@ fixtures are small and committed; the GPU box never reads /root/reference.
   rmat16.npz   config 1: RMAT s16 EF16 u32 U{0..255}, source 0; reference
                sssp() (par, push, sparse: the CLI default) and
                reference_dijkstra() distances (full) + stats.
+  bfs.npz      acceptance.cpp:180-199 (C5): 50 graphs random_edges(5 + 7i,
+               6000 + i), transpose built; the reference bfs() depth,
+               supersteps, relaxations for seq/push/sparse and seq/pull/dense
+               (sources 0 and n/2), plus the hand-checked graphs of
+               test_algorithms.cpp:185-192.
   ops.npz      operator contracts on random_graph(40, seed) seeds 1..5:
                push and pull recorded (src, dst, edge) triples of the
                reference's own neighbors_expand / neighbors_expand_pull.
@@ -76,6 +81,28 @@ def main():
                         supersteps=st, csr_digest=np.frombuffer(
                             bytes.fromhex(digest(ro, col, val)), np.uint8),
                         edge_digest=np.frombuffer(bytes.fromhex(digest(s, d, wb)), np.uint8))
+
+    # ---- bfs (acceptance C5) ----
+    bfs = {}
+    rows = []
+    for i in range(50):
+        n = 5 + 7 * i
+        s, d, w = O.ref_random_edges(n, 6000 + i)
+        g = O.RefGraph(n, s, d, w, transpose=True)
+        for src in (0, n // 2):
+            dp, st_p, rl_p = g.bfs(src, mode=0, workers=1, direction=0, repr_=0)
+            dq, st_q, rl_q = g.bfs(src, mode=0, workers=1, direction=1, repr_=1)
+            assert np.array_equal(dp, dq)
+            rows.append((n, 6000 + i, src, st_p, rl_p, st_q, rl_q))
+            bfs[f"depth_{i}_{src}"] = dp
+    bfs["meta"] = np.array(rows, dtype=np.uint64)
+    tri = O.RefGraph(3, np.array([0, 0, 1], np.uint32), np.array([1, 2, 2], np.uint32),
+                     np.array([1.0, 4.0, 2.0]))
+    bfs["triangle"] = tri.bfs(0)[0]
+    path = O.RefGraph(4, np.array([0, 1, 2], np.uint32), np.array([1, 2, 3], np.uint32),
+                      np.array([5.0, 0.5, 2.0]))
+    bfs["path"] = path.bfs(0, mode=1, workers=2)[0]
+    np.savez_compressed(os.path.join(HERE, "bfs.npz"), **bfs)
 
     # ---- operator contracts ----
     ops = {}

@@ -196,3 +196,23 @@ def test_live_reference_f32_vs_f64_ulps():
     a = d32[fin].view(np.int32).astype(np.int64)
     b = ref[fin].astype(np.float32).view(np.int32).astype(np.int64)
     assert np.abs(a - b).max() <= 4
+
+
+def test_bfs_restatement_matches_reference_goldens():
+    """orc_bfs (algorithms.hpp:194-233 restated) against the reference's own
+    bfs() on acceptance C5's 50 graphs (tests/golden/bfs.npz): depth,
+    supersteps and relaxations, push and pull alike."""
+    gold = np.load(os.path.join(GOLD, "bfs.npz"))
+    for n, seed, src, st_p, rl_p, st_q, rl_q in gold["meta"].astype(np.int64):
+        s, d, w = O.random_edges(int(n), int(seed))
+        ro, col, _ = O.build_csr(int(n), s, d, w)
+        depth, st, rl = O.bfs(int(n), ro, col, int(src))
+        assert np.array_equal(depth, gold[f"depth_{(seed - 6000)}_{src}"])
+        assert (st, rl) == (st_p, rl_p) == (st_q, rl_q)
+        # C5: depths equal unit-weight Dijkstra
+        unit, _ = O.dijkstra(int(n), ro, col, np.ones(len(col)), int(src), "f64")
+        assert np.array_equal(depth, unit)
+    assert gold["triangle"].tolist() == [0.0, 1.0, 1.0]  # test_algorithms.cpp:186-187
+    assert gold["path"].tolist() == [0.0, 1.0, 2.0, 3.0]  # :189-191
+    with pytest.raises(IndexError):
+        O.bfs(3, np.array([0, 0, 0, 0], np.uint32), np.zeros(0, np.uint32), 3)
