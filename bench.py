@@ -251,7 +251,7 @@ def run_ours(args):
     # properties): no edge can still relax, reach counts match
     check = fixpoint_check(gb, g, st)
 
-    secondary = [] if args.no_secondary else secondary_configs(gb, ctx, args)
+    secondary = [] if args.no_secondary else secondary_configs(gb, ctx, args, g)
 
     cpu = None
     if not args.no_cpu:
@@ -320,11 +320,26 @@ def fixpoint_check(gb, g, st):
             "property": "dist[v] <= dist[u] + w for every edge; n_reach/m_reach recount"}
 
 
-def secondary_configs(gb, ctx, args):
+def secondary_configs(gb, ctx, args, g_main=None):
     """The other BASELINE.json configs as extra measurements (not the headline):
     configs[1] RMAT s22 push-only, configs[3] 4096^2 grid (near-far filter vs
-    plain BSP, device-side convergence)."""
+    plain BSP, device-side convergence), and the device BFS (algorithms.hpp
+    bfs()) on the headline graph."""
     out = []
+    if g_main is not None:
+        for _ in range(2):
+            gb.bfs(g_main, 0, want_result=False)
+        ts = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            _, bst, brl = gb.bfs(g_main, 0, want_result=False)
+            ts.append((time.perf_counter() - t0) * 1e3)
+        bms = statistics.median(ts)
+        out.append({"config": f"bfs() on the headline RMAT s{args.scale} graph, source 0 "
+                              f"(push, level-synchronous)",
+                    "gteps": brl / (bms * 1e-3) / 1e9, "ms": bms, "supersteps": bst,
+                    "relaxations": brl,
+                    "timing": "host wall clock around the synchronous gfb_bfs call"})
 
     def timed(g, runs, **kw):
         ms = []
