@@ -125,6 +125,7 @@ struct Workspace {
   int loop_key[4] = {-1, -1, -1, -1};
   cudaGraphExec_t bfs_exec = nullptr;  // bfs.cu device loop
   cudaGraph_t bfs_graph = nullptr;
+  int bfs_key = -1;
   Ctl* ctl_host = nullptr;  // pinned
   uint32_t compact_tiles = 0;
   uint32_t status_len = 0;
