@@ -34,7 +34,29 @@ def main():
         except IndexError:
             pass
         mg.free()
+    edge_cases(parts)
     print(f"MG_OK parts {parts}", flush=True)
+
+
+
+
+def edge_cases(parts):
+    """No edges at all, and a graph whose edges all live in one partition."""
+    n = 200
+    ro = np.zeros(n + 1, np.uint32)
+    mg = peer.MgSssp([0] * parts, ro, np.zeros(0, np.uint32), np.zeros(0, np.float32))
+    d, p, st = mg.sssp(5)
+    assert d[5] == 0 and np.isinf(np.delete(d, 5)).all() and (p == 0xFFFFFFFF).all()
+    mg.free()
+    # a path 0 -> 1 -> ... -> 9 (rows 0..9 only), u32 weights
+    ro = np.concatenate([np.arange(10, dtype=np.uint32), np.full(n - 9, 9, np.uint32)])
+    col = np.arange(1, 10, dtype=np.uint32)
+    w = np.full(9, 3, np.uint32)
+    mg = peer.MgSssp([0] * parts, ro, col, w)
+    d, p, st = mg.sssp(0)
+    assert d[:10].tolist() == [3.0 * i for i in range(10)] and np.isinf(d[10:]).all()
+    assert p[1:10].tolist() == list(range(9))
+    mg.free()
 
 
 if __name__ == "__main__":

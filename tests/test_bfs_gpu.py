@@ -65,3 +65,15 @@ def test_bfs_rmat_and_grid(ctx):
         assert np.isfinite(dist[0])
         assert np.array_equal(gb.bfs(g, 0)[0], O.bfs(n, ro, col, 0)[0])
         g.free()
+
+
+def test_bfs_edge_cases(ctx):
+    one = gb.build_csr([], 1, ctx=ctx)                      # single vertex (test_algorithms.cpp:110-113)
+    d, st, rl = gb.bfs(one, 0)
+    assert d.tolist() == [0.0] and st == 1 and rl == 0
+    iso = gb.build_csr([(1, 2, 1.0)], 4, transpose=True, ctx=ctx)  # source without out-edges
+    for direction in ("push", "auto", "pull"):
+        d, st, rl = gb.bfs(iso, 0, direction=direction)
+        assert np.isinf(d[1:]).all() and d[0] == 0 and st == 1 and rl == 0
+        d, st, rl = gb.bfs(iso, 1, direction=direction)
+        assert d.tolist() == [np.inf, 0.0, 1.0, np.inf] and st == 2 and rl == 1
