@@ -266,14 +266,15 @@ __device__ __forceinline__ uint32_t obucket(const D* dist, uint32_t v, uint32_t 
 template <bool DEXP, class D>
 __device__ __forceinline__ void drop_unchanged(WarpWords& w, const D* dist, const uint32_t* dexp,
                                                uint32_t wbase) {
-  if constexpr (!DEXP) return;
-  const int lane = threadIdx.x & 31;
+  if constexpr (DEXP) {
+    const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int j = 0; j < F_WPW; ++j) {
-    const uint32_t v = (wbase + j) * 32 + lane;
-    bool k = (w.keep[j] >> lane) & 1u;
-    if (k) k = dbits(dist[v]) != dexp[v];
-    w.keep[j] = __ballot_sync(0xffffffffu, k);
+    for (int j = 0; j < F_WPW; ++j) {
+      const uint32_t v = (wbase + j) * 32 + lane;
+      bool k = (w.keep[j] >> lane) & 1u;
+      if (k) k = dbits(dist[v]) != dexp[v];
+      w.keep[j] = __ballot_sync(0xffffffffu, k);
+    }
   }
 }
 

@@ -401,7 +401,13 @@ __device__ __forceinline__ void relax_reds(D* dist, unsigned long long* pkey, ui
 // (shared-memory copy `pt`): the test gather and the reductions go to the
 // owner's slab (NVLink peer memory for remote owners), the packed key names
 // the source by its global id.
-template <class W, int VT, bool COH = false, int OPT = 0, bool PEER = false>
+// REC (f64 distances: no room for a packed key): the distance goes down with
+// a returning 64-bit integer min on its bits (non-negative doubles order like
+// their bit patterns); the relaxation that saw the old value above its own
+// stores {u, csr edge} into predrec and sets the frontier bit.  A later,
+// smaller relaxation may land its record first: k_pred_verify checks every
+// record's tightness and the repair rounds fix the rest.
+template <class W, int VT, bool COH = false, int OPT = 0, bool PEER = false, bool REC = false>
 __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, uint32_t e1,
                                              uint32_t k, uint32_t total, unsigned* err,
                                              uint32_t* fmin = nullptr,
@@ -446,6 +452,7 @@ __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, u
     const uint32_t c1 = min(nxt, e1);
     for (uint32_t x = c0; x < c1; x += 32 * VT) {
       uint32_t dst[VT], uu[VT];
+      uint32_t eid[REC ? VT : 1];
       D nd[VT], cur[VT];
 #pragma unroll
       for (int r = 0; r < VT; ++r) {  // A: segment search + record stream
@@ -465,9 +472,27 @@ __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, u
           EdgeRec<W> rec = ld_rec(a.adj + (ss + (le - so)));
           dst[r] = rec.v;
           nd[r] = dadd(sd, rec.w, err);
+          if constexpr (REC) eid[r] = ss + (le - so);
         }
       }
-      if constexpr (PEER) {
+      if constexpr (REC) {
+#pragma unroll
+        for (int r = 0; r < VT; ++r)  // B: distance gathers (test before atomic)
+          if (dst[r] != NIL) cur[r] = test_gather<OPT>(a.dist + dst[r]);
+#pragma unroll
+        for (int r = 0; r < VT; ++r) {  // C: returning mins, all in flight
+          if (dst[r] != NIL && nd[r] < cur[r]) cur[r] = atomic_min_d(a.dist + dst[r], nd[r]);
+          else dst[r] = NIL;
+        }
+#pragma unroll
+        for (int r = 0; r < VT; ++r) {  // D: winners record themselves
+          if (dst[r] != NIL && nd[r] < cur[r]) {
+            a.predrec[dst[r]] = make_uint2(uu[r], eid[r]);
+            red_or_u32(a.bm_out + (dst[r] >> 5), 1u << (dst[r] & 31));
+            if (fmin) *fmin = min(*fmin, fkey(nd[r]));
+          }
+        }
+      } else if constexpr (PEER) {
         uint32_t q[VT];
 #pragma unroll
         for (int r = 0; r < VT; ++r) {  // B: owner; local test (own dist or proposal cache)
@@ -515,10 +540,10 @@ __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, u
 // with the smallest distances: relaxing them first lets their improvements
 // reach later edges of the SAME superstep (measured: contiguous shares do
 // 4.4 relaxations per reached edge at s24, the sweep 3.5).
-template <class W, int VT, int MINB, int TILE, int OPT = 0, bool PEER = false>
+template <class W, int VT, int MINB, int TILE, int OPT = 0, bool PEER = false, bool REC = false>
 __global__ void __launch_bounds__(256, MINB) k_push_range(AdvArgs<W> a) {
   using D = typename DT<W>::D;
-  static_assert(sizeof(D) == 4, "packed predecessor keys need 32-bit distances");
+  static_assert(REC || sizeof(D) == 4, "packed predecessor keys need 32-bit distances");
   static_assert(TILE % 32 == 0, "tiles are whole warp rows");
   __shared__ PeerTab s_pt[1];  // (eliminated when !PEER)
   if constexpr (PEER) {  // the peer table in shared memory (indexed per edge)
@@ -542,10 +567,10 @@ __global__ void __launch_bounds__(256, MINB) k_push_range(AdvArgs<W> a) {
     const uint32_t per = (uint32_t)((((uint64_t)total + nwarps - 1) / nwarps + 31) & ~31ull);
     const uint32_t e0 = (uint32_t)min((uint64_t)gwarp * per, (uint64_t)total);
     const uint32_t e1 = min(e0 + per, total);
-    if (e0 < e1) range_expand<W, VT, false, OPT, PEER>(a, e0, e1, k, total, err, &fmin, s_pt);
+    if (e0 < e1) range_expand<W, VT, false, OPT, PEER, REC>(a, e0, e1, k, total, err, &fmin, s_pt);
   } else {
     for (uint64_t e0 = (uint64_t)gwarp * TILE; e0 < total; e0 += (uint64_t)nwarps * TILE)
-      range_expand<W, VT, false, OPT, PEER>(a, (uint32_t)e0,
+      range_expand<W, VT, false, OPT, PEER, REC>(a, (uint32_t)e0,
                                              (uint32_t)min(e0 + TILE, (uint64_t)total), k, total,
                                              err, &fmin, s_pt);
   }

@@ -1049,6 +1049,50 @@ __global__ void k_pred_inedges_big(const uint32_t* __restrict__ ro,
   }
 }
 
+// Few unresolved vertices (the usual case): one flat, coalesced pass over the
+// edge records; a 64 Kbit shared-memory filter of the unresolved list
+// (ctl->unresolved entries of `list`) screens destinations, and only filter
+// hits read the repair bitmap and binary-search the source row.  The
+// row-structured k_pred_inedges reads the same records but checks the global
+// bitmap per edge (f64 s24: 5.0 ms for 357 unresolved vertices).
+constexpr uint32_t PR_FILTER_BITS = 1u << 16;
+constexpr uint32_t PR_FLAT_MAX = 8192;  // unresolved vertices the filter screens well
+__device__ __forceinline__ uint32_t pr_hash(uint32_t v) { return (v * 2654435761u) >> 16; }
+
+template <class W>
+__global__ void __launch_bounds__(256)
+k_pred_inedges_flat(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ adj,
+                    uint32_t n, uint64_t m, const uint32_t* __restrict__ repair_bm,
+                    const uint32_t* __restrict__ list, uint4* out, uint32_t cap, Ctl* ctl) {
+  __shared__ uint32_t s_f[PR_FILTER_BITS / 32];
+  for (uint32_t i = threadIdx.x; i < PR_FILTER_BITS / 32; i += blockDim.x) s_f[i] = 0;
+  __syncthreads();
+  const uint32_t cnt = ctl->unresolved;
+  for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const uint32_t h = pr_hash(list[i]);
+    atomicOr(&s_f[h >> 5], 1u << (h & 31));
+  }
+  __syncthreads();
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const EdgeRec<W> r = ld_rec(adj + e);
+    const uint32_t h = pr_hash(r.v);
+    if (!((s_f[h >> 5] >> (h & 31)) & 1u)) continue;
+    if (!((repair_bm[r.v >> 5] >> (r.v & 31)) & 1u)) continue;
+    uint32_t lo = 0, hi = n;  // source row: the last u with ro[u] <= e
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if ((uint64_t)ro[mid] <= e) lo = mid;
+      else hi = mid;
+    }
+    const uint32_t i = atomicAdd(&ctl->out_count, 1u);
+    if (i < cap)
+      out[i] = make_uint4(lo, r.v, *reinterpret_cast<const uint32_t*>(&r.w),
+                          sizeof(W) == 8 ? reinterpret_cast<const uint32_t*>(&r.w)[1] : 0u);
+    else atomicOr(&ctl->err, 4u);
+  }
+}
+
 // One repair round over the collected in-edges (same acceptance rule as
 // k_pred_csc_block; smallest source wins through atomicMin on cand[v]).
 template <class W>

@@ -109,7 +109,10 @@ struct Runner {
   // distance-ordered plan (frontier.cuh k_fcount_o / k_fwrite_o); variants
   // 60/61 keep the ascending-id plan for comparison, 62 = ordered plan on the
   // caller's ids
-  bool ordered() const { return key_mode() && variant != 60 && variant != 61; }
+  bool ordered() const { return (key_mode() || rec_fast()) && variant != 60 && variant != 61; }
+  // f64 distances on the same ordered / deferred loop, with {u, edge} records
+  // instead of packed keys (k_push_range<REC>); variant 10 keeps the old path
+  bool rec_fast() const { return sizeof(D) == 8 && variant != 10; }
 
   // Soft near-far inside BSP (k_fscan_o): in a superstep whose frontier has
   // >= m/4 edges, only the closest distance buckets up to 10% of those edges
@@ -179,7 +182,7 @@ struct Runner {
   // frontier compaction: count -> scan (+ loop/direction decision) -> write
   void compact(int dir, float alpha, cudaGraphConditionalHandle hloop,
                cudaGraphConditionalHandle hmode, bool set_loop, bool set_mode) {
-    if constexpr (sizeof(D) == 4) {
+    {
       if (ordered()) {
         const uint32_t tiles = ws->ftiles;
         unsigned long long* bt = ws->obuck.as<unsigned long long>();
@@ -248,14 +251,21 @@ struct Runner {
   void range_launch(cudaStream_t st) {
     if constexpr (sizeof(D) == 4) {
       k_push_range<W, VT, MINB, TILE, OPT><<<c->num_sms * MINB, 256, 0, st>>>(args(false));
+    } else {
+      k_push_range<W, VT, MINB, TILE, OPT, false, true><<<c->num_sms * MINB, 256, 0, st>>>(
+          args(false));
     }
   }
 
   // total == UINT32_MAX: unknown on the host (device loop) -> full grid
   void push(cudaStream_t st, uint32_t total) {
     const bool full = total == 0xFFFFFFFFu;
-    if (variant == 10 || !key_mode()) {  // {u, edge} records (f64; legacy experiment)
+    if (variant == 10 || (!key_mode() && !rec_fast())) {  // legacy warp-tile kernel
       warp_launch<(sizeof(W) == 8 ? 4 : 8), 4>(st, total, full);
+      return;
+    }
+    if (rec_fast()) {  // f64: the range kernel with {u, edge} records
+      range_launch<2, 4, 256, 1>(st);
       return;
     }
     // measured at RMAT s24 (profiles/r01_variants_s24.txt): 2 edges per lane,
@@ -731,13 +741,20 @@ struct Runner {
       list.alloc((size_t)cap * 16, s);
       GFB_CUDA(cudaMemsetAsync(&dctl->out_count, 0, 8, s));  // out_count, rec_count
       GFB_CUDA(cudaMemsetAsync(&dctl->err, 0, 4, s));
-      k_pred_inedges<W><<<stride_grid(c), 256, 0, s>>>(
-          g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(), ws->repair_bm.as<uint32_t>(), n,
-          list.as<uint4>(), cap, big.as<uint32_t>(), dctl);
-      k_pred_inedges_big<W><<<stride_grid(c), 256, 0, s>>>(
-          g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(), ws->repair_bm.as<uint32_t>(),
-          list.as<uint4>(), cap, big.as<uint32_t>(), dctl);
-      kernels += 2;
+      if (h.unresolved <= PR_FLAT_MAX && variant != 64) {  // few: flat filtered pass
+        k_pred_inedges_flat<W><<<c->num_sms * 8, 256, 0, s>>>(
+            g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(), n, g->m,
+            ws->repair_bm.as<uint32_t>(), ws->cand.as<uint32_t>(), list.as<uint4>(), cap, dctl);
+        kernels += 1;
+      } else {
+        k_pred_inedges<W><<<stride_grid(c), 256, 0, s>>>(
+            g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(), ws->repair_bm.as<uint32_t>(), n,
+            list.as<uint4>(), cap, big.as<uint32_t>(), dctl);
+        k_pred_inedges_big<W><<<stride_grid(c), 256, 0, s>>>(
+            g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(), ws->repair_bm.as<uint32_t>(),
+            list.as<uint4>(), cap, big.as<uint32_t>(), dctl);
+        kernels += 2;
+      }
       const Ctl r = c->read_ctl(dctl);
       if (!(r.err & 4u)) break;
       if (attempt > 0) fail(GFB_ELOGIC, "sssp: predecessor repair list overflow");
