@@ -123,6 +123,7 @@ struct Runner {
     if (variant == 0) return 10;
     switch (variant) {
       case 63: return 10;  // deferral on the caller's ids (no relabel): the peer path's loop
+      case 65: case 66: case 67: case 68: case 69: return 10;  // f64 advance shapes
       case 99: return 100;
       case 100: return 50;
       case 101: return 70;
@@ -265,7 +266,13 @@ struct Runner {
       return;
     }
     if (rec_fast()) {  // f64: the range kernel with {u, edge} records
-      range_launch<2, 4, 256, 1>(st);
+      // s24 without predecessors (tools/f64_breakdown.py): <2,4> 6.37 ms,
+      // <1,8> 5.94, <2,6> 5.82, <4,4> 6.29, <2,3> 7.21 (variants 65-68)
+      if (variant == 65) range_launch<1, 8, 256, 1>(st);
+      else if (variant == 67) range_launch<4, 4, 256, 1>(st);
+      else if (variant == 68) range_launch<2, 3, 256, 1>(st);
+      else if (variant == 69) range_launch<2, 4, 256, 1>(st);
+      else range_launch<2, 6, 256, 1>(st);
       return;
     }
     // measured at RMAT s24 (profiles/r01_variants_s24.txt): 2 edges per lane,
