@@ -456,6 +456,7 @@ int gfb_sssp_read(gfb_graph* g, double* dist, void* dist_native, uint32_t* pred)
 int gfb_debug_relabel(gfb_graph* g, uint32_t* ro, uint32_t* adj_pairs, uint32_t* perm) {
   return guard([&] {
     NEED(g);
+    if (g->rec_bytes() != 8) gfb::fail(GFB_EINVAL, "relabel view: 4-byte weights only");
     set_device(g->ctx);
     gfb::ensure_relabel(g);
     if (g->rl_skip) gfb::fail(GFB_ELOGIC, "relabel: in-degrees not skewed, no relabelled view");

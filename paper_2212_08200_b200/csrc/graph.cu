@@ -388,7 +388,6 @@ static __global__ void k_rl_big(const uint32_t* __restrict__ ro, const EdgeRec<W
 
 void ensure_relabel(Graph* g) {
   if (g->rl_valid) return;
-  if (g->rec_bytes() != 8) fail(GFB_EINVAL, "relabel: 4-byte weights only");
   Ctx* c = g->ctx;
   cudaStream_t s = c->stream;
   const uint32_t n = (uint32_t)g->n;
@@ -402,7 +401,7 @@ void ensure_relabel(Graph* g) {
     g->rl_perm.alloc((size_t)n * 4, s);
     g->rl_iperm.alloc((size_t)n * 4, s);
     g->rl_ro.alloc((size_t)(n + 1) * 4, s);
-    g->rl_adj.alloc(m * 8, s);
+    g->rl_adj.alloc(m * g->rec_bytes(), s);
   }
   if (g->has_csc) {  // in-degrees from the transpose's offsets
     k_indeg_csc<<<stride_grid(c), 256, 0, s>>>(g->co.as<uint32_t>(), n, cnt.as<uint32_t>());
@@ -411,6 +410,9 @@ void ensure_relabel(Graph* g) {
     if (g->wtype == GFB_W_F32)
       k_indeg<float><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<float>>(), m,
                                                     cnt.as<uint32_t>());
+    else if (g->wtype == GFB_W_F64)
+      k_indeg<double><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<double>>(), m,
+                                                     cnt.as<uint32_t>());
     else
       k_indeg<uint32_t><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<uint32_t>>(), m,
                                                        cnt.as<uint32_t>());
@@ -461,6 +463,15 @@ void ensure_relabel(Graph* g) {
     k_rl_big<float><<<stride_grid(c), 256, 0, s>>>(
         g->ro.as<uint32_t>(), g->adj.as<EdgeRec<float>>(), g->rl_ro.as<uint32_t>(),
         g->rl_iperm.as<uint32_t>(), g->rl_perm.as<uint32_t>(), g->rl_adj.as<EdgeRec<float>>(),
+        big.as<uint32_t>(), nbig);
+  } else if (g->wtype == GFB_W_F64) {
+    k_rl_rows<double><<<stride_grid(c), 256, 0, s>>>(
+        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<double>>(), g->rl_ro.as<uint32_t>(),
+        g->rl_iperm.as<uint32_t>(), g->rl_perm.as<uint32_t>(), g->rl_adj.as<EdgeRec<double>>(), n,
+        big.as<uint32_t>(), nbig);
+    k_rl_big<double><<<stride_grid(c), 256, 0, s>>>(
+        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<double>>(), g->rl_ro.as<uint32_t>(),
+        g->rl_iperm.as<uint32_t>(), g->rl_perm.as<uint32_t>(), g->rl_adj.as<EdgeRec<double>>(),
         big.as<uint32_t>(), nbig);
   } else {
     k_rl_rows<uint32_t><<<stride_grid(c), 256, 0, s>>>(

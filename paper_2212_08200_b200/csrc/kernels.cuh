@@ -770,6 +770,7 @@ struct PermView {
   const unsigned long long* key_int;
   D* dist_out;
   unsigned long long* key_out;
+  const void* adj_int;  // relabelled CSR records (record mode: {u', edge'} keys)
 };
 
 template <class W, bool KEY = false, bool PERM = false>
@@ -781,7 +782,6 @@ k_pred_verify(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ ad
               uint32_t n, uint32_t source, Ctl* ctl,
               PermView<typename DT<W>::D> pv = PermView<typename DT<W>::D>{}) {
   using D = typename DT<W>::D;
-  static_assert(!PERM || KEY, "the relabelled loop uses packed keys");
   constexpr int U = 4;  // vertices per thread per round, loads issued together
   __shared__ unsigned long long s_nr[8], s_mr[8];
   __shared__ uint32_t s_un[8];
@@ -833,6 +833,12 @@ k_pred_verify(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ ad
         if constexpr (PERM) du[r] = pv.dist_int[uint_[r]];
         else du[r] = dist[pr[r].x];
         rec[r].v = pr[r].y == *reinterpret_cast<const uint32_t*>(&dv[r]) ? v : NIL;
+      } else if (look && PERM) {
+        // record mode on the relabelled loop: {u', edge'} index the relabelled
+        // CSR; the edge must end at v's relabelled id
+        rec[r] = reinterpret_cast<const EdgeRec<W>*>(pv.adj_int)[pr[r].y];
+        rec[r].v = rec[r].v == pv.perm[v] ? v : NIL;
+        du[r] = pv.dist_int[uint_[r]];
       } else if (look) {
         if (pr[r].y & PRED_CSC_SLOT) {  // recorded by a pull step: CSC slot of v
           const uint32_t sl = pr[r].y & ~PRED_CSC_SLOT;

@@ -574,7 +574,7 @@ struct Runner {
     // saves ~0.3 ms per call, so it pays on reuse, not for a one-shot
     // upload + SSSP); variant 41 forces it, 60-62 keep the caller's ids.
     const bool reuse = g->runs_since_fill++ > 0 || g->rl_valid;
-    rl = key_mode() && o->delta <= 0 &&
+    rl = (key_mode() || rec_fast()) && o->delta <= 0 &&
          (variant == 41 || ((variant == 0 || variant >= 99) && n >= (1u << 20) && reuse)) &&
          (dir == GFB_DIR_PUSH || (dir == GFB_DIR_AUTO && (alpha <= 1.0f || !g->has_csc)));
     if (rl) {
@@ -677,13 +677,15 @@ struct Runner {
     PermView<D> pv{};
     if constexpr (sizeof(D) == 4) {
       if (key_mode()) verify = k_pred_verify<W, true, false>;
-      if (rl) {  // back to the caller's ids, fused into the verification
-        verify = k_pred_verify<W, true, true>;
-        pv = PermView<D>{g->rl_perm.as<uint32_t>(), g->rl_iperm.as<uint32_t>(),
-                         ws->dist_int.as<D>(), ws->pkey_int.as<unsigned long long>(),
-                         ws->dist.as<D>(), ws->predrec.as<unsigned long long>()};
-      }
+      if (rl) verify = k_pred_verify<W, true, true>;
+    } else {
+      if (rl) verify = k_pred_verify<W, false, true>;  // f64 records, relabelled loop
     }
+    if (rl)  // back to the caller's ids, fused into the verification
+      pv = PermView<D>{g->rl_perm.as<uint32_t>(), g->rl_iperm.as<uint32_t>(),
+                       ws->dist_int.as<D>(), ws->pkey_int.as<unsigned long long>(),
+                       ws->dist.as<D>(), ws->predrec.as<unsigned long long>(),
+                       g->rl_adj.p};
     verify<<<c->num_sms * 8, 256, 0, s>>>(
         g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(),
         g->has_csc ? g->co.as<uint32_t>() : nullptr,

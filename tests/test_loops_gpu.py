@@ -169,3 +169,22 @@ def test_relabel_on_reuse_same_result(ctx):
     d, p, st = gb.sssp_stats(g, 0)  # first call after the refill: no relabel
     assert np.array_equal(d, first[0])
     assert np.array_equal(gb.sssp_stats(g2, 0)[0], first[0])
+
+
+def test_f64_s20_relabel_records(ctx):
+    """f64 arithmetic on the ordered loop (k_push_range<REC>) at 2^20 vertices:
+    the first call runs on the caller's ids, later calls on the in-degree-
+    relabelled CSR (records {u', edge'} mapped back in k_pred_verify<PERM>).
+    Bit-exact vs the f64 restatement of reference_dijkstra, valid trees."""
+    g32 = gb.rmat(20, 16, seed=4, wtype="f32", transpose=False, ctx=ctx)
+    ro, col, w = g32.csr()
+    n = g32.num_vertices
+    g32.free()
+    w64 = w.astype(np.float64)
+    g = gb.Graph.from_csr(n, ro, col, w64, wtype="f64", ctx=ctx)
+    for src in (0, 0, 12345):
+        dist, pred, st = gb.sssp_stats(g, src, direction="push")
+        want, _ = O.dijkstra(n, ro, col, w64, src, "f64")
+        assert np.array_equal(dist, want), src
+        assert O.check_pred_tree(n, ro, col, w64, dist, src, pred) == -1, src
+    g.free()
