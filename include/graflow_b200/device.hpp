@@ -28,6 +28,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <limits>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -126,10 +127,14 @@ struct DeviceSsspConfig {
 
   void validate() const {
     policy.validate();
-    // queue <=> par-nosync (algorithms.hpp:479-488): the async model has no
-    // device counterpart, so the queue representation is rejected outright.
-    if (frontier_repr == FrontierRepr::queue)
-      throw std::invalid_argument("config: queue frontier requires the par-nosync policy");
+    // The queue representation is the reference's asynchronous model
+    // (par-nosync, algorithms.hpp:479-488): on the device it runs as one
+    // persistent work-queue launch (the near-far kernel with no far set);
+    // like the reference it is push-only and reports no supersteps.
+    if (frontier_repr == FrontierRepr::queue && direction != Direction::push)
+      throw std::invalid_argument("config: queue frontier requires push direction");
+    if (frontier_repr == FrontierRepr::queue && policy.devices.size() > 1)
+      throw std::invalid_argument("config: the queue model is single-GPU");
   }
 };
 
@@ -259,12 +264,17 @@ inline SsspResult sssp(const Graph& g, vertex_t source, const DeviceSsspConfig& 
     o.delta = cfg.policy.delta;
     o.direction = GFB_DIR_PUSH;  // the near-far loop is push-only
   }
+  const bool queue = cfg.frontier_repr == FrontierRepr::queue;
+  if (queue) {  // asynchronous work queue: near-far with an unbounded near set
+    o.delta = std::numeric_limits<double>::infinity();
+    o.direction = GFB_DIR_PUSH;
+  }
   SsspResult r;
   r.dist.resize(n);
   r.pred.resize(n);
   gfb_sssp_stats st{};
   device_detail::check(gfb_sssp(dg.ctx(), dg.handle(), source, &o, r.dist.data(), r.pred.data(), &st));
-  r.supersteps = st.supersteps;
+  r.supersteps = queue ? 0 : st.supersteps;  // the async model has no supersteps
   r.relaxations = st.relaxations;
   return r;
 }

@@ -235,9 +235,16 @@ def sssp(g, source, policy="device", direction="auto", frontier="dense", workers
     """
     if policy != "device":
         raise ValueError("policy must be device (the CPU policies live in the reference)")
-    if frontier not in ("sparse", "dense"):
-        raise ValueError("frontier must be sparse|dense (queue is the async model)")
+    if frontier not in ("sparse", "dense", "queue"):
+        raise ValueError("frontier must be sparse|dense|queue")
+    if frontier == "queue":  # the asynchronous model: one persistent work-queue launch
+        if direction == "pull":
+            raise ValueError("config: queue frontier requires push direction")
+        direction = "push"
+        kw = dict(kw, delta=float("inf"))
     dist, pred, st = sssp_stats(g, source, direction=direction, **kw)
+    if frontier == "queue":
+        st.supersteps = 0  # like the reference's async loop (algorithms.hpp:600-602)
     if as_lists:
         return (dist.tolist(), [None if p == NIL else int(p) for p in pred], st.supersteps,
                 st.relaxations)

@@ -411,7 +411,8 @@ struct Runner {
       a.n = n;
       a.nwords = nwords;
       if constexpr (std::is_same<D, float>::value) a.delta = (float)delta;
-      else a.delta = (D)std::min(std::max(std::llround(delta), 1ll), 0xFFFFFFFEll);
+      else a.delta = std::isinf(delta) ? (D)0xFFFFFFFEu  // the queue model: no far set
+                                       : (D)std::min(std::max(std::llround(delta), 1ll), 0xFFFFFFFEll);
       const char* tr = getenv("GFB_TRACE");
       TBuf trace;
       if (tr && tr[0] == '1') {

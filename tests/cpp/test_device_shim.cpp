@@ -111,8 +111,9 @@ int main() {
     DeviceSsspConfig pull;
     pull.direction = Direction::pull;
     CHECK(throws<std::invalid_argument>([&] { sssp(g, 0, pull); }));
-    DeviceSsspConfig q;
+    DeviceSsspConfig q;  // the queue (async) model is push-only, like the reference
     q.frontier_repr = FrontierRepr::queue;
+    q.direction = Direction::pull;
     CHECK(throws<std::invalid_argument>([&] { sssp(g, 0, q); }));
   }
   // --- acceptance.cpp:95-122 (C1 + C4): 200 graphs, every device config,
@@ -175,6 +176,23 @@ int main() {
       bool threw = false;
       try {
         sssp(g, 0, bad);
+      } catch (const std::invalid_argument&) {
+        threw = true;
+      }
+      CHECK(threw);
+    }
+    // the queue representation (the reference's async model) on the device
+    {
+      DeviceSsspConfig qc = cfg;
+      qc.frontier_repr = FrontierRepr::queue;
+      auto rq = sssp(g, 0, qc);
+      CHECK(rq.dist == r.dist);
+      CHECK(valid_pred_tree(g, 0, rq.dist, rq.pred));
+      CHECK(rq.supersteps == 0);
+      qc.direction = Direction::pull;
+      bool threw = false;
+      try {
+        sssp(g, 0, qc);
       } catch (const std::invalid_argument&) {
         threw = true;
       }

@@ -188,3 +188,19 @@ def test_f64_s20_relabel_records(ctx):
         assert np.array_equal(dist, want), src
         assert O.check_pred_tree(n, ro, col, w64, dist, src, pred) == -1, src
     g.free()
+
+
+def test_queue_model_fixpoint(ctx):
+    """frontier="queue": the reference's asynchronous model (par-nosync,
+    algorithms.hpp:600-602) as one persistent work-queue launch (near-far with
+    no far set).  Same fixpoint, no supersteps reported."""
+    cases = [(gb.rmat(12, 16, seed=5, wtype="f32", transpose=False, ctx=ctx), "f32"),
+             (gb.rmat(12, 16, seed=6, wtype="u32", transpose=False, ctx=ctx), "u32"),
+             (gb.grid(96, seed=7, transpose=False, ctx=ctx), "f32")]
+    for g, wt in cases:
+        for src in (0, 77):
+            dist, pred, steps, relax = gb.sssp(g, src, frontier="queue")
+            _check(g, dist, pred, source=src, wtype=wt)
+            assert steps == 0 and relax > 0
+    with pytest.raises(ValueError):
+        gb.sssp(cases[0][0], 0, frontier="queue", direction="pull")
