@@ -191,6 +191,7 @@ static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const 
                        int htype) {
   g->nz_valid = false;
   g->rl_valid = false;
+  g->max_outdeg = -1;
   g->runs_since_fill = 0;
   Ctx* c = g->ctx;
   cudaStream_t s = c->stream;
@@ -258,6 +259,31 @@ static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const 
 
 // Nonzero-out-degree bitmap (one bit per vertex, the layout of the frontier
 // bitmaps) for the persistent loop's frontier count.
+static __global__ void k_max_outdeg(const uint32_t* __restrict__ ro, uint32_t n, uint32_t* out) {
+  uint32_t mx = 0;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    mx = max(mx, ro[v + 1] - ro[v]);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
+}
+
+// Largest out-degree (cached until a refill): picks the near-far kernel's
+// heavy-row handling.
+uint32_t max_out_degree(Graph* g) {
+  if (g->max_outdeg >= 0) return (uint32_t)g->max_outdeg;
+  Ctx* c = g->ctx;
+  TBuf mx;
+  mx.alloc(16, c->stream);
+  GFB_CUDA(cudaMemsetAsync(mx.p, 0, 4, c->stream));
+  k_max_outdeg<<<stride_grid(c), 256, 0, c->stream>>>(g->ro.as<uint32_t>(), (uint32_t)g->n,
+                                                      mx.as<uint32_t>());
+  uint32_t h = 0;
+  GFB_CUDA(cudaMemcpyAsync(&h, mx.p, 4, cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  g->max_outdeg = h;
+  return h;
+}
+
 static __global__ void k_nz(const uint32_t* __restrict__ ro, uint32_t n, uint32_t* nz) {
   const uint32_t nwords = (n + 31) / 32;
   for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwords;

@@ -57,7 +57,14 @@ struct NfArgs {
   D delta;
   unsigned long long* trace;  // optional (GFB_TRACE=1): per phase (time << 24 | K)
   uint32_t trace_cap;
+  // Heavy rows: an activated vertex with more than NF_HEAVY out-edges is not
+  // expanded by the warp that dequeued it but listed here and expanded by
+  // every warp (32-edge chunks) in the next phase -- one warp serialising a
+  // hub's edges made the queue loop 50x slower than BSP on RMAT.
+  uint2* hq[2];
+  uint32_t hcap;
 };
+constexpr uint32_t NF_HEAVY = 2048;
 
 
 // Append e to queue q (count *c) if this lane's flag is set: one atomicAdd per
@@ -81,7 +88,7 @@ __device__ __forceinline__ void warp_append(bool flag, uint2 e, uint2* q, uint32
 // vertex has since been lowered again is stale (the lowering appended a newer
 // entry) and is skipped -- dedup without a membership bitmap or a returning
 // atomic on the critical path.
-template <class W, int LH = 0, uint32_t CH = 32>
+template <class W, int LH = 0, uint32_t CH = 32, bool HV = false>
 __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
   using D = typename DT<W>::D;
   static_assert(sizeof(D) == 4, "packed predecessor keys need 32-bit distances");
@@ -107,6 +114,7 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
     a.cnt[0] = 1;
     a.cnt[1] = a.cnt[2] = a.cnt[3] = a.cnt[4] = 0;
     a.cnt[5] = a.cnt[6] = 0xFFFFFFFFu;
+    a.cnt[7] = a.cnt[8] = a.cnt[9] = 0;  // heavy-list counts (rotating like the near ones)
   }
   grid.sync();
 
@@ -121,12 +129,17 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
     uint2* qout = a.nq[nxt];
     uint32_t* cout = a.cnt + (ph + 1) % 3;
     if (gtid == 0) a.cnt[(ph + 2) % 3] = 0;  // the count two phases ahead
+    const uint32_t H = HV ? min(__ldcg(a.cnt + 7 + ph % 3), a.hcap) : 0u;  // heavy rows
+    const uint2* hin = a.hq[ph & 1];
+    uint2* hout = a.hq[(ph + 1) & 1];
+    uint32_t* hcout = a.cnt + 7 + (ph + 1) % 3;
+    if (gtid == 0) a.cnt[7 + (ph + 2) % 3] = 0;
     if (a.trace && gtid == 0 && ph < a.trace_cap) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       a.trace[ph] = (t << 24) | min(K, 0xFFFFFFu);
     }
-    if (K > 0) {
+    if (K > 0 || H > 0) {
       // ---------------- near phase: expand the near queue ----------------
       ++phases;
       uint32_t lq_n = 0;  // warp-local queue fill (warp-uniform)
@@ -142,6 +155,12 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
           const D cu = __ldcg(a.dist + u);
           du = dfrom<D>(e.y);
           deg = dbits(cu) == e.y ? en - st : 0u;  // stale entry: skip
+        }
+        // hubs go to the heavy list (whole-grid expansion next phase)
+        if constexpr (HV) {
+          const bool heavy = deg > NF_HEAVY;
+          warp_append(heavy, e, hout, hcout, a.hcap, err);
+          if (heavy) deg = 0;
         }
         const uint32_t incl = warp_incl_scan(deg, lane);
         const uint32_t off = incl - deg;  // first chunk edge of this lane's vertex
@@ -187,6 +206,34 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
           warp_append(to_far, ent, a.fq[fp], a.cnt + 3 + fp, a.cap, err);
         }
       };
+      // heavy rows listed last phase: one CTA per row (rows strided over the
+      // CTAs), its warps taking 32-edge chunks
+      for (uint32_t hi = blockIdx.x; hi < H; hi += gridDim.x) {
+        const uint2 e = __ldcg(hin + hi);
+        const D cu = __ldcg(a.dist + e.x);
+        if (dbits(cu) != e.y) continue;  // stale (block-uniform)
+        const uint32_t st = a.ro[e.x], deg = a.ro[e.x + 1] - st;
+        const D du = dfrom<D>(e.y);
+        if (threadIdx.x == 0) relax += deg;
+        for (uint32_t base = warp * 32; base < deg; base += NF_THREADS) {
+          const uint32_t le = base + lane;
+          bool to_near = false, to_far = false;
+          uint2 ent = make_uint2(0, 0);
+          if (le < deg) {
+            const EdgeRec<W> rec = ld_rec(a.adj + st + le);
+            const D nd = dadd(du, rec.w, err);
+            if (nd < __ldcg(a.dist + rec.v)) {
+              red_min_u32(reinterpret_cast<unsigned*>(a.dist + rec.v), dbits(nd));
+              red_min_u64(a.pkey + rec.v, pred_key(nd, e.x));
+              ent = make_uint2(rec.v, dbits(nd));
+              to_near = nd < thr;
+              to_far = !to_near;
+            }
+          }
+          warp_append(to_near, ent, qout, cout, a.cap, err);
+          warp_append(to_far, ent, a.fq[fp], a.cnt + 3 + fp, a.cap, err);
+        }
+      }
       // CH queue entries per warp: fewer than 32 spreads a small near queue
       // (and the chasing of its activations) over more warps
       for (uint32_t base = gwarp * CH; base < K; base += nwarps * CH) {

@@ -373,7 +373,10 @@ struct Runner {
       // delta 32 = 55 ms; CH 8: LH 4 33.5, LH 8 32.7, LH 16 36.9 ms; CH 4 LH 8
       // delta 16 32.5 ms (profiles/r01_nearfar_chunk.txt).  Variants keep the
       // other settings measurable.
-      auto kern = k_nearfar<W, 8, 8>;
+      // rows longer than NF_HEAVY edges: expanded by a whole CTA in the next
+      // phase (RMAT s24, delta = inf: 212 -> 58 ms); compiled out otherwise
+      const bool hv = max_out_degree(g) > NF_HEAVY || variant == 89;
+      auto kern = hv ? k_nearfar<W, 8, 8, true> : k_nearfar<W, 8, 8>;
       if (variant == 90) kern = k_nearfar<W, 0>;
       else if (variant == 91) kern = k_nearfar<W, 4>;
       else if (variant == 92) kern = k_nearfar<W, 16>;
@@ -390,8 +393,10 @@ struct Runner {
       // activate at most min(m, n x in-degree) vertices -- size for 2n or m/4
       const uint64_t cap64 = std::min<uint64_t>(std::max<uint64_t>(2ull * n, g->m / 4), 0xFFFFFFF0ull);
       const uint32_t cap = (uint32_t)cap64;
-      if (ws->nf_q.bytes < (size_t)cap * 32) {
-        ws->nf_q.alloc((size_t)cap * 32, s);
+      const uint32_t hcap = (uint32_t)std::min<uint64_t>(g->m / NF_HEAVY + 4096, 0xFFFFFFF0ull);
+      const size_t qbytes = (size_t)cap * 32 + (size_t)hcap * 16;
+      if (ws->nf_q.bytes < qbytes) {
+        ws->nf_q.alloc(qbytes, s);
         ws->nf_cnt.alloc(64, s);
       }
       NfArgs<W> a{};
@@ -404,6 +409,9 @@ struct Runner {
       a.nq[1] = q + cap;
       a.fq[0] = q + 2 * (size_t)cap;
       a.fq[1] = q + 3 * (size_t)cap;
+      a.hq[0] = q + 4 * (size_t)cap;
+      a.hq[1] = q + 4 * (size_t)cap + hcap;
+      a.hcap = hcap;
       a.cap = cap;
       a.cnt = ws->nf_cnt.as<uint32_t>();
       a.ctl = ws->ctl.as<Ctl>();

@@ -70,7 +70,7 @@ def test_nearfar_corpus_f32(ctx):
         _check(g, dist, pred)
 
 
-@pytest.mark.parametrize("variant", [90, 91, 93, 96, 98])
+@pytest.mark.parametrize("variant", [89, 90, 91, 93, 96, 98])
 def test_nearfar_chunk_variants(ctx, variant):
     """Other (chase rounds, entries per warp) settings of k_nearfar."""
     g = gb.grid(128, seed=3, transpose=True, ctx=ctx)
@@ -204,3 +204,25 @@ def test_queue_model_fixpoint(ctx):
             assert steps == 0 and relax > 0
     with pytest.raises(ValueError):
         gb.sssp(cases[0][0], 0, frontier="queue", direction="pull")
+
+
+@pytest.mark.parametrize("wtype", ["f32", "u32"])
+def test_nearfar_heavy_rows(ctx, wtype):
+    """Rows longer than NF_HEAVY (2048) edges are expanded by a whole CTA in
+    the next phase: hubs with 6000 / 3000 out-edges, queue model and near-far."""
+    rng = np.random.default_rng(11)
+    n = 20000
+    src = np.concatenate([np.zeros(6000, np.int64), np.full(3000, 7),
+                          rng.integers(0, n, 60000)])
+    dst = np.concatenate([rng.integers(0, n, 6000), rng.integers(0, n, 3000),
+                          rng.integers(0, n, 60000)])
+    src[6000:9000] = 7
+    w = rng.integers(0, 100, len(src)).astype(np.float64)
+    if wtype == "f32":
+        w = w / 7.0
+    g = gb.build_csr((src.astype(np.uint32), dst.astype(np.uint32), w), n, wtype=wtype,
+                     ctx=ctx)
+    for kw in (dict(frontier="queue"), dict(delta=3.0, direction="push")):
+        for s in (0, 7, 123):
+            dist, pred, _, _ = gb.sssp(g, s, **kw)
+            _check(g, dist, pred, source=s, wtype=wtype)
