@@ -83,8 +83,10 @@ def test_rejections(ctx):
         gb.sssp(g, 0, direction="pull")  # no transpose built
     with pytest.raises(ValueError):
         gb.sssp(g, 0, policy="par")
-    with pytest.raises(ValueError):
-        gb.sssp(g, 0, frontier="queue")
+    with pytest.raises(ValueError):  # the queue (async) model is push-only
+        gb.sssp(g, 0, frontier="queue", direction="pull")
+    d, _, steps, _ = gb.sssp(g, 0, frontier="queue")  # runs as the device work queue
+    assert list(d) == [0.0, 1.0, 3.0] and steps == 0
 
 
 def test_upload_validation(ctx):
