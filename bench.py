@@ -349,6 +349,17 @@ def secondary_configs(gb, ctx, args, g_main=None):
                 ms.append(st.device_ms)
         return statistics.median(ms), st
 
+    if g_main is not None:  # f64 arithmetic: the C++ policy default, bit-exact vs the reference
+        ro, col, w = g_main.csr()
+        g64 = gb.Graph.from_csr(g_main.num_vertices, ro, col, w.astype("float64"), wtype="f64",
+                                ctx=ctx)
+        del ro, col, w
+        ms, st = timed(g64, 5, direction="push")
+        out.append({"config": f"RMAT s{args.scale} EF{args.edgefactor}, f64 arithmetic (the same "
+                              f"weights widened; bit-exact vs the reference's doubles), push",
+                    "gteps": st.m_reach / (ms * 1e-3) / 1e9, "ms": ms,
+                    "supersteps": st.supersteps, "work_inflation": st.relaxations / st.m_reach})
+        g64.free()
     g = gb.rmat(22, args.edgefactor, seed=args.seed, wtype="f32", transpose=True, ctx=ctx)
     ms, st = timed(g, 5, direction="push")
     out.append({"config": "BASELINE configs[1]: RMAT s22 EF16 fp32, push-only",
