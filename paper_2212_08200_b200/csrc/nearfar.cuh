@@ -64,7 +64,7 @@ struct NfArgs {
   uint2* hq[2];
   uint32_t hcap;
 };
-constexpr uint32_t NF_HEAVY = 2048;
+constexpr uint32_t NF_HEAVY = 256;
 
 
 // Append e to queue q (count *c) if this lane's flag is set: one atomicAdd per

@@ -374,7 +374,7 @@ struct Runner {
       // delta 16 32.5 ms (profiles/r01_nearfar_chunk.txt).  Variants keep the
       // other settings measurable.
       // rows longer than NF_HEAVY edges: expanded by a whole CTA in the next
-      // phase (RMAT s24, delta = inf: 212 -> 58 ms); compiled out otherwise
+      // phase (RMAT s24, delta = inf: 212 -> 36 ms at 256 edges); compiled out otherwise
       const bool hv = max_out_degree(g) > NF_HEAVY || variant == 89;
       auto kern = hv ? k_nearfar<W, 8, 8, true> : k_nearfar<W, 8, 8>;
       if (variant == 90) kern = k_nearfar<W, 0>;
