@@ -192,6 +192,7 @@ static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const 
   g->nz_valid = false;
   g->rl_valid = false;
   g->max_outdeg = -1;
+  g->mean_w = -1;
   g->runs_since_fill = 0;
   Ctx* c = g->ctx;
   cudaStream_t s = c->stream;
@@ -282,6 +283,42 @@ uint32_t max_out_degree(Graph* g) {
   c->sync();
   g->max_outdeg = h;
   return h;
+}
+
+template <class W>
+static __global__ void k_weight_sum(const EdgeRec<W>* __restrict__ adj, uint64_t m, double* out) {
+  double acc = 0;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+       e += (uint64_t)gridDim.x * blockDim.x)
+    acc += (double)adj[e].w;
+  for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+  if ((threadIdx.x & 31) == 0 && acc != 0) atomicAdd(out, acc);
+}
+
+// Mean edge weight (cached until a refill): scales the automatic near-far
+// delta for mesh-like graphs.
+double mean_weight(Graph* g) {
+  if (g->mean_w >= 0) return g->mean_w;
+  Ctx* c = g->ctx;
+  TBuf acc;
+  acc.alloc(16, c->stream);
+  GFB_CUDA(cudaMemsetAsync(acc.p, 0, 8, c->stream));
+  if (g->m) {
+    if (g->wtype == GFB_W_F32)
+      k_weight_sum<float><<<stride_grid(c), 256, 0, c->stream>>>(g->adj.as<EdgeRec<float>>(), g->m,
+                                                                 acc.as<double>());
+    else if (g->wtype == GFB_W_F64)
+      k_weight_sum<double><<<stride_grid(c), 256, 0, c->stream>>>(g->adj.as<EdgeRec<double>>(),
+                                                                  g->m, acc.as<double>());
+    else
+      k_weight_sum<uint32_t><<<stride_grid(c), 256, 0, c->stream>>>(
+          g->adj.as<EdgeRec<uint32_t>>(), g->m, acc.as<double>());
+  }
+  double h = 0;
+  GFB_CUDA(cudaMemcpyAsync(&h, acc.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  g->mean_w = g->m ? h / (double)g->m : 0.0;
+  return g->mean_w;
 }
 
 static __global__ void k_nz(const uint32_t* __restrict__ ro, uint32_t n, uint32_t* nz) {

@@ -71,6 +71,7 @@ struct Graph {
   bool rl_valid = false;
   uint32_t runs_since_fill = 0;  // sssp calls on the current contents (relabel pays on reuse)
   int64_t max_outdeg = -1;        // cached (max_out_degree), -1: not computed
+  double mean_w = -1;             // cached (mean_weight), -1: not computed
   bool rl_skip = false;  // in-degrees not skewed enough to pay (no arrays built)
   // static pull plan (destinations with in-degree > 0)
   uint32_t pull_k = 0, pull_total = 0;
@@ -185,6 +186,7 @@ void build_pull_plan(Graph* g);
 void ensure_nz(Graph* g);
 void ensure_relabel(Graph* g);
 uint32_t max_out_degree(Graph* g);
+double mean_weight(Graph* g);
 // bfs.cu
 void bfs_run(Ctx* c, Graph* g, uint32_t source, int direction, double* depth,
              uint64_t* supersteps, uint64_t* relaxations);

@@ -123,6 +123,7 @@ struct Runner {
     if (variant == 0) return 10;
     switch (variant) {
       case 63: return 10;  // deferral on the caller's ids (no relabel): the peer path's loop
+      case 122: return 10;  // the default loop without the automatic near-far choice
       case 65: case 66: case 67: case 68: case 69: return 10;  // f64 advance shapes
       case 99: return 100;
       case 100: return 50;
@@ -583,7 +584,17 @@ struct Runner {
     // saves ~0.3 ms per call, so it pays on reuse, not for a one-shot
     // upload + SSSP); variant 41 forces it, 60-62 keep the caller's ids.
     const bool reuse = g->runs_since_fill++ > 0 || g->rl_valid;
-    rl = (key_mode() || rec_fast()) && o->delta <= 0 &&
+    // Default configuration on a low-degree mesh (max out-degree <= 8, e.g.
+    // grids and road networks: thousands of BSP supersteps): the near-far
+    // loop with delta = 32 x the mean edge weight (the 4096^2 grid's tuned
+    // value: 570 -> 32 ms).  Same fixpoint; variant 122 keeps the BSP loop.
+    double delta = o->delta;
+    if (delta == 0 && variant == 0 && key_mode() && dir != GFB_DIR_PULL &&
+        n >= (1u << 16) && max_out_degree(g) <= 8 && g->m >= n) {
+      const double mw = mean_weight(g);
+      if (mw > 0) delta = 32.0 * mw;
+    }
+    rl = (key_mode() || rec_fast()) && delta <= 0 &&
          (variant == 41 || ((variant == 0 || variant >= 99) && n >= (1u << 20) && reuse)) &&
          (dir == GFB_DIR_PUSH || (dir == GFB_DIR_AUTO && (alpha <= 1.0f || !g->has_csc)));
     if (rl) {
@@ -605,9 +616,9 @@ struct Runner {
     float adv_ms = 0;
     GFB_CUDA(cudaEventRecord(c->ev[0], s));
     bool done = false;
-    if (o->delta > 0 && key_mode() && !rl) {
+    if (delta > 0 && key_mode() && !rl) {
       if (dir == GFB_DIR_PULL) fail(GFB_EINVAL, "sssp: the near-far filter (delta > 0) is push-only");
-      done = nearfar_launch(o->delta);
+      done = nearfar_launch(delta);
       if (done && (c->read_ctl(ws->ctl.as<Ctl>()).err & 2u)) done = false;  // queue overflow: BSP
     }
     if (!done && o->device_loop && persistent()) done = bsp_run(dir, alpha);

@@ -226,3 +226,19 @@ def test_nearfar_heavy_rows(ctx, wtype):
         for s in (0, 7, 123):
             dist, pred, _, _ = gb.sssp(g, s, **kw)
             _check(g, dist, pred, source=s, wtype=wtype)
+
+
+def test_auto_nearfar_on_mesh(ctx):
+    """The default configuration picks the near-far loop on a low-degree mesh
+    (max out-degree <= 8, n >= 2^16; delta = 32 x mean weight) and the BSP loop
+    otherwise; variant 122 forces BSP.  Same distances either way."""
+    g = gb.grid(300, seed=9, transpose=False, ctx=ctx)
+    ro, col, w = g.csr()
+    want, _ = O.dijkstra(g.num_vertices, ro, col, w, 0, "f32")
+    d_auto, p_auto, st_auto = gb.sssp_stats(g, 0, direction="push")
+    d_bsp, p_bsp, st_bsp = gb.sssp_stats(g, 0, direction="push", variant=122)
+    for d, p in ((d_auto, p_auto), (d_bsp, p_bsp)):
+        assert np.array_equal(d.astype(np.float32), want)
+        assert O.check_pred_tree(g.num_vertices, ro, col, w, d.astype(np.float32), 0, p) == -1
+    assert st_auto.supersteps * 2 < st_bsp.supersteps  # phases vs BSP supersteps
+    g.free()
