@@ -63,8 +63,55 @@ struct NfArgs {
   // hub's edges made the queue loop 50x slower than BSP on RMAT.
   uint2* hq[2];
   uint32_t hcap;
+  unsigned long long* fmin64;  // [2] minimum live far distance (order key), by parity
 };
 constexpr uint32_t NF_HEAVY = 256;
+
+// Queue entries are (v, tag of the distance that activated v).  4-byte
+// distances: the tag is the distance's bits (exact stale test).  f64: the
+// folded 64-bit pattern -- a collision only lets a stale entry expand again
+// with v's CURRENT distance, which is correct, just redundant.
+__device__ __forceinline__ uint32_t ntag(float d) { return __float_as_uint(d); }
+__device__ __forceinline__ uint32_t ntag(uint32_t d) { return d; }
+__device__ __forceinline__ uint32_t ntag(double d) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+  return (uint32_t)(b ^ (b >> 32));
+}
+// order-preserving 64-bit key of a distance (non-negative)
+__device__ __forceinline__ unsigned long long okey(float d) { return __float_as_uint(d); }
+__device__ __forceinline__ unsigned long long okey(uint32_t d) { return d; }
+__device__ __forceinline__ unsigned long long okey(double d) {
+  return (unsigned long long)__double_as_longlong(d);
+}
+template <class D> __device__ __forceinline__ D dfrom_okey(unsigned long long k);
+template <> __device__ __forceinline__ float dfrom_okey<float>(unsigned long long k) {
+  return __uint_as_float((uint32_t)k);
+}
+template <> __device__ __forceinline__ uint32_t dfrom_okey<uint32_t>(unsigned long long k) {
+  return (uint32_t)k;
+}
+template <> __device__ __forceinline__ double dfrom_okey<double>(unsigned long long k) {
+  return __longlong_as_double((long long)k);
+}
+
+// One relaxation u -> v (edge eid) with candidate nd; true when it lowered
+// dist[v] (as far as this thread can tell).  4-byte: fire-and-forget min and
+// packed (dist, u) key (k_push_range); f64: returning 64-bit min and a
+// {u, edge} record by the winner (k_push_range<REC>).
+template <class D>
+__device__ __forceinline__ bool nf_relax(D* dist, unsigned long long* pkey, uint32_t v, D nd,
+                                         uint32_t u, uint32_t eid) {
+  if (!(nd < __ldcg(dist + v))) return false;
+  if constexpr (sizeof(D) == 8) {
+    const D old = atomic_min_d(dist + v, nd);
+    if (!(nd < old)) return false;
+    reinterpret_cast<uint2*>(pkey)[v] = make_uint2(u, eid);
+  } else {
+    red_min_u32(reinterpret_cast<unsigned*>(dist + v), dbits(nd));
+    red_min_u64(pkey + v, pred_key(nd, u));
+  }
+  return true;
+}
 
 
 // Append e to queue q (count *c) if this lane's flag is set: one atomicAdd per
@@ -91,7 +138,6 @@ __device__ __forceinline__ void warp_append(bool flag, uint2 e, uint2* q, uint32
 template <class W, int LH = 0, uint32_t CH = 32, bool HV = false>
 __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
   using D = typename DT<W>::D;
-  static_assert(sizeof(D) == 4, "packed predecessor keys need 32-bit distances");
   cgn::grid_group grid = cgn::this_grid();
   const int lane = threadIdx.x & 31;
   const uint32_t gtid = blockIdx.x * NF_THREADS + threadIdx.x;
@@ -113,7 +159,8 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
     a.nq[0][0] = make_uint2(source, 0u);  // dist bits of +0.0 / 0u
     a.cnt[0] = 1;
     a.cnt[1] = a.cnt[2] = a.cnt[3] = a.cnt[4] = 0;
-    a.cnt[5] = a.cnt[6] = 0xFFFFFFFFu;
+    a.cnt[5] = a.cnt[6] = 0xFFFFFFFFu;  // (unused: the far minimum lives in fmin64)
+    a.fmin64[0] = a.fmin64[1] = ~0ull;
     a.cnt[7] = a.cnt[8] = a.cnt[9] = 0;  // heavy-list counts (rotating like the near ones)
   }
   grid.sync();
@@ -153,8 +200,8 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
           st = a.ro[u];
           const uint32_t en = a.ro[u + 1];
           const D cu = __ldcg(a.dist + u);
-          du = dfrom<D>(e.y);
-          deg = dbits(cu) == e.y ? en - st : 0u;  // stale entry: skip
+          du = cu;
+          deg = ntag(cu) == e.y ? en - st : 0u;  // stale entry: skip
         }
         // hubs go to the heavy list (whole-grid expansion next phase)
         if constexpr (HV) {
@@ -183,10 +230,8 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
           if (le < tot) {
             const EdgeRec<W> rec = ld_rec(a.adj + ost + (le - ooff));
             const D nd = dadd(odu, rec.w, err);
-            if (nd < __ldcg(a.dist + rec.v)) {
-              red_min_u32(reinterpret_cast<unsigned*>(a.dist + rec.v), dbits(nd));
-              red_min_u64(a.pkey + rec.v, pred_key(nd, ou));
-              ent = make_uint2(rec.v, dbits(nd));
+            if (nf_relax(a.dist, a.pkey, rec.v, nd, ou, ost + (le - ooff))) {
+              ent = make_uint2(rec.v, ntag(nd));
               to_near = nd < thr;
               to_far = !to_near;
             }
@@ -211,9 +256,9 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
       for (uint32_t hi = blockIdx.x; hi < H; hi += gridDim.x) {
         const uint2 e = __ldcg(hin + hi);
         const D cu = __ldcg(a.dist + e.x);
-        if (dbits(cu) != e.y) continue;  // stale (block-uniform)
+        if (ntag(cu) != e.y) continue;  // stale (block-uniform)
         const uint32_t st = a.ro[e.x], deg = a.ro[e.x + 1] - st;
-        const D du = dfrom<D>(e.y);
+        const D du = cu;
         if (threadIdx.x == 0) relax += deg;
         for (uint32_t base = warp * 32; base < deg; base += NF_THREADS) {
           const uint32_t le = base + lane;
@@ -222,10 +267,8 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
           if (le < deg) {
             const EdgeRec<W> rec = ld_rec(a.adj + st + le);
             const D nd = dadd(du, rec.w, err);
-            if (nd < __ldcg(a.dist + rec.v)) {
-              red_min_u32(reinterpret_cast<unsigned*>(a.dist + rec.v), dbits(nd));
-              red_min_u64(a.pkey + rec.v, pred_key(nd, e.x));
-              ent = make_uint2(rec.v, dbits(nd));
+            if (nf_relax(a.dist, a.pkey, rec.v, nd, e.x, st + le)) {
+              ent = make_uint2(rec.v, ntag(nd));
               to_near = nd < thr;
               to_far = !to_near;
             }
@@ -266,22 +309,23 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
     // ---------------- split phase: refill the near queue from the far pile ----
     const uint32_t F = min(__ldcg(a.cnt + 3 + fp), a.cap);
     const uint2* fin = a.fq[fp];
-    // pass 1: minimum live far distance
-    uint32_t mloc = 0xFFFFFFFFu;
+    // pass 1: minimum live far distance (64-bit order key for every type)
+    unsigned long long mloc = ~0ull;
     for (uint32_t i = gtid; i < F; i += gthreads) {
       const uint2 e = __ldcg(fin + i);
-      if (dbits(__ldcg(a.dist + e.x)) == e.y) mloc = min(mloc, e.y);
+      const D cd = __ldcg(a.dist + e.x);
+      if (ntag(cd) == e.y) mloc = min(mloc, okey(cd));
     }
     for (int d = 16; d > 0; d >>= 1) mloc = min(mloc, __shfl_xor_sync(0xffffffffu, mloc, d));
-    if (lane == 0 && mloc != 0xFFFFFFFFu) atomicMin(a.cnt + 5 + mp, mloc);
+    if (lane == 0 && mloc != ~0ull) atomicMin(a.fmin64 + mp, mloc);
     if (gtid == 0) {
       a.cnt[3 + (fp ^ 1)] = 0;
-      a.cnt[5 + (mp ^ 1)] = 0xFFFFFFFFu;
+      a.fmin64[mp ^ 1] = ~0ull;
     }
     grid.sync();
-    const uint32_t mbits = __ldcg(a.cnt + 5 + mp);
-    if (mbits == 0xFFFFFFFFu) break;  // no live far entry: converged
-    const D mfar = dfrom<D>(mbits);
+    const unsigned long long mbits = __ldcg(a.fmin64 + mp);
+    if (mbits == ~0ull) break;  // no live far entry: converged
+    const D mfar = dfrom_okey<D>(mbits);
     thr = dadd(mfar, a.delta, nullptr);
     if (!(mfar < thr)) thr = dinf<W>();  // delta absorbed by rounding: take everything
     // pass 2: live entries below thr -> near queue, the rest stay far
@@ -291,8 +335,9 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
       bool near = false, keep = false;
       if (i < F) {
         e = __ldcg(fin + i);
-        if (dbits(__ldcg(a.dist + e.x)) == e.y) {
-          near = dfrom<D>(e.y) < thr;
+        const D cd = __ldcg(a.dist + e.x);
+        if (ntag(cd) == e.y) {
+          near = cd < thr;
           keep = !near;
         }
       }

@@ -368,7 +368,7 @@ struct Runner {
 
   // Near-far filter (opts.delta > 0): one persistent launch (nearfar.cuh).
   bool nearfar_launch(double delta) {
-    if constexpr (sizeof(D) == 4) {
+    {
       // 8 queue entries per warp (one edge per lane on degree-4 meshes) and
       // warp-local chasing of 8 rounds.  4096^2 grid: 32 entries/warp, LH 4,
       // delta 32 = 55 ms; CH 8: LH 4 33.5, LH 8 32.7, LH 16 36.9 ms; CH 4 LH 8
@@ -378,14 +378,16 @@ struct Runner {
       // phase (RMAT s24, delta = inf: 212 -> 36 ms at 256 edges); compiled out otherwise
       const bool hv = max_out_degree(g) > NF_HEAVY || variant == 89;
       auto kern = hv ? k_nearfar<W, 8, 8, true> : k_nearfar<W, 8, 8>;
-      if (variant == 90) kern = k_nearfar<W, 0>;
-      else if (variant == 91) kern = k_nearfar<W, 4>;
-      else if (variant == 92) kern = k_nearfar<W, 16>;
-      else if (variant == 93) kern = k_nearfar<W, 4, 8>;
-      else if (variant == 94) kern = k_nearfar<W, 4, 16>;
-      else if (variant == 96) kern = k_nearfar<W, 8, 4>;
-      else if (variant == 97) kern = k_nearfar<W, 16, 8>;
-      else if (variant == 98) kern = k_nearfar<W, 16, 4>;
+      if constexpr (sizeof(D) == 4) {  // shape experiments: 4-byte distances only
+        if (variant == 90) kern = k_nearfar<W, 0>;
+        else if (variant == 91) kern = k_nearfar<W, 4>;
+        else if (variant == 92) kern = k_nearfar<W, 16>;
+        else if (variant == 93) kern = k_nearfar<W, 4, 8>;
+        else if (variant == 94) kern = k_nearfar<W, 4, 16>;
+        else if (variant == 96) kern = k_nearfar<W, 8, 4>;
+        else if (variant == 97) kern = k_nearfar<W, 16, 8>;
+        else if (variant == 98) kern = k_nearfar<W, 16, 4>;
+      }
       int per_sm = 0;
       GFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NF_THREADS, 0));
       if (per_sm <= 0) return false;
@@ -415,11 +417,13 @@ struct Runner {
       a.hcap = hcap;
       a.cap = cap;
       a.cnt = ws->nf_cnt.as<uint32_t>();
+      a.fmin64 = reinterpret_cast<unsigned long long*>(ws->nf_cnt.as<uint32_t>() + 10);
       a.ctl = ws->ctl.as<Ctl>();
       a.src_ptr = ws->src_dev.as<uint32_t>();
       a.n = n;
       a.nwords = nwords;
       if constexpr (std::is_same<D, float>::value) a.delta = (float)delta;
+      else if constexpr (std::is_same<D, double>::value) a.delta = delta;
       else a.delta = std::isinf(delta) ? (D)0xFFFFFFFEu  // the queue model: no far set
                                        : (D)std::min(std::max(std::llround(delta), 1ll), 0xFFFFFFFEll);
       const char* tr = getenv("GFB_TRACE");
@@ -589,7 +593,7 @@ struct Runner {
     // loop with delta = 32 x the mean edge weight (the 4096^2 grid's tuned
     // value: 570 -> 32 ms).  Same fixpoint; variant 122 keeps the BSP loop.
     double delta = o->delta;
-    if (delta == 0 && variant == 0 && key_mode() && dir != GFB_DIR_PULL &&
+    if (delta == 0 && variant == 0 && (key_mode() || rec_fast()) && dir != GFB_DIR_PULL &&
         n >= (1u << 16) && max_out_degree(g) <= 8 && g->m >= n) {
       const double mw = mean_weight(g);
       if (mw > 0) delta = 32.0 * mw;
@@ -616,7 +620,7 @@ struct Runner {
     float adv_ms = 0;
     GFB_CUDA(cudaEventRecord(c->ev[0], s));
     bool done = false;
-    if (delta > 0 && key_mode() && !rl) {
+    if (delta > 0 && (key_mode() || rec_fast()) && !rl) {
       if (dir == GFB_DIR_PULL) fail(GFB_EINVAL, "sssp: the near-far filter (delta > 0) is push-only");
       done = nearfar_launch(delta);
       if (done && (c->read_ctl(ws->ctl.as<Ctl>()).err & 2u)) done = false;  // queue overflow: BSP

@@ -242,3 +242,31 @@ def test_auto_nearfar_on_mesh(ctx):
         assert O.check_pred_tree(g.num_vertices, ro, col, w, d.astype(np.float32), 0, p) == -1
     assert st_auto.supersteps * 2 < st_bsp.supersteps  # phases vs BSP supersteps
     g.free()
+
+
+def _f64(g32, ctx):
+    ro, col, w = g32.csr()
+    n = g32.num_vertices
+    g32.free()
+    w64 = w.astype(np.float64)
+    return gb.Graph.from_csr(n, ro, col, w64, wtype="f64", ctx=ctx), ro, col, w64
+
+
+def test_nearfar_f64(ctx):
+    """f64 arithmetic in the near-far / queue kernel (returning 64-bit mins,
+    {u, edge} records, 32-bit entry tags): bit-exact vs the f64 restatement of
+    reference_dijkstra; includes the automatic choice on a mesh."""
+    for g32, kws in ((gb.grid(128, seed=4, transpose=False, ctx=ctx),
+                      [dict(delta=4.0, direction="push"), dict(frontier="queue")]),
+                     (gb.rmat(12, 16, seed=8, wtype="f32", transpose=False, ctx=ctx),
+                      [dict(delta=0.1, direction="push"), dict(frontier="queue")]),
+                     (gb.grid(300, seed=9, transpose=False, ctx=ctx), [dict()])):
+        g, ro, col, w64 = _f64(g32, ctx)
+        n = g.num_vertices
+        for kw in kws:
+            for src in (0, n // 2):
+                dist, pred, _, _ = gb.sssp(g, src, **kw)
+                want, _ = O.dijkstra(n, ro, col, w64, src, "f64")
+                assert np.array_equal(dist, want), kw
+                assert O.check_pred_tree(n, ro, col, w64, dist, src, pred) == -1, kw
+        g.free()
