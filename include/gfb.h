@@ -168,8 +168,11 @@ typedef struct gfb_sssp_opts {
   int32_t device_loop;   /* 1: device-side convergence (CUDA graph) */
   double delta;          /* >0: near-far filter of this width (push only; one
                             persistent launch with queue frontiers, for
-                            high-diameter graphs); 0: BSP loop.  u32/f32
-                            arithmetic (f64 ignores it).  Same distances. */
+                            high-diameter graphs); +inf: the async queue model
+                            (no far set); 0: the device chooses -- near-far
+                            with delta = 32 x mean weight on low-degree meshes
+                            (max out-degree <= 8, n >= 2^16), else the BSP
+                            loop.  Any arithmetic.  Same distances. */
   int32_t compute_pred;  /* 1: fill pred (tight-edge tree) */
   int32_t reserved[7];   /* reserved[0]: kernel-shape experiment id (0 = the
                             measured default; see sssp.cu Runner::variant) */
@@ -204,8 +207,9 @@ int gfb_sssp(gfb_ctx* ctx, gfb_graph* g, uint32_t source,
 int gfb_sssp_read(gfb_graph* g, double* dist, void* dist_native, uint32_t* pred);
 
 /* ---- inspection (tests / tools; no reference counterpart) ----------------
- * The in-degree-relabelled CSR the BSP loop runs on for 32-bit weights
- * (built on first use, cached until a refill): row offsets (n+1), records as
+ * The in-degree-relabelled CSR the BSP loop runs on for skewed graphs (the
+ * loop also uses it for f64; this view serves 4-byte weights only; built on
+ * first use, cached until a refill): row offsets (n+1), records as
  * {dst, weight bits} u32 pairs (2m), perm old->new id (n).  Any pointer may
  * be 0.  4-byte weights only (else GFB_EINVAL). */
 int gfb_debug_relabel(gfb_graph* g, uint32_t* row_offsets, uint32_t* adj_pairs,

@@ -89,7 +89,8 @@ struct DevicePolicy {
   bool auto_direction = true;  // push<->pull switch on the device
   float pull_alpha = 0.25f;    // pull when frontier edges > m / pull_alpha
   double delta = 0.0;          // > 0: near-far filter (push only; high-diameter
-                               // graphs, u32/f32 arithmetic) -- same distances
+                               // graphs, any arithmetic) -- same distances.  0: the
+                               // device chooses (near-far on low-degree meshes)
   // More than one entry: the graph is cut into edge-balanced vertex ranges,
   // partition q runs on devices[q] and relaxes remote vertices directly in
   // their owner's memory (gfb_mg_*, NVLink peer access; entries may repeat a

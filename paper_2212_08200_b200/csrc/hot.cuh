@@ -8,8 +8,10 @@
 //                 edges per lane, 64 warps per SM; record stream -> distance
 //                 gather (test before atomic) -> fire-and-forget red.* of the
 //                 distance, the packed (dist, pred) key and the frontier bit.
-//   k_push_warp   the same tiling with atomicMin-with-return and {u, edge}
-//                 records (f64 distances; the partitioned multi-GPU advance).
+//                 REC (f64): returning 64-bit mins and {u, edge} records.
+//   k_push_warp   the previous warp-tile kernel with atomicMin-with-return and
+//                 {u, edge} records (variant 10; the host-driven partitioned
+//                 advance of mg.cu).
 //   k_pull_relax  pull over the CSC plan (CTA tiles in shared memory).
 // Each step of the design is a measurement: profiles/r01_variants_s24.txt.
 #pragma once
