@@ -1,3 +1,4 @@
+"""One f64 SSSP at RMAT s24 in host-loop mode twice (ncu launch-list target)."""
 import sys; sys.path.insert(0, '/root/repo')
 import paper_2212_08200_b200 as gb
 g32 = gb.rmat(24, 16, seed=1, wtype="f32", transpose=False)

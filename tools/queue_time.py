@@ -1,3 +1,4 @@
+"""Queue (async) model vs the BSP loop on RMAT s24 and the 4096^2 grid (device ms, work)."""
 import sys, time, json, statistics
 sys.path.insert(0, '/root/repo')
 import paper_2212_08200_b200 as gb
