@@ -252,6 +252,12 @@ k_fwrite(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur, u
 constexpr int OB_N = 32;          // buckets: 16 octaves above the minimum
 constexpr int OB_SHIFT = 22;      // float bits >> 22 = exponent + 1 mantissa bit (half octaves)
 
+// Default deferral cut: in a superstep whose frontier has >= m/4 edges only
+// the closest distance buckets up to DEFER_PCT% of its edges are expanded.
+// Re-swept on the final loop (RMAT s24 / s22, ms): 3% 3.82 / 1.38, 5% 3.85 /
+// 1.36, 10% 3.92 / 1.42, 15% 3.99, 20% 4.50, 30% 4.72 (tools/variants.py).
+constexpr uint32_t DEFER_PCT = 5;
+
 template <class D>
 __device__ __forceinline__ uint32_t obucket(const D* dist, uint32_t v, uint32_t base) {
   const uint32_t k = fkey(dist[v]) >> OB_SHIFT;

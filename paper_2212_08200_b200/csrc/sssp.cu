@@ -115,16 +115,16 @@ struct Runner {
   bool rec_fast() const { return sizeof(D) == 8 && variant != 10; }
 
   // Soft near-far inside BSP (k_fscan_o): in a superstep whose frontier has
-  // >= m/4 edges, only the closest distance buckets up to 10% of those edges
-  // are expanded; the rest stay pending in the bitmap.  RMAT s24: work 3.0 ->
-  // 1.45 relaxations per reached edge, 5.77 -> 4.11 ms (sweep over 1-95% and
+  // >= m/4 edges, only the closest distance buckets up to DEFER_PCT (5)% of
+  // those edges are expanded; the rest stay pending in the bitmap.  RMAT s24:
+  // work 3.0 -> 1.27 relaxations per reached edge (sweeps over 1-95% and
   // m/2..m/64 thresholds: tools/variants.py).  Variant 99 = off.
   uint32_t defer_pct() const {
-    if (variant == 0) return 10;
+    if (variant == 0) return DEFER_PCT;
     switch (variant) {
-      case 63: return 10;  // deferral on the caller's ids (no relabel): the peer path's loop
-      case 122: return 10;  // the default loop without the automatic near-far choice
-      case 65: case 66: case 67: case 68: case 69: return 10;  // f64 advance shapes
+      case 63: return DEFER_PCT;  // deferral on the caller's ids (no relabel): the peer path's loop
+      case 122: return DEFER_PCT;  // the default loop without the automatic near-far choice
+      case 65: case 66: case 67: case 68: case 69: return DEFER_PCT;  // f64 advance shapes
       case 99: return 100;
       case 100: return 50;
       case 101: return 70;
