@@ -278,7 +278,10 @@ struct Runner {
     }
     // measured at RMAT s24 (profiles/r01_variants_s24.txt): 2 edges per lane,
     // 8 x 256-thread CTAs per SM, strided 256-edge tiles, PTX red.*
-    range_launch<2, 8, 256, 1>(st);
+    // tile size by graph size (final loop, ms): 128 / 256 / 512-edge tiles
+    // at s24 3.91 / 3.86 / 3.94, at s22 1.27 / 1.31 / 1.35
+    if (g->m <= (1ull << 27)) range_launch<2, 8, 128, 1>(st);
+    else range_launch<2, 8, 256, 1>(st);
   }
 
   // The persistent single-launch loop (bsp.cuh) for 32-bit distances.
