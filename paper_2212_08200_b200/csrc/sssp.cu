@@ -276,12 +276,14 @@ struct Runner {
       else range_launch<2, 6, 256, 1>(st);
       return;
     }
-    // measured at RMAT s24 (profiles/r01_variants_s24.txt): 2 edges per lane,
-    // 8 x 256-thread CTAs per SM, strided 256-edge tiles, PTX red.*
+    // measured at RMAT s24 (profiles/r01_variants_s24.txt): 8 x 256-thread
+    // CTAs per SM, strided edge tiles, PTX red.*
     // tile size by graph size (final loop, ms): 128 / 256 / 512-edge tiles
     // at s24 3.91 / 3.86 / 3.94, at s22 1.27 / 1.31 / 1.35
-    if (g->m <= (1ull << 27)) range_launch<2, 8, 128, 1>(st);
-    else range_launch<2, 8, 256, 1>(st);
+    // final-loop re-sweep (ms, s24 / s22): 1 edge per lane 3.81 / 1.24 vs 2
+    // edges 3.85 / 1.27; 4 edges 4.14; 6 CTAs/SM 3.82-3.87; <4,4> 4.25
+    if (g->m <= (1ull << 27)) range_launch<1, 8, 128, 1>(st);
+    else range_launch<1, 8, 256, 1>(st);
   }
 
   // The persistent single-launch loop (bsp.cuh) for 32-bit distances.
