@@ -603,7 +603,7 @@ struct PeerRun {
       if (p->nparts == 1 && (exp_bits() & 1))  // experiment: plain advance (all owners local)
         k_push_range<W, 2, 8, 256, 1, false><<<c->num_sms * 8, 256, 0, st>>>(a);
       else
-        k_push_range<W, 2, 8, 256, 1, true><<<c->num_sms * 8, 256, 0, st>>>(a);
+        k_push_range<W, 1, 8, 256, 1, true><<<c->num_sms * 8, 256, 0, st>>>(a);
     }
     ++p->launches;
   }
