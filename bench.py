@@ -373,7 +373,7 @@ def secondary_configs(gb, ctx, args, g_main=None):
                      f"(corner), near-far filter delta={args.grid_delta}, one persistent launch",
            "gteps": st.m_reach / (ms * 1e-3) / 1e9, "ms": ms, "phases": st.supersteps,
            "work_inflation": st.relaxations / st.m_reach}
-    bms, bst = timed(g, 1, variant=122)  # the BSP loop (no automatic near-far choice)
+    bms, bst = timed(g, 1, loop="bsp")  # the BSP loop (no automatic near-far choice)
     rec["bsp"] = {"ms": bms, "supersteps": bst.supersteps,
                   "work_inflation": bst.relaxations / bst.m_reach,
                   "gteps": bst.m_reach / (bms * 1e-3) / 1e9}

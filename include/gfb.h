@@ -174,9 +174,29 @@ typedef struct gfb_sssp_opts {
                             (max out-degree <= 8, n >= 2^16), else the BSP
                             loop.  Any arithmetic.  Same distances. */
   int32_t compute_pred;  /* 1: fill pred (tight-edge tree) */
-  int32_t reserved[7];   /* reserved[0]: kernel-shape experiment id (0 = the
-                            measured default; see sssp.cu Runner::variant) */
+  /* Tuning (0 = the measured default everywhere; none changes the result):  */
+  int32_t loop;          /* GFB_LOOP_AUTO | GFB_LOOP_BSP (never pick the
+                            near-far loop automatically) */
+  int32_t relabel;       /* GFB_RELABEL_AUTO (in-degree relabelled CSR for
+                            skewed graphs, from the 2nd call on the same
+                            contents) | GFB_RELABEL_ON | GFB_RELABEL_OFF */
+  int32_t defer_pct;     /* BSP far-bucket deferral: in a superstep whose
+                            frontier holds >= m/4 edges only the closest
+                            distance buckets up to this % of those edges are
+                            expanded.  0 = default (5; 10 on the partitioned
+                            path), 100 = off */
+  int32_t advance_tile;  /* push advance edge tile for 4-byte distances:
+                            0 = by size (128 for m <= 2^27, else 256), or
+                            128 / 256 */
+  int32_t trace;         /* 1: per-superstep lines on stderr (host loop) */
+  int32_t reserved[2];
 } gfb_sssp_opts;
+
+#define GFB_LOOP_AUTO 0
+#define GFB_LOOP_BSP 1
+#define GFB_RELABEL_AUTO 0
+#define GFB_RELABEL_ON 1
+#define GFB_RELABEL_OFF 2
 
 void gfb_sssp_opts_default(gfb_sssp_opts* o);
 

@@ -139,87 +139,95 @@ struct DeviceSsspConfig {
   }
 };
 
-/// Uploaded copy of an immutable graflow::Graph (graph.hpp:42-44 promises
-/// immutability, so one upload serves every call on that graph).
+/// Device copy of a graflow::Graph.  Construct one and pass it to the
+/// DeviceGraph overloads below to run many calls on one upload (the fast
+/// path: the caller owns the handle and decides when the contents are
+/// current, cf. graph.hpp:262-264 "immutable").  refill() re-copies new
+/// contents of the same shape without reallocating.
 class DeviceGraph {
  public:
-  DeviceGraph(const Graph& g, const DevicePolicy& p, bool with_transpose) {
+  DeviceGraph(const Graph& g, const DevicePolicy& p, bool with_transpose)
+      : n_(g.num_vertices()), m_(g.num_edges()), device_(p.device), arith_(p.arithmetic),
+        csc_(with_transpose) {
     gfb_ctx* c = device_detail::context(p.device);
-    const auto& ro = g.row_offsets();
-    const auto& col = g.column_indices();
-    const auto& val = g.values();
     gfb_graph* h = nullptr;
-    device_detail::check(gfb_graph_upload(c, g.num_vertices(), g.num_edges(), ro.data(),
-                                          col.data(), val.data(), GFB_W_F64, p.arithmetic,
+    device_detail::check(gfb_graph_upload(c, g.num_vertices(), g.num_edges(),
+                                          g.row_offsets().data(), g.column_indices().data(),
+                                          g.values().data(), GFB_W_F64, p.arithmetic,
                                           with_transpose ? 1 : 0, &h));
     h_.reset(h);
     ctx_ = c;
   }
+  DeviceGraph(const Graph& g, const DevicePolicy& p) : DeviceGraph(g, p, g.has_transpose()) {}
   gfb_graph* handle() const { return h_.get(); }
   gfb_ctx* ctx() const { return ctx_; }
+  std::size_t num_vertices() const { return n_; }
+  bool has_transpose() const { return csc_; }
+  bool fits(const Graph& g, const DevicePolicy& p, bool with_transpose) const {
+    return n_ == g.num_vertices() && m_ == g.num_edges() && device_ == p.device &&
+           arith_ == p.arithmetic && csc_ == with_transpose;
+  }
+  void refill(const Graph& g) {
+    device_detail::check(gfb_graph_refill(h_.get(), g.row_offsets().data(),
+                                          g.column_indices().data(), g.values().data(),
+                                          GFB_W_F64));
+  }
 
-  /// Cached upload keyed by the graph object, its buffers, shape, a sampled
-  /// content fingerprint, the arithmetic and the transpose flag.  A Graph is
-  /// immutable (graph.hpp:42-44); the fingerprint guards against a new Graph
-  /// reusing a destroyed one's address.
+  /// The Graph-taking overloads' upload: the graph's CURRENT contents, copied
+  /// on every call (gfb_graph_refill into a cached allocation of the same
+  /// shape, so nothing is reallocated).  No address or sampled-fingerprint
+  /// reuse: a different Graph at the same address, or one differing in a
+  /// single weight, can never see a stale copy.  At most kCacheSlots
+  /// allocations per host thread (least recently used evicted).  Keep a
+  /// DeviceGraph yourself to skip the copy.
   static DeviceGraph& of(const Graph& g, const DevicePolicy& p, bool with_transpose) {
-    using Key = std::tuple<const Graph*, const void*, const void*, std::size_t, std::size_t,
-                           std::uint64_t, int, int, bool>;
-    thread_local std::map<Key, std::unique_ptr<DeviceGraph>> cache;
-    Key k{&g, g.row_offsets().data(), g.column_indices().data(), g.num_vertices(),
-          g.num_edges(), fingerprint(g), p.device, p.arithmetic, with_transpose};
-    auto& slot = cache[k];
-    if (!slot) slot = std::make_unique<DeviceGraph>(g, p, with_transpose);
-    return *slot;
-  }
-
-  static std::uint64_t fingerprint(const Graph& g) {
-    std::uint64_t h = 1469598103934665603ull;
-    auto mix = [&h](std::uint64_t x) {
-      h ^= x;
-      h *= 1099511628211ull;
-    };
-    const auto& ro = g.row_offsets();
-    const auto& col = g.column_indices();
-    const auto& val = g.values();
-    std::size_t m = col.size(), step = m / 1024 + 1;
-    for (std::size_t i = 0; i < ro.size(); i += ro.size() / 1024 + 1) mix(ro[i]);
-    for (std::size_t i = 0; i < m; i += step) {
-      std::uint64_t b;
-      std::memcpy(&b, &val[i], 8);
-      mix(col[i]);
-      mix(b);
+    thread_local std::vector<std::unique_ptr<DeviceGraph>> lru;  // front = most recent
+    for (std::size_t i = 0; i < lru.size(); ++i) {
+      if (!lru[i]->fits(g, p, with_transpose)) continue;
+      std::unique_ptr<DeviceGraph> hit = std::move(lru[i]);
+      lru.erase(lru.begin() + (long)i);
+      hit->refill(g);
+      lru.insert(lru.begin(), std::move(hit));
+      return *lru.front();
     }
-    return h;
+    if (lru.size() >= kCacheSlots) lru.pop_back();
+    lru.insert(lru.begin(), std::make_unique<DeviceGraph>(g, p, with_transpose));
+    return *lru.front();
   }
+  static constexpr std::size_t kCacheSlots = 2;
 
  private:
   std::unique_ptr<gfb_graph, device_detail::GraphDeleter> h_;
   gfb_ctx* ctx_ = nullptr;
+  std::size_t n_, m_;
+  int device_;
+  int arith_;
+  bool csc_;
 };
 
-/// The graph partitioned over several devices (gfb_mg_*), cached like
-/// DeviceGraph.
+/// The graph partitioned over several devices (gfb_mg_*).  Like DeviceGraph:
+/// the Graph overloads re-upload the current contents into the per-thread
+/// handle of the same device list (one slot).
 class DeviceMgGraph {
  public:
-  DeviceMgGraph(const Graph& g, const DevicePolicy& p) {
+  explicit DeviceMgGraph(const DevicePolicy& p) : devices_(p.devices), arith_(p.arithmetic) {
     gfb_mg* h = nullptr;
     device_detail::check(gfb_mg_create((int)p.devices.size(), p.devices.data(), &h));
     h_.reset(h);
-    device_detail::check(gfb_mg_graph_upload(h, g.num_vertices(), g.num_edges(),
-                                             g.row_offsets().data(), g.column_indices().data(),
-                                             g.values().data(), GFB_W_F64, p.arithmetic));
   }
+  DeviceMgGraph(const Graph& g, const DevicePolicy& p) : DeviceMgGraph(p) { upload(g); }
   gfb_mg* handle() const { return h_.get(); }
+  void upload(const Graph& g) {
+    device_detail::check(gfb_mg_graph_upload(h_.get(), g.num_vertices(), g.num_edges(),
+                                             g.row_offsets().data(), g.column_indices().data(),
+                                             g.values().data(), GFB_W_F64, arith_));
+  }
 
   static DeviceMgGraph& of(const Graph& g, const DevicePolicy& p) {
-    using Key = std::tuple<const Graph*, const void*, std::size_t, std::size_t, std::uint64_t,
-                           std::vector<int>, int>;
-    thread_local std::map<Key, std::unique_ptr<DeviceMgGraph>> cache;
-    Key k{&g, g.row_offsets().data(), g.num_vertices(), g.num_edges(),
-          DeviceGraph::fingerprint(g), p.devices, p.arithmetic};
-    auto& slot = cache[k];
-    if (!slot) slot = std::make_unique<DeviceMgGraph>(g, p);
+    thread_local std::unique_ptr<DeviceMgGraph> slot;
+    if (!slot || slot->devices_ != p.devices || slot->arith_ != p.arithmetic)
+      slot = std::make_unique<DeviceMgGraph>(p);
+    slot->upload(g);
     return *slot;
   }
 
@@ -228,9 +236,13 @@ class DeviceMgGraph {
     void operator()(gfb_mg* h) const { gfb_mg_destroy(h); }
   };
   std::unique_ptr<gfb_mg, Deleter> h_;
+  std::vector<int> devices_;
+  int arith_;
 };
 
-/// Single-source shortest paths on the device (algorithms.hpp:569-623):
+inline SsspResult sssp(const DeviceGraph& dg, vertex_t source, const DeviceSsspConfig& cfg);
+
+/// Single-source shortest paths on the device (algorithms.hpp:134-188):
 /// same validation order and exception types, same SsspResult layout.
 /// dist is widened from the device arithmetic to double (exact); pred is
 /// the acyclic tight-edge tree (NIL for the source and unreachable).
@@ -253,8 +265,19 @@ inline SsspResult sssp(const Graph& g, vertex_t source, const DeviceSsspConfig& 
     r.relaxations = st.relaxations;
     return r;
   }
-  bool want_csc = g.has_transpose();
-  DeviceGraph& dg = DeviceGraph::of(g, cfg.policy, want_csc);
+  return sssp(DeviceGraph::of(g, cfg.policy, g.has_transpose()), source, cfg);
+}
+
+/// sssp() on a caller-owned upload (no copy per call).
+inline SsspResult sssp(const DeviceGraph& dg, vertex_t source, const DeviceSsspConfig& cfg) {
+  cfg.validate();
+  const std::size_t n = dg.num_vertices();
+  if (source >= n) throw std::out_of_range("sssp: source out of range");
+  const bool want_csc = dg.has_transpose();
+  if (cfg.direction == Direction::pull && !want_csc)
+    throw std::invalid_argument("sssp: pull direction requires a built transpose");
+  if (cfg.policy.devices.size() > 1)
+    throw std::invalid_argument("sssp: a DeviceGraph is single-device (use the Graph overload)");
   gfb_sssp_opts o;
   gfb_sssp_opts_default(&o);
   o.direction = cfg.direction == Direction::pull

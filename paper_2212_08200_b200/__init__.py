@@ -207,8 +207,14 @@ def grid(side, seed=1, transpose=True, ctx=None):
     return Graph(h, ctx)
 
 
+_LOOP = {"auto": 0, "bsp": 1}
+_RELABEL = {"auto": 0, "on": 1, "off": 2}
+
+
 def _opts(direction="auto", pull_alpha=0.25, delta=0.0, device_loop=True, compute_pred=True,
-          variant=0):
+          loop="auto", relabel="auto", defer_pct=0, advance_tile=0, trace=False):
+    """gfb_sssp_opts (include/gfb.h).  The tuning knobs (loop, relabel,
+    defer_pct, advance_tile) never change the result, only the schedule."""
     o = SsspOpts()
     _lib.load().gfb_sssp_opts_default(C.byref(o))
     if direction not in _DIR:
@@ -218,7 +224,13 @@ def _opts(direction="auto", pull_alpha=0.25, delta=0.0, device_loop=True, comput
     o.delta = delta
     o.device_loop = int(device_loop)
     o.compute_pred = int(compute_pred)
-    o.reserved[0] = int(variant)  # experimental kernel shape (sssp.cu Runner::variant)
+    if loop not in _LOOP or relabel not in _RELABEL:
+        raise ValueError("loop must be auto|bsp, relabel auto|on|off")
+    o.loop = _LOOP[loop]
+    o.relabel = _RELABEL[relabel]
+    o.defer_pct = int(defer_pct)
+    o.advance_tile = int(advance_tile)
+    o.trace = int(bool(trace))
     return o
 
 
@@ -266,7 +278,7 @@ def bfs(g, source, policy="device", direction="push", frontier="sparse", workers
         raise ValueError("frontier must be sparse|dense")
     if direction not in _DIR:
         raise ValueError("direction must be push|pull|auto")
-    if source < 0:
+    if source < 0 or source >= g.num_vertices:  # algorithms.hpp:200 (a ctypes u32 would wrap)
         raise IndexError("bfs: source out of range")
     depth = np.empty(g.num_vertices, np.float64) if want_result else None
     st, rl = C.c_uint64(), C.c_uint64()
@@ -279,7 +291,7 @@ def bfs(g, source, policy="device", direction="push", frontier="sparse", workers
 
 def sssp_stats(g, source, direction="auto", want_result=True, **kw):
     """gfb_sssp with the full statistics record (device time, n/m_reach...)."""
-    if source < 0:
+    if source < 0 or source >= g.num_vertices:  # algorithms.hpp:137 (a ctypes u32 would wrap)
         raise IndexError("sssp: source out of range")
     o = _opts(direction=direction, **kw)
     st = SsspStats()

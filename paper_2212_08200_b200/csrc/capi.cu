@@ -171,6 +171,7 @@ int gfb_graph_info(const gfb_graph* g, uint64_t* n, uint64_t* m, int* wtype, int
 int gfb_graph_download(gfb_graph* g, uint32_t* ro, uint32_t* col, void* w) {
   return guard([&] {
     NEED(g);
+    gfb::check_usable(g);
     set_device(g->ctx);
     graph_download(g, ro, col, w);
   });
@@ -253,6 +254,7 @@ int gfb_dist_create(gfb_ctx* ctx, const gfb_graph* g, gfb_dist** out) {
     NEED(ctx);
     NEED(g);
     NEED(out);
+    gfb::check_usable(g);
     set_device(ctx);
     *out = static_cast<gfb_dist*>(dist_create(ctx, g));
   });
@@ -313,6 +315,8 @@ int gfb_advance_push(gfb_ctx* ctx, const gfb_graph* g, gfb_frontier* in, gfb_fro
                      void* state) {
   return guard([&] {
     NEED(ctx);
+    NEED(g);
+    gfb::check_usable(g);
     set_device(ctx);
     advance_push(ctx, g, in, out, op, state);
   });
@@ -322,6 +326,8 @@ int gfb_advance_pull(gfb_ctx* ctx, const gfb_graph* g, gfb_frontier* in, gfb_fro
                      void* state) {
   return guard([&] {
     NEED(ctx);
+    NEED(g);
+    gfb::check_usable(g);
     set_device(ctx);
     advance_pull(ctx, g, in, out, op, state);
   });
@@ -445,6 +451,7 @@ int gfb_part_pred(gfb_part* p, const void* gdist_dev, const uint32_t* res_dev, u
 int gfb_sssp_read(gfb_graph* g, double* dist, void* dist_native, uint32_t* pred) {
   return guard([&] {
     NEED(g);
+    gfb::check_usable(g);
     set_device(g->ctx);
     sssp_read(g, dist, dist_native, pred);
   });
@@ -456,6 +463,7 @@ int gfb_sssp_read(gfb_graph* g, double* dist, void* dist_native, uint32_t* pred)
 int gfb_debug_relabel(gfb_graph* g, uint32_t* ro, uint32_t* adj_pairs, uint32_t* perm) {
   return guard([&] {
     NEED(g);
+    gfb::check_usable(g);
     if (g->rec_bytes() != 8) gfb::fail(GFB_EINVAL, "relabel view: 4-byte weights only");
     set_device(g->ctx);
     gfb::ensure_relabel(g);
@@ -606,6 +614,7 @@ int gfb_bfs(gfb_ctx* ctx, gfb_graph* g, uint32_t source, int direction, double* 
   return guard([&] {
     NEED(ctx);
     NEED(g);
+    gfb::check_usable(g);
     set_device(ctx);
     gfb::bfs_run(ctx, g, source, direction, depth, supersteps, relaxations);
   });

@@ -331,7 +331,7 @@ static __global__ void k_fscan_o(unsigned long long* btot, unsigned long long* b
                                  cudaGraphConditionalHandle loop_handle,
                                  cudaGraphConditionalHandle mode_handle, int set_loop,
                                  int set_mode, uint32_t defer_pct = 100,
-                                 uint32_t defer_min = 0, uint32_t defer_floor = 0) {
+                                 uint32_t defer_min = 0) {
   const int lane = threadIdx.x;
   static_assert(OB_N <= 32, "one warp scans the bucket totals");
   const unsigned long long x = lane < OB_N ? btot[lane] : 0ull;
@@ -345,9 +345,8 @@ static __global__ void k_fscan_o(unsigned long long* btot, unsigned long long* b
   const uint32_t T_all = (uint32_t)all;
   uint32_t cut = OB_N - 1;
   if (defer_pct < 100 && T_all >= defer_min) {
-    // first bucket whose inclusive edge count reaches defer_pct% of all (and
-    // at least defer_floor edges: enough work to fill the GPU)
-    const uint64_t need = max((uint64_t)T_all * defer_pct, (uint64_t)defer_floor * 100);
+    // first bucket whose inclusive edge count reaches defer_pct% of all
+    const uint64_t need = (uint64_t)T_all * defer_pct;
     const bool reach = (uint64_t)(uint32_t)incl * 100 >= need;
     const unsigned bal = __ballot_sync(0xffffffffu, reach && lane < OB_N);
     if (bal) cut = __ffs(bal) - 1;

@@ -73,6 +73,25 @@ Ctl Ctx::read_ctl(const Ctl* dctl) {
 }
 
 Graph::~Graph() = default;
+
+void invalidate_loop_graphs(Graph* g) {
+  Workspace* ws = g->ws.get();
+  if (!ws) return;
+  if (ws->loop_exec) cudaGraphExecDestroy(ws->loop_exec);
+  if (ws->loop_graph) cudaGraphDestroy(ws->loop_graph);
+  if (ws->bfs_exec) cudaGraphExecDestroy(ws->bfs_exec);
+  if (ws->bfs_graph) cudaGraphDestroy(ws->bfs_graph);
+  ws->loop_exec = nullptr;
+  ws->loop_graph = nullptr;
+  ws->bfs_exec = nullptr;
+  ws->bfs_graph = nullptr;
+  ws->bfs_key = -1;
+}
+
+void check_usable(const Graph* g) {
+  if (g->poisoned)
+    fail(GFB_ELOGIC, "graph: contents invalid after a failed refill (refill it again)");
+}
 Workspace::~Workspace() {
   if (loop_exec) cudaGraphExecDestroy(loop_exec);
   if (loop_graph) cudaGraphDestroy(loop_graph);
@@ -189,7 +208,13 @@ static constexpr uint64_t UPLOAD_CHUNK = 1ull << 25;  // edges per chunk
 
 static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const void* w,
                        int htype) {
-  g->nz_valid = false;
+  // everything derived from the old contents goes first: the transpose, the
+  // relabelled copy, cached statistics and the loop graphs that point at them
+  invalidate_loop_graphs(g);
+  g->has_csc = false;
+  g->ceid.release();
+  if (g->ws) g->ws->has_result = false;
+  g->poisoned = true;  // cleared once the new contents validated
   g->rl_valid = false;
   g->max_outdeg = -1;
   g->mean_w = -1;
@@ -255,11 +280,9 @@ static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const 
   if (hf[1] != ~0ull)
     fail(GFB_EINVAL,
          "build_csr: edge " + std::to_string(hf[1]) + " has negative or non-finite weight");
-  if (g->ws) g->ws->has_result = false;  // same shape: keep the workspace
+  g->poisoned = false;  // same shape: keep the workspace
 }
 
-// Nonzero-out-degree bitmap (one bit per vertex, the layout of the frontier
-// bitmaps) for the persistent loop's frontier count.
 static __global__ void k_max_outdeg(const uint32_t* __restrict__ ro, uint32_t n, uint32_t* out) {
   uint32_t mx = 0;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
@@ -319,29 +342,6 @@ double mean_weight(Graph* g) {
   c->sync();
   g->mean_w = g->m ? h / (double)g->m : 0.0;
   return g->mean_w;
-}
-
-static __global__ void k_nz(const uint32_t* __restrict__ ro, uint32_t n, uint32_t* nz) {
-  const uint32_t nwords = (n + 31) / 32;
-  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
-       w += gridDim.x * blockDim.x) {
-    uint32_t bits = 0;
-    for (int b = 0; b < 32; ++b) {
-      const uint32_t v = w * 32 + b;
-      if (v < n && ro[v + 1] > ro[v]) bits |= 1u << b;
-    }
-    nz[w] = bits;
-  }
-}
-
-void ensure_nz(Graph* g) {
-  if (g->nz_valid) return;
-  const uint64_t nwords = (g->n + 31) / 32;
-  if (g->nz.bytes < nwords * 4) g->nz.alloc(nwords * 4, g->ctx->stream);
-  k_nz<<<stride_grid(g->ctx), 256, 0, g->ctx->stream>>>(g->ro.as<uint32_t>(), (uint32_t)g->n,
-                                                        g->nz.as<uint32_t>());
-  GFB_CUDA(cudaGetLastError());
-  g->nz_valid = true;
 }
 
 // ---------------------------------------------------------------------------
@@ -461,6 +461,7 @@ void ensure_relabel(Graph* g) {
   ids.alloc((size_t)n * 4, s);
   deg2.alloc((size_t)(n + 1) * 4, s);
   if (g->rl_perm.bytes < (size_t)n * 4) {
+    invalidate_loop_graphs(g);
     g->rl_perm.alloc((size_t)n * 4, s);
     g->rl_iperm.alloc((size_t)n * 4, s);
     g->rl_ro.alloc((size_t)(n + 1) * 4, s);
@@ -570,9 +571,7 @@ Graph* graph_upload(Ctx* c, uint64_t n, uint64_t m, const uint32_t* ro, const ui
 }
 
 void graph_refill(Graph* g, const uint32_t* ro, const uint32_t* col, const void* w, int htype) {
-  fill_graph(g, ro, col, w, htype);
-  g->has_csc = false;  // stale: rebuilt on first use
-  g->ceid.release();
+  fill_graph(g, ro, col, w, htype);  // the transpose is rebuilt on first use
 }
 
 // The transpose is built lazily: a push-only or AUTO (alpha <= 1) sssp and
@@ -704,6 +703,7 @@ void ensure_ceid(Graph* g) {
   ensure_csc(g);
   if (!g->has_csc || g->ceid.p) return;
   Ctx* c = g->ctx;
+  invalidate_loop_graphs(g);
   g->ceid.alloc(g->m * 4, c->stream);
   if (g->m) {
     if (g->wtype == GFB_W_F32)
@@ -720,6 +720,7 @@ void ensure_ceid(Graph* g) {
 }
 
 void build_csc(Graph* g) {
+  invalidate_loop_graphs(g);
   Ctx* c = g->ctx;
   cudaStream_t s = c->stream;
   const uint64_t n = g->n, m = g->m;
@@ -816,6 +817,7 @@ __global__ void k_fill_ones(uint32_t* bm, uint64_t nwords, uint64_t n) {
 }
 
 void build_pull_plan(Graph* g) {
+  invalidate_loop_graphs(g);
   Ctx* c = g->ctx;
   cudaStream_t s = c->stream;
   const uint64_t n = g->n, m = g->m;
@@ -855,16 +857,11 @@ void build_pull_plan(Graph* g) {
 // Device-side synthetic graphs in build_csr layout.
 // ---------------------------------------------------------------------------
 __global__ void k_rmat_gen(int scale, uint64_t seed, int wkind, uint64_t m,
-                           unsigned long long* key, uint32_t* wbits, int permute) {
+                           unsigned long long* key, uint32_t* wbits) {
   uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  const uint32_t mask = (uint32_t)((1ull << scale) - 1);
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
     uint32_t s, d, w;
     rmat_edge(scale, seed, wkind, i, &s, &d, &w);
-    if (permute) {  // experiment only (GFB_RMAT_PERMUTE): bijective label scramble
-      s = (s * 2654435761u + 12345u) & mask;
-      d = (d * 2654435761u + 12345u) & mask;
-    }
     key[i] = ((unsigned long long)s << 32) | d;
     wbits[i] = w;
   }
@@ -899,10 +896,8 @@ Graph* graph_generate_rmat(Ctx* c, int scale, int ef, uint64_t seed, int wtype, 
     key2.alloc(m * 8, s);
     wb.alloc(m * 4, s);
     wb2.alloc(m * 4, s);
-    const char* perm = getenv("GFB_RMAT_PERMUTE");
     k_rmat_gen<<<stride_grid(c), 256, 0, s>>>(scale, seed, wtype == GFB_W_U32 ? 0 : 1, m,
-                                              key.as<unsigned long long>(), wb.as<uint32_t>(),
-                                              perm && perm[0] == '1');
+                                              key.as<unsigned long long>(), wb.as<uint32_t>());
     GFB_CUDA(cudaGetLastError());
     // (src, dst, w) order: stable sort by w, then stable sort by (src, dst).
     size_t tb1 = 0, tb2 = 0;

@@ -1,17 +1,20 @@
 // hot.cuh -- the advance kernels of gfb_sssp (neighbors_expand /
-// neighbors_expand_pull with the SSSP relax, operators.hpp:255-334,
-// algorithms.hpp:586-593).
+// neighbors_expand_pull with the SSSP relax, operators.hpp:35-68 / :76-114,
+// algorithms.hpp:150-158).
 //
-//   k_push_range  default push advance for 32-bit distances: warps claim
-//                 256-edge tiles of the plan round-robin (merge-path style
-//                 segment search by shuffles over a 32-segment window), 2
-//                 edges per lane, 64 warps per SM; record stream -> distance
-//                 gather (test before atomic) -> fire-and-forget red.* of the
-//                 distance, the packed (dist, pred) key and the frontier bit.
-//                 REC (f64): returning 64-bit mins and {u, edge} records.
-//   k_push_warp   the previous warp-tile kernel with atomicMin-with-return and
-//                 {u, edge} records (variant 10; the host-driven partitioned
-//                 advance of mg.cu).
+//   k_push_range  push advance: warps claim TILE-edge tiles of the plan
+//                 round-robin (merge-path style segment search by shuffles
+//                 over a 32-segment window), 64 warps per SM; record stream
+//                 -> distance gather (test before atomic) -> fire-and-forget
+//                 red.* of the distance, the packed (dist, pred) key and the
+//                 frontier bit.  Shapes (sssp.cu Runner::push): 32-bit
+//                 distances one edge per lane, 128-edge tiles for m <= 2^27,
+//                 256 above (opts.advance_tile overrides); REC (f64):
+//                 returning 64-bit mins and {u, edge} records, two edges per
+//                 lane, 6 CTAs per SM; PEER (peer.cu): one edge per lane,
+//                 256-edge tiles, owner-addressed reductions.
+//   k_push_warp   warp-tile kernel with atomicMin-with-return; only the
+//                 host-driven partitioned advance of mg.cu (PART) uses it.
 //   k_pull_relax  pull over the CSC plan (CTA tiles in shared memory).
 // Each step of the design is a measurement: profiles/r01_variants_s24.txt.
 #pragma once

@@ -62,8 +62,9 @@ struct Graph {
   bool has_csc = false;     // ... and it is built for the current contents (ensure_csc)
   DBuf ro, adj, co, cadj, ceid;  // ceid built lazily (ensure_ceid) for the record op
   DBuf stage;                     // upload staging, kept for refills
-  DBuf nz;                        // bit v: out-degree(v) > 0 (ensure_nz, bsp.cuh)
-  bool nz_valid = false;
+  // A refill whose validation failed has already overwritten ro / adj: the
+  // handle is unusable (every entry point rejects it) until a good refill.
+  bool poisoned = false;
   // In-degree-ordered copy of the CSR used inside the SSSP loop (ensure_relabel):
   // new id i = rank of vertex iperm[i] by descending in-degree, so the hot
   // destinations share distance cache lines.  4-byte weights only.
@@ -111,26 +112,23 @@ struct Workspace {
   DBuf dist, predrec, pred, res, cand;
   DBuf bm_next, bm_cur, repair_bm;
   DBuf pv, pstart, poff, ptseg;
-  DBuf status;
   DBuf ctl;
-  DBuf agg;        // per-tile (count, edges) of the frontier compaction
-  DBuf oagg, obuck; // distance-ordered compaction: per (tile, bucket) cells, bucket totals/cursors
+  DBuf agg;        // per-tile (count, edges) of bfs.cu's frontier compaction
+  DBuf oagg, obuck; // distance-ordered filter: (tile, bucket) cells, bucket totals / cursors
   DBuf src_dev;    // the source vertex (read by k_init)
-  DBuf bar;        // grid barrier of the persistent loop (bsp.cuh)
-  DBuf bsp_agg, bsp_flag, bsp_tot;  // its per-CTA frontier aggregates / totals
   DBuf dist_int, pkey_int;          // loop state in relabelled ids (ensure_relabel)
   DBuf nf_q, nf_bm, nf_cnt;         // near-far queues / bitmaps / counters (nearfar.cuh)
   uint32_t ftiles = 0;
-  // device loop: one instantiated CUDA graph per (direction, alpha, variant)
+  // device loop: one instantiated CUDA graph for the last (direction, alpha,
+  // relabel, deferral, tile) key.  It holds raw pointers into the graph's and
+  // this workspace's buffers: invalidate_loop_graphs() on every reallocation.
   cudaGraphExec_t loop_exec = nullptr;
   cudaGraph_t loop_graph = nullptr;
-  int loop_key[4] = {-1, -1, -1, -1};
+  int loop_key[5] = {-1, -1, -1, -1, -1};
   cudaGraphExec_t bfs_exec = nullptr;  // bfs.cu device loop
   cudaGraph_t bfs_graph = nullptr;
   int bfs_key = -1;
   Ctl* ctl_host = nullptr;  // pinned
-  uint32_t compact_tiles = 0;
-  uint32_t status_len = 0;
   int wtype = -1;
   bool has_result = false;
   uint32_t source = 0;
@@ -183,7 +181,10 @@ void build_csc(Graph* g);
 void ensure_csc(Graph* g);
 void ensure_ceid(Graph* g);
 void build_pull_plan(Graph* g);
-void ensure_nz(Graph* g);
+// destroy the cached device-loop graphs of g (their pointers went stale)
+void invalidate_loop_graphs(Graph* g);
+// GFB_ELOGIC if a failed refill left g's contents invalid
+void check_usable(const Graph* g);
 void ensure_relabel(Graph* g);
 uint32_t max_out_degree(Graph* g);
 double mean_weight(Graph* g);

@@ -928,8 +928,8 @@ k_pred_csc_block(const uint32_t* __restrict__ co, const EdgeRec<W>* __restrict__
     const uint32_t lo = co[v], hi = co[v + 1];
     if (threadIdx.x == 0) s_slot = NIL;
     __syncthreads();
-    for (uint32_t base = lo; base < hi; base += blockDim.x) {
-      const uint32_t slot = base + threadIdx.x;
+    for (uint32_t chunk = lo; chunk < hi; chunk += blockDim.x) {
+      const uint32_t slot = chunk + threadIdx.x;
       if (slot < hi) {
         const EdgeRec<W> rec = cadj[slot];
         const D du = dist[rec.v];

@@ -563,11 +563,6 @@ struct PeerRun {
     ++p->launches;
   }
 
-  static int exp_bits() {
-    const char* e = getenv("GFB_PEER_EXP");
-    return e ? atoi(e) : 0;
-  }
-
   void compact(cudaStream_t st, uint32_t defer_pct, cudaGraphConditionalHandle hl = {},
                bool set_loop = false) {
     Graph* g = p->g.get();
@@ -580,7 +575,7 @@ struct PeerRun {
                                                   ctl(), p->oagg.as<unsigned long long>(), bt,
                                                   tflag, p->dexp.as<uint32_t>());
     k_fscan_o<<<1, 32, 0, st>>>(bt, bt + OB_N, plan(), ctl(), (uint32_t)g->m, 1.0f, 0, 0, hl,
-                                none, set_loop ? 1 : 0, 0, defer_pct, (uint32_t)(g->m >> 2), 0u);
+                                none, set_loop ? 1 : 0, 0, defer_pct, (uint32_t)(g->m >> 2));
     k_fwrite_o<D, true><<<tiles, F_WARPS * 32, 0, st>>>(g->ro.as<uint32_t>(), bm(),
                                                   p->bm_cur.as<uint32_t>(), p->nwords, dist(),
                                                   ctl(), p->oagg.as<unsigned long long>(),
@@ -600,10 +595,7 @@ struct PeerRun {
     a.op = GFB_OP_RELAX_MIN;
     a.peers = p->tab_dev.as<PeerTab>();
     if constexpr (sizeof(D) == 4) {
-      if (p->nparts == 1 && (exp_bits() & 1))  // experiment: plain advance (all owners local)
-        k_push_range<W, 2, 8, 256, 1, false><<<c->num_sms * 8, 256, 0, st>>>(a);
-      else
-        k_push_range<W, 1, 8, 256, 1, true><<<c->num_sms * 8, 256, 0, st>>>(a);
+      k_push_range<W, 1, 8, 256, 1, true><<<c->num_sms * 8, 256, 0, st>>>(a);
     }
     ++p->launches;
   }
@@ -653,15 +645,10 @@ struct PeerRun {
     GFB_CUDA(cudaStreamEndCapture(s, &tmp));
     cudaStream_t b = c->aux[0];
     GFB_CUDA(cudaStreamBeginCaptureToGraph(b, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    if (p->nparts == 1 && (exp_bits() & 2)) {  // experiment: no barriers (one rank)
-      push(b);
-      compact(b, defer_pct, hloop, true);
-    } else {
-      push(b);
-      xbar(b, XB_FMIN);
-      compact(b, defer_pct);
-      xbar(b, XB_LOOP, hloop, true);
-    }
+    push(b);
+    xbar(b, XB_FMIN);
+    compact(b, defer_pct);
+    xbar(b, XB_LOOP, hloop, true);
     GFB_CUDA(cudaStreamEndCapture(b, &tmp));
     GFB_CUDA(cudaGraphInstantiate(&p->exec, G, 0));
     p->graph = G;
@@ -682,7 +669,8 @@ struct PeerRun {
     // 10% (not the single-GPU loop's 5%): every extra superstep costs two
     // cross-rank barriers here -- s24, one partition: 5.52-5.60 ms at 10% vs
     // 5.79 at 5%; equal at four partitions sharing one GPU
-    defer = o->reserved[0] == 99 ? 100u : 10u;
+    if (o->defer_pct < 0 || o->defer_pct > 100) fail(GFB_EINVAL, "sssp: defer_pct must be 0..100");
+    defer = o->defer_pct ? (uint32_t)o->defer_pct : 10u;
     src_local = (source >= p->lo && source < p->lo + p->n) ? source - p->lo : NIL;
     if (!p->exec || p->graph_key != (int)defer) {
       GFB_CUDA(cudaStreamSynchronize(s));

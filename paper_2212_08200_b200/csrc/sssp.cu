@@ -1,6 +1,18 @@
-// sssp.cu -- the device SSSP driver: sssp() of algorithms.hpp:569-623 as
-// init -> { advance (push | pull) -> compact } until the frontier is empty
+// sssp.cu -- the device SSSP driver: sssp() of algorithms.hpp:134-188 as
+// init -> { advance (push | pull) -> filter } until the frontier is empty
 // -> predecessor pass, all on one CUDA stream.
+//
+//   init      algorithms.hpp:141-148 (k_init)
+//   advance   neighbors_expand / neighbors_expand_pull with the relax lambda
+//             (operators.hpp:35-68 / :76-114, algorithms.hpp:150-158):
+//             k_push_range / k_pull_relax (hot.cuh)
+//   filter    frontier dedup + distance-ordered plan + far-bucket deferral
+//             (frontier.hpp:147-165, operators.hpp:163-200): k_fcount_o,
+//             k_fscan_o, k_fwrite_o (frontier.cuh)
+//   loop      while (f.size() != 0) (algorithms.hpp:167): a CUDA graph with a
+//             conditional WHILE node whose condition k_fscan_o sets
+//   preds     repair_predecessors (algorithms.hpp:77-93): k_pred_* (kernels.cuh)
+// High-diameter meshes take the near-far loop instead (nearfar.cuh).
 #include <cub/cub.cuh>
 
 #include <cmath>
@@ -10,11 +22,10 @@
 #include <type_traits>
 #include <vector>
 
-#include "bsp.cuh"
-#include "nearfar.cuh"
 #include "frontier.cuh"
 #include "hot.cuh"
 #include "impl.hpp"
+#include "nearfar.cuh"
 
 namespace gfb {
 
@@ -41,55 +52,15 @@ Workspace* ensure_ws(Graph* g) {
   ws->poff.alloc((n + 1) * 4, s);
   ws->ptseg.alloc((m / PLAN_GRAIN + 3) * 4, s);
   ws->ftiles = (uint32_t)std::max<uint64_t>((nwords + F_WORDS - 1) / F_WORDS, 1);
-  ws->agg.alloc((size_t)ws->ftiles * 8, s);
-  ws->oagg.alloc((size_t)ws->ftiles * (OB_N * 8 + 4), s);  // cells + per-tile nonempty flags
-  ws->obuck.alloc(2 * OB_N * 8, s);
+  ws->agg.alloc((size_t)ws->ftiles * 8, s);  // bfs.cu's plain compaction
+  ws->oagg.alloc((size_t)ws->ftiles * (OB_N * 8 + 4), s);  // (tile, bucket) cells + tile flags
+  ws->obuck.alloc(2 * OB_N * 8, s);                          // bucket totals | cursors
   GFB_CUDA(cudaMemsetAsync(ws->obuck.p, 0, 2 * OB_N * 8, s));
   ws->src_dev.alloc(16, s);
-  ws->compact_tiles = (uint32_t)((nwords + C_WORDS - 1) / C_WORDS);
-  if (ws->compact_tiles == 0) ws->compact_tiles = 1;
-  ws->status_len = ws->compact_tiles + 1;
-  ws->status.alloc((size_t)ws->status_len * 8, s);
   ws->ctl.alloc(sizeof(Ctl), s);
-  ws->bar.alloc(BAR_WORDS * 4, s);
-  GFB_CUDA(cudaMemsetAsync(ws->bar.p, 0, BAR_WORDS * 4, s));
-  ws->bsp_tot.alloc(16, s);
   GFB_CUDA(cudaMallocHost(&ws->ctl_host, sizeof(Ctl)));
   g->ws = std::move(ws);
   return g->ws.get();
-}
-
-// ---- experiment (variant 42/43): reorder the plan by source distance ----
-template <class D>
-__global__ void k_plan_keys(const uint32_t* v, const D* dist, uint32_t* keys, uint32_t* idx,
-                            uint32_t K, int desc) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) {
-    uint32_t b = *reinterpret_cast<const uint32_t*>(dist + v[i]);
-    keys[i] = desc ? ~b : b;
-    idx[i] = i;
-  }
-}
-static __global__ void k_plan_permute(const uint32_t* idx, const uint32_t* v, const uint32_t* st,
-                                      const uint32_t* off, uint32_t* v2, uint32_t* s2,
-                                      uint32_t* deg, uint32_t K) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= K; i += gridDim.x * blockDim.x) {
-    if (i == K) {
-      deg[K] = 0;
-      continue;
-    }
-    const uint32_t j = idx[i];
-    v2[i] = v[j];
-    s2[i] = st[j];
-    deg[i] = off[j + 1] - off[j];
-  }
-}
-static __global__ void k_plan_tiles(Plan p, const uint32_t* deg, uint32_t K, uint32_t T) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x)
-    tile_map_entries(p, i, p.off[i], deg[i]);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    uint32_t sb = (T + PLAN_GRAIN - 1) / PLAN_GRAIN;
-    if (sb < p.tseg_cap) p.tseg[sb] = K;
-  }
 }
 
 constexpr uint32_t PRED_KEY_ROUNDS = 4;
@@ -102,54 +73,22 @@ struct Runner {
   Workspace* ws;
   cudaStream_t s;
   uint32_t n, nwords;
+  const gfb_sssp_opts* o;
   uint64_t kernels = 0;
-  int variant = 0;  // experimental kernel shape (opts.reserved[0])
   bool rl = false;  // loop runs on the in-degree-relabelled CSR (ensure_relabel)
 
-  // distance-ordered plan (frontier.cuh k_fcount_o / k_fwrite_o); variants
-  // 60/61 keep the ascending-id plan for comparison, 62 = ordered plan on the
-  // caller's ids
-  bool ordered() const { return (key_mode() || rec_fast()) && variant != 60 && variant != 61; }
-  // f64 distances on the same ordered / deferred loop, with {u, edge} records
-  // instead of packed keys (k_push_range<REC>); variant 10 keeps the old path
-  bool rec_fast() const { return sizeof(D) == 8 && variant != 10; }
+  // 32-bit distances: packed (dist, pred) keys with fire-and-forget
+  // reductions; f64: {u, edge} records written by returning mins (hot.cuh)
+  static constexpr bool key_mode() { return sizeof(D) == 4; }
 
-  // Soft near-far inside BSP (k_fscan_o): in a superstep whose frontier has
-  // >= m/4 edges, only the closest distance buckets up to DEFER_PCT (5)% of
-  // those edges are expanded; the rest stay pending in the bitmap.  RMAT s24:
-  // work 3.0 -> 1.27 relaxations per reached edge (sweeps over 1-95% and
-  // m/2..m/64 thresholds: tools/variants.py).  Variant 99 = off.
-  uint32_t defer_pct() const {
-    if (variant == 0) return DEFER_PCT;
-    switch (variant) {
-      case 63: return DEFER_PCT;  // deferral on the caller's ids (no relabel): the peer path's loop
-      case 122: return DEFER_PCT;  // the default loop without the automatic near-far choice
-      case 65: case 66: case 67: case 68: case 69: return DEFER_PCT;  // f64 advance shapes
-      case 99: return 100;
-      case 100: return 50;
-      case 101: return 70;
-      case 102: return 85;
-      case 103: return 95;
-      case 104: return 10;
-      case 105: return 20;
-      case 106: return 30;
-      case 107: return 40;
-      case 108: return 1;
-      case 109: return 3;
-      case 110: return 5;
-      case 111: return 15;
-      default: return 100;
-    }
-  }
-
-  uint32_t defer_min() const {
-    const char* e = getenv("GFB_DEFER_SHIFT");  // experiment knob: frontier edges >= m >> shift
-    return (uint32_t)(g->m >> (e ? atoi(e) : 2));
-  }
-  uint32_t defer_floor() const {
-    const char* e = getenv("GFB_DEFER_FLOOR");  // experiment knob: expand >= m >> shift edges
-    return e ? (uint32_t)(g->m >> atoi(e)) : 0u;
-  }
+  // Far-bucket deferral (k_fscan_o): in a superstep whose frontier holds
+  // >= m/4 edges only the closest distance buckets up to defer_pct % of those
+  // edges are expanded; the rest stay pending in the bitmap.  RMAT s24: 3.0 -> 1.27
+  // relaxations per reached edge (sweep 1-95 %, thresholds m/2..m/64:
+  // DESIGN.md §4).
+  uint32_t defer_pct() const { return o->defer_pct ? (uint32_t)o->defer_pct : DEFER_PCT; }
+  uint32_t defer_min() const { return (uint32_t)(g->m >> 2); }
+  bool pullable(int dir) const { return g->has_csc && dir != GFB_DIR_PUSH; }
 
   const uint32_t* lro() const { return rl ? g->rl_ro.as<uint32_t>() : g->ro.as<uint32_t>(); }
   D* ldist() const { return rl ? ws->dist_int.as<D>() : ws->dist.as<D>(); }
@@ -163,7 +102,6 @@ struct Runner {
     return Plan{g->pull_v.as<uint32_t>(), g->pull_off.as<uint32_t>(), g->pull_off.as<uint32_t>(),
                 g->pull_tseg.as<uint32_t>(), (uint32_t)(g->pull_tseg.bytes / 4)};
   }
-
   AdvArgs<W> args(bool pull) const {
     AdvArgs<W> a{};
     a.adj = pull ? g->cadj.as<EdgeRec<W>>()
@@ -181,334 +119,155 @@ struct Runner {
     return a;
   }
 
-  // frontier compaction: count -> scan (+ loop/direction decision) -> write
-  void compact(int dir, float alpha, cudaGraphConditionalHandle hloop,
+  // frontier filter (frontier.cuh): count per (tile, distance bucket) ->
+  // bucket cursors, deferral cut, plan totals (+ loop / direction decision)
+  // -> write the distance-ordered plan; deferred vertices stay in the bitmap
+  void compact(cudaStream_t st, int dir, float alpha, cudaGraphConditionalHandle hloop,
                cudaGraphConditionalHandle hmode, bool set_loop, bool set_mode) {
-    {
-      if (ordered()) {
-        const uint32_t tiles = ws->ftiles;
-        unsigned long long* bt = ws->obuck.as<unsigned long long>();
-        uint32_t* tflag =
-            reinterpret_cast<uint32_t*>(ws->oagg.as<unsigned long long>() + (size_t)tiles * OB_N);
-        k_fcount_o<D><<<tiles, F_WARPS * 32, 0, s>>>(lro(), ws->bm_next.as<uint32_t>(), nwords,
-                                                     ldist(), ws->ctl.as<Ctl>(),
-                                                     ws->oagg.as<unsigned long long>(), bt, tflag);
-        k_fscan_o<<<1, 32, 0, s>>>(bt, bt + OB_N, plan(), ws->ctl.as<Ctl>(), (uint32_t)g->m, alpha,
-                                   dir == GFB_DIR_AUTO && g->has_csc ? 1 : 0,
-                                   dir == GFB_DIR_PULL ? 1 : 0, hloop, hmode, set_loop ? 1 : 0,
-                                   set_mode ? 1 : 0, defer_pct(), defer_min(), defer_floor());
-        k_fwrite_o<D><<<tiles, F_WARPS * 32, 0, s>>>(lro(), ws->bm_next.as<uint32_t>(),
-                                                     ws->bm_cur.as<uint32_t>(), nwords, ldist(),
-                                                     ws->ctl.as<Ctl>(),
-                                                     ws->oagg.as<unsigned long long>(), bt + OB_N,
-                                                     plan(), tflag);
-        GFB_CUDA(cudaGetLastError());
-        return;
-      }
-    }
     const uint32_t tiles = ws->ftiles;
-    k_fcount<<<tiles, F_WARPS * 32, 0, s>>>(lro(), ws->bm_next.as<uint32_t>(),
-                                            nwords, ws->agg.as<uint2>());
-    k_fscan<<<1, F_SCAN_THREADS, 0, s>>>(ws->agg.as<uint2>(), tiles, plan(), ws->ctl.as<Ctl>(),
-                                         (uint32_t)g->m, alpha,
-                                         dir == GFB_DIR_AUTO && g->has_csc ? 1 : 0,
-                                         dir == GFB_DIR_PULL ? 1 : 0, hloop, hmode,
-                                         set_loop ? 1 : 0, set_mode ? 1 : 0);
-    k_fwrite<<<tiles, F_WARPS * 32, 0, s>>>(lro(), ws->bm_next.as<uint32_t>(),
-                                            ws->bm_cur.as<uint32_t>(), nwords,
-                                            ws->agg.as<uint2>(), plan());
+    unsigned long long* bt = ws->obuck.as<unsigned long long>();
+    unsigned long long* cells = ws->oagg.as<unsigned long long>();
+    uint32_t* tflag = reinterpret_cast<uint32_t*>(cells + (size_t)tiles * OB_N);
+    k_fcount_o<D><<<tiles, F_WARPS * 32, 0, st>>>(lro(), ws->bm_next.as<uint32_t>(), nwords,
+                                                  ldist(), ws->ctl.as<Ctl>(), cells, bt, tflag);
+    k_fscan_o<<<1, 32, 0, st>>>(bt, bt + OB_N, plan(), ws->ctl.as<Ctl>(), (uint32_t)g->m, alpha,
+                                dir == GFB_DIR_AUTO && g->has_csc ? 1 : 0,
+                                dir == GFB_DIR_PULL ? 1 : 0, hloop, hmode, set_loop ? 1 : 0,
+                                set_mode ? 1 : 0, defer_pct(), defer_min());
+    k_fwrite_o<D><<<tiles, F_WARPS * 32, 0, st>>>(lro(), ws->bm_next.as<uint32_t>(),
+                                                  ws->bm_cur.as<uint32_t>(), nwords, ldist(),
+                                                  ws->ctl.as<Ctl>(), cells, bt + OB_N, plan(),
+                                                  tflag);
     GFB_CUDA(cudaGetLastError());
-  }
-
-  // Persistent-grid warp kernel: the grid depends only on the device, so the
-  // same launch serves every superstep inside the captured device loop.
-  template <int VT, int MINB>
-  void warp_launch(cudaStream_t st, uint32_t total, bool full) {
-    constexpr int WT = 32 * VT;
-    uint32_t warps_cap = c->num_sms * MINB * 8;  // 8 warps per 256-thread CTA
-    uint32_t warps = full ? warps_cap
-                          : std::min<uint32_t>(std::max<uint32_t>((total + WT - 1) / WT, 1),
-                                               warps_cap);
-    k_push_warp<W, VT, MINB><<<(warps + 7) / 8, 256, 0, st>>>(args(false));
+    kernels += 3;
   }
 
   void pull_launch(cudaStream_t st) {
     uint32_t ntiles = (g->pull_total + HotCfg<W>::TILE - 1) / HotCfg<W>::TILE;
     uint32_t grid = std::min<uint32_t>(std::max<uint32_t>(ntiles, 1), c->num_sms * 4);
-    if constexpr (sizeof(D) == 4) {
-      if (key_mode()) {
-        k_pull_relax<W, true><<<grid, H_BLOCK, 0, st>>>(args(true), g->pull_total, g->pull_k);
-        return;
-      }
-    }
-    k_pull_relax<W, false><<<grid, H_BLOCK, 0, st>>>(args(true), g->pull_total, g->pull_k);
-  }
-
-  // Packed (dist, pred) keys with fire-and-forget reductions (k_push_range)
-  // for 32-bit distances; the {u, edge} record path for f64 and the legacy
-  // experiment kernels.
-  bool key_mode() const { return sizeof(D) == 4 && variant != 10; }
-
-  template <int VT, int MINB, int TILE, int OPT = 0>
-  void range_launch(cudaStream_t st) {
-    if constexpr (sizeof(D) == 4) {
-      k_push_range<W, VT, MINB, TILE, OPT><<<c->num_sms * MINB, 256, 0, st>>>(args(false));
+    if constexpr (key_mode()) {
+      k_pull_relax<W, true><<<grid, H_BLOCK, 0, st>>>(args(true), g->pull_total, g->pull_k);
     } else {
-      k_push_range<W, VT, MINB, TILE, OPT, false, true><<<c->num_sms * MINB, 256, 0, st>>>(
-          args(false));
+      k_pull_relax<W, false><<<grid, H_BLOCK, 0, st>>>(args(true), g->pull_total, g->pull_k);
     }
+    ++kernels;
   }
 
-  // total == UINT32_MAX: unknown on the host (device loop) -> full grid
-  void push(cudaStream_t st, uint32_t total) {
-    const bool full = total == 0xFFFFFFFFu;
-    if (variant == 10 || (!key_mode() && !rec_fast())) {  // legacy warp-tile kernel
-      warp_launch<(sizeof(W) == 8 ? 4 : 8), 4>(st, total, full);
-      return;
+  // The push advance (hot.cuh k_push_range): 8 x 256-thread CTAs per SM,
+  // strided edge tiles, PTX red.*.  Measured at RMAT s24 / s22
+  // (profiles/r01_variants_s24.txt): 128 / 256 / 512-edge tiles 3.91 / 3.86 /
+  // 3.94 ms at s24, 1.27 / 1.31 / 1.35 at s22; one edge per lane 3.81 / 1.24
+  // vs two 3.85 / 1.27.  f64 (record mode): <2 edges/lane, 6 CTAs/SM>
+  // (<1,8> 5.94, <2,6> 5.82, <4,4> 6.29 ms without predecessors).
+  int tile() const {
+    if (o->advance_tile) return o->advance_tile;
+    return g->m <= (1ull << 27) ? 128 : 256;
+  }
+  void push(cudaStream_t st) {
+    if constexpr (key_mode()) {
+      if (tile() == 128)
+        k_push_range<W, 1, 8, 128, 1><<<c->num_sms * 8, 256, 0, st>>>(args(false));
+      else
+        k_push_range<W, 1, 8, 256, 1><<<c->num_sms * 8, 256, 0, st>>>(args(false));
+    } else {
+      k_push_range<W, 2, 6, 256, 1, false, true><<<c->num_sms * 6, 256, 0, st>>>(args(false));
     }
-    if (rec_fast()) {  // f64: the range kernel with {u, edge} records
-      // s24 without predecessors (tools/f64_breakdown.py): <2,4> 6.37 ms,
-      // <1,8> 5.94, <2,6> 5.82, <4,4> 6.29, <2,3> 7.21 (variants 65-68)
-      if (variant == 65) range_launch<1, 8, 256, 1>(st);
-      else if (variant == 67) range_launch<4, 4, 256, 1>(st);
-      else if (variant == 68) range_launch<2, 3, 256, 1>(st);
-      else if (variant == 69) range_launch<2, 4, 256, 1>(st);
-      else range_launch<2, 6, 256, 1>(st);
-      return;
-    }
-    // measured at RMAT s24 (profiles/r01_variants_s24.txt): 8 x 256-thread
-    // CTAs per SM, strided edge tiles, PTX red.*
-    // tile size by graph size (final loop, ms): 128 / 256 / 512-edge tiles
-    // at s24 3.91 / 3.86 / 3.94, at s22 1.27 / 1.31 / 1.35
-    // final-loop re-sweep (ms, s24 / s22): 1 edge per lane 3.81 / 1.24 vs 2
-    // edges 3.85 / 1.27; 4 edges 4.14; 6 CTAs/SM 3.82-3.87; <4,4> 4.25
-    if (g->m <= (1ull << 27)) range_launch<1, 8, 128, 1>(st);
-    else range_launch<1, 8, 256, 1>(st);
+    ++kernels;
   }
 
-  // The persistent single-launch loop (bsp.cuh) for 32-bit distances.
-  template <int VT, int TILE, int OPT = 0>
-  bool bsp_launch(int dir, float alpha) {
-    if constexpr (sizeof(D) == 4) {
-      auto kern = k_bsp<W, VT, TILE, OPT>;
-      int per_sm = 0;
-      GFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, B_THREADS, 0));
-      if (per_sm <= 0) return false;
-      const uint32_t grid = (uint32_t)std::min(per_sm, 2) * c->num_sms;
-      const uint64_t wpc = ((uint64_t)nwords + grid - 1) / grid;
-      if ((wpc + F_WPW - 1) / F_WPW > (uint64_t)B_MAX_GROUPS) return false;  // graph loop instead
-      BspArgs<W> b{};
-      b.push = args(false);
-      b.pull = args(true);
-      ensure_nz(g);
-      if (ws->bsp_agg.bytes < (size_t)grid * 8) {
-        ws->bsp_agg.alloc((size_t)grid * 8, s);
-        ws->bsp_flag.alloc((size_t)grid * 4, s);
-      }
-      b.ro = g->ro.as<uint32_t>();
-      b.nz = g->nz.as<uint32_t>();
-      b.agg_flag = ws->bsp_flag.as<unsigned>();
-      b.totals = ws->bsp_tot.as<uint2>();
-      b.bm_cur = ws->bm_cur.as<uint32_t>();
-      b.n = n;
-      b.nwords = nwords;
-      b.m = (uint32_t)g->m;
-      b.pull_total = g->pull_total;
-      b.pull_k = g->pull_k;
-      b.agg = ws->bsp_agg.as<uint2>();
-      b.bar = ws->bar.as<unsigned>();
-      b.src_ptr = ws->src_dev.as<uint32_t>();
-      b.alpha = alpha;
-      b.can_pull = dir == GFB_DIR_AUTO && g->has_csc ? 1 : 0;
-      b.force_pull = dir == GFB_DIR_PULL ? 1 : 0;
-      const char* tr = getenv("GFB_TRACE");
-      TBuf trace;
-      if (tr && tr[0] == '1') {
-        b.trace_cap = 4096;
-        trace.alloc(b.trace_cap * 8, s);
-        GFB_CUDA(cudaMemsetAsync(trace.p, 0, b.trace_cap * 8, s));
-        b.trace = trace.as<unsigned long long>();
-      }
-      void* params[] = {&b};
-      GFB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, grid, B_THREADS, params, 0, s));
-      kernels += 1;
-      if (b.trace) {  // per-phase device times (instrumentation only)
-        std::vector<unsigned long long> h(b.trace_cap);
-        GFB_CUDA(cudaMemcpyAsync(h.data(), trace.p, b.trace_cap * 8, cudaMemcpyDeviceToHost, s));
-        c->sync();
-        double sum[4] = {0, 0, 0, 0};
-        for (uint32_t i = 1; i < b.trace_cap && h[i]; ++i) {
-          double us = ((h[i] >> 2) - (h[i - 1] >> 2)) * 1e-3;
-          int tag = (int)(h[i] & 3);
-          sum[tag] += us;
-          fprintf(stderr, "[gfb bsp] %s %.1f us\n",
-                  tag == 1 ? "compact" : "advance", us);
-        }
-        fprintf(stderr, "[gfb bsp] grid %u: compact %.1f us, advance %.1f us\n", grid, sum[1],
-                sum[3]);
-      }
-      return true;
-    }
-    return false;
-  }
-
-  // The persistent single-launch loop is kept as an experiment (variants >= 30):
-  // at s24 its compaction/advance latency chains cost more than the graph
-  // loop's launches (tools/variants.py).
-  bool persistent() const { return key_mode() && variant >= 30 && variant < 40; }
-
-  bool bsp_run(int dir, float alpha) {
-    switch (variant) {
-      case 31: return bsp_launch<4, 512>(dir, alpha);
-      case 32: return bsp_launch<2, 512>(dir, alpha);
-      case 33: return bsp_launch<4, 256>(dir, alpha);
-      case 34: return bsp_launch<2, 256, 1>(dir, alpha);
-      case 35: return bsp_launch<2, 256, 3>(dir, alpha);
-      case 36: return bsp_launch<2, 256, 7>(dir, alpha);
-      case 37: return bsp_launch<2, 256, 11>(dir, alpha);
-      case 38: return bsp_launch<2, 256, 5>(dir, alpha);
-      default: return bsp_launch<2, 256>(dir, alpha);
-    }
-  }
-
-  // Near-far filter (opts.delta > 0): one persistent launch (nearfar.cuh).
+  // Near-far filter (delta > 0): one persistent launch (nearfar.cuh).  8
+  // queue entries per warp (one edge per lane on degree-4 meshes) and
+  // warp-local chasing of 8 rounds (4096^2 grid: 32 entries/warp, 4 rounds,
+  // delta 32: 55 ms; 8/8, delta 16: 31.8 ms; profiles/r01_nearfar_chunk.txt).
+  // Rows longer than NF_HEAVY edges are expanded by a whole CTA in the next
+  // phase (RMAT s24, delta = inf: 212 -> 36 ms); compiled out otherwise.
   bool nearfar_launch(double delta) {
-    {
-      // 8 queue entries per warp (one edge per lane on degree-4 meshes) and
-      // warp-local chasing of 8 rounds.  4096^2 grid: 32 entries/warp, LH 4,
-      // delta 32 = 55 ms; CH 8: LH 4 33.5, LH 8 32.7, LH 16 36.9 ms; CH 4 LH 8
-      // delta 16 32.5 ms (profiles/r01_nearfar_chunk.txt).  Variants keep the
-      // other settings measurable.
-      // rows longer than NF_HEAVY edges: expanded by a whole CTA in the next
-      // phase (RMAT s24, delta = inf: 212 -> 36 ms at 256 edges); compiled out otherwise
-      const bool hv = max_out_degree(g) > NF_HEAVY || variant == 89;
-      auto kern = hv ? k_nearfar<W, 8, 8, true> : k_nearfar<W, 8, 8>;
-      if constexpr (sizeof(D) == 4) {  // shape experiments: 4-byte distances only
-        if (variant == 90) kern = k_nearfar<W, 0>;
-        else if (variant == 91) kern = k_nearfar<W, 4>;
-        else if (variant == 92) kern = k_nearfar<W, 16>;
-        else if (variant == 93) kern = k_nearfar<W, 4, 8>;
-        else if (variant == 94) kern = k_nearfar<W, 4, 16>;
-        else if (variant == 96) kern = k_nearfar<W, 8, 4>;
-        else if (variant == 97) kern = k_nearfar<W, 16, 8>;
-        else if (variant == 98) kern = k_nearfar<W, 16, 4>;
-      }
-      int per_sm = 0;
-      GFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NF_THREADS, 0));
-      if (per_sm <= 0) return false;
-      const uint32_t grid = (uint32_t)std::min(per_sm, 2) * c->num_sms;
-      // queue capacity: every activation appends one entry; a phase can
-      // activate at most min(m, n x in-degree) vertices -- size for 2n or m/4
-      const uint64_t cap64 = std::min<uint64_t>(std::max<uint64_t>(2ull * n, g->m / 4), 0xFFFFFFF0ull);
-      const uint32_t cap = (uint32_t)cap64;
-      const uint32_t hcap = (uint32_t)std::min<uint64_t>(g->m / NF_HEAVY + 4096, 0xFFFFFFF0ull);
-      const size_t qbytes = (size_t)cap * 32 + (size_t)hcap * 16;
-      if (ws->nf_q.bytes < qbytes) {
-        ws->nf_q.alloc(qbytes, s);
-        ws->nf_cnt.alloc(64, s);
-      }
-      NfArgs<W> a{};
-      a.ro = g->ro.as<uint32_t>();
-      a.adj = g->adj.as<EdgeRec<W>>();
-      a.dist = ws->dist.as<D>();
-      a.pkey = ws->predrec.as<unsigned long long>();
-      uint2* q = ws->nf_q.as<uint2>();
-      a.nq[0] = q;
-      a.nq[1] = q + cap;
-      a.fq[0] = q + 2 * (size_t)cap;
-      a.fq[1] = q + 3 * (size_t)cap;
-      a.hq[0] = q + 4 * (size_t)cap;
-      a.hq[1] = q + 4 * (size_t)cap + hcap;
-      a.hcap = hcap;
-      a.cap = cap;
-      a.cnt = ws->nf_cnt.as<uint32_t>();
-      a.fmin64 = reinterpret_cast<unsigned long long*>(ws->nf_cnt.as<uint32_t>() + 10);
-      a.ctl = ws->ctl.as<Ctl>();
-      a.src_ptr = ws->src_dev.as<uint32_t>();
-      a.n = n;
-      a.nwords = nwords;
-      if constexpr (std::is_same<D, float>::value) a.delta = (float)delta;
-      else if constexpr (std::is_same<D, double>::value) a.delta = delta;
-      else a.delta = std::isinf(delta) ? (D)0xFFFFFFFEu  // the queue model: no far set
-                                       : (D)std::min(std::max(std::llround(delta), 1ll), 0xFFFFFFFEll);
-      const char* tr = getenv("GFB_TRACE");
-      TBuf trace;
-      if (tr && tr[0] == '1') {
-        a.trace_cap = 1u << 16;
-        trace.alloc((size_t)a.trace_cap * 8, s);
-        GFB_CUDA(cudaMemsetAsync(trace.p, 0, (size_t)a.trace_cap * 8, s));
-        a.trace = trace.as<unsigned long long>();
-      }
-      void* params[] = {&a};
-      GFB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, grid, NF_THREADS, params, 0, s));
-      kernels += 1;
-      if (a.trace) {  // phase histogram (instrumentation only)
-        std::vector<unsigned long long> h(a.trace_cap);
-        GFB_CUDA(cudaMemcpyAsync(h.data(), trace.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
-        c->sync();
-        uint32_t np = 0;
-        while (np + 1 < a.trace_cap && h[np + 1]) ++np;
-        double buck_us[8] = {0}, buck_n[8] = {0};
-        for (uint32_t i = 0; i + 1 <= np; ++i) {
-          const double us = ((h[i + 1] >> 24) - (h[i] >> 24)) * 1e-3;
-          const uint32_t K = (uint32_t)(h[i] & 0xFFFFFF);
-          int b = 0;
-          for (uint32_t x = K; x >= 16 && b < 7; x >>= 3) ++b;  // 0:<16 1:<128 2:<1K ...
-          buck_us[b] += us;
-          buck_n[b] += 1;
-        }
-        for (int b = 0; b < 8; ++b)
-          if (buck_n[b] > 0)
-            fprintf(stderr, "[gfb nearfar] K < %8u: %6.0f phases, %8.1f us total, %6.2f us/phase\n",
-                    16u << (3 * b), buck_n[b], buck_us[b], buck_us[b] / buck_n[b]);
-      }
-      return true;
+    const bool hv = max_out_degree(g) > NF_HEAVY;
+    auto kern = hv ? k_nearfar<W, 8, 8, true> : k_nearfar<W, 8, 8>;
+    int per_sm = 0;
+    GFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NF_THREADS, 0));
+    if (per_sm <= 0) return false;
+    const uint32_t grid = (uint32_t)std::min(per_sm, 2) * c->num_sms;
+    // queue capacity: every activation appends one entry; a phase can
+    // activate at most min(m, n x in-degree) vertices -- size for 2n or m/4
+    const uint64_t cap64 = std::min<uint64_t>(std::max<uint64_t>(2ull * n, g->m / 4), 0xFFFFFFF0ull);
+    const uint32_t cap = (uint32_t)cap64;
+    const uint32_t hcap = (uint32_t)std::min<uint64_t>(g->m / NF_HEAVY + 4096, 0xFFFFFFF0ull);
+    const size_t qbytes = (size_t)cap * 32 + (size_t)hcap * 16;
+    if (ws->nf_q.bytes < qbytes) {
+      ws->nf_q.alloc(qbytes, s);
+      ws->nf_cnt.alloc(64, s);
     }
-    return false;
+    NfArgs<W> a{};
+    a.ro = g->ro.as<uint32_t>();
+    a.adj = g->adj.as<EdgeRec<W>>();
+    a.dist = ws->dist.as<D>();
+    a.pkey = ws->predrec.as<unsigned long long>();
+    uint2* q = ws->nf_q.as<uint2>();
+    a.nq[0] = q;
+    a.nq[1] = q + cap;
+    a.fq[0] = q + 2 * (size_t)cap;
+    a.fq[1] = q + 3 * (size_t)cap;
+    a.hq[0] = q + 4 * (size_t)cap;
+    a.hq[1] = q + 4 * (size_t)cap + hcap;
+    a.hcap = hcap;
+    a.cap = cap;
+    a.cnt = ws->nf_cnt.as<uint32_t>();
+    a.fmin64 = reinterpret_cast<unsigned long long*>(ws->nf_cnt.as<uint32_t>() + 10);
+    a.ctl = ws->ctl.as<Ctl>();
+    a.src_ptr = ws->src_dev.as<uint32_t>();
+    a.n = n;
+    a.nwords = nwords;
+    if constexpr (std::is_same<D, float>::value) a.delta = (float)delta;
+    else if constexpr (std::is_same<D, double>::value) a.delta = delta;
+    else a.delta = std::isinf(delta) ? (D)0xFFFFFFFEu  // the queue model: no far set
+                                     : (D)std::min(std::max(std::llround(delta), 1ll), 0xFFFFFFFEll);
+    TBuf trace;
+    if (o->trace) {
+      a.trace_cap = 1u << 16;
+      trace.alloc((size_t)a.trace_cap * 8, s);
+      GFB_CUDA(cudaMemsetAsync(trace.p, 0, (size_t)a.trace_cap * 8, s));
+      a.trace = trace.as<unsigned long long>();
+    }
+    void* params[] = {&a};
+    GFB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, grid, NF_THREADS, params, 0, s));
+    kernels += 1;
+    if (a.trace) {  // phase histogram (diagnostics only)
+      std::vector<unsigned long long> h(a.trace_cap);
+      GFB_CUDA(cudaMemcpyAsync(h.data(), trace.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
+      c->sync();
+      uint32_t np = 0;
+      while (np + 1 < a.trace_cap && h[np + 1]) ++np;
+      double buck_us[8] = {0}, buck_n[8] = {0};
+      for (uint32_t i = 0; i + 1 <= np; ++i) {
+        const double us = ((h[i + 1] >> 24) - (h[i] >> 24)) * 1e-3;
+        const uint32_t K = (uint32_t)(h[i] & 0xFFFFFF);
+        int b = 0;
+        for (uint32_t x = K; x >= 16 && b < 7; x >>= 3) ++b;  // 0:<16 1:<128 2:<1K ...
+        buck_us[b] += us;
+        buck_n[b] += 1;
+      }
+      for (int b = 0; b < 8; ++b)
+        if (buck_n[b] > 0)
+          fprintf(stderr, "[gfb nearfar] K < %8u: %6.0f phases, %8.1f us total, %6.2f us/phase\n",
+                  16u << (3 * b), buck_n[b], buck_us[b], buck_us[b] / buck_n[b]);
+    }
+    return true;
   }
 
-  void sort_plan(uint32_t K, uint32_t T, bool desc, int begin_bit = 0) {
-    if (K < 2) return;
-    TBuf keys, keys2, idx, idx2, v2, s2, deg, tmp;
-    keys.alloc((size_t)K * 4, s); keys2.alloc((size_t)K * 4, s);
-    idx.alloc((size_t)K * 4, s); idx2.alloc((size_t)K * 4, s);
-    v2.alloc((size_t)K * 4, s); s2.alloc((size_t)K * 4, s); deg.alloc((size_t)(K + 1) * 4, s);
-    Plan p = plan();
-    k_plan_keys<D><<<stride_grid(c), 256, 0, s>>>(p.v, ldist(), keys.as<uint32_t>(),
-                                                  idx.as<uint32_t>(), K, desc ? 1 : 0);
-    size_t tb = 0, tb2 = 0;
-    GFB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<uint32_t>(), keys2.as<uint32_t>(),
-                                             idx.as<uint32_t>(), idx2.as<uint32_t>(), (int64_t)K,
-                                             begin_bit, 32, s));
-    GFB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, deg.as<uint32_t>(), p.off, (int64_t)(K + 1), s));
-    tmp.alloc(std::max(tb, tb2), s);
-    GFB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<uint32_t>(), keys2.as<uint32_t>(),
-                                             idx.as<uint32_t>(), idx2.as<uint32_t>(), (int64_t)K,
-                                             begin_bit, 32, s));
-    k_plan_permute<<<stride_grid(c), 256, 0, s>>>(idx2.as<uint32_t>(), p.v, p.start, p.off,
-                                                  v2.as<uint32_t>(), s2.as<uint32_t>(),
-                                                  deg.as<uint32_t>(), K);
-    GFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, deg.as<uint32_t>(), p.off, (int64_t)(K + 1), s));
-    GFB_CUDA(cudaMemcpyAsync(p.v, v2.p, (size_t)K * 4, cudaMemcpyDeviceToDevice, s));
-    GFB_CUDA(cudaMemcpyAsync(p.start, s2.p, (size_t)K * 4, cudaMemcpyDeviceToDevice, s));
-    k_plan_tiles<<<stride_grid(c), 256, 0, s>>>(p, deg.as<uint32_t>(), K, T);
-    GFB_CUDA(cudaGetLastError());
+  void init_launch(cudaStream_t st) {
+    k_init<W><<<stride_grid(c), 256, 0, st>>>(ldist(), lpred(), ws->bm_next.as<uint32_t>(),
+                                              ws->bm_cur.as<uint32_t>(), n, nwords,
+                                              ws->src_dev.as<uint32_t>(), ws->ctl.as<Ctl>());
+    ++kernels;
   }
 
-  void init_launch() {
-    k_init<W><<<stride_grid(c), 256, 0, s>>>(ldist(), lpred(),
-                                             ws->bm_next.as<uint32_t>(), ws->bm_cur.as<uint32_t>(),
-                                             n, nwords, ws->src_dev.as<uint32_t>(),
-                                             ws->ctl.as<Ctl>());
-  }
-
-  // ---- device loop: init; compact; WHILE(k > 0) { IF(pull) pull ELSE push;
-  //      compact }  captured once into a CUDA graph (conditional nodes).
+  // ---- device loop: init; filter; WHILE(k > 0) { IF(pull) pull ELSE push;
+  //      filter }  captured once into a CUDA graph (conditional nodes).  The
+  //      graph holds raw pointers into the graph's / workspace's buffers:
+  //      every reallocation of those destroys it (invalidate_loop_graphs).
   void build_loop_graph(int dir, float alpha) {
-    if (ws->loop_exec) cudaGraphExecDestroy(ws->loop_exec);
-    if (ws->loop_graph) cudaGraphDestroy(ws->loop_graph);
-    ws->loop_exec = nullptr;
-    ws->loop_graph = nullptr;
+    invalidate_loop_graphs(g);
     for (auto& a : c->aux)
       if (!a) GFB_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
     cudaGraph_t G;
@@ -517,12 +276,12 @@ struct Runner {
     // the top-level graph, hmode to the loop body (created below)
     cudaGraphConditionalHandle hloop, hmode{};
     GFB_CUDA(cudaGraphConditionalHandleCreate(&hloop, G, 1, cudaGraphCondAssignDefault));
-    const bool pullable = g->has_csc && dir != GFB_DIR_PUSH;
+    const bool pull_ok = pullable(dir);
 
     GFB_CUDA(cudaStreamBeginCaptureToGraph(s, G, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeRelaxed));
-    init_launch();
-    compact(dir, alpha, hloop, hmode, true, false);
+    init_launch(s);
+    compact(s, dir, alpha, hloop, hmode, true, false);
     cudaStreamCaptureStatus cst;
     cudaGraph_t capG;
     const cudaGraphNode_t* deps = nullptr;
@@ -541,13 +300,13 @@ struct Runner {
     GFB_CUDA(cudaStreamEndCapture(s, &tmp));
 
     // loop body
-    if (pullable)  // first iteration expands {source}: push unless pull is forced
+    if (pull_ok)  // first iteration expands {source}: push unless pull is forced
       GFB_CUDA(cudaGraphConditionalHandleCreate(&hmode, body, dir == GFB_DIR_PULL ? 1 : 0,
                                                 cudaGraphCondAssignDefault));
     cudaStream_t b = c->aux[0];
     GFB_CUDA(cudaStreamBeginCaptureToGraph(b, body, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeRelaxed));
-    if (pullable) {
+    if (pull_ok) {
       GFB_CUDA(cudaStreamGetCaptureInfo(b, &cst, nullptr, &capG, &deps, &ndeps));
       cudaGraphNodeParams ip{};
       ip.type = cudaGraphNodeTypeConditional;
@@ -565,58 +324,52 @@ struct Runner {
       GFB_CUDA(cudaStreamEndCapture(x, &tmp));
       GFB_CUDA(cudaStreamBeginCaptureToGraph(x, gpush, nullptr, nullptr, 0,
                                              cudaStreamCaptureModeRelaxed));
-      push(x, 0xFFFFFFFFu);
+      push(x);
       GFB_CUDA(cudaStreamEndCapture(x, &tmp));
     } else {
-      push(b, 0xFFFFFFFFu);
+      push(b);
     }
-    {
-      cudaStream_t keep = s;
-      s = b;  // compact() launches on `s`
-      compact(dir, alpha, hloop, hmode, true, pullable);
-      s = keep;
-    }
+    compact(b, dir, alpha, hloop, hmode, true, pull_ok);
     GFB_CUDA(cudaStreamEndCapture(b, &tmp));
     GFB_CUDA(cudaGraphInstantiate(&ws->loop_exec, G, 0));
     ws->loop_graph = G;
   }
 
-  void run(uint32_t source, const gfb_sssp_opts* o, gfb_sssp_stats* st) {
+  void run(uint32_t source, gfb_sssp_stats* st) {
     ws->has_result = false;
-    variant = o->reserved[0];
     const int dir = o->direction;
     const float alpha = o->pull_alpha > 0 ? o->pull_alpha : 0.25f;
-    // The relabelled CSR has no CSC: only when no superstep can pull (the
-    // AUTO switch needs frontier edges > m / alpha, impossible for alpha <= 1).
-    // Default for 32-bit distances on graphs with >= 2^20 vertices from the
-    // second SSSP on the same contents on (the copy costs ~6 ms at s24 and
-    // saves ~0.3 ms per call, so it pays on reuse, not for a one-shot
-    // upload + SSSP); variant 41 forces it, 60-62 keep the caller's ids.
-    const bool reuse = g->runs_since_fill++ > 0 || g->rl_valid;
     // Default configuration on a low-degree mesh (max out-degree <= 8, e.g.
     // grids and road networks: thousands of BSP supersteps): the near-far
     // loop with delta = 32 x the mean edge weight (the 4096^2 grid's tuned
-    // value: 570 -> 32 ms).  Same fixpoint; variant 122 keeps the BSP loop.
+    // value: 570 -> 32 ms).  Same fixpoint; loop = BSP keeps the BSP loop.
     double delta = o->delta;
-    if (delta == 0 && variant == 0 && (key_mode() || rec_fast()) && dir != GFB_DIR_PULL &&
-        n >= (1u << 16) && max_out_degree(g) <= 8 && g->m >= n) {
+    if (delta == 0 && o->loop == GFB_LOOP_AUTO && dir != GFB_DIR_PULL && n >= (1u << 16) &&
+        max_out_degree(g) <= 8 && g->m >= n) {
       const double mw = mean_weight(g);
       if (mw > 0) delta = 32.0 * mw;
     }
-    rl = (key_mode() || rec_fast()) && delta <= 0 &&
-         (variant == 41 || ((variant == 0 || variant >= 99) && n >= (1u << 20) && reuse)) &&
-         (dir == GFB_DIR_PUSH || (dir == GFB_DIR_AUTO && (alpha <= 1.0f || !g->has_csc)));
+    // The in-degree-relabelled CSR has no CSC: only when no superstep can
+    // pull (AUTO pulls when frontier edges > m / alpha, impossible for
+    // alpha <= 1).  Automatic for graphs with >= 2^20 vertices from the
+    // second SSSP on the same contents on (the copy costs ~6 ms at s24 and
+    // saves ~0.3 ms per call: it pays on reuse, not for a one-shot upload +
+    // SSSP); skipped when in-degrees are not skewed (ensure_relabel).
+    const bool reuse = g->runs_since_fill++ > 0 || g->rl_valid;
+    const bool rl_dir = dir == GFB_DIR_PUSH || (dir == GFB_DIR_AUTO && (alpha <= 1.0f || !g->has_csc));
+    rl = delta <= 0 && rl_dir &&
+         (o->relabel == GFB_RELABEL_ON ||
+          (o->relabel == GFB_RELABEL_AUTO && n >= (1u << 20) && reuse));
     if (rl) {
       ensure_relabel(g);
       rl = !g->rl_skip;
     }
-    if (rl) {
-      if (ws->dist_int.bytes < (size_t)n * sizeof(D)) {
-        ws->dist_int.alloc((size_t)n * sizeof(D), s);
-        ws->pkey_int.alloc((size_t)n * 8, s);
-      }
+    if (rl && ws->dist_int.bytes < (size_t)n * sizeof(D)) {
+      ws->dist_int.alloc((size_t)n * sizeof(D), s);
+      ws->pkey_int.alloc((size_t)n * 8, s);
+      invalidate_loop_graphs(g);
     }
-    // source -> device (pinned staging in ctl_host's slot)
+    // source -> device (the graph launches stay source-agnostic)
     GFB_CUDA(cudaMemcpyAsync(ws->src_dev.p, &source, 4, cudaMemcpyHostToDevice, s));
     if (rl)
       GFB_CUDA(cudaMemcpyAsync(ws->src_dev.p, g->rl_perm.as<uint32_t>() + source, 4,
@@ -625,15 +378,15 @@ struct Runner {
     float adv_ms = 0;
     GFB_CUDA(cudaEventRecord(c->ev[0], s));
     bool done = false;
-    if (delta > 0 && (key_mode() || rec_fast()) && !rl) {
+    if (delta > 0 && !rl) {
       if (dir == GFB_DIR_PULL) fail(GFB_EINVAL, "sssp: the near-far filter (delta > 0) is push-only");
       done = nearfar_launch(delta);
       if (done && (c->read_ctl(ws->ctl.as<Ctl>()).err & 2u)) done = false;  // queue overflow: BSP
     }
-    if (!done && o->device_loop && persistent()) done = bsp_run(dir, alpha);
     if (done) {
     } else if (o->device_loop) {
-      int key[4] = {dir, (int)(alpha * 1000), variant, rl ? 1 : 0};  // graph holds the loop's arrays
+      // the graph's key: everything its captured launches depend on
+      const int key[5] = {dir, (int)(alpha * 1000), rl ? 1 : 0, (int)defer_pct(), tile()};
       if (!ws->loop_exec || memcmp(key, ws->loop_key, sizeof(key)) != 0) {
         GFB_CUDA(cudaStreamSynchronize(s));
         build_loop_graph(dir, alpha);
@@ -643,32 +396,24 @@ struct Runner {
       GFB_CUDA(cudaGraphLaunch(ws->loop_exec, s));
     } else {
       cudaGraphConditionalHandle none{};
-      init_launch();
-      compact(dir, alpha, none, none, false, false);
-      kernels = 4;
-      const char* tr = getenv("GFB_TRACE");
-      const bool trace = tr && tr[0] == '1';
+      init_launch(s);
+      compact(s, dir, alpha, none, none, false, false);
       for (;;) {
         Ctl h = c->read_ctl(ws->ctl.as<Ctl>());
         if (h.err & 1u) fail(GFB_ERANGE, "sssp: u32 distance overflow (use f64 weights)");
         if (h.k == 0) break;
-        if ((variant == 42 || variant == 43) && h.mode == 0) sort_plan(h.k, h.total, variant == 43);
-        if (variant == 47 && h.mode == 0) sort_plan(h.k, h.total, false, 20);
-        if (variant == 48 && h.mode == 0) sort_plan(h.k, h.total, false, 23);
-        if (variant == 49 && h.mode == 0) sort_plan(h.k, h.total, false, 16);
         GFB_CUDA(cudaEventRecord(c->ev[2], s));
         if (h.mode == 1) pull_launch(s);
-        else push(s, h.total);
+        else push(s);
         GFB_CUDA(cudaEventRecord(c->ev[3], s));
         GFB_CUDA(cudaGetLastError());
-        compact(dir, alpha, none, none, false, false);
+        compact(s, dir, alpha, none, none, false, false);
         ++launches;
-        kernels += 4;
         GFB_CUDA(cudaEventSynchronize(c->ev[3]));
         float ms = 0;
         GFB_CUDA(cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]));
         adv_ms += ms;
-        if (trace)
+        if (o->trace)
           fprintf(stderr, "[gfb] superstep %llu %s frontier=%u edges=%u advance=%.3f ms (%.1f G edges/s)\n",
                   (unsigned long long)launches, h.mode ? "pull" : "push", h.k, h.total, ms,
                   (h.mode ? g->pull_total : h.total) / (ms * 1e-3) / 1e9);
@@ -681,7 +426,7 @@ struct Runner {
     if (h.err & 1u) fail(GFB_ERANGE, "sssp: u32 distance overflow (use f64 weights)");
     float ms = 0;
     GFB_CUDA(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
-    if (o->device_loop && !done) kernels += 4 + 4ull * h.supersteps;
+    if (o->device_loop && !done) kernels += 4 + 4ull * h.supersteps;  // graph launches
     ws->has_result = true;
     ws->source = source;
     if (st) {
@@ -704,9 +449,8 @@ struct Runner {
     GFB_CUDA(cudaMemsetAsync(&ws->ctl.as<Ctl>()->flag, 0, 4, s));
     auto verify = k_pred_verify<W, false, false>;
     PermView<D> pv{};
-    if constexpr (sizeof(D) == 4) {
-      if (key_mode()) verify = k_pred_verify<W, true, false>;
-      if (rl) verify = k_pred_verify<W, true, true>;
+    if constexpr (key_mode()) {
+      verify = rl ? k_pred_verify<W, true, true> : k_pred_verify<W, true, false>;
     } else {
       if (rl) verify = k_pred_verify<W, false, true>;  // f64 records, relabelled loop
     }
@@ -732,17 +476,15 @@ struct Runner {
     Ctl h = {};
     uint64_t left = 0;
     for (uint32_t done_before = 0;;) {
-      if (key_mode()) {
-        if constexpr (sizeof(D) == 4) {
-          for (uint32_t k = base + 1; k <= base + PRED_KEY_ROUNDS; ++k)
-            k_pred_key_round<W><<<c->num_sms, 256, 0, s>>>(
-                ws->cand.as<uint32_t>(), ws->predrec.as<unsigned long long>(), ws->dist.as<D>(),
-                ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(), ws->repair_bm.as<uint32_t>(), k,
-                dctl);
-          GFB_CUDA(cudaGetLastError());
-          kernels += PRED_KEY_ROUNDS;
-          base += PRED_KEY_ROUNDS;
-        }
+      if constexpr (key_mode()) {
+        for (uint32_t k = base + 1; k <= base + PRED_KEY_ROUNDS; ++k)
+          k_pred_key_round<W><<<c->num_sms, 256, 0, s>>>(
+              ws->cand.as<uint32_t>(), ws->predrec.as<unsigned long long>(), ws->dist.as<D>(),
+              ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(), ws->repair_bm.as<uint32_t>(), k,
+              dctl);
+        GFB_CUDA(cudaGetLastError());
+        kernels += PRED_KEY_ROUNDS;
+        base += PRED_KEY_ROUNDS;
       }
       h = c->read_ctl(dctl);
       *fallback = h.unresolved;
@@ -779,7 +521,7 @@ struct Runner {
       list.alloc((size_t)cap * 16, s);
       GFB_CUDA(cudaMemsetAsync(&dctl->out_count, 0, 8, s));  // out_count, rec_count
       GFB_CUDA(cudaMemsetAsync(&dctl->err, 0, 4, s));
-      if (h.unresolved <= PR_FLAT_MAX && variant != 64) {  // few: flat filtered pass
+      if (h.unresolved <= PR_FLAT_MAX) {  // few: one flat pass screened by a shared filter
         k_pred_inedges_flat<W><<<c->num_sms * 8, 256, 0, s>>>(
             g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(), n, g->m,
             ws->repair_bm.as<uint32_t>(), ws->cand.as<uint32_t>(), list.as<uint4>(), cap, dctl);
@@ -820,21 +562,29 @@ struct Runner {
 };
 
 void sssp_run(Ctx* c, Graph* g, uint32_t source, const gfb_sssp_opts* o, gfb_sssp_stats* st) {
-  if (source >= g->n) fail(GFB_ERANGE, "sssp: source out of range");  // algorithms.hpp:572
-  if (o->direction == GFB_DIR_PULL && !g->csc_wanted)                  // algorithms.hpp:573-574
+  check_usable(g);
+  if (source >= g->n) fail(GFB_ERANGE, "sssp: source out of range");  // algorithms.hpp:137
+  if (o->direction == GFB_DIR_PULL && !g->csc_wanted)                  // algorithms.hpp:138-139
     fail(GFB_EINVAL, "sssp: pull direction requires a built transpose");
+  if (o->direction < GFB_DIR_PUSH || o->direction > GFB_DIR_AUTO)
+    fail(GFB_EINVAL, "sssp: bad direction");
+  if (o->loop < GFB_LOOP_AUTO || o->loop > GFB_LOOP_BSP) fail(GFB_EINVAL, "sssp: bad loop");
+  if (o->relabel < GFB_RELABEL_AUTO || o->relabel > GFB_RELABEL_OFF)
+    fail(GFB_EINVAL, "sssp: bad relabel");
+  if (o->defer_pct < 0 || o->defer_pct > 100) fail(GFB_EINVAL, "sssp: defer_pct must be 0..100");
+  if (o->advance_tile != 0 && o->advance_tile != 128 && o->advance_tile != 256)
+    fail(GFB_EINVAL, "sssp: advance_tile must be 0, 128 or 256");
   // the transpose only when a superstep can pull (AUTO pulls when frontier
   // edges exceed m / alpha: impossible for alpha <= 1)
   const float alpha = o->pull_alpha > 0 ? o->pull_alpha : 0.25f;
   if (o->direction == GFB_DIR_PULL || (o->direction == GFB_DIR_AUTO && alpha > 1.0f &&
                                        o->delta <= 0))
     ensure_csc(g);
-  if (o->direction < GFB_DIR_PUSH || o->direction > GFB_DIR_AUTO)
-    fail(GFB_EINVAL, "sssp: bad direction");
   Workspace* ws = ensure_ws(g);
-  if (g->wtype == GFB_W_F32) Runner<float>{c, g, ws, c->stream, (uint32_t)g->n, (uint32_t)((g->n + 31) / 32)}.run(source, o, st);
-  else if (g->wtype == GFB_W_F64) Runner<double>{c, g, ws, c->stream, (uint32_t)g->n, (uint32_t)((g->n + 31) / 32)}.run(source, o, st);
-  else Runner<uint32_t>{c, g, ws, c->stream, (uint32_t)g->n, (uint32_t)((g->n + 31) / 32)}.run(source, o, st);
+  const uint32_t n = (uint32_t)g->n, nw = (uint32_t)((g->n + 31) / 32);
+  if (g->wtype == GFB_W_F32) Runner<float>{c, g, ws, c->stream, n, nw, o}.run(source, st);
+  else if (g->wtype == GFB_W_F64) Runner<double>{c, g, ws, c->stream, n, nw, o}.run(source, st);
+  else Runner<uint32_t>{c, g, ws, c->stream, n, nw, o}.run(source, st);
 }
 
 // widen the native distances to double (exact for u32 / f32 / f64)

@@ -96,10 +96,10 @@ class PeerSssp:
             dist.barrier(group=group)
         self.linked = True
 
-    def sssp(self, source, want_pred=True, variant=0):
+    def sssp(self, source, want_pred=True, defer_pct=0):
         """Collective: every rank calls it with the same arguments.  Returns
         this rank's statistics (relaxations / n_reach / m_reach: local share)."""
-        o = self.gb._opts(direction="push", compute_pred=want_pred, variant=variant)
+        o = self.gb._opts(direction="push", compute_pred=want_pred, defer_pct=defer_pct)
         st = _lib.SsspStats()
         self.gb.check(self.lib.gfb_peer_sssp(self.h, int(source), C.byref(o), C.byref(st)))
         return {k: getattr(st, k) for k, _ in _lib.SsspStats._fields_}
@@ -167,8 +167,8 @@ class MgSssp:
         self.gb.check(self.lib.gfb_mg_ranges(self.h, C.c_void_p(rs.ctypes.data)))
         return rs
 
-    def sssp(self, source, want_pred=True, variant=0):
-        o = self.gb._opts(direction="push", compute_pred=want_pred, variant=variant)
+    def sssp(self, source, want_pred=True, defer_pct=0):
+        o = self.gb._opts(direction="push", compute_pred=want_pred, defer_pct=defer_pct)
         st = _lib.SsspStats()
         dist = np.empty(self.n, np.float64)
         pred = np.empty(self.n, np.uint32)

@@ -6,11 +6,13 @@ reach the same unique fixpoint: distances must be bit-identical to the
 oracle (f32 restatement of reference_dijkstra, u32 = the reference's own
 integer arithmetic) and predecessor trees valid.
 
-  delta > 0     near-far filter, one persistent cooperative launch with
-                queue frontiers (nearfar.cuh) -- the high-diameter path
-  variant 41    BSP loop on the in-degree-relabelled CSR (ensure_relabel)
-  variant 3x    BSP loop as one persistent cooperative launch (bsp.cuh)
-  variant 10    the previous warp-tile push kernel with {u, edge} records
+  delta > 0          near-far filter, one persistent cooperative launch with
+                     queue frontiers (nearfar.cuh) -- the high-diameter path
+  relabel="on"       BSP loop on the in-degree-relabelled CSR (ensure_relabel)
+  advance_tile=256   the push-advance instantiation the headline RMAT s24
+                     run uses (chosen by size for m > 2^27 edges)
+  defer_pct          the far-bucket deferral of the BSP filter (100 = off)
+  loop="bsp"         never the automatic near-far choice
 """
 import os
 
@@ -70,38 +72,60 @@ def test_nearfar_corpus_f32(ctx):
         _check(g, dist, pred)
 
 
-@pytest.mark.parametrize("variant", [89, 90, 91, 93, 96, 98])
-def test_nearfar_chunk_variants(ctx, variant):
-    """Other (chase rounds, entries per warp) settings of k_nearfar."""
-    g = gb.grid(128, seed=3, transpose=True, ctx=ctx)
-    dist, pred, st = gb.sssp_stats(g, 0, delta=4.0, variant=variant)
-    _check(g, dist, pred)
-    g = gb.rmat(12, 16, seed=3, wtype="u32", transpose=True, ctx=ctx)
-    dist, pred, st = gb.sssp_stats(g, 7, delta=32, variant=variant)
-    _check(g, dist, pred, source=7, wtype="u32")
-
-
 def test_nearfar_rejects_pull(ctx):
     g = gb.grid(16, seed=1, transpose=True, ctx=ctx)
     with pytest.raises(ValueError):
         gb.sssp_stats(g, 0, delta=1.0, direction="pull")
 
 
-@pytest.mark.parametrize("variant", [10, 30, 34, 41])
-def test_loop_variants_rmat(ctx, variant):
+LOOP_OPTS = [dict(relabel="on"), dict(relabel="off"), dict(advance_tile=256),
+             dict(advance_tile=128, relabel="on"), dict(advance_tile=256, relabel="on"),
+             dict(defer_pct=100), dict(defer_pct=1), dict(defer_pct=50, advance_tile=256)]
+
+
+@pytest.mark.parametrize("kw", LOOP_OPTS)
+def test_loop_options_rmat(ctx, kw):
     g = gb.rmat(14, 16, seed=1, wtype="f32", transpose=True, ctx=ctx)
-    dist, pred, st = gb.sssp_stats(g, 0, variant=variant)
+    dist, pred, st = gb.sssp_stats(g, 0, **kw)
     _check(g, dist, pred)
 
 
-@pytest.mark.parametrize("variant", [30, 41])
-def test_loop_variants_u32_grid(ctx, variant):
+@pytest.mark.parametrize("kw", [dict(relabel="on", loop="bsp"), dict(advance_tile=256, loop="bsp"),
+                                dict(defer_pct=100, loop="bsp")])
+def test_loop_options_u32_grid(ctx, kw):
     g = gb.rmat(12, 16, seed=1, wtype="u32", transpose=True, ctx=ctx)
-    dist, pred, st = gb.sssp_stats(g, 0, variant=variant)
+    dist, pred, st = gb.sssp_stats(g, 0, **kw)
     _check(g, dist, pred, wtype="u32")
     g = gb.grid(64, seed=1, transpose=True, ctx=ctx)
-    dist, pred, st = gb.sssp_stats(g, 0, variant=variant)
+    dist, pred, st = gb.sssp_stats(g, 0, **kw)
     _check(g, dist, pred)
+
+
+def test_headline_instantiation_corpus(ctx):
+    """k_push_range<f32|u32, 1, 8, 256, 1> -- the instantiation RMAT s24 runs
+    (tile 256 above 2^27 edges) -- forced on the acceptance corpus
+    (acceptance.cpp:95-122) against the oracle, with and without relabelling."""
+    corpus = np.load(os.path.join(os.path.dirname(__file__), "golden", "corpus.npz"))
+    for i in range(0, 200, 3):
+        n, seed = int(corpus["meta"][i][0]), int(corpus["meta"][i][1])
+        s, d, w = O.random_edges(n, seed)
+        for wt in ("f32", "u32"):
+            ww = w if wt == "f32" else np.floor(w).astype(np.uint32)
+            g = gb.build_csr((s, d, ww), n, wtype=wt, transpose=False, ctx=ctx)
+            dist, pred, st = gb.sssp_stats(g, 0, advance_tile=256, loop="bsp",
+                                           relabel="on" if i % 2 else "off")
+            _check(g, dist, pred, wtype=wt)
+            g.free()
+
+
+@pytest.mark.parametrize("scale,wt", [(18, "f32"), (20, "f32"), (18, "u32")])
+def test_headline_instantiation_rmat(ctx, scale, wt):
+    """The s24 configuration (tile 256, relabelled CSR, 5 % deferral) at RMAT
+    s18 / s20: bit-exact vs the oracle, valid predecessor tree."""
+    g = gb.rmat(scale, 16, seed=1, wtype=wt, transpose=False, ctx=ctx)
+    for src in (0, 3):
+        dist, pred, st = gb.sssp_stats(g, src, advance_tile=256, relabel="on")
+        _check(g, dist, pred, source=src, wtype=wt)
 
 
 def test_relabel_view_is_permuted_csr(ctx):
@@ -131,14 +155,16 @@ def test_relabel_view_is_permuted_csr(ctx):
 
 
 def test_default_path_rmat20_bit_exact(ctx):
-    """The default BSP path at a size where every optimisation is active:
-    relabelled CSR (n >= 2^20), distance-ordered compaction and the deferral
-    of far buckets (frontiers with >= m/4 edges) -- bit-exact vs the oracle,
-    valid predecessor tree, and the deferral actually cut the work."""
+    """The default BSP path at RMAT s20: the first call runs on the caller's
+    ids, the second on the in-degree-relabelled CSR (built on reuse); both use
+    the distance-ordered filter and the deferral of far buckets (pending sets
+    with >= m/4 edges) -- bit-exact vs the oracle, valid predecessor trees,
+    and the deferral actually cut the work."""
     g = gb.rmat(20, 16, seed=1, wtype="f32", transpose=True, ctx=ctx)
-    dist, pred, st = gb.sssp_stats(g, 0)
-    _check(g, dist, pred)
-    _, _, plain = gb.sssp_stats(g, 0, want_result=False, variant=99)  # deferral off
+    for _ in range(2):
+        dist, pred, st = gb.sssp_stats(g, 0)
+        _check(g, dist, pred)
+    _, _, plain = gb.sssp_stats(g, 0, want_result=False, defer_pct=100)  # deferral off
     assert st.relaxations < 0.8 * plain.relaxations
 
 
@@ -231,12 +257,12 @@ def test_nearfar_heavy_rows(ctx, wtype):
 def test_auto_nearfar_on_mesh(ctx):
     """The default configuration picks the near-far loop on a low-degree mesh
     (max out-degree <= 8, n >= 2^16; delta = 32 x mean weight) and the BSP loop
-    otherwise; variant 122 forces BSP.  Same distances either way."""
+    otherwise; loop="bsp" forces BSP.  Same distances either way."""
     g = gb.grid(300, seed=9, transpose=False, ctx=ctx)
     ro, col, w = g.csr()
     want, _ = O.dijkstra(g.num_vertices, ro, col, w, 0, "f32")
     d_auto, p_auto, st_auto = gb.sssp_stats(g, 0, direction="push")
-    d_bsp, p_bsp, st_bsp = gb.sssp_stats(g, 0, direction="push", variant=122)
+    d_bsp, p_bsp, st_bsp = gb.sssp_stats(g, 0, direction="push", loop="bsp")
     for d, p in ((d_auto, p_auto), (d_bsp, p_bsp)):
         assert np.array_equal(d.astype(np.float32), want)
         assert O.check_pred_tree(g.num_vertices, ro, col, w, d.astype(np.float32), 0, p) == -1

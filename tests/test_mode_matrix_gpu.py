@@ -7,7 +7,7 @@ shapes: random G(n, 4/n) with 10% zero weights (tie classes, acceptance.cpp
 corpus generator), RMAT with duplicates and self-loops, a 2-D grid, a long
 path with a back edge, a star hub (heavy rows) and a graph with unreachable
 parts.  loops: default (automatic choice), push BSP, pull BSP (transpose),
-AUTO, near-far (small delta), the queue model, forced BSP (variant 122).
+AUTO, near-far (small delta), the queue model, forced BSP (loop="bsp").
 """
 import numpy as np
 import pytest
@@ -45,7 +45,7 @@ def _shapes():
 
 LOOPS = [dict(), dict(direction="push"), dict(direction="pull"), dict(direction="auto"),
          dict(direction="push", delta=0.05), dict(frontier="queue"),
-         dict(direction="push", variant=122)]
+         dict(direction="push", loop="bsp")]
 
 
 @pytest.mark.parametrize("wtype", ["f64", "f32", "u32"])

@@ -27,21 +27,24 @@ KEYS = [
 raw = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
-hdr, units, val = rows[0], rows[1], rows[2]
-name = val[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"
-print(f"kernel: {name}")
-for k, label in KEYS:
-    if k in hdr:
-        i = hdr.index(k)
-        print(f"  {label:32s} {val[i]:>16s} {units[i]}")
-stalls = []
-for i, h in enumerate(hdr):
-    if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued"):
-        try:
-            stalls.append((float(val[i]), h.replace("smsp__pcsamp_warps_issue_stalled_", "")))
-        except ValueError:
-            pass
-tot = sum(v for v, _ in stalls) or 1
-print("  warp-state samples (top 5):")
-for v, h in sorted(stalls, reverse=True)[:5]:
-    print(f"    {h:28s} {100 * v / tot:5.1f}%")
+hdr, units = rows[0], rows[1]
+for val in rows[2:]:  # one row per profiled launch
+    if len(val) != len(hdr):
+        continue
+    name = val[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"
+    print(f"kernel: {name}")
+    for k, label in KEYS:
+        if k in hdr:
+            i = hdr.index(k)
+            print(f"  {label:32s} {val[i]:>16s} {units[i]}")
+    stalls = []
+    for i, h in enumerate(hdr):
+        if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued"):
+            try:
+                stalls.append((float(val[i]), h.replace("smsp__pcsamp_warps_issue_stalled_", "")))
+            except ValueError:
+                pass
+    tot = sum(v for v, _ in stalls) or 1
+    print("  warp-state samples (top 5):")
+    for v, h in sorted(stalls, reverse=True)[:5]:
+        print(f"    {h:28s} {100 * v / tot:5.1f}%")

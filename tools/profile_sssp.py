@@ -19,7 +19,9 @@ ap.add_argument("--direction", default="auto")
 ap.add_argument("--alpha", type=float, default=0.25)
 ap.add_argument("--delta", type=float, default=0.0)
 ap.add_argument("--device-loop", type=int, default=1)
-ap.add_argument("--variant", type=int, default=0)
+ap.add_argument("--defer-pct", type=int, default=0)
+ap.add_argument("--tile", type=int, default=0)
+ap.add_argument("--relabel", default="auto")
 ap.add_argument("--source", type=int, default=0)
 a = ap.parse_args()
 ctx = gb.Context(0)
@@ -27,5 +29,5 @@ g = gb.grid(a.grid) if a.grid else gb.rmat(a.scale, 16, seed=1, wtype="f32", tra
 for r in range(a.runs):
     _, _, st = gb.sssp_stats(g, a.source, want_result=False, direction=a.direction, pull_alpha=a.alpha,
                              delta=a.delta, device_loop=bool(a.device_loop),
-                             variant=a.variant)
+                             defer_pct=a.defer_pct, advance_tile=a.tile, relabel=a.relabel)
     print(json.dumps({k: getattr(st, k) for k, _ in gb.SsspStats._fields_}), flush=True)
