@@ -8,6 +8,7 @@
 #include "graflow_oracle.h"
 
 #include <math.h>
+#include <omp.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -387,6 +388,54 @@ void orc_rmat_edges(int scale, uint64_t m, uint64_t seed, int wkind,
       memcpy(&wbits[k], &f, 4);
     }
   }
+}
+
+/* The RMAT graph in build_csr's layout (graph.hpp:352-382: rows ascending
+ * by src, each row sorted by (dst, weight), parallel edges kept), built on the
+ * host for the CPU baseline at full size: edges generated in parallel, a
+ * counting sort by source, then each row sorted.  Equal to sorting the whole
+ * edge list by (src, dst, w) -- the reference's own std::sort -- because the
+ * row order and the in-row order are both total.  threads <= 0: all cores. */
+static int edge_dw_cmp(const void* a, const void* b) {
+  const uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+  return x < y ? -1 : x > y;
+}
+
+uint64_t orc_rmat_csr(int scale, int edgefactor, uint64_t seed, int wkind, int threads,
+                      uint32_t* ro, uint32_t* col, uint32_t* wbits) {
+  const uint64_t n = 1ull << scale, m = (uint64_t)edgefactor << scale;
+  if (threads > 0) omp_set_num_threads(threads);
+  uint32_t* s = (uint32_t*)malloc(m * 4);
+  uint64_t* dw = (uint64_t*)malloc(m * 8); /* (dst << 32 | weight bits): in-row key */
+  const uint64_t chunk = 1u << 14;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (uint64_t c = 0; c < (m + chunk - 1) / chunk; ++c) {
+    const uint64_t first = c * chunk, cnt = first + chunk > m ? m - first : chunk;
+    uint32_t d[1u << 14], w[1u << 14];
+    orc_rmat_edges(scale, m, seed, wkind, first, cnt, s + first, d, w);
+    for (uint64_t k = 0; k < cnt; ++k) dw[first + k] = ((uint64_t)d[k] << 32) | w[k];
+  }
+  memset(ro, 0, (n + 1) * 4);
+  for (uint64_t i = 0; i < m; ++i) ++ro[s[i] + 1];
+  for (uint64_t v = 0; v < n; ++v) ro[v + 1] += ro[v];
+  uint64_t* sorted = (uint64_t*)malloc(m * 8);
+  uint32_t* cur = (uint32_t*)malloc(n * 4);
+  memcpy(cur, ro, n * 4);
+  for (uint64_t i = 0; i < m; ++i) sorted[cur[s[i]]++] = dw[i]; /* stable scatter by source */
+  free(cur);
+  free(dw);
+  free(s);
+  /* f32 weights are non-negative: their bits order like the values; u32 the same */
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (uint64_t v = 0; v < n; ++v)
+    qsort(sorted + ro[v], ro[v + 1] - ro[v], 8, edge_dw_cmp);
+#pragma omp parallel for schedule(static)
+  for (uint64_t i = 0; i < m; ++i) {
+    col[i] = (uint32_t)(sorted[i] >> 32);
+    wbits[i] = (uint32_t)sorted[i];
+  }
+  free(sorted);
+  return m;
 }
 
 uint64_t orc_grid_csr(uint32_t side, uint64_t seed, uint32_t* ro,

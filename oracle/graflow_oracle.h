@@ -112,6 +112,9 @@ int64_t orc_check_pred_tree(size_t n, const uint32_t* ro, const uint32_t* col,
 int orc_bfs(size_t n, const uint32_t* ro, const uint32_t* col, uint32_t source, double* depth,
             uint64_t* supersteps, uint64_t* relaxations);
 
+/* build_csr layout of the RMAT graph, host-parallel (CPU-baseline input) */
+uint64_t orc_rmat_csr(int scale, int edgefactor, uint64_t seed, int wkind, int threads,
+                      uint32_t* ro, uint32_t* col, uint32_t* wbits);
 void orc_rmat_edges(int scale, uint64_t m, uint64_t seed, int wkind,
                     uint64_t first, uint64_t count, uint32_t* src,
                     uint32_t* dst, uint32_t* wbits);

@@ -59,6 +59,9 @@ def orc():
                               C.POINTER(C.c_uint64)]
         L.orc_grid_csr.restype = C.c_uint64
         L.orc_grid_csr.argtypes = [C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_rmat_csr.restype = C.c_uint64
+        L.orc_rmat_csr.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, C.c_void_p,
+                                   C.c_void_p, C.c_void_p]
         _ORC = L
     return _ORC
 
@@ -195,6 +198,17 @@ def rmat_edges(scale, edgefactor=16, seed=1, wkind=1, first=0, count=None):
     s = np.empty(count, np.uint32); d = np.empty(count, np.uint32); w = np.empty(count, np.uint32)
     orc().orc_rmat_edges(scale, m, seed, wkind, first, count, s, d, w)
     return s, d, w
+
+
+def rmat_csr(scale, edgefactor=16, seed=1, wkind=1, threads=0):
+    """RMAT in build_csr layout, built on the host (orc_rmat_csr): (ro, col, w)
+    with w float32 (wkind 1) or uint32 (wkind 0)."""
+    L = orc()
+    n, m = 1 << scale, edgefactor << scale
+    ro = np.empty(n + 1, np.uint32); col = np.empty(m, np.uint32); w = np.empty(m, np.uint32)
+    L.orc_rmat_csr(scale, edgefactor, seed, wkind, threads, ro.ctypes.data, col.ctypes.data,
+                   w.ctypes.data)
+    return ro, col, (w.view(np.float32) if wkind == 1 else w)
 
 
 def grid_csr(side, seed=1):

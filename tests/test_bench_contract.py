@@ -14,7 +14,7 @@ def test_reference_arm_json_line():
     from oracle import oracle as O
     if O.ref() is None:
         pytest.skip("oracle/_ref not built (the reference sources are absent)")
-    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--ref-scale", "12",
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--scale", "12",
                         "--steps", "1", "--warmup", "3"], cwd=ROOT, capture_output=True,
                        text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]

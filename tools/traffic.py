@@ -1,10 +1,13 @@
-"""DRAM traffic of the advance kernel per launch, for bench.py's roofline.traffic.
+"""DRAM traffic of the advance kernel over one SSSP step, for bench.py's
+roofline.traffic (compare with the algorithmic bytes B_alg x m_reach).
 
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
       --clock-control none -k regex:k_push_range --csv --log-file gpurun_out/traffic.csv \
-      python tools/profile_sssp.py --scale 24 --runs 1 --device-loop 0
+      python tools/profile_sssp.py --scale 24 --runs 1 --device-loop 0 --relabel on
   python tools/traffic.py gpurun_out/traffic.csv 24 > profiles/advance_traffic.json
-Algorithmic bytes per launch = B_alg x visits / launches.
+(--relabel on: the timed configuration of bench.py from the first call on.)
+ncu replays each launch with flushed caches, so this is an upper bound of the
+live traffic (the 64 MB distance array stays in L2 across live launches).
 """
 import csv
 import json
@@ -34,9 +37,11 @@ wr = sum(per[i]["dram__bytes_write.sum"] for i in ids)
 t = sum(per[i]["gpu__time_duration.sum"] for i in ids)
 print(json.dumps({"scale": int(sys.argv[2]), "kernel": names[ids[0]] if ids else None,
                   "launches": len(ids), "dram_read_bytes_total": rd,
+                  "dram_bytes_per_step": rd + wr,
                   "dram_write_bytes_total": wr, "dram_bytes_per_launch": (rd + wr) / max(len(ids), 1),
                   "kernel_time_s_total_cold": t,
                   "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,"
                             "gpu__time_duration.sum --clock-control none -k regex:k_push_range "
-                            "python tools/profile_sssp.py --scale %s --runs 1 --device-loop 0"
+                            "python tools/profile_sssp.py --scale %s --runs 1 --device-loop 0 --relabel on "
+                            "(flushed caches per launch)"
                             % sys.argv[2]}, indent=1))
