@@ -314,6 +314,36 @@ DEFINE_BSP(orc_sssp_bsp_f32, float)
 DEFINE_REPAIR(orc_repair_pred_f64, double)
 DEFINE_REPAIR(orc_repair_pred_f32, float)
 
+static int tight_edge(const uint32_t* ro, const uint32_t* col, const double* wd,
+                      const float* wf, const double* dd, const float* df, int kind,
+                      uint32_t u, uint32_t v) {
+  /* build_csr rows are sorted by (dst, weight) (graph.hpp:364-367): binary
+   * search for v, then its parallel edges; a linear scan if that misses
+   * (rows of other layouts) */
+  uint32_t lo = ro[u], hi = ro[u + 1];
+  while (lo < hi) {
+    uint32_t mid = lo + (hi - lo) / 2;
+    if (col[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    uint32_t e0 = pass ? ro[u] : lo, e1 = ro[u + 1];
+    for (uint32_t e = e0; e < e1; ++e) {
+      if (col[e] != v) {
+        if (pass == 0) break;
+        continue;
+      }
+      if (kind ? (float)(df[u] + wf[e]) == df[v] : dd[u] + wd[e] == dd[v]) return 1;
+    }
+  }
+  return 0;
+}
+
+/* acceptance.cpp:56-91: NIL at the source and unreachable vertices; every
+ * other v has an edge pred[v] -> v with dist[pred] + w == dist[v], and the
+ * chain reaches the source.  Chains are walked once (memoised: a vertex is
+ * marked when its chain is known to end at the source), so the check is
+ * linear even on high-diameter graphs.  Returns -1, or the first bad v. */
 int64_t orc_check_pred_tree(size_t n, const uint32_t* ro, const uint32_t* col,
                             const void* wv, const void* dv, int kind,
                             uint32_t source, const uint32_t* pred) {
@@ -329,20 +359,26 @@ int64_t orc_check_pred_tree(size_t n, const uint32_t* ro, const uint32_t* col,
     }
     uint32_t u = pred[v];
     if (u == ORC_NIL || u >= n) return v;
-    int found = 0;
-    for (uint32_t e = ro[u]; e < ro[u + 1] && !found; ++e) {
-      if (col[e] != v) continue;
-      if (kind) found = (float)(df[u] + wf[e]) == df[v];
-      else found = dd[u] + wd[e] == dd[v];
-    }
-    if (!found) return v;
-    uint32_t walk = v;
-    for (size_t steps = 0; walk != source; ++steps) {
-      walk = pred[walk];
-      if (walk == ORC_NIL || walk >= n || steps > n) return v;
-    }
+    if (!tight_edge(ro, col, wd, wf, dd, df, kind, u, v)) return v;
   }
-  return -1;
+  /* 0 = unknown, 1 = on the walk in progress, 2 = reaches the source */
+  uint8_t* state = (uint8_t*)calloc(n ? n : 1, 1);
+  if (source < n) state[source] = 2;
+  int64_t bad = -1;
+  for (uint32_t v = 0; v < n && bad < 0; ++v) {
+    if (state[v] || pred[v] == ORC_NIL) continue;
+    uint32_t walk = v;
+    while (state[walk] == 0) {
+      state[walk] = 1;
+      walk = pred[walk];
+      if (walk == ORC_NIL || walk >= n) break;
+    }
+    int ok = walk < n && state[walk] == 2;  /* else a cycle or a dead end */
+    if (!ok) bad = v;
+    for (uint32_t x = v; x < n && state[x] == 1; x = pred[x]) state[x] = ok ? 2 : 3;
+  }
+  free(state);
+  return bad;
 }
 
 /* ------------------------------------------------------------------------ */

@@ -216,3 +216,32 @@ def test_bfs_restatement_matches_reference_goldens():
     assert gold["path"].tolist() == [0.0, 1.0, 2.0, 3.0]  # :189-191
     with pytest.raises(IndexError):
         O.bfs(3, np.array([0, 0, 0, 0], np.uint32), np.zeros(0, np.uint32), 3)
+
+
+def test_pred_tree_checker_rejects_cycles_and_loose_edges():
+    """orc_check_pred_tree (acceptance.cpp:56-91 semantics), linear version:
+    a zero-weight tight cycle and a non-tight edge are both rejected."""
+    nil = 0xFFFFFFFF
+    ro = np.array([0, 2, 4, 5], np.uint32)
+    col = np.array([1, 2, 0, 2, 1], np.uint32)
+    w = np.array([1, 4, 5, 2, 0], np.float64)
+    d = np.array([0, 1, 3], np.float64)
+    assert O.check_pred_tree(3, ro, col, w, d, 0, np.array([nil, 0, 1], np.uint32)) == -1
+    assert O.check_pred_tree(3, ro, col, w, d, 0, np.array([nil, 2, 1], np.uint32)) == 1
+    w0 = np.array([1, 4, 5, 0, 0], np.float64)  # 1 <-> 2 both tight at distance 1
+    d0 = np.array([0, 1, 1], np.float64)
+    assert O.check_pred_tree(3, ro, col, w0, d0, 0, np.array([nil, 2, 1], np.uint32)) == 1
+    assert O.check_pred_tree(3, ro, col, w0, d0, 0, np.array([nil, 0, 1], np.uint32)) == -1
+
+
+def test_host_rmat_csr_matches_generator():
+    """orc_rmat_csr (the CPU baseline's full-size input) == the edge generator
+    sorted like build_csr (graph.hpp:364-367)."""
+    for sc in (8, 13):
+        ro, col, w = O.rmat_csr(sc, 16, 1, 1)
+        s, dd, wb = O.rmat_edges(sc, 16, seed=1, wkind=1)
+        order = np.lexsort((wb.view(np.float32), dd, s))
+        want = np.concatenate([[0], np.cumsum(np.bincount(s, minlength=1 << sc))])
+        assert np.array_equal(ro, want.astype(np.uint32))
+        assert np.array_equal(col, dd[order])
+        assert np.array_equal(w, wb.view(np.float32)[order])
