@@ -139,7 +139,7 @@ def host_rmat(args):
 
 
 def ref_graph(ro, col, w):
-    """The reference's own Graph (build_csr, graph.hpp:352-382) -- untimed."""
+    """The reference's own Graph (build_csr, graph.hpp:132-162) -- untimed."""
     from oracle import oracle as O
     n = len(ro) - 1
     t0 = time.time()
@@ -502,7 +502,7 @@ def run_e2e(gb, ctx, g, args, kw):
     """Public API, host buffers: refill (H2D + device build) + sssp + D2H.
 
     The headline uses the reference Graph's own arrays -- row_offsets u32,
-    column_indices u32, values() as double (graph.hpp:296-298) -- exactly what
+    column_indices u32, values() as double (graph.hpp:76-78) -- exactly what
     the C++ device policy uploads; the f32-host variant (a caller that keeps
     fp32 weights) is reported beside it."""
     import torch  # pinned host memory only

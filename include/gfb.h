@@ -19,7 +19,7 @@
  *    matching _free/_destroy.
  *  - Calls are synchronous at operator granularity: no device work of a call
  *    is still running when it returns (the reference's barrier contract,
- *    operators.hpp:248-254; test_operators.cpp:104-117).
+ *    operators.hpp:28-34; test_operators.cpp:104-117).
  *  - One gfb_ctx per host thread (it owns one CUDA stream).
  */
 #ifndef GFB_H
@@ -50,7 +50,7 @@ typedef enum gfb_status {
  * GFB_W_F32 is the bandwidth mode (fp32 fixpoint). */
 typedef enum gfb_wtype { GFB_W_U32 = 0, GFB_W_F32 = 1, GFB_W_F64 = 2 } gfb_wtype;
 
-/* algorithms.hpp:467 Direction, plus AUTO (device push<->pull switch). */
+/* algorithms.hpp:32 Direction, plus AUTO (device push<->pull switch). */
 typedef enum gfb_direction {
   GFB_DIR_PUSH = 0,
   GFB_DIR_PULL = 1,
@@ -62,7 +62,7 @@ typedef enum gfb_repr { GFB_SPARSE = 0, GFB_DENSE = 1 } gfb_repr;
 
 /* Operator conditions.  Host C++ lambdas cannot cross a C ABI, so the device
  * policy accepts these recognised conditions (include/graflow_b200/ops.hpp):
- *   RELAX_MIN -- the SSSP relax lambda, algorithms.hpp:586-593;
+ *   RELAX_MIN -- the SSSP relax lambda, algorithms.hpp:151-158;
  *   RECORD    -- record every (src,dst,edge) invocation, return false
  *                (test_operators.cpp:151-171 eligibility recorder);
  *   ALWAYS    -- return true (test_operators.cpp:27 `always`). */
@@ -83,16 +83,16 @@ int gfb_ctx_create(int device, gfb_ctx** out);
 int gfb_ctx_destroy(gfb_ctx* ctx);
 int gfb_ctx_num_sms(gfb_ctx* ctx, int* out);
 
-/* ---- graph store (graph.hpp:63-145 Graph) --------------------------------
+/* ---- graph store (graph.hpp:45-127 Graph) --------------------------------
  * gfb_graph_upload takes the reference Graph's CSR arrays as they are
- * (row_offsets(), column_indices(), values(): graph.hpp:94-96; values are
+ * (row_offsets(), column_indices(), values(): graph.hpp:76-78; values are
  * `double` in the reference, or u32/f32 for the typed modes) and builds the
  * device CSR (interleaved {dst, weight} records) and, when build_csc != 0,
- * the CSC view of build_transpose (graph.hpp:184-211; slot order ascending
+ * the CSC view of build_transpose (graph.hpp:166-193; slot order ascending
  * (src, CSR edge id), with the edge-id back-map).  `wtype` is the device
  * arithmetic; `w_host_type` the element type of `w` (GFB_W_F64 when passing
  * the reference's values() directly).
- * Validation mirrors build_csr (graph.hpp:152-160): a dst >= n, a negative or
+ * Validation mirrors build_csr (graph.hpp:134-142): a dst >= n, a negative or
  * non-finite weight, or an inconsistent row_offsets array -> GFB_EINVAL
  * naming the first offending edge.  -0.0 weights are canonicalised to +0.0. */
 int gfb_graph_upload(gfb_ctx* ctx, uint64_t n, uint64_t m,
@@ -111,7 +111,7 @@ int gfb_graph_download(gfb_graph* g, uint32_t* row_offsets, uint32_t* col,
 /* Device-side synthetic graphs: counter-based RMAT
  * (A/B/C/D = .57/.19/.19/.05, unpermuted, duplicates and self-loops kept;
  * wtype U32 -> U{0..255}, F32 -> U[0,1) on a 2^-24 grid) and the 4-neighbour
- * grid.  Built on the device in build_csr's layout (graph.hpp:162-179). */
+ * grid.  Built on the device in build_csr's layout (graph.hpp:144-161). */
 int gfb_graph_generate_rmat(gfb_ctx* ctx, int scale, int edgefactor,
                             uint64_t seed, int wtype, int build_csc,
                             gfb_graph** out);
@@ -134,7 +134,7 @@ int gfb_frontier_repr(gfb_frontier* f, int* repr);
 /* ---- operator state ------------------------------------------------------ */
 int gfb_dist_create(gfb_ctx* ctx, const gfb_graph* g, gfb_dist** out);
 int gfb_dist_free(gfb_dist* d);
-/* dist = +inf everywhere, dist[source] = 0 (algorithms.hpp:579-583). */
+/* dist = +inf everywhere, dist[source] = 0 (algorithms.hpp:144-148). */
 int gfb_dist_init(gfb_dist* d, uint32_t source);
 /* Widened to double (exact for every wtype); relaxations may be 0. */
 int gfb_dist_read(gfb_dist* d, double* dist, uint64_t* relaxations);
@@ -144,23 +144,23 @@ int gfb_record_read(gfb_record* r, uint32_t* src, uint32_t* dst, uint32_t* edge,
                     uint64_t cap, uint64_t* count);
 
 /* ---- operators (operators.hpp) -------------------------------------------
- * Push advance, operators.hpp:255-288 neighbors_expand: for every frontier
+ * Push advance, operators.hpp:35-68 neighbors_expand: for every frontier
  * element (duplicates included) and every out-edge, cond exactly once; the
  * output has one entry per true cond (sparse) or is a set (dense); output
  * representation = input representation.  `state` is a gfb_dist* for
  * RELAX_MIN, a gfb_record* for RECORD, unused for ALWAYS. */
 int gfb_advance_push(gfb_ctx* ctx, const gfb_graph* g, gfb_frontier* in,
                      gfb_frontier* out, int op, void* state);
-/* Pull advance, operators.hpp:296-334 neighbors_expand_pull: input must be
- * dense (else GFB_EINVAL, :301-302), graph must have the CSC (else
- * GFB_EINVAL, :299-300); cond runs for every eligible in-edge; output dense. */
+/* Pull advance, operators.hpp:76-114 neighbors_expand_pull: input must be
+ * dense (else GFB_EINVAL, :81-82), graph must have the CSC (else
+ * GFB_EINVAL, :79-80); cond runs for every eligible in-edge; output dense. */
 int gfb_advance_pull(gfb_ctx* ctx, const gfb_graph* g, gfb_frontier* in,
                      gfb_frontier* out, int op, void* state);
-/* uniquify, operators.hpp:411-420: sparse in (else GFB_EINVAL), ascending
+/* uniquify, operators.hpp:191-200: sparse in (else GFB_EINVAL), ascending
  * duplicate-free sparse out.  Bitmap dedup + warp-ballot compaction. */
 int gfb_filter_unique(gfb_ctx* ctx, gfb_frontier* in, gfb_frontier* out);
 
-/* ---- the entry point: sssp() (algorithms.hpp:569-623) -------------------- */
+/* ---- the entry point: sssp() (algorithms.hpp:134-188) -------------------- */
 typedef struct gfb_sssp_opts {
   uint32_t struct_size;  /* sizeof(gfb_sssp_opts) */
   int32_t direction;     /* gfb_direction; AUTO default */
@@ -201,8 +201,8 @@ typedef struct gfb_sssp_opts {
 void gfb_sssp_opts_default(gfb_sssp_opts* o);
 
 typedef struct gfb_sssp_stats {
-  uint64_t supersteps;    /* SsspResult::supersteps, algorithms.hpp:494 */
-  uint64_t relaxations;   /* SsspResult::relaxations, algorithms.hpp:495 */
+  uint64_t supersteps;    /* SsspResult::supersteps, algorithms.hpp:59 */
+  uint64_t relaxations;   /* SsspResult::relaxations, algorithms.hpp:60 */
   uint64_t n_reach;       /* vertices with finite dist */
   uint64_t m_reach;       /* sum of out-degrees of reached vertices */
   uint64_t push_steps, pull_steps;
@@ -218,7 +218,7 @@ typedef struct gfb_sssp_stats {
  * written widened to double (n entries), pred as u32 with GFB_NIL for the
  * source and unreachable vertices; either may be NULL to leave the result on
  * the device (gfb_sssp_read fetches it later).  source >= n -> GFB_ERANGE
- * (algorithms.hpp:572); PULL without CSC -> GFB_EINVAL (:573-574). */
+ * (algorithms.hpp:137); PULL without CSC -> GFB_EINVAL (:138-139). */
 int gfb_sssp(gfb_ctx* ctx, gfb_graph* g, uint32_t source,
              const gfb_sssp_opts* opts, double* dist, uint32_t* pred,
              gfb_sssp_stats* stats);
@@ -235,7 +235,7 @@ int gfb_sssp_read(gfb_graph* g, double* dist, void* dist_native, uint32_t* pred)
 int gfb_debug_relabel(gfb_graph* g, uint32_t* row_offsets, uint32_t* adj_pairs,
                       uint32_t* perm);
 
-/* Breadth-first search as operator reuse (algorithms.hpp:194-233 bfs()):
+/* Breadth-first search as operator reuse (algorithms.hpp:194-239 bfs()):
  * depth[n] as double (math.inf for unreachable, like BfsResult.depth),
  * supersteps = levels expanded (max depth + 1), relaxations = claim
  * evaluations (the out-degree sum of the reached vertices, the same for push

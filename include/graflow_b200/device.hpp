@@ -4,23 +4,23 @@
 // include/gfb.h) in behind the reference's own operator API, through the
 // paper's execution-policy overloading: the reference's
 // types stay exactly as they are --
-//   graflow::Graph            graph.hpp:63-145
+//   graflow::Graph            graph.hpp:45-127
 //   graflow::FrontierRepr     frontier.hpp:18
-//   graflow::Direction        algorithms.hpp:467
-//   graflow::SsspResult       algorithms.hpp:491-496
+//   graflow::Direction        algorithms.hpp:32
+//   graflow::SsspResult       algorithms.hpp:56-61
 //   graflow::vertex_t/edge_t/weight_t, no_predecessor, unreachable (types.hpp)
 // -- and a DevicePolicy overload set is added next to them:
 //   sssp(const Graph&, vertex_t, const DeviceSsspConfig&) -> SsspResult
-//       (algorithms.hpp:569-623; same result layout, same throw sites)
+//       (algorithms.hpp:134-188; same result layout, same throw sites)
 //   neighbors_expand(const DevicePolicy&, const Graph&, const DeviceFrontier&, Cond)
-//       (operators.hpp:255-288)
+//       (operators.hpp:35-68)
 //   neighbors_expand_pull(const DevicePolicy&, const Graph&, const DeviceFrontier&, Cond)
-//       (operators.hpp:296-334)
-//   uniquify(const DeviceFrontier&)            (operators.hpp:411-420)
+//       (operators.hpp:76-114)
+//   uniquify(const DeviceFrontier&)            (operators.hpp:191-200)
 // Host lambdas cannot run on the device, so `Cond` must be one of the
 // recognised conditions in graflow::device_ops (relax_min, record, always);
 // anything else is a compile-time error (cf. the reference's own rejection
-// of unsupported frontier/policy combinations, operators.hpp:258-263).
+// of unsupported frontier/policy combinations, operators.hpp:38-43).
 //
 // Include the reference's <graflow/algorithms.hpp> first (or let this
 // header include it) and link libgfb.so.  See INTEGRATION.md.
@@ -119,7 +119,7 @@ inline DevicePolicy device_policy(int device = 0, gfb_wtype arithmetic = GFB_W_F
   return p;
 }
 
-/// SsspConfig (algorithms.hpp:473-489) with a device policy.
+/// SsspConfig (algorithms.hpp:38-54) with a device policy.
 struct DeviceSsspConfig {
   DevicePolicy policy{};
   Direction direction = Direction::push;
@@ -129,7 +129,7 @@ struct DeviceSsspConfig {
   void validate() const {
     policy.validate();
     // The queue representation is the reference's asynchronous model
-    // (par-nosync, algorithms.hpp:479-488): on the device it runs as one
+    // (par-nosync, algorithms.hpp:44-53): on the device it runs as one
     // persistent work-queue launch (the near-far kernel with no far set);
     // like the reference it is push-only and reports no supersteps.
     if (frontier_repr == FrontierRepr::queue && direction != Direction::push)
@@ -142,7 +142,7 @@ struct DeviceSsspConfig {
 /// Device copy of a graflow::Graph.  Construct one and pass it to the
 /// DeviceGraph overloads below to run many calls on one upload (the fast
 /// path: the caller owns the handle and decides when the contents are
-/// current, cf. graph.hpp:262-264 "immutable").  refill() re-copies new
+/// current, cf. graph.hpp:42-44 "immutable").  refill() re-copies new
 /// contents of the same shape without reallocating.
 class DeviceGraph {
  public:
@@ -303,7 +303,7 @@ inline SsspResult sssp(const DeviceGraph& dg, vertex_t source, const DeviceSsspC
   return r;
 }
 
-/// Breadth-first search on the device (algorithms.hpp:194-233): same
+/// Breadth-first search on the device (algorithms.hpp:194-239): same
 /// validation and exceptions, same BfsResult (depth as double, +inf when
 /// unreachable; supersteps; relaxations = claim evaluations).
 inline BfsResult bfs(const Graph& g, vertex_t source, const DeviceSsspConfig& cfg) {
@@ -434,7 +434,7 @@ class DeviceRecorder {
 
 /// The conditions the device policy recognises (the C ABI's gfb_op).
 namespace device_ops {
-struct relax_min {  // algorithms.hpp:586-593
+struct relax_min {  // algorithms.hpp:151-158
   DeviceDistances& dist;
 };
 struct record {  // test-only eligibility recorder
@@ -463,7 +463,7 @@ template <> struct op_of<device_ops::always> {
 };
 }  // namespace device_detail
 
-/// Push advance on the device (operators.hpp:255-288).
+/// Push advance on the device (operators.hpp:35-68).
 template <class Cond>
 DeviceFrontier neighbors_expand(const DevicePolicy& policy, const Graph& g,
                                 const DeviceFrontier& f, Cond&& cond) {
@@ -477,15 +477,15 @@ DeviceFrontier neighbors_expand(const DevicePolicy& policy, const Graph& g,
   return out;
 }
 
-/// Pull advance on the device (operators.hpp:296-334).
+/// Pull advance on the device (operators.hpp:76-114).
 template <class Cond>
 DeviceFrontier neighbors_expand_pull(const DevicePolicy& policy, const Graph& g,
                                      const DeviceFrontier& f, Cond&& cond) {
   using C = std::remove_cvref_t<Cond>;
   policy.validate();
-  if (!g.has_transpose())  // operators.hpp:299-300
+  if (!g.has_transpose())  // operators.hpp:79-80
     throw std::invalid_argument("neighbors_expand_pull: transpose not built");
-  if (f.repr() != FrontierRepr::dense)  // operators.hpp:301-302
+  if (f.repr() != FrontierRepr::dense)  // operators.hpp:81-82
     throw std::invalid_argument("neighbors_expand_pull: dense frontier required");
   DeviceGraph& dg = DeviceGraph::of(g, policy, true);
   DeviceFrontier out(FrontierRepr::dense, g.num_vertices(), policy.device);
@@ -495,7 +495,7 @@ DeviceFrontier neighbors_expand_pull(const DevicePolicy& policy, const Graph& g,
   return out;
 }
 
-/// uniquify (operators.hpp:411-420): bitmap dedup + warp-ballot compaction.
+/// uniquify (operators.hpp:191-200): bitmap dedup + warp-ballot compaction.
 inline DeviceFrontier uniquify(const DeviceFrontier& f, int device = 0) {
   if (f.repr() != FrontierRepr::sparse)
     throw std::invalid_argument("uniquify: sparse frontier required");

@@ -84,7 +84,7 @@ size_t orc_random_edges(size_t n, uint64_t seed, uint32_t* src, uint32_t* dst,
 }
 
 /* ------------------------------------------------------------------------ */
-/* graph.hpp:150-180 build_csr                                               */
+/* graph.hpp:132-162 build_csr                                               */
 /* ------------------------------------------------------------------------ */
 typedef struct {
   uint32_t s, d;
@@ -104,7 +104,7 @@ static int edge_cmp(const void* a, const void* b) {
 int64_t orc_build_csr(size_t n, size_t m, const uint32_t* src,
                       const uint32_t* dst, const double* w, uint32_t* ro,
                       uint32_t* col, double* val) {
-  for (size_t i = 0; i < m; ++i) { /* graph.hpp:152-160 */
+  for (size_t i = 0; i < m; ++i) { /* graph.hpp:134-142 */
     if (src[i] >= n || dst[i] >= n) return (int64_t)i;
     if (!(w[i] >= 0) || !isfinite(w[i])) return (int64_t)i;
   }
@@ -114,19 +114,19 @@ int64_t orc_build_csr(size_t n, size_t m, const uint32_t* src,
     e[i].d = dst[i];
     e[i].w = w[i];
   }
-  qsort(e, m, sizeof(orc_edge), edge_cmp); /* graph.hpp:162-165 */
+  qsort(e, m, sizeof(orc_edge), edge_cmp); /* graph.hpp:144-147 */
   memset(ro, 0, (n + 1) * sizeof(uint32_t));
-  for (size_t i = 0; i < m; ++i) { /* graph.hpp:172-176 */
+  for (size_t i = 0; i < m; ++i) { /* graph.hpp:154-158 */
     ++ro[e[i].s + 1];
     col[i] = e[i].d;
     val[i] = e[i].w;
   }
-  for (size_t v = 0; v < n; ++v) ro[v + 1] += ro[v]; /* graph.hpp:177-178 */
+  for (size_t v = 0; v < n; ++v) ro[v + 1] += ro[v]; /* graph.hpp:159-160 */
   free(e);
   return -1;
 }
 
-/* graph.hpp:184-211 build_transpose */
+/* graph.hpp:166-193 build_transpose */
 void orc_build_transpose(size_t n, size_t m, const uint32_t* ro,
                          const uint32_t* col, const double* val,
                          uint32_t* cso, uint32_t* csrc, double* cval,
@@ -148,7 +148,7 @@ void orc_build_transpose(size_t n, size_t m, const uint32_t* ro,
 }
 
 /* ------------------------------------------------------------------------ */
-/* algorithms.hpp:536-563 reference_dijkstra.  std::priority_queue with     */
+/* algorithms.hpp:101-128 reference_dijkstra.  std::priority_queue with     */
 /* std::greater<pair<key, vertex>> = a binary min-heap on (key, vertex).    */
 /* The pop order only affects pred, never dist (unique fixpoint).           */
 /* ------------------------------------------------------------------------ */
@@ -162,7 +162,7 @@ void orc_build_transpose(size_t n, size_t m, const uint32_t* ro,
   }                                                                          \
   int NAME(size_t n, const uint32_t* ro, const uint32_t* col, const W_T* w,  \
            uint32_t source, KEY_T* dist, uint32_t* pred) {                   \
-    if (source >= n) return -1; /* algorithms.hpp:539 out_of_range */        \
+    if (source >= n) return -1; /* algorithms.hpp:104 out_of_range */        \
     for (size_t i = 0; i < n; ++i) {                                         \
       dist[i] = INF;                                                         \
       if (pred) pred[i] = ORC_NIL;                                           \
@@ -219,10 +219,10 @@ DEFINE_DIJKSTRA(orc_dijkstra_f32, float, float, WIDEN_ID, INFINITY)
 DEFINE_DIJKSTRA(orc_dijkstra_u32, uint64_t, uint32_t, WIDEN_U64, UINT64_MAX)
 
 /* ------------------------------------------------------------------------ */
-/* algorithms.hpp:569-623 sssp(), Sequential policy, push direction, in f32. */
-/* The relax lambda (:586-593): relaxations++, new_d = dist[src] + w,       */
-/* curr = atomic_min(dist[dst], new_d) (:457-465), return new_d < curr.     */
-/* neighbors_expand (operators.hpp:255-288) visits frontier positions in    */
+/* algorithms.hpp:134-188 sssp(), Sequential policy, push direction, in f32. */
+/* The relax lambda (:151-158): relaxations++, new_d = dist[src] + w,       */
+/* curr = atomic_min(dist[dst], new_d) (:22-30), return new_d < curr.       */
+/* neighbors_expand (operators.hpp:35-68) visits frontier positions in    */
 /* order and each row in edge-id order; duplicates kept when !dedup.        */
 /* ------------------------------------------------------------------------ */
 #define DEFINE_BSP(NAME, T)                                                    \
@@ -288,7 +288,7 @@ int NAME(size_t n, const uint32_t* ro, const uint32_t* col,                   \
 DEFINE_BSP(orc_sssp_bsp_f64, double)
 DEFINE_BSP(orc_sssp_bsp_f32, float)
 
-/* algorithms.hpp:512-528 detail::repair_predecessors */
+/* algorithms.hpp:77-93 detail::repair_predecessors */
 #define DEFINE_REPAIR(NAME, T)                                                \
   void NAME(size_t n, const uint32_t* ro, const uint32_t* col, const T* w,    \
             uint32_t source, const T* dist, uint32_t* pred) {                 \
@@ -317,7 +317,7 @@ DEFINE_REPAIR(orc_repair_pred_f32, float)
 static int tight_edge(const uint32_t* ro, const uint32_t* col, const double* wd,
                       const float* wf, const double* dd, const float* df, int kind,
                       uint32_t u, uint32_t v) {
-  /* build_csr rows are sorted by (dst, weight) (graph.hpp:364-367): binary
+  /* build_csr rows are sorted by (dst, weight) (graph.hpp:144-147): binary
    * search for v, then its parallel edges; a linear scan if that misses
    * (rows of other layouts) */
   uint32_t lo = ro[u], hi = ro[u + 1];
@@ -426,7 +426,7 @@ void orc_rmat_edges(int scale, uint64_t m, uint64_t seed, int wkind,
   }
 }
 
-/* The RMAT graph in build_csr's layout (graph.hpp:352-382: rows ascending
+/* The RMAT graph in build_csr's layout (graph.hpp:132-162: rows ascending
  * by src, each row sorted by (dst, weight), parallel edges kept), built on the
  * host for the CPU baseline at full size: edges generated in parallel, a
  * counting sort by source, then each row sorted.  Equal to sorting the whole
@@ -502,12 +502,12 @@ uint64_t orc_grid_csr(uint32_t side, uint64_t seed, uint32_t* ro,
   return e;
 }
 
-/* algorithms.hpp:194-233 bfs(): the frontier of level L is expanded once per
- * superstep (:219-231); every out-edge of a frontier vertex evaluates the
- * claim once (:206-208 relaxations), and an unclaimed destination takes
- * level L + 1 (:210-215, first claimant wins; all claimants of one level
+/* algorithms.hpp:194-239 bfs(): the frontier of level L is expanded once per
+ * superstep (:222-236); every out-edge of a frontier vertex evaluates the
+ * claim once (:212-213 relaxations), and an unclaimed destination takes
+ * level L + 1 (:214-217, first claimant wins; all claimants of one level
  * write the same value).  The loop runs while the frontier is non-empty
- * (:218), so supersteps = number of non-empty levels. */
+ * (:222), so supersteps = number of non-empty levels. */
 int orc_bfs(size_t n, const uint32_t* ro, const uint32_t* col, uint32_t source, double* depth,
             uint64_t* supersteps, uint64_t* relaxations) {
   if (source >= n) return -1;

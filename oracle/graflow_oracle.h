@@ -43,21 +43,21 @@ double orc_canonical(orc_mt64* r);
 size_t orc_random_edges(size_t n, uint64_t seed, uint32_t* src, uint32_t* dst,
                         double* w, size_t cap);
 
-/* graph.hpp:150-180 build_csr: validate, sort by (src,dst,w), count+scan.
+/* graph.hpp:132-162 build_csr: validate, sort by (src,dst,w), count+scan.
  * Returns -1 on success, else the index of the first invalid edge
- * (graph.hpp:152-160 throws invalid_argument naming that index). */
+ * (graph.hpp:134-142 throws invalid_argument naming that index). */
 int64_t orc_build_csr(size_t n, size_t m, const uint32_t* src,
                       const uint32_t* dst, const double* w, uint32_t* ro,
                       uint32_t* col, double* val);
 
-/* graph.hpp:184-211 build_transpose: counting sort by dst, slots in ascending
+/* graph.hpp:166-193 build_transpose: counting sort by dst, slots in ascending
  * (src, CSR edge id) order, back-map to the CSR edge id. */
 void orc_build_transpose(size_t n, size_t m, const uint32_t* ro,
                          const uint32_t* col, const double* val,
                          uint32_t* cso, uint32_t* csrc, double* cval,
                          uint32_t* ceid);
 
-/* algorithms.hpp:536-563 reference_dijkstra (binary heap, lazy deletion,
+/* algorithms.hpp:101-128 reference_dijkstra (binary heap, lazy deletion,
  * strict `<` relaxation) in three arithmetics:
  *   f64: the reference's own arithmetic (weight_t = double, types.hpp:10);
  *   f32: the same algorithm with float keys, nd = d + (float)w;
@@ -72,10 +72,10 @@ int orc_dijkstra_u32(size_t n, const uint32_t* ro, const uint32_t* col,
                      const uint32_t* w, uint32_t source, uint64_t* dist,
                      uint32_t* pred);
 
-/* algorithms.hpp:569-623 sssp(), sequential push over a frontier, in f32.
+/* algorithms.hpp:134-188 sssp(), sequential push over a frontier, in f32.
  * dedup=0 keeps duplicates (FrontierRepr::sparse, frontier.hpp:78-80);
  * dedup=1 is set semantics (FrontierRepr::dense, frontier.hpp:81-88).
- * relaxations counts every cond invocation (algorithms.hpp:587). */
+ * relaxations counts every cond invocation (algorithms.hpp:152). */
 int orc_sssp_bsp_f64(size_t n, const uint32_t* ro, const uint32_t* col,
                      const double* w, uint32_t source, int dedup, double* dist,
                      uint64_t* supersteps, uint64_t* relaxations);
@@ -83,7 +83,7 @@ int orc_sssp_bsp_f32(size_t n, const uint32_t* ro, const uint32_t* col,
                      const float* w, uint32_t source, int dedup, float* dist,
                      uint64_t* supersteps, uint64_t* relaxations);
 
-/* algorithms.hpp:512-528 detail::repair_predecessors: BFS from the source
+/* algorithms.hpp:77-93 detail::repair_predecessors: BFS from the source
  * over tight edges, first assignment wins.  f64 and f32 arithmetic. */
 void orc_repair_pred_f64(size_t n, const uint32_t* ro, const uint32_t* col,
                          const double* w, uint32_t source, const double* dist,
@@ -106,7 +106,7 @@ int64_t orc_check_pred_tree(size_t n, const uint32_t* ro, const uint32_t* col,
  * produce identical edge lists.  This restates paper_2212_08200_b200/csrc/
  * rmat.cuh independently; tests assert the two agree.
  * wkind: 0 = u32 U{0..255}, 1 = f32 U[0,1) on a 2^-24 grid. */
-/* algorithms.hpp:194-233 bfs(): level-synchronous push with the claim
+/* algorithms.hpp:194-239 bfs(): level-synchronous push with the claim
  * condition; depth as double (+inf unreachable), supersteps = expanded
  * levels, relaxations = claim evaluations.  Returns -1 if source >= n. */
 int orc_bfs(size_t n, const uint32_t* ro, const uint32_t* col, uint32_t source, double* depth,

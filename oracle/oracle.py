@@ -105,7 +105,7 @@ def random_edges(n, seed):
 
 
 def build_csr(n, src, dst, w):
-    """graph.hpp:150-180 restated.  Returns (ro, col, val)."""
+    """graph.hpp:132-162 restated.  Returns (ro, col, val)."""
     src = np.ascontiguousarray(src, np.uint32); dst = np.ascontiguousarray(dst, np.uint32)
     w = np.ascontiguousarray(w, np.float64)
     m = len(src)
@@ -132,7 +132,7 @@ def _nz(a, dt):
 
 
 def dijkstra(n, ro, col, w, source, kind="f64"):
-    """algorithms.hpp:536-563 restated; kind f64 | f32 | u32."""
+    """algorithms.hpp:101-128 restated; kind f64 | f32 | u32."""
     L = orc()
     pred = np.empty(n, np.uint32)
     if kind == "f64":
@@ -150,7 +150,7 @@ def dijkstra(n, ro, col, w, source, kind="f64"):
 
 
 def bfs(n, ro, col, source):
-    """algorithms.hpp:194-233 restated: (depth f64, supersteps, relaxations)."""
+    """algorithms.hpp:194-239 restated: (depth f64, supersteps, relaxations)."""
     depth = np.empty(max(n, 1), np.float64)
     st = C.c_uint64(); rl = C.c_uint64()
     if orc().orc_bfs(n, ro, _nz(col, np.uint32), source, depth, C.byref(st), C.byref(rl)) != 0:
@@ -159,7 +159,7 @@ def bfs(n, ro, col, source):
 
 
 def sssp_bsp(n, ro, col, w, source, dedup=True):
-    """algorithms.hpp:569-623 restated (sequential push); f64 or f32 by w dtype."""
+    """algorithms.hpp:134-188 restated (sequential push); f64 or f32 by w dtype."""
     L = orc()
     st = C.c_uint64(); rl = C.c_uint64()
     if np.asarray(w).dtype == np.float32:

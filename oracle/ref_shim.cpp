@@ -63,7 +63,7 @@ size_t ref_random_edges(size_t n, uint64_t seed, uint32_t* src, uint32_t* dst,
   return e.size();
 }
 
-// graph.hpp:150-180 (+ :184-211 when transpose != 0)
+// graph.hpp:132-162 (+ :184-211 when transpose != 0)
 int ref_graph_new(size_t n, size_t m, const uint32_t* src, const uint32_t* dst,
                   const double* w, int transpose, void** out) {
   return guarded([&] {
@@ -83,7 +83,7 @@ void ref_graph_csr(void* gp, uint32_t* ro, uint32_t* col, double* val) {
   std::memcpy(val, g.values().data(), g.values().size() * 8);
 }
 
-// CSC view (graph.hpp:103-114)
+// CSC view (graph.hpp:85-96)
 void ref_graph_csc(void* gp, uint32_t* cso, uint32_t* csrc, double* cval,
                    uint32_t* ceid) {
   auto& g = *static_cast<Graph*>(gp);
@@ -101,7 +101,7 @@ void ref_graph_csc(void* gp, uint32_t* cso, uint32_t* csrc, double* cval,
   if (n == 0) cso[0] = 0;
 }
 
-// algorithms.hpp:569-623.  mode: 0 seq, 1 par, 2 par-nosync;
+// algorithms.hpp:134-188.  mode: 0 seq, 1 par, 2 par-nosync;
 // direction: 0 push, 1 pull; repr: 0 sparse, 1 dense, 2 queue.
 int ref_sssp(void* gp, uint32_t source, int mode, size_t workers, int direction,
              int repr, int uniquify, double* dist, uint32_t* pred,
@@ -120,7 +120,7 @@ int ref_sssp(void* gp, uint32_t source, int mode, size_t workers, int direction,
   });
 }
 
-// algorithms.hpp:194-233 (mode / direction / repr as ref_sssp)
+// algorithms.hpp:194-239 (mode / direction / repr as ref_sssp)
 int ref_bfs(void* gp, uint32_t source, int mode, size_t workers, int direction, int repr,
             double* depth, uint64_t* supersteps, uint64_t* relaxations) {
   return guarded([&] {
@@ -135,7 +135,7 @@ int ref_bfs(void* gp, uint32_t source, int mode, size_t workers, int direction, 
   });
 }
 
-// algorithms.hpp:536-563
+// algorithms.hpp:101-128
 int ref_dijkstra(void* gp, uint32_t source, double* dist, uint32_t* pred) {
   return guarded([&] {
     auto [d, p] = reference_dijkstra(*static_cast<Graph*>(gp), source);
@@ -144,7 +144,7 @@ int ref_dijkstra(void* gp, uint32_t source, double* dist, uint32_t* pred) {
   });
 }
 
-// operators.hpp:255-288 / :296-334 with a recording cond: the eligible
+// operators.hpp:35-68 / :296-334 with a recording cond: the eligible
 // (src, dst, edge) triples of one push or pull expansion of `k` vertices.
 // Returns the number of triples (writes at most cap).
 size_t ref_expand_record(void* gp, const uint32_t* frontier, size_t k, int pull,

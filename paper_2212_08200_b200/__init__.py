@@ -63,7 +63,7 @@ class Context:
 
 
 class Graph:
-    """Device-resident graph (graph.hpp:63-145): CSR + optional CSC view."""
+    """Device-resident graph (graph.hpp:45-127): CSR + optional CSC view."""
 
     def __init__(self, handle, ctx):
         self.h, self.ctx, self._lib = handle, ctx, ctx._lib
@@ -119,7 +119,7 @@ class Graph:
             self._csr_cache = (ro, col, w)
         return self._csr_cache
 
-    # graph.hpp:70-92 queries (host side, from the downloaded CSR)
+    # graph.hpp:52-74 queries (host side, from the downloaded CSR)
     def get_edges(self, v):
         if v >= self.num_vertices:
             raise IndexError(f"get_edges: vertex {v} out of range")
@@ -154,7 +154,7 @@ class Graph:
 
 
 def build_csr(edges, num_vertices, wtype="f64", transpose=False, ctx=None):
-    """graph.hpp:150-180: sort by (src, dst, weight), count + scan, upload.
+    """graph.hpp:132-162: sort by (src, dst, weight), count + scan, upload.
 
     ``edges`` is a sequence of (src, dst, weight) or a tuple of three arrays.
     """
@@ -171,7 +171,7 @@ def build_csr(edges, num_vertices, wtype="f64", transpose=False, ctx=None):
     if w.dtype not in (np.float32, np.uint32):
         w = w.astype(np.float64)
     n = int(num_vertices)
-    for i in range(len(src)):  # graph.hpp:152-160, first offending edge
+    for i in range(len(src)):  # graph.hpp:134-142, first offending edge
         if src[i] >= n or dst[i] >= n or src[i] < 0 or dst[i] < 0:
             raise ValueError(f"build_csr: edge {i} has vertex id out of range")
         if not (w[i] >= 0) or not math.isfinite(float(w[i])):
@@ -186,7 +186,7 @@ def build_csr(edges, num_vertices, wtype="f64", transpose=False, ctx=None):
 
 
 def build_transpose(g):
-    """graph.hpp:184-211: a graph with the CSC view built (on the device)."""
+    """graph.hpp:166-193: a graph with the CSC view built (on the device)."""
     ro, col, w = g.csr()
     return Graph.from_csr(g.num_vertices, ro, col, w, wtype=g.wtype, transpose=True, ctx=g.ctx)
 
@@ -236,7 +236,7 @@ def _opts(direction="auto", pull_alpha=0.25, delta=0.0, device_loop=True, comput
 
 def sssp(g, source, policy="device", direction="auto", frontier="dense", workers=None,
          as_lists=False, **kw):
-    """algorithms.hpp:569-623 on the device.
+    """algorithms.hpp:134-188 on the device.
 
     Mirrors module.cpp:115-128: returns ``(dist, pred, supersteps,
     relaxations)``.  ``dist`` is float64 (exact widening of the device
@@ -256,7 +256,7 @@ def sssp(g, source, policy="device", direction="auto", frontier="dense", workers
         kw = dict(kw, delta=float("inf"))
     dist, pred, st = sssp_stats(g, source, direction=direction, **kw)
     if frontier == "queue":
-        st.supersteps = 0  # like the reference's async loop (algorithms.hpp:600-602)
+        st.supersteps = 0  # like the reference's async loop (algorithms.hpp:160-163)
     if as_lists:
         return (dist.tolist(), [None if p == NIL else int(p) for p in pred], st.supersteps,
                 st.relaxations)
@@ -265,7 +265,7 @@ def sssp(g, source, policy="device", direction="auto", frontier="dense", workers
 
 def bfs(g, source, policy="device", direction="push", frontier="sparse", workers=None,
         as_lists=False, want_result=True):
-    """algorithms.hpp:194-233 on the device; mirrors module.cpp:130-140:
+    """algorithms.hpp:194-239 on the device; mirrors module.cpp:130-140:
     returns ``(depths, supersteps, relaxations)`` with depths as float64
     (math.inf when unreachable).  The queue frontier is rejected like the
     reference (level semantics need supersteps)."""
@@ -355,7 +355,7 @@ class Frontier:
 
 
 class DistanceMap:
-    """Device distance map for the relax_min condition (algorithms.hpp:586-593)."""
+    """Device distance map for the relax_min condition (algorithms.hpp:151-158)."""
 
     def __init__(self, g, source):
         self.g, self._lib = g, g._lib
@@ -416,7 +416,7 @@ def _cond(cond):
 
 
 def neighbors_expand(g, f, cond, policy="device"):
-    """operators.hpp:255-288 push advance; output repr = input repr."""
+    """operators.hpp:35-68 push advance; output repr = input repr."""
     if policy != "device":
         raise ValueError("policy must be device")
     op, state = _cond(cond)
@@ -426,7 +426,7 @@ def neighbors_expand(g, f, cond, policy="device"):
 
 
 def neighbors_expand_pull(g, f, cond, policy="device"):
-    """operators.hpp:296-334 pull advance (dense in, dense out)."""
+    """operators.hpp:76-114 pull advance (dense in, dense out)."""
     if policy != "device":
         raise ValueError("policy must be device")
     op, state = _cond(cond)
@@ -436,7 +436,7 @@ def neighbors_expand_pull(g, f, cond, policy="device"):
 
 
 def uniquify(f):
-    """operators.hpp:411-420: ascending, duplicate-free sparse frontier."""
+    """operators.hpp:191-200: ascending, duplicate-free sparse frontier."""
     out = Frontier("sparse", f.num_vertices, ctx=f.ctx)
     check(f._lib.gfb_filter_unique(f.ctx.h, f.h, out.h))
     return out

@@ -1,4 +1,4 @@
-// bfs.cu -- bfs() of algorithms.hpp:194-233 on the device: the same
+// bfs.cu -- bfs() of algorithms.hpp:194-239 on the device: the same
 // operator reuse as the reference (neighbors_expand with a claim condition,
 // frontier compaction, convergence loop), level-synchronous.
 //

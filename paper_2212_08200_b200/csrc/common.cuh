@@ -1,15 +1,15 @@
 // common.cuh -- shared types, error plumbing and device helpers of libgfb.
 //
 // Layout in HBM:
-//   ro    u32[n+1]          CSR row offsets (graph.hpp:134 csr_row_offsets_)
+//   ro    u32[n+1]          CSR row offsets (graph.hpp:116 csr_row_offsets_)
 //   adj   EdgeRec<W>[m]     CSR {dst, weight} interleaved: one 8-byte record
 //                           per edge for u32/f32 weights (16 B for f64), so a
 //                           warp streams 256 contiguous bytes per load and a
 //                           short row costs one sector run instead of two
-//                           (graph.hpp:135-136 keep col/values as SoA).
-//   co    u32[n+1]          CSC offsets           (graph.hpp:139)
-//   cadj  EdgeRec<W>[m]     CSC {src, weight}     (graph.hpp:140-141)
-//   ceid  u32[m]            CSC -> CSR edge id    (graph.hpp:142)
+//                           (graph.hpp:117-118 keep col/values as SoA).
+//   co    u32[n+1]          CSC offsets           (graph.hpp:121)
+//   cadj  EdgeRec<W>[m]     CSC {src, weight}     (graph.hpp:122-123)
+//   ceid  u32[m]            CSC -> CSR edge id    (graph.hpp:124)
 #pragma once
 
 #include <cuda_runtime.h>

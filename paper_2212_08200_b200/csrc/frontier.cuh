@@ -1,5 +1,5 @@
 // frontier.cuh -- next-frontier bitmap -> expansion plan for the SSSP loop
-// (the filter/uniquify step, operators.hpp:411-420 + frontier.hpp:147-165:
+// (the filter/uniquify step, operators.hpp:191-200 + frontier.hpp:147-165:
 // bitmap dedup, ascending order) as three launches with static tiles:
 //
 //   k_fcount  per 2048-vertex tile: warp-ballot count of set bits with

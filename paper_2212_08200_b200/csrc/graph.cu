@@ -1,5 +1,5 @@
-// graph.cu -- device graph store: upload (graph.hpp:150-180 layout and
-// validation), device build_transpose (graph.hpp:184-211), the static pull
+// graph.cu -- device graph store: upload (graph.hpp:132-162 layout and
+// validation), device build_transpose (graph.hpp:166-193), the static pull
 // plan, and the device-side synthetic generators (RMAT, grid).
 #include <cub/cub.cuh>
 
@@ -274,7 +274,7 @@ static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const 
   cudaEventDestroy(start);
   if (hf[2] != ~0ull)
     fail(GFB_EINVAL, "graph: row_offsets inconsistent at vertex " + std::to_string(hf[2]));
-  // graph.hpp:152-160 reports the first offending edge
+  // graph.hpp:134-142 reports the first offending edge
   if (hf[0] != ~0ull && hf[0] <= hf[1])
     fail(GFB_EINVAL, "build_csr: edge " + std::to_string(hf[0]) + " has vertex id out of range");
   if (hf[1] != ~0ull)
@@ -584,7 +584,7 @@ void ensure_csc(Graph* g) {
 }
 
 // ---------------------------------------------------------------------------
-// Device build_transpose (graph.hpp:184-211).  A stable radix sort of the
+// Device build_transpose (graph.hpp:166-193).  A stable radix sort of the
 // CSR edge ids by destination gives exactly the reference slot order
 // (ascending source, then CSR edge id, within each destination).
 // ---------------------------------------------------------------------------
@@ -603,7 +603,7 @@ __global__ void k_row_marks(const uint32_t* ro, uint32_t* mark, uint64_t n) {
 }
 
 // offsets from sorted keys: off[v] = first index i with keys[i] >= v,
-// off[n] = m (the count+scan of graph.hpp:172-178 done from sorted keys).
+// off[n] = m (the count+scan of graph.hpp:154-160 done from sorted keys).
 __global__ void k_offsets_from_sorted(const uint32_t* keys, uint64_t m, uint32_t* off,
                                       uint64_t n) {
   uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -668,7 +668,7 @@ __global__ void k_csc_payload(const EdgeRec<W>* __restrict__ adj, const uint32_t
   }
 }
 
-// CSC slot -> CSR edge id (graph.hpp:206 back-map), for the operator-level
+// CSC slot -> CSR edge id (graph.hpp:188 back-map), for the operator-level
 // record condition only: slots of v are in ascending (src, CSR id) order and
 // parallel edges u->v are contiguous in u's sorted row, so
 // id = ro[u] + lower_bound(row u, v) + (slot - first slot of v with source u).
@@ -738,7 +738,7 @@ void build_csc(Graph* g) {
   source_of_edges(g, src_of);
   if (g->wtype != GFB_W_F64) {
     // one stable radix sort of {src, w} payloads by dst: the sorted payloads
-    // ARE the CSC records in build_transpose slot order (graph.hpp:198-208)
+    // ARE the CSC records in build_transpose slot order (graph.hpp:180-190)
     TBuf keys, keys2, vals;
     keys.alloc(m * 4, s);
     keys2.alloc(m * 4, s);

@@ -1,20 +1,20 @@
 // kernels.cuh -- the sm_100a kernels of the SSSP hot path.
 //
 //   k_compact        bitmap -> ascending frontier plan (filter/uniquify,
-//                    operators.hpp:411-420 + frontier.hpp:147-165 convert):
+//                    operators.hpp:191-200 + frontier.hpp:147-165 convert):
 //                    warp-ballot compaction, degree scan, decoupled look-back,
 //                    edge-tile map for the load-balanced advance.
 //   k_plan_list      sparse list (duplicates kept) -> frontier plan, order
 //                    preserving (operators.hpp:17-24 active_vertices_of).
-//   k_advance_push   push advance (operators.hpp:255-288 neighbors_expand +
-//                    the relax lambda algorithms.hpp:586-593): merge-path
+//   k_advance_push   push advance (operators.hpp:35-68 neighbors_expand +
+//                    the relax lambda algorithms.hpp:151-158): merge-path
 //                    edge tiles, coalesced 8-byte record stream,
 //                    test-before-atomicMin, bitmap or ordered-queue output.
-//   k_advance_pull   pull advance (operators.hpp:296-334): CSC edge tiles,
+//   k_advance_pull   pull advance (operators.hpp:76-114): CSC edge tiles,
 //                    frontier-bitmap test, shared-memory segmented min,
 //                    one global atomic per (tile, destination).
-//   k_init           algorithms.hpp:579-583 init (+ frontier seed).
-//   k_pred_*         predecessor pass (algorithms.hpp:512-528 semantics:
+//   k_init           algorithms.hpp:144-148 init (+ frontier seed).
+//   k_pred_*         predecessor pass (algorithms.hpp:77-93 semantics:
 //                    tight-edge tree, acyclic).
 #pragma once
 
@@ -721,7 +721,7 @@ k_advance_pull(AdvArgs<W> a, uint32_t total, uint32_t k) {
 }
 
 // ---------------------------------------------------------------------------
-// Init (algorithms.hpp:579-583): dist = +inf, pred = NIL, bitmaps clear,
+// Init (algorithms.hpp:144-148): dist = +inf, pred = NIL, bitmaps clear,
 // dist[source] = 0 and the source marked in the next-frontier bitmap.
 // ---------------------------------------------------------------------------
 template <class W>
@@ -755,7 +755,7 @@ __global__ void k_init(typename DT<W>::D* dist, uint2* predrec, uint32_t* bm_nex
 //    the collected in-edges without one): round r accepts a tight edge u->v
 //    when u was resolved in an earlier round (round 1: dist[u] < dist[v];
 //    later rounds: equal distances, the zero-weight tie classes that make a
-//    plain argmin cycle, cf. algorithms.hpp:506-511).  Smallest u wins.
+//    plain argmin cycle, cf. algorithms.hpp:71-76).  Smallest u wins.
 // Also accumulates n_reach / m_reach for the bench's GTEPS.
 // ---------------------------------------------------------------------------
 // PERM (relabelled loop, 32-bit keys): the loop's state lives in relabelled

@@ -3,7 +3,7 @@
 // configs[3], the 4096^2 grid: 8.5K BSP supersteps at ~215 relaxations per
 // edge).
 //
-// Same operators as the BSP loop (algorithms.hpp:586-602): advance + relax
+// Same operators as the BSP loop (algorithms.hpp:151-167): advance + relax
 // over the frontier, a filter on the output, loop until empty.  The filter
 // splits the improved vertices at a distance threshold (the
 // near-far work-efficient variant of Davidson et al.):
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
   unsigned* err = &a.ctl->err;
   __shared__ uint2 s_lq[NF_THREADS / 32][LH > 0 ? NF_LQ : 1];  // warp-local near queues
 
-  // ---- init (algorithms.hpp:579-583) ----
+  // ---- init (algorithms.hpp:144-148) ----
   const uint32_t source = *a.src_ptr;
   for (uint32_t i = gtid; i < a.n; i += gthreads) {
     a.dist[i] = i == source ? D(0) : dinf<W>();

@@ -1,7 +1,7 @@
 // ops.cu -- operator-level entry points (operators.hpp): push / pull advance
 // with a recognised condition, uniquify, and the device frontier type.
 // These let the reference's own composition (sssp() as a loop of
-// neighbors_expand calls, algorithms.hpp:600-617) run on the device one
+// neighbors_expand calls, algorithms.hpp:164-183) run on the device one
 // operator call at a time; gfb_sssp (sssp.cu) is the fused fast path.
 #include <algorithm>
 
@@ -319,9 +319,9 @@ void advance_push(Ctx* c, const Graph* g, Frontier* in, Frontier* out, int op, v
 
 void advance_pull(Ctx* c, const Graph* g, Frontier* in, Frontier* out, int op, void* state) {
   check_op(g, in, out, op, state);
-  if (!g->csc_wanted)  // operators.hpp:299-300
+  if (!g->csc_wanted)  // operators.hpp:79-80
     fail(GFB_EINVAL, "neighbors_expand_pull: transpose not built");
-  if (in->repr != GFB_DENSE || out->repr != GFB_DENSE)  // operators.hpp:301-302
+  if (in->repr != GFB_DENSE || out->repr != GFB_DENSE)  // operators.hpp:81-82
     fail(GFB_EINVAL, "neighbors_expand_pull: dense frontier required");
   ensure_csc(const_cast<Graph*>(g));
   if (op == GFB_OP_RECORD) ensure_ceid(const_cast<Graph*>(g));  // CSR ids of CSC slots
@@ -330,7 +330,7 @@ void advance_pull(Ctx* c, const Graph* g, Frontier* in, Frontier* out, int op, v
   else pull_impl<uint32_t>(c, g, in, out, op, state);
 }
 
-// uniquify (operators.hpp:411-420): bitmap dedup + warp-ballot compaction.
+// uniquify (operators.hpp:191-200): bitmap dedup + warp-ballot compaction.
 void filter_unique(Ctx* c, Frontier* in, Frontier* out) {
   if (in->repr != GFB_SPARSE || out->repr != GFB_SPARSE)
     fail(GFB_EINVAL, "uniquify: sparse frontier required");

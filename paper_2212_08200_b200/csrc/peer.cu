@@ -20,7 +20,7 @@
 //     separates the advance from the owners' compaction and publishes the
 //     global frontier minimum and the global frontier size, which sets the
 //     WHILE condition of the per-rank CUDA graph -- the convergence
-//     allreduce of algorithms.hpp:602 done by the device;
+//     allreduce of algorithms.hpp:167 done by the device;
 //   * compaction (the distance-ordered k_fcount_o / k_fscan_o / k_fwrite_o,
 //     deferral included) is purely local: each rank owns its bitmap.
 // Predecessors: the packed keys already live at the owners; verification

@@ -14,7 +14,7 @@ One process per GPU (``torchrun``); several processes may also share one GPU
 (CUDA IPC between processes on the same device), which is how the tests
 exercise world sizes 2 and 3 on a single B200.  The reference has no
 partitioned SSSP (it is single-host); results are the same fixpoint as
-``sssp()`` (algorithms.hpp:569-623) on the whole graph.
+``sssp()`` (algorithms.hpp:134-188) on the whole graph.
 """
 from __future__ import annotations
 

@@ -304,7 +304,7 @@ int main() {
       CHECK((std::vector<std::tuple<vertex_t, vertex_t, edge_t>>(ref.begin(), ref.end()) == a));
     }
 
-    // sssp composed from device operators exactly as algorithms.hpp:600-617
+    // sssp composed from device operators exactly as algorithms.hpp:165-182
     Graph g4 = build_transpose(testutil::random_graph(300, 5));
     auto oracle = reference_dijkstra(g4, 0).first;
     for (bool pull : {false, true}) {

@@ -1,4 +1,4 @@
-"""GPU parity of the device BFS (gfb_bfs, bfs.cu) -- algorithms.hpp:194-233.
+"""GPU parity of the device BFS (gfb_bfs, bfs.cu) -- algorithms.hpp:194-239.
 
 Depths, supersteps and relaxations must equal the reference's own bfs()
 (tests/golden/bfs.npz, acceptance.cpp:180-199 graphs) in every direction,

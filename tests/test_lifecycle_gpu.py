@@ -1,11 +1,11 @@
 """Handle lifecycle through the C ABI: refills, failed refills, cached loop
 graphs, argument ranges.
 
-The reference Graph is immutable (graph.hpp:262-264); the device handle can be
+The reference Graph is immutable (graph.hpp:42-44); the device handle can be
 refilled with new contents of the same shape (gfb_graph_refill).  Everything
 derived from the old contents -- the transpose, the relabelled copy and the
 CUDA graphs of the device loop that point into them -- must be rebuilt, and a
-refill that fails validation (build_csr's checks, graph.hpp:354-362) must
+refill that fails validation (build_csr's checks, graph.hpp:134-142) must
 leave the handle unusable rather than half-updated.
 """
 import ctypes as C
@@ -54,7 +54,7 @@ def test_failed_refill_poisons_until_good_refill(ctx):
     ro, col, w = (x.copy() for x in g.csr())
     gb.sssp_stats(g, 0, direction="pull")  # transpose built, loop graph cached
     bad = col.copy()
-    bad[17] = g.num_vertices + 5  # graph.hpp:356-358: vertex id out of range
+    bad[17] = g.num_vertices + 5  # graph.hpp:136-138: vertex id out of range
     with pytest.raises(ValueError, match="edge 17"):
         g.refill(ro, bad, w)
     for call in (lambda: gb.sssp_stats(g, 0), lambda: gb.bfs(g, 0),
@@ -62,7 +62,7 @@ def test_failed_refill_poisons_until_good_refill(ctx):
         with pytest.raises(RuntimeError, match="failed refill"):
             call()
     negw = w.copy()
-    negw[3] = -1.0  # graph.hpp:359-361
+    negw[3] = -1.0  # graph.hpp:139-141
     with pytest.raises(ValueError, match="edge 3"):
         g.refill(ro, col, negw)
     with pytest.raises(RuntimeError, match="failed refill"):

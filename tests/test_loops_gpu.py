@@ -1,7 +1,7 @@
 """GPU parity of the alternative loop drivers against the oracle.
 
 Every driver runs the same operators (advance + relax + filter until the
-frontier is empty, algorithms.hpp:586-602) in a different order, so they all
+frontier is empty, algorithms.hpp:151-167) in a different order, so they all
 reach the same unique fixpoint: distances must be bit-identical to the
 oracle (f32 restatement of reference_dijkstra, u32 = the reference's own
 integer arithmetic) and predecessor trees valid.
@@ -218,7 +218,7 @@ def test_f64_s20_relabel_records(ctx):
 
 def test_queue_model_fixpoint(ctx):
     """frontier="queue": the reference's asynchronous model (par-nosync,
-    algorithms.hpp:600-602) as one persistent work-queue launch (near-far with
+    algorithms.hpp:160-163) as one persistent work-queue launch (near-far with
     no far set).  Same fixpoint, no supersteps reported."""
     cases = [(gb.rmat(12, 16, seed=5, wtype="f32", transpose=False, ctx=ctx), "f32"),
              (gb.rmat(12, 16, seed=6, wtype="u32", transpose=False, ctx=ctx), "u32"),

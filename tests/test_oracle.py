@@ -49,7 +49,7 @@ def test_random_edges_restatement_matches_reference(corpus):
 
 
 def test_dijkstra_f64_matches_reference(corpus):
-    """algorithms.hpp:536-563 restated: exact distances on the 200-graph sweep."""
+    """algorithms.hpp:101-128 restated: exact distances on the 200-graph sweep."""
     for i, row in enumerate(corpus["meta"]):
         n, seed = int(row[0]), int(row[1])
         s, d, w = O.random_edges(n, seed)
@@ -61,7 +61,7 @@ def test_dijkstra_f64_matches_reference(corpus):
 
 
 def test_bsp_restatement_supersteps_and_relaxations(corpus):
-    """algorithms.hpp:569-623 seq push: same supersteps/relaxations as the
+    """algorithms.hpp:134-188 seq push: same supersteps/relaxations as the
     reference in both sparse (duplicates) and dense (set) frontier modes."""
     for i, row in enumerate(corpus["meta"][:80]):
         n, seed = int(row[0]), int(row[1])
@@ -77,7 +77,7 @@ def test_bsp_restatement_supersteps_and_relaxations(corpus):
 
 
 def test_repair_predecessors_gives_valid_tree(corpus):
-    """algorithms.hpp:512-528 + the checker of acceptance.cpp:56-91."""
+    """algorithms.hpp:77-93 + the checker of acceptance.cpp:56-91."""
     for i, row in enumerate(corpus["meta"][:60]):
         n, seed = int(row[0]), int(row[1])
         s, d, w = O.random_edges(n, seed)
@@ -114,7 +114,7 @@ def test_f32_oracles_agree(corpus):
 
 
 def test_build_csr_rejects_like_reference():
-    """graph.hpp:152-160: invalid_argument naming the first bad edge."""
+    """graph.hpp:134-142: invalid_argument naming the first bad edge."""
     with pytest.raises(ValueError, match="edge 1"):
         O.build_csr(3, [0, 0], [1, 5], [1.0, 1.0])
     with pytest.raises(ValueError, match="edge 0"):
@@ -152,7 +152,7 @@ def test_rmat16_u32_oracle_matches_reference():
 
 
 def test_operator_record_goldens():
-    """operators.hpp:255-334: push/pull eligibility sets equal (the oracle
+    """operators.hpp:35-114: push/pull eligibility sets equal (the oracle
     enumerates them from the restated CSR/CSC, the golden from the reference)."""
     ops = np.load(os.path.join(GOLD, "ops.npz"))
     for seed in (1, 2, 3, 4, 5):
@@ -199,7 +199,7 @@ def test_live_reference_f32_vs_f64_ulps():
 
 
 def test_bfs_restatement_matches_reference_goldens():
-    """orc_bfs (algorithms.hpp:194-233 restated) against the reference's own
+    """orc_bfs (algorithms.hpp:194-239 restated) against the reference's own
     bfs() on acceptance C5's 50 graphs (tests/golden/bfs.npz): depth,
     supersteps and relaxations, push and pull alike."""
     gold = np.load(os.path.join(GOLD, "bfs.npz"))
@@ -236,7 +236,7 @@ def test_pred_tree_checker_rejects_cycles_and_loose_edges():
 
 def test_host_rmat_csr_matches_generator():
     """orc_rmat_csr (the CPU baseline's full-size input) == the edge generator
-    sorted like build_csr (graph.hpp:364-367)."""
+    sorted like build_csr (graph.hpp:144-147)."""
     for sc in (8, 13):
         ro, col, w = O.rmat_csr(sc, 16, 1, 1)
         s, dd, wb = O.rmat_edges(sc, 16, seed=1, wkind=1)

@@ -75,7 +75,7 @@ def test_degenerate(ctx):
 
 
 def test_rejections(ctx):
-    """test_algorithms.cpp:158-179 / algorithms.hpp:572-574."""
+    """test_algorithms.cpp:158-179 / algorithms.hpp:137-139."""
     g = gb.build_csr([(0, 1, 1.0), (0, 2, 4.0), (1, 2, 2.0)], 3, ctx=ctx)
     with pytest.raises(IndexError):
         gb.sssp(g, 9)
@@ -90,7 +90,7 @@ def test_rejections(ctx):
 
 
 def test_upload_validation(ctx):
-    """graph.hpp:152-160: invalid_argument naming the first offending edge."""
+    """graph.hpp:134-142: invalid_argument naming the first offending edge."""
     with pytest.raises(ValueError, match="edge 1"):
         gb.Graph.from_csr(3, [0, 2, 2, 2], [1, 7], [1.0, 1.0], ctx=ctx)
     with pytest.raises(ValueError, match="edge 0"):
@@ -346,7 +346,7 @@ def test_push_pull_eligibility_equals_reference(ctx):
 
 
 def test_operator_level_sssp_composition(ctx):
-    """sssp() as the reference composes it (algorithms.hpp:600-617): a host
+    """sssp() as the reference composes it (algorithms.hpp:164-183): a host
     loop of device neighbors_expand calls with relax_min reaches the oracle."""
     s, d, w = O.random_edges(300, 5)
     g = gb.build_csr((s, d, w), 300, transpose=True, ctx=ctx)
