@@ -160,6 +160,22 @@ int gfb_advance_pull(gfb_ctx* ctx, const gfb_graph* g, gfb_frontier* in,
  * duplicate-free sparse out.  Bitmap dedup + warp-ballot compaction. */
 int gfb_filter_unique(gfb_ctx* ctx, gfb_frontier* in, gfb_frontier* out);
 
+/* filter, operators.hpp:163-188: out = the elements of `in` whose predicate
+ * holds, same representation (else GFB_EINVAL); sparse keeps the input order
+ * and duplicates (the reference's sequential order).  Host predicates cannot
+ * cross the ABI; the recognised ones read a device distance map (gfb_dist)
+ * and compare in double (exact for every arithmetic):
+ *   DIST_BELOW     dist[v] <  threshold   (the near side of a near-far split)
+ *   DIST_AT_LEAST  dist[v] >= threshold   (the far side)
+ *   REACHED        dist[v] <  +inf        (threshold unused) */
+typedef enum gfb_pred {
+  GFB_PRED_DIST_BELOW = 0,
+  GFB_PRED_DIST_AT_LEAST = 1,
+  GFB_PRED_REACHED = 2
+} gfb_pred;
+int gfb_filter(gfb_ctx* ctx, gfb_frontier* in, gfb_frontier* out, int pred,
+               const gfb_dist* dist, double threshold);
+
 /* ---- the entry point: sssp() (algorithms.hpp:134-188) -------------------- */
 typedef struct gfb_sssp_opts {
   uint32_t struct_size;  /* sizeof(gfb_sssp_opts) */

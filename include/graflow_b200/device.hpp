@@ -441,6 +441,18 @@ struct record {  // test-only eligibility recorder
   DeviceRecorder& rec;
 };
 struct always {};  // test_operators.cpp:27
+// filter predicates (operators.hpp:163-188), compared in double
+struct dist_below {  // dist[v] < threshold: the near side of a near-far split
+  DeviceDistances& dist;
+  double threshold;
+};
+struct dist_at_least {  // dist[v] >= threshold: the far side
+  DeviceDistances& dist;
+  double threshold;
+};
+struct reached {  // dist[v] < +inf
+  DeviceDistances& dist;
+};
 }  // namespace device_ops
 
 namespace device_detail {
@@ -492,6 +504,43 @@ DeviceFrontier neighbors_expand_pull(const DevicePolicy& policy, const Graph& g,
   device_detail::check(gfb_advance_pull(dg.ctx(), dg.handle(), f.handle(), out.handle(),
                                         device_detail::op_of<C>::op(),
                                         device_detail::op_of<C>::state(cond)));
+  return out;
+}
+
+namespace device_detail {
+template <class P> struct pred_of {
+  static_assert(sizeof(P) == 0,
+                "device policy: host predicates cannot run on the device; use "
+                "graflow::device_ops::{dist_below, dist_at_least, reached}");
+};
+template <> struct pred_of<device_ops::dist_below> {
+  static int id() { return GFB_PRED_DIST_BELOW; }
+  static gfb_dist* dist(const device_ops::dist_below& p) { return p.dist.handle(); }
+  static double thr(const device_ops::dist_below& p) { return p.threshold; }
+};
+template <> struct pred_of<device_ops::dist_at_least> {
+  static int id() { return GFB_PRED_DIST_AT_LEAST; }
+  static gfb_dist* dist(const device_ops::dist_at_least& p) { return p.dist.handle(); }
+  static double thr(const device_ops::dist_at_least& p) { return p.threshold; }
+};
+template <> struct pred_of<device_ops::reached> {
+  static int id() { return GFB_PRED_REACHED; }
+  static gfb_dist* dist(const device_ops::reached& p) { return p.dist.handle(); }
+  static double thr(const device_ops::reached&) { return 0.0; }
+};
+}  // namespace device_detail
+
+/// filter on the device (operators.hpp:163-188): same representation, the
+/// sparse input order and duplicates kept.
+template <class Pred>
+DeviceFrontier filter(const DevicePolicy& policy, const DeviceFrontier& f, Pred&& pred) {
+  using P = std::remove_cvref_t<Pred>;
+  policy.validate();
+  DeviceFrontier out(f.repr(), f.num_vertices(), policy.device);
+  device_detail::check(gfb_filter(device_detail::context(policy.device), f.handle(), out.handle(),
+                                  device_detail::pred_of<P>::id(),
+                                  device_detail::pred_of<P>::dist(pred),
+                                  device_detail::pred_of<P>::thr(pred)));
   return out;
 }
 

@@ -89,6 +89,9 @@ def ref():
                               C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.ref_expand_record.restype = sz
         L.ref_expand_record.argtypes = [C.c_void_p, u32p, sz, C.c_int, u32p, u32p, u32p, sz]
+        L.ref_filter.restype = sz
+        L.ref_filter.argtypes = [sz, u32p, sz, C.c_int, C.c_int, f64p, C.c_double, C.c_int, sz,
+                                 u32p, sz]
         _REF = L
     return _REF
 
@@ -289,6 +292,18 @@ class RefGraph:
         s = np.empty(max(cnt, 1), np.uint32); d = np.empty_like(s); e = np.empty_like(s)
         self.L.ref_expand_record(self.h, _nz(f, np.uint32), len(f), int(pull), s, d, e, cnt)
         return s[:cnt], d[:cnt], e[:cnt]
+
+
+def ref_filter(n, frontier, repr_, pred, dist, thr=0.0, mode=0, workers=1):
+    """The reference's own filter (operators.hpp:163-188) with a distance
+    predicate (0 below, 1 at least, 2 reached); contents in its order."""
+    L = ref()
+    f = np.ascontiguousarray(frontier, np.uint32)
+    d = np.ascontiguousarray(dist, np.float64)
+    out = np.empty(max(len(f), 1), np.uint32)
+    cnt = L.ref_filter(n, _nz(f, np.uint32), len(f), repr_, pred, d, thr, mode, workers, out,
+                       len(out))
+    return out[:cnt]
 
 
 def ref_random_edges(n, seed):

@@ -169,4 +169,22 @@ size_t ref_expand_record(void* gp, const uint32_t* frontier, size_t k, int pull,
   return cnt;
 }
 
+// operators.hpp:163-188 filter with the predicate `dist[v] < thr` (pred 0),
+// `dist[v] >= thr` (1) or `dist[v] < +inf` (2), on a sparse (repr 0) or
+// dense (1) frontier of `k` vertices; the result's contents in the
+// reference's order (dense: ascending).  Returns the count (writes <= cap).
+size_t ref_filter(size_t n, const uint32_t* frontier, size_t k, int repr, int pred,
+                  const double* dist, double thr, int mode, size_t workers, uint32_t* out,
+                  size_t cap) {
+  Frontier f(repr ? FrontierRepr::dense : FrontierRepr::sparse, n);
+  for (size_t i = 0; i < k; ++i) f.add_vertex(frontier[i]);
+  ExecutionPolicy p{static_cast<ExecutionMode>(mode), workers};
+  Frontier r = filter(p, f, [&](vertex_t v) {
+    return pred == 0 ? dist[v] < thr : pred == 1 ? dist[v] >= thr : dist[v] != unreachable;
+  });
+  const size_t cnt = r.size();
+  for (size_t i = 0; i < cnt && i < cap; ++i) out[i] = r.get_active_vertex(i);
+  return cnt;
+}
+
 }  // extern "C"

@@ -20,7 +20,7 @@ from ._lib import (DENSE, DIR_AUTO, DIR_PULL, DIR_PUSH, NIL, OP_ALWAYS, OP_RECOR
                    check)
 
 __all__ = ["Context", "Graph", "Frontier", "build_csr", "build_transpose", "rmat", "grid",
-           "sssp", "sssp_stats", "neighbors_expand", "neighbors_expand_pull", "uniquify",
+           "sssp", "sssp_stats", "neighbors_expand", "neighbors_expand_pull", "uniquify", "filter",
            "DistanceMap", "Recorder", "NIL", "GfbError"]
 
 _WT = {"u32": W_U32, "f32": W_F32, "f64": W_F64}
@@ -439,4 +439,23 @@ def uniquify(f):
     """operators.hpp:191-200: ascending, duplicate-free sparse frontier."""
     out = Frontier("sparse", f.num_vertices, ctx=f.ctx)
     check(f._lib.gfb_filter_unique(f.ctx.h, f.h, out.h))
+    return out
+
+
+_PRED = {"dist_below": 0, "dist_at_least": 1, "reached": 2}
+
+
+def filter(f, pred, dist, threshold=0.0, policy="device"):
+    """operators.hpp:163-188: the elements of ``f`` whose predicate holds,
+    same representation, sparse order and duplicates kept.  Host callables
+    cannot run on the device: ``pred`` is a recognised predicate over the
+    DistanceMap ``dist`` -- "dist_below" (dist[v] < threshold), "dist_at_least"
+    (dist[v] >= threshold) or "reached" (dist[v] < inf)."""
+    if policy != "device":
+        raise ValueError("policy must be device")
+    if pred not in _PRED:
+        raise ValueError("device policy accepts the recognised predicates only: "
+                         + ", ".join(_PRED))
+    out = Frontier(f.repr, f.num_vertices, ctx=f.ctx)
+    check(f._lib.gfb_filter(f.ctx.h, f.h, out.h, _PRED[pred], dist.h, float(threshold)))
     return out

@@ -34,6 +34,7 @@ void frontier_read(Frontier*, uint32_t*, uint64_t, uint64_t*);
 void advance_push(Ctx*, const Graph*, Frontier*, Frontier*, int, void*);
 void advance_pull(Ctx*, const Graph*, Frontier*, Frontier*, int, void*);
 void filter_unique(Ctx*, Frontier*, Frontier*);
+void filter(Ctx*, Frontier*, Frontier*, int, const Dist*, double);
 Dist* dist_create(Ctx*, const Graph*);
 void dist_init(Dist*, uint32_t);
 void dist_read(Dist*, double*, uint64_t*);
@@ -340,6 +341,18 @@ int gfb_filter_unique(gfb_ctx* ctx, gfb_frontier* in, gfb_frontier* out) {
     NEED(out);
     set_device(ctx);
     filter_unique(ctx, in, out);
+  });
+}
+
+int gfb_filter(gfb_ctx* ctx, gfb_frontier* in, gfb_frontier* out, int pred, const gfb_dist* dist,
+               double threshold) {
+  return guard([&] {
+    NEED(ctx);
+    NEED(in);
+    NEED(out);
+    if (dist) gfb::check_usable(dist->g);
+    set_device(ctx);
+    filter(ctx, in, out, pred, dist, threshold);
   });
 }
 

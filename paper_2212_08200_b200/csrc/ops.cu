@@ -4,6 +4,7 @@
 // neighbors_expand calls, algorithms.hpp:164-183) run on the device one
 // operator call at a time; gfb_sssp (sssp.cu) is the fused fast path.
 #include <algorithm>
+#include <cmath>
 
 #include "impl.hpp"
 
@@ -350,6 +351,162 @@ void filter_unique(Ctx* c, Frontier* in, Frontier* out) {
   if (len) GFB_CUDA(cudaMemcpyAsync(out->list.p, lst.p, len * 4, cudaMemcpyDeviceToDevice, s));
   out->len = len;
   c->sync();
+}
+
+// ---------------------------------------------------------------------------
+// filter (operators.hpp:163-188): keep exactly the frontier elements whose
+// predicate holds, same representation; a sparse frontier keeps its order and
+// duplicates (the reference's sequential order, :184-186).  Host predicates
+// cannot cross the ABI: the recognised ones compare a device distance map
+// with a threshold in the reference's double domain (every device arithmetic
+// widens exactly) -- the near-far split of the SSSP loop (nearfar.cuh).
+// Sparse: count per 2048-element tile -> one-CTA exclusive scan -> ordered
+// write (warp ballots); dense: one pass over the bitmap words.
+// ---------------------------------------------------------------------------
+constexpr int FL_THREADS = 256, FL_VT = 8, FL_TILE = FL_THREADS * FL_VT;
+
+template <class D>
+__device__ __forceinline__ bool filter_pred(const D* dist, uint32_t v, int pred, double thr) {
+  const D x = dist[v];  // widened exactly; the device's "unreachable" is +inf
+  const double d = x == dinf<D>() ? __longlong_as_double(0x7FF0000000000000ll) : (double)x;
+  if (pred == GFB_PRED_DIST_BELOW) return d < thr;
+  if (pred == GFB_PRED_DIST_AT_LEAST) return d >= thr;
+  return !isinf(d);  // GFB_PRED_REACHED (dist < +inf)
+}
+
+template <class D>
+__global__ void __launch_bounds__(FL_THREADS)
+k_filter_count(const uint32_t* __restrict__ list, uint64_t k, const D* __restrict__ dist, int pred,
+               double thr, uint32_t* cnt) {
+  __shared__ uint32_t s_w[FL_THREADS / 32];
+  const uint64_t base = (uint64_t)blockIdx.x * FL_TILE;
+  uint32_t c = 0;
+#pragma unroll
+  for (int r = 0; r < FL_VT; ++r) {
+    const uint64_t i = base + r * FL_THREADS + threadIdx.x;
+    if (i < k && filter_pred(dist, list[i], pred, thr)) ++c;
+  }
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < FL_THREADS / 32; ++w) t += s_w[w];
+    cnt[blockIdx.x] = t;
+  }
+}
+
+// one CTA: exclusive scan of the tile counts in place; total -> cnt[tiles]
+__global__ void __launch_bounds__(1024) k_filter_scan(uint32_t* cnt, uint32_t tiles) {
+  __shared__ uint32_t s_w[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t carry = 0;
+  for (uint32_t i0 = 0; i0 < tiles; i0 += 1024) {
+    const uint32_t i = i0 + tid;
+    const uint32_t x = i < tiles ? cnt[i] : 0u;
+    const uint32_t incl = warp_incl_scan(x, lane);
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    if (warp == 0) s_w[lane] = warp_incl_scan(s_w[lane], lane);
+    __syncthreads();
+    const uint32_t pre = carry + (warp ? s_w[warp - 1] : 0u) + incl - x;
+    if (i < tiles) cnt[i] = pre;
+    carry += s_w[31];
+    __syncthreads();
+  }
+  if (tid == 0) cnt[tiles] = carry;
+}
+
+template <class D>
+__global__ void __launch_bounds__(FL_THREADS)
+k_filter_write(const uint32_t* __restrict__ list, uint64_t k, const D* __restrict__ dist, int pred,
+               double thr, const uint32_t* __restrict__ off, uint32_t* out) {
+  __shared__ uint32_t s_w[FL_THREADS / 32];
+  __shared__ uint32_t s_run;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t base = (uint64_t)blockIdx.x * FL_TILE;
+  if (threadIdx.x == 0) s_run = off[blockIdx.x];
+  __syncthreads();
+  for (int r = 0; r < FL_VT; ++r) {  // rows of FL_THREADS consecutive elements, in order
+    const uint64_t i = base + r * FL_THREADS + threadIdx.x;
+    const uint32_t v = i < k ? list[i] : 0u;
+    const bool keep = i < k && filter_pred(dist, v, pred, thr);
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) s_w[warp] = __popc(bal);
+    __syncthreads();
+    uint32_t pre = s_run;
+    for (int w = 0; w < warp; ++w) pre += s_w[w];
+    if (keep) out[pre + __popc(bal & lanemask_lt())] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (int w = 0; w < FL_THREADS / 32; ++w) t += s_w[w];
+      s_run += t;
+    }
+    __syncthreads();
+  }
+}
+
+template <class D>
+__global__ void k_filter_bits(const uint32_t* __restrict__ in, uint64_t nwords, uint64_t n,
+                              const D* __restrict__ dist, int pred, double thr, uint32_t* out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t wi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; wi < nwords; wi += stride) {
+    uint32_t word = in[wi], keep = 0;
+    while (word) {
+      const int b = __ffs(word) - 1;
+      word &= word - 1;
+      const uint64_t v = wi * 32 + b;
+      if (v < n && filter_pred(dist, (uint32_t)v, pred, thr)) keep |= 1u << b;
+    }
+    out[wi] = keep;
+  }
+}
+
+template <class D>
+static void filter_impl(Ctx* c, Frontier* in, Frontier* out, int pred, const D* dist, double thr) {
+  cudaStream_t s = c->stream;
+  if (in->repr == GFB_DENSE) {
+    k_filter_bits<D><<<stride_grid(c), 256, 0, s>>>(in->bits.as<uint32_t>(), in->nwords(), in->n,
+                                                    dist, pred, thr, out->bits.as<uint32_t>());
+    GFB_CUDA(cudaGetLastError());
+    c->sync();
+    return;
+  }
+  const uint64_t k = in->len;
+  if (k == 0) {
+    out->len = 0;
+    return;
+  }
+  const uint32_t tiles = (uint32_t)((k + FL_TILE - 1) / FL_TILE);
+  TBuf cnt;
+  cnt.alloc((size_t)(tiles + 1) * 4, s);
+  k_filter_count<D><<<tiles, FL_THREADS, 0, s>>>(in->list.as<uint32_t>(), k, dist, pred, thr,
+                                                 cnt.as<uint32_t>());
+  k_filter_scan<<<1, 1024, 0, s>>>(cnt.as<uint32_t>(), tiles);
+  uint32_t total = 0;
+  GFB_CUDA(cudaMemcpyAsync(&total, cnt.as<uint32_t>() + tiles, 4, cudaMemcpyDeviceToHost, s));
+  c->sync();
+  out->reserve(std::max<uint64_t>(total, 1));
+  k_filter_write<D><<<tiles, FL_THREADS, 0, s>>>(in->list.as<uint32_t>(), k, dist, pred, thr,
+                                                 cnt.as<uint32_t>(), out->list.as<uint32_t>());
+  GFB_CUDA(cudaGetLastError());
+  out->len = total;
+  c->sync();
+}
+
+void filter(Ctx* c, Frontier* in, Frontier* out, int pred, const Dist* d, double thr) {
+  if (pred < GFB_PRED_DIST_BELOW || pred > GFB_PRED_REACHED)
+    fail(GFB_EINVAL, "filter: unrecognised predicate (device policy: dist_below, "
+                     "dist_at_least, reached)");
+  if (!d) fail(GFB_EINVAL, "filter: the distance predicates need a distance map");
+  if (in->repr != out->repr) fail(GFB_EINVAL, "filter: output representation must match input");
+  if (in->n != out->n || in->n != d->g->n) fail(GFB_EINVAL, "filter: vertex counts differ");
+  if (std::isnan(thr)) fail(GFB_EINVAL, "filter: threshold is NaN");
+  const int wt = d->g->wtype;
+  if (wt == GFB_W_F32) filter_impl<float>(c, in, out, pred, d->dist.as<float>(), thr);
+  else if (wt == GFB_W_F64) filter_impl<double>(c, in, out, pred, d->dist.as<double>(), thr);
+  else filter_impl<uint32_t>(c, in, out, pred, d->dist.as<uint32_t>(), thr);
 }
 
 // ---------------------------------------------------------------------------

@@ -321,6 +321,40 @@ int main() {
       CHECK(steps > 1);
     }
 
+    // filter (operators.hpp:163-188): the reference's own filter with the same
+    // predicate as a lambda, sparse (order + duplicates) and dense
+    {
+      DeviceDistances dist(g4, pol, 0, true);
+      DeviceFrontier cur(FrontierRepr::sparse, 300);
+      cur.assign({0});
+      while (cur.size() != 0) cur = neighbors_expand(pol, g4, cur, device_ops::relax_min{dist});
+      const DistanceMap d = dist.read();
+      std::vector<vertex_t> lst;
+      for (vertex_t v = 0; v < 300; ++v) lst.push_back((v * 37u) % 300u);
+      for (vertex_t v = 0; v < 300; v += 3) lst.push_back(v);  // duplicates
+      const double thr = d[lst[7]] == unreachable ? 1.0 : d[lst[7]];
+      for (FrontierRepr repr : {FrontierRepr::sparse, FrontierRepr::dense}) {
+        Frontier hf(repr, 300);
+        DeviceFrontier df(repr, 300);
+        for (vertex_t v : lst) hf.add_vertex(v);
+        df.assign(lst);
+        auto contents = [](const Frontier& f) {
+          std::vector<vertex_t> out;
+          for (std::size_t i = 0; i < f.size(); ++i) out.push_back(f.get_active_vertex(i));
+          return out;
+        };
+        CHECK(filter(pol, df, device_ops::dist_below{dist, thr}).contents() ==
+              contents(filter(ExecutionPolicy::sequential(), hf,
+                              [&](vertex_t v) { return d[v] < thr; })));
+        CHECK(filter(pol, df, device_ops::dist_at_least{dist, thr}).contents() ==
+              contents(filter(ExecutionPolicy::sequential(), hf,
+                              [&](vertex_t v) { return d[v] >= thr; })));
+        CHECK(filter(pol, df, device_ops::reached{dist}).contents() ==
+              contents(filter(ExecutionPolicy::sequential(), hf,
+                              [&](vertex_t v) { return d[v] != unreachable; })));
+      }
+    }
+
     DeviceFrontier dup(FrontierRepr::sparse, 10);
     dup.assign({5, 3, 5, 1, 3, 9});
     CHECK((uniquify(dup).contents() == std::vector<vertex_t>{1, 3, 5, 9}));
