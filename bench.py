@@ -2,7 +2,10 @@
 """SSSP GTEPS bench (BASELINE.json metric) for the B200 path and the reference.
 
 Default workload: BASELINE configs[2] -- RMAT scale 24, edge factor 16, fp32
-U[0,1) weights, source 0, direction auto (push/pull switch), one B200.
+U[0,1) weights, source 0, one B200.  Direction push: the push/pull switch
+(AUTO, pull when frontier edges > m / alpha at the measured break-even
+alpha = 1.05) never fires with the far-bucket deferral (no superstep
+exceeds 0.22 m); its measurement is a secondary line.
 A "step" is one full sssp() (init .. last superstep .. predecessor pass).
 
   value   GTEPS = m_reach / device time per step, graph resident in HBM
@@ -208,7 +211,9 @@ def run_reference_arm(args):
 
 def config_dict(args):
     return {"workload": f"RMAT scale {args.scale} EF{args.edgefactor} fp32 U[0,1) weights, "
-                        f"source 0, direction {args.direction} (BASELINE.json configs[2])",
+                        f"source 0, direction {args.direction} (BASELINE.json configs[2]; the "
+                        f"push/pull switch is measured as a secondary line: it never pulls "
+                        f"under the deferral)",
             "scale": args.scale, "edgefactor": args.edgefactor, "weights": "f32",
             "direction": args.direction, "seed": args.seed,
             "l2": "inputs larger than L2 (CSR ~2.1 GB at scale 24 vs 126 MB L2)"}
@@ -464,6 +469,17 @@ def secondary_configs(gb, ctx, args, g_main=None):
                     "supersteps": st.supersteps, "work_inflation": st.relaxations / st.m_reach,
                     "_dist": d64})
         g64.free()
+        # the push/pull switch at its break-even (needs the transpose; the
+        # relabelled CSR has none): with the deferral (default) and without
+        for dp in (0, 100):
+            ms, st = timed(g_main, 3, direction="auto", pull_alpha=1.05, defer_pct=dp)
+            out.append({"config": f"push/pull switch (AUTO, alpha 1.05: pull when frontier edges "
+                                  f"> 0.95 m) on the headline graph, deferral "
+                                  f"{'off' if dp == 100 else 'on (default)'}",
+                        "gteps": st.m_reach / (ms * 1e-3) / 1e9, "ms": ms,
+                        "push_steps": st.push_steps, "pull_steps": st.pull_steps,
+                        "supersteps": st.supersteps,
+                        "work_inflation": st.relaxations / st.m_reach})
     g = gb.rmat(22, args.edgefactor, seed=args.seed, wtype="f32", transpose=True, ctx=ctx)
     ms, st = timed(g, 5, direction="push")
     out.append({"config": "BASELINE configs[1]: RMAT s22 EF16 fp32, push-only",
@@ -569,8 +585,8 @@ def main():
     ap.add_argument("--scale", type=int, default=24)
     ap.add_argument("--edgefactor", type=int, default=16)
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--direction", default="auto", choices=["auto", "push", "pull"])
-    ap.add_argument("--alpha", type=float, default=0.25)
+    ap.add_argument("--direction", default="push", choices=["auto", "push", "pull"])
+    ap.add_argument("--alpha", type=float, default=1.05)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--soak", type=float, default=1.5, help="min warm-up seconds (clock samples)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the full-size oracle/CPU legs")

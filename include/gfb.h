@@ -179,8 +179,11 @@ int gfb_filter(gfb_ctx* ctx, gfb_frontier* in, gfb_frontier* out, int pred,
 /* ---- the entry point: sssp() (algorithms.hpp:134-188) -------------------- */
 typedef struct gfb_sssp_opts {
   uint32_t struct_size;  /* sizeof(gfb_sssp_opts) */
-  int32_t direction;     /* gfb_direction; AUTO default */
-  float pull_alpha;      /* AUTO: pull when frontier edges > m / pull_alpha */
+  int32_t direction;     /* gfb_direction; PUSH default (algorithms.hpp:40) */
+  float pull_alpha;      /* AUTO: pull when frontier edges > m / pull_alpha
+                            (default 1.05, the measured break-even; a plan
+                            holds each vertex once, so alpha <= 1 never
+                            pulls) */
   int32_t device_loop;   /* 1: device-side convergence (CUDA graph) */
   double delta;          /* >0: near-far filter of this width (push only; one
                             persistent launch with queue frontiers, for

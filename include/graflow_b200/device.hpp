@@ -86,8 +86,16 @@ inline gfb_ctx* context(int device) {
 struct DevicePolicy {
   int device = 0;
   gfb_wtype arithmetic = GFB_W_F64;
-  bool auto_direction = true;  // push<->pull switch on the device
-  float pull_alpha = 0.25f;    // pull when frontier edges > m / pull_alpha
+  // push<->pull switch on the device (Direction::push in the config): a
+  // superstep pulls when its frontier edges exceed m / pull_alpha.  A plan
+  // holds each vertex once, so its edges never exceed m: alpha <= 1 never
+  // pulls.  Measured break-even at RMAT s24: the pull streams
+  // all m in-edges in 1.40 ms, push takes ~1.45 ms for 0.95 m edges, so
+  // alpha ~1.05; with the far-bucket deferral no superstep exceeds 0.22 m and
+  // pulling never pays -- hence off by default (the reference's default is
+  // Direction::push, algorithms.hpp:40).
+  bool auto_direction = false;
+  float pull_alpha = 1.05f;
   double delta = 0.0;          // > 0: near-far filter (push only; high-diameter
                                // graphs, any arithmetic) -- same distances.  0: the
                                // device chooses (near-far on low-degree meshes)

@@ -211,7 +211,7 @@ _LOOP = {"auto": 0, "bsp": 1}
 _RELABEL = {"auto": 0, "on": 1, "off": 2}
 
 
-def _opts(direction="auto", pull_alpha=0.25, delta=0.0, device_loop=True, compute_pred=True,
+def _opts(direction="push", pull_alpha=1.05, delta=0.0, device_loop=True, compute_pred=True,
           loop="auto", relabel="auto", defer_pct=0, advance_tile=0, trace=False):
     """gfb_sssp_opts (include/gfb.h).  The tuning knobs (loop, relabel,
     defer_pct, advance_tile) never change the result, only the schedule."""
@@ -234,7 +234,7 @@ def _opts(direction="auto", pull_alpha=0.25, delta=0.0, device_loop=True, comput
     return o
 
 
-def sssp(g, source, policy="device", direction="auto", frontier="dense", workers=None,
+def sssp(g, source, policy="device", direction="push", frontier="sparse", workers=None,
          as_lists=False, **kw):
     """algorithms.hpp:134-188 on the device.
 
@@ -242,8 +242,16 @@ def sssp(g, source, policy="device", direction="auto", frontier="dense", workers
     relaxations)``.  ``dist`` is float64 (exact widening of the device
     arithmetic), ``pred`` uint32 with NIL for the source / unreachable
     vertices (``as_lists=True`` gives Python lists with ``None`` like the
-    reference binding).  The device frontier is always deduplicated (bitmap);
-    ``frontier`` is accepted for signature compatibility (sparse | dense).
+    reference binding).  Distances equal the reference's for any frontier
+    and direction (one fixpoint).  ``supersteps`` / ``relaxations`` are the
+    DEVICE loop's counts: its frontier is always deduplicated (a bitmap, like
+    the reference's ``uniquify_frontier`` / dense modes), expanded closest
+    distance buckets first and with far buckets deferred to later supersteps
+    (DESIGN.md §4), so they are NOT the reference's sparse-mode counts (which
+    expand duplicates).  ``frontier`` selects the model: sparse | dense run
+    the BSP loop, queue the asynchronous one (no supersteps, like the
+    reference).  ``direction="auto"`` adds the push<->pull switch (pull when
+    frontier edges > m / pull_alpha).
     """
     if policy != "device":
         raise ValueError("policy must be device (the CPU policies live in the reference)")
@@ -289,7 +297,7 @@ def bfs(g, source, policy="device", direction="push", frontier="sparse", workers
     return depth, st.value, rl.value
 
 
-def sssp_stats(g, source, direction="auto", want_result=True, **kw):
+def sssp_stats(g, source, direction="push", want_result=True, **kw):
     """gfb_sssp with the full statistics record (device time, n/m_reach...)."""
     if source < 0 or source >= g.num_vertices:  # algorithms.hpp:137 (a ctypes u32 would wrap)
         raise IndexError("sssp: source out of range")

@@ -360,8 +360,8 @@ void gfb_sssp_opts_default(gfb_sssp_opts* o) {
   if (!o) return;
   std::memset(o, 0, sizeof(*o));
   o->struct_size = sizeof(*o);
-  o->direction = GFB_DIR_AUTO;
-  o->pull_alpha = 0.25f;
+  o->direction = GFB_DIR_PUSH;  // the reference's default (algorithms.hpp:40)
+  o->pull_alpha = 1.05f;         // AUTO: the measured push/pull break-even
   o->device_loop = 1;
   o->delta = 0.0;
   o->compute_pred = 1;

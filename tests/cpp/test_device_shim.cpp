@@ -54,6 +54,9 @@ static std::vector<DeviceSsspConfig> device_configs() {
       DeviceSsspConfig c;
       c.direction = dir;
       c.policy.auto_direction = autod;
+      // AUTO pulls when a superstep's frontier edges exceed m / alpha: alpha = 8
+      // makes the switch fire on these small graphs (alpha <= 1 never pulls)
+      if (autod) c.policy.pull_alpha = 8.0f;
       out.push_back(c);
     }
   return out;

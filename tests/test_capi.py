@@ -72,7 +72,8 @@ def test_opts_default(lib):
     o = _lib.SsspOpts()
     _lib.load().gfb_sssp_opts_default(C.byref(o))
     assert o.struct_size == C.sizeof(_lib.SsspOpts)
-    assert o.direction == _lib.DIR_AUTO and o.compute_pred == 1
+    assert o.direction == _lib.DIR_PUSH and o.compute_pred == 1  # algorithms.hpp:40
+    assert abs(o.pull_alpha - 1.05) < 1e-6 and o.defer_pct == 0 and o.advance_tile == 0
 
 
 def test_product_never_references_oracle():

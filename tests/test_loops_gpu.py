@@ -296,3 +296,20 @@ def test_nearfar_f64(ctx):
                 assert np.array_equal(dist, want), kw
                 assert O.check_pred_tree(n, ro, col, w64, dist, src, pred) == -1, kw
         g.free()
+
+
+@pytest.mark.parametrize("kw", [dict(pull_alpha=1.5, defer_pct=100), dict(pull_alpha=8.0),
+                                dict(pull_alpha=8.0, defer_pct=100)])
+def test_auto_switch_pulls(ctx, kw):
+    """direction="auto": a superstep pulls when its frontier edges exceed
+    m / pull_alpha (the reference's direction branch, algorithms.hpp:169-179,
+    taken per superstep on the device).  At the measured break-even (1.05)
+    only the densest deferral-free superstep of RMAT s24 qualifies (bench.py
+    secondary line); here alpha 1.5 / 8 make the switch fire at s16.  Both
+    directions must run and the distances stay bit-exact."""
+    g = gb.rmat(16, 16, seed=1, wtype="f32", transpose=True, ctx=ctx)
+    dist, pred, st = gb.sssp_stats(g, 0, direction="auto", **kw)
+    assert st.pull_steps > 0 and st.push_steps > 0, (st.pull_steps, st.push_steps)
+    _check(g, dist, pred)
+    _, _, st2 = gb.sssp_stats(g, 0, direction="auto", pull_alpha=1.0)
+    assert st2.pull_steps == 0  # a plan's edges never exceed m
