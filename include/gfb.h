@@ -340,6 +340,23 @@ int gfb_peer_free(gfb_peer* p);
  * (device_ms = max over partitions).  f32 / u32 device arithmetic. */
 typedef struct gfb_mg gfb_mg;
 int gfb_mg_create(int ndev, const int* devices, gfb_mg** out);
+/* The same, choosing the exchange:
+ *   GFB_EXCHANGE_PEER  device-initiated: remote relaxations are reductions
+ *                      into the owner's memory over NVLink, device barriers
+ *                      (the default, peer.cu)
+ *   GFB_EXCHANGE_NCCL  host-driven, the north star's baseline: remote
+ *                      candidates min-combined per destination into 16-byte
+ *                      messages bucketed by owner, one NCCL group of
+ *                      send/recv per superstep (all-to-all-v) and an NCCL
+ *                      allreduce of the frontier sizes for convergence
+ *                      (xmg.cu).  NCCL needs distinct devices; partitions
+ *                      that share a device exchange by device copies (same
+ *                      protocol).  device_ms is the call's wall time. */
+#define GFB_EXCHANGE_PEER 0
+#define GFB_EXCHANGE_NCCL 1
+int gfb_mg_create_ex(int ndev, const int* devices, int exchange, gfb_mg** out);
+/* 1 if the exchange runs over NCCL communicators, 0 otherwise */
+int gfb_mg_uses_nccl(gfb_mg* mg, int* out);
 int gfb_mg_graph_upload(gfb_mg* mg, uint64_t n, uint64_t m, const uint32_t* row_offsets,
                         const uint32_t* col, const void* w, int w_host_type, int wtype);
 int gfb_mg_ranges(gfb_mg* mg, uint32_t* range_starts /* ndev + 1 */);

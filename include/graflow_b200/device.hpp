@@ -104,6 +104,10 @@ struct DevicePolicy {
   // their owner's memory (gfb_mg_*, NVLink peer access; entries may repeat a
   // device).  u32 / f32 arithmetic, push, no near-far.  `device` is unused.
   std::vector<int> devices;
+  // exchange of the multi-device path: GFB_EXCHANGE_PEER (device-initiated
+  // reductions over NVLink peer memory) or GFB_EXCHANGE_NCCL (remote
+  // candidates bucketed per owner, NCCL send/recv + allreduce per superstep)
+  int exchange = GFB_EXCHANGE_PEER;
 
   void validate() const {
     if (device < 0) throw std::invalid_argument("device policy: device must be >= 0");
@@ -218,9 +222,11 @@ class DeviceGraph {
 /// handle of the same device list (one slot).
 class DeviceMgGraph {
  public:
-  explicit DeviceMgGraph(const DevicePolicy& p) : devices_(p.devices), arith_(p.arithmetic) {
+  explicit DeviceMgGraph(const DevicePolicy& p)
+      : devices_(p.devices), arith_(p.arithmetic), exchange_(p.exchange) {
     gfb_mg* h = nullptr;
-    device_detail::check(gfb_mg_create((int)p.devices.size(), p.devices.data(), &h));
+    device_detail::check(
+        gfb_mg_create_ex((int)p.devices.size(), p.devices.data(), p.exchange, &h));
     h_.reset(h);
   }
   DeviceMgGraph(const Graph& g, const DevicePolicy& p) : DeviceMgGraph(p) { upload(g); }
@@ -233,7 +239,8 @@ class DeviceMgGraph {
 
   static DeviceMgGraph& of(const Graph& g, const DevicePolicy& p) {
     thread_local std::unique_ptr<DeviceMgGraph> slot;
-    if (!slot || slot->devices_ != p.devices || slot->arith_ != p.arithmetic)
+    if (!slot || slot->devices_ != p.devices || slot->arith_ != p.arithmetic ||
+        slot->exchange_ != p.exchange)
       slot = std::make_unique<DeviceMgGraph>(p);
     slot->upload(g);
     return *slot;
@@ -246,6 +253,7 @@ class DeviceMgGraph {
   std::unique_ptr<gfb_mg, Deleter> h_;
   std::vector<int> devices_;
   int arith_;
+  int exchange_;
 };
 
 inline SsspResult sssp(const DeviceGraph& dg, vertex_t source, const DeviceSsspConfig& cfg);

@@ -73,6 +73,8 @@ SIGNATURES = {
     "gfb_advance_pull": ([_vp, _vp, _vp, _vp, _int, _vp], _int),
     "gfb_filter_unique": ([_vp, _vp, _vp], _int),
     "gfb_filter": ([_vp, _vp, _vp, _int, _vp, C.c_double], _int),
+    "gfb_mg_create_ex": ([_int, _vp, _int, C.POINTER(_vp)], _int),
+    "gfb_mg_uses_nccl": ([_vp, C.POINTER(_int)], _int),
     "gfb_sssp_opts_default": ([C.POINTER(SsspOpts)], None),
     "gfb_sssp": ([_vp, _vp, _u32, C.POINTER(SsspOpts), _vp, _vp, C.POINTER(SsspStats)], _int),
     "gfb_sssp_read": ([_vp, _vp, _vp, _vp], _int),

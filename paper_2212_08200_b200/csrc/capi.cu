@@ -579,6 +579,35 @@ int gfb_mg_create(int ndev, const int* devices, gfb_mg** out) {
   });
 }
 
+int gfb_mg_create_ex(int ndev, const int* devices, int exchange, gfb_mg** out) {
+  return guard([&] {
+    NEED(out);
+    if (exchange != GFB_EXCHANGE_PEER && exchange != GFB_EXCHANGE_NCCL)
+      gfb::fail(GFB_EINVAL, "mg: exchange must be GFB_EXCHANGE_PEER or GFB_EXCHANGE_NCCL");
+    gfb_mg* mg = nullptr;
+    const int rc = gfb_mg_create(ndev, devices, &mg);
+    if (rc != GFB_OK) gfb::fail(rc, gfb_last_error());
+    mg->exchange = exchange;
+    if (exchange == GFB_EXCHANGE_NCCL) {
+      try {
+        mg->x = gfb::xmg_create(mg->ctx);
+      } catch (...) {
+        gfb_mg_destroy(mg);
+        throw;
+      }
+    }
+    *out = mg;
+  });
+}
+
+int gfb_mg_uses_nccl(gfb_mg* mg, int* out) {
+  return guard([&] {
+    NEED(mg);
+    NEED(out);
+    *out = mg->x && gfb::xmg_uses_nccl(mg->x) ? 1 : 0;
+  });
+}
+
 int gfb_mg_graph_upload(gfb_mg* mg, uint64_t n, uint64_t m, const uint32_t* row_offsets,
                         const uint32_t* col, const void* w, int w_host_type, int wtype) {
   return guard([&] {

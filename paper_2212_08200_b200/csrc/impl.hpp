@@ -159,13 +159,25 @@ void peer_read(Peer*, double* dist, void* dist_native, uint32_t* pred);
 void peer_free(Peer*);
 Ctx* peer_ctx(Peer*);
 // One process driving every partition (peer.cu): ctx[q] runs partition q.
+// exchange: GFB_EXCHANGE_PEER (device-initiated over peer memory, peer.cu)
+// or GFB_EXCHANGE_NCCL (host-driven bucketed messages over NCCL, xmg.cu).
+struct Xmg;
 struct Mg {
   std::vector<Ctx*> ctx;  // owned through the C ABI (gfb_ctx_create / destroy)
   std::vector<Peer*> peers;
   std::vector<uint32_t> starts;
   uint64_t n = 0;
   int wtype = -1;
+  int exchange = GFB_EXCHANGE_PEER;
+  Xmg* x = nullptr;
 };
+Xmg* xmg_create(const std::vector<Ctx*>& ctx);
+void xmg_free(Xmg*);
+bool xmg_uses_nccl(const Xmg*);
+void xmg_upload(Xmg*, const std::vector<uint32_t>& starts, uint64_t n, const uint32_t* ro,
+                const uint32_t* col, const void* w, int htype, int wtype);
+void xmg_sssp(Xmg*, uint32_t source, const gfb_sssp_opts*, double* dist, uint32_t* pred,
+              gfb_sssp_stats*);
 void mg_upload(Mg*, uint64_t n, uint64_t m, const uint32_t* ro, const uint32_t* col,
                const void* w, int htype, int wtype);
 void mg_sssp(Mg*, uint32_t source, const gfb_sssp_opts*, double* dist, uint32_t* pred,

@@ -347,6 +347,18 @@ uint64_t part_pending(Part* p) {
   return h;
 }
 
+// part_pending without the host read: the device counter (for an allreduce)
+unsigned long long* part_pending_launch(Part* p) {
+  Ctx* c = p->ctx;
+  const uint32_t nwords = (uint32_t)((p->g->n + 31) / 32);
+  unsigned long long* cnt =
+      reinterpret_cast<unsigned long long*>(p->counts.as<uint32_t>() + 4096 + 4098);
+  GFB_CUDA(cudaMemsetAsync(cnt, 0, 8, c->stream));
+  k_count_bits<<<stride_grid(c), 256, 0, c->stream>>>(p->bm_next.as<uint32_t>(), nwords, cnt);
+  GFB_CUDA(cudaGetLastError());
+  return cnt;
+}
+
 void part_read(Part* p, void* dist_native, uint64_t* relax, uint64_t* supersteps) {
   Ctx* c = p->ctx;
   if (dist_native)

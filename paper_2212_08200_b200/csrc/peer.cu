@@ -885,6 +885,11 @@ void mg_upload(Mg* mg, uint64_t n, uint64_t m, const uint32_t* ro, const uint32_
   mg->starts = mg_ranges(ro, n, P);
   mg->n = n;
   mg->wtype = wtype;
+  if (mg->exchange == GFB_EXCHANGE_NCCL) {  // xmg.cu
+    if (wtype == GFB_W_F64) fail(GFB_EINVAL, "mg: f32 or u32 arithmetic only");
+    xmg_upload(mg->x, mg->starts, n, ro, col, w, htype, wtype);
+    return;
+  }
   const size_t wsz = htype == GFB_W_F64 ? 8 : 4;
   for (int q = 0; q < P; ++q) {
     const uint32_t lo = mg->starts[q], hi = mg->starts[q + 1];
@@ -901,6 +906,7 @@ void mg_upload(Mg* mg, uint64_t n, uint64_t m, const uint32_t* ro, const uint32_
 
 void mg_sssp(Mg* mg, uint32_t source, const gfb_sssp_opts* o, double* dist, uint32_t* pred,
              gfb_sssp_stats* st) {
+  if (mg->exchange == GFB_EXCHANGE_NCCL) return xmg_sssp(mg->x, source, o, dist, pred, st);
   if (mg->peers.empty()) fail(GFB_ELOGIC, "mg: no graph uploaded");
   std::vector<gfb_sssp_stats> v;
   peer_call(mg->peers, source, o, &v);
@@ -922,6 +928,10 @@ void mg_sssp(Mg* mg, uint32_t source, const gfb_sssp_opts* o, double* dist, uint
 }
 
 void mg_free(Mg* mg) {
+  if (mg->x) {
+    xmg_free(mg->x);
+    mg->x = nullptr;
+  }
   for (Peer* p : mg->peers) {
     GFB_CUDA(cudaSetDevice(p->ctx->device));
     p->ctx->sync();

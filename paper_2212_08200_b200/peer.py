@@ -141,13 +141,17 @@ class MgSssp:
     on ``devices[q]`` (entries may repeat a device).  Takes the whole
     reference-layout CSR; returns whole-graph results."""
 
-    def __init__(self, devices, row_offsets, col, w):
+    def __init__(self, devices, row_offsets, col, w, exchange="peer"):
+        """exchange: "peer" (device-initiated over peer memory) or "nccl"
+        (host-driven bucketed messages, NCCL send/recv + allreduce;
+        partitions sharing a device use device copies instead)."""
         import paper_2212_08200_b200 as gb
         self.gb = gb
         self.lib = _lib.load()
         devs = (C.c_int * len(devices))(*devices)
         h = C.c_void_p()
-        gb.check(self.lib.gfb_mg_create(len(devices), devs, C.byref(h)))
+        ex = {"peer": 0, "nccl": 1}[exchange]
+        gb.check(self.lib.gfb_mg_create_ex(len(devices), devs, ex, C.byref(h)))
         self.h = h
         self.parts = len(devices)
         ro = np.ascontiguousarray(row_offsets, np.uint32)
@@ -161,6 +165,11 @@ class MgSssp:
             self.h, self.n, self.m, C.c_void_p(ro.ctypes.data),
             C.c_void_p(col.ctypes.data) if self.m else None,
             C.c_void_p(w.ctypes.data) if self.m else None, ht, self.wtype))
+
+    def uses_nccl(self):
+        x = C.c_int()
+        self.gb.check(self.lib.gfb_mg_uses_nccl(self.h, C.byref(x)))
+        return bool(x.value)
 
     def ranges(self):
         rs = np.empty(self.parts + 1, np.uint32)

@@ -163,15 +163,19 @@ int main() {
     CHECK(valid_pred_tree(g, 0, r.dist, r.pred));
     // the partitioned loop (policy.devices, gfb_mg_*): 2 and 3 partitions
     // on device 0, same fixpoint; f64 arithmetic is rejected
-    for (int parts : {2, 3}) {
-      DeviceSsspConfig mc = cfg;
-      mc.policy.devices.assign(parts, 0);
-      auto rm = sssp(g, 0, mc);
-      CHECK(rm.dist == r.dist);
-      CHECK(valid_pred_tree(g, 0, rm.dist, rm.pred));
-      auto rm7 = sssp(g, 7, mc);
-      CHECK(rm7.dist == reference_dijkstra(g, 7).first);
-    }
+    // -- with both exchanges (device-initiated peer reductions; bucketed
+    // messages over NCCL / device copies)
+    for (int ex : {GFB_EXCHANGE_PEER, GFB_EXCHANGE_NCCL})
+      for (int parts : {2, 3}) {
+        DeviceSsspConfig mc = cfg;
+        mc.policy.devices.assign(parts, 0);
+        mc.policy.exchange = ex;
+        auto rm = sssp(g, 0, mc);
+        CHECK(rm.dist == r.dist);
+        CHECK(valid_pred_tree(g, 0, rm.dist, rm.pred));
+        auto rm7 = sssp(g, 7, mc);
+        CHECK(rm7.dist == reference_dijkstra(g, 7).first);
+      }
     {
       DeviceSsspConfig bad = cfg;
       bad.policy.devices = {0, 0};
