@@ -41,7 +41,9 @@ typedef enum gfb_status {
   GFB_ELOGIC = 3, /* std::logic_error */
   GFB_ECUDA = 4,  /* std::runtime_error (CUDA) */
   GFB_ENOMEM = 5, /* std::runtime_error (device memory) */
-  GFB_ENCCL = 6   /* std::runtime_error (NCCL) */
+  GFB_ENCCL = 6,  /* std::runtime_error (NCCL) */
+  GFB_EPARSE = 7  /* graflow::ParseError (io.hpp:27-36): "line N: ...";
+                     the line via gfb_last_error_line() */
 } gfb_status;
 
 /* Edge-weight / distance arithmetic.  The reference computes in double
@@ -117,6 +119,27 @@ int gfb_graph_generate_rmat(gfb_ctx* ctx, int scale, int edgefactor,
                             gfb_graph** out);
 int gfb_graph_generate_grid(gfb_ctx* ctx, uint32_t side, uint64_t seed,
                             int build_csc, gfb_graph** out);
+
+/* ---- Matrix Market ingest (io.hpp:17-123) --------------------------------
+ * gfb_mm_parse: parse_matrix_market on a text buffer, the reference's
+ * acceptance rules and error lines (GFB_EPARSE; MatrixMarketOptions
+ * force_unit_weights / expand_symmetric, io.hpp:22-25) into a host edge list
+ * (EdgeList, io.hpp:17-20: 0-based ids, weights as double, file order).
+ * gfb_graph_from_edges: build_csr (graph.hpp:132-162) on the device from a
+ * host edge list: validation naming the first bad edge (GFB_EINVAL), rows
+ * sorted by (dst, weight), parallel edges kept. */
+typedef struct gfb_edge_list gfb_edge_list;
+int gfb_mm_parse(const char* text, size_t len, int force_unit_weights, int expand_symmetric,
+                 gfb_edge_list** out);
+int gfb_edge_list_info(const gfb_edge_list* e, uint64_t* num_vertices, uint64_t* num_edges);
+int gfb_edge_list_read(const gfb_edge_list* e, uint32_t* src, uint32_t* dst, double* w);
+int gfb_edge_list_free(gfb_edge_list* e);
+uint64_t gfb_last_error_line(void);
+int gfb_graph_from_edges(gfb_ctx* ctx, uint64_t n, uint64_t m, const uint32_t* src,
+                         const uint32_t* dst, const double* w, int wtype, int build_csc,
+                         gfb_graph** out);
+int gfb_graph_from_edge_list(gfb_ctx* ctx, const gfb_edge_list* e, int wtype, int build_csc,
+                             gfb_graph** out);
 
 /* ---- frontier (frontier.hpp:37-218 Frontier, sparse + dense) ------------ */
 int gfb_frontier_create(gfb_ctx* ctx, uint64_t n, int repr, gfb_frontier** out);

@@ -89,6 +89,9 @@ def ref():
                               C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.ref_expand_record.restype = sz
         L.ref_expand_record.argtypes = [C.c_void_p, u32p, sz, C.c_int, u32p, u32p, u32p, sz]
+        L.ref_mm_parse.restype = C.c_longlong
+        L.ref_mm_parse.argtypes = [C.c_char_p, sz, C.c_int, C.c_int, C.POINTER(sz), u32p, u32p,
+                                   f64p, sz, C.POINTER(sz), C.c_char_p, sz]
         L.ref_filter.restype = sz
         L.ref_filter.argtypes = [sz, u32p, sz, C.c_int, C.c_int, f64p, C.c_double, C.c_int, sz,
                                  u32p, sz]
@@ -304,6 +307,25 @@ def ref_filter(n, frontier, repr_, pred, dist, thr=0.0, mode=0, workers=1):
     cnt = L.ref_filter(n, _nz(f, np.uint32), len(f), repr_, pred, d, thr, mode, workers, out,
                        len(out))
     return out[:cnt]
+
+
+def ref_mm_parse(text, force_unit_weights=False, expand_symmetric=False):
+    """The reference's parse_matrix_market (io.hpp:43-123) on a text buffer:
+    (n, src, dst, w), or ("error", line, message) on ParseError."""
+    L = ref()
+    b = text.encode() if isinstance(text, str) else bytes(text)
+    n = C.c_size_t()
+    line = C.c_size_t()
+    msg = C.create_string_buffer(512)
+    e = np.empty(1, np.uint32)
+    cnt = L.ref_mm_parse(b, len(b), int(force_unit_weights), int(expand_symmetric), C.byref(n),
+                         e, e, np.empty(1, np.float64), 0, C.byref(line), msg, 512)
+    if cnt < 0:
+        return ("error", line.value, msg.value.decode())
+    s = np.empty(max(cnt, 1), np.uint32); d = np.empty_like(s); w = np.empty(max(cnt, 1))
+    L.ref_mm_parse(b, len(b), int(force_unit_weights), int(expand_symmetric), C.byref(n), s, d, w,
+                   cnt, C.byref(line), msg, 512)
+    return n.value, s[:cnt], d[:cnt], w[:cnt]
 
 
 def ref_random_edges(n, seed):

@@ -8,6 +8,7 @@
 // restatement (graflow_oracle.c), and (2) time the reference CPU path in
 // bench.py (--impl reference and the cpu_baseline leg).
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <stdexcept>
@@ -16,6 +17,7 @@
 #include <vector>
 
 #include "graflow/algorithms.hpp"
+#include "graflow/io.hpp"
 #include "random_graphs.hpp"
 
 using namespace graflow;
@@ -185,6 +187,31 @@ size_t ref_filter(size_t n, const uint32_t* frontier, size_t k, int repr, int pr
   const size_t cnt = r.size();
   for (size_t i = 0; i < cnt && i < cap; ++i) out[i] = r.get_active_vertex(i);
   return cnt;
+}
+
+// io.hpp:43-123 parse_matrix_market on a text buffer.  Returns the edge
+// count (writes <= cap edges and *n), or -1 on ParseError with its line and
+// message (msg of msg_cap bytes).
+long long ref_mm_parse(const char* text, size_t len, int force_unit, int expand_sym, size_t* n,
+                       uint32_t* src, uint32_t* dst, double* w, size_t cap, size_t* err_line,
+                       char* msg, size_t msg_cap) {
+  try {
+    MatrixMarketOptions opt;
+    opt.force_unit_weights = force_unit != 0;
+    opt.expand_symmetric = expand_sym != 0;
+    EdgeList el = parse_matrix_market(std::string(text, len), opt);
+    *n = el.num_vertices;
+    for (size_t i = 0; i < el.edges.size() && i < cap; ++i) {
+      src[i] = el.edges[i].src;
+      dst[i] = el.edges[i].dst;
+      w[i] = el.edges[i].weight;
+    }
+    return (long long)el.edges.size();
+  } catch (const ParseError& e) {
+    *err_line = e.line();
+    std::snprintf(msg, msg_cap, "%s", e.what());
+    return -1;
+  }
 }
 
 }  // extern "C"

@@ -16,12 +16,13 @@ import numpy as np
 
 from . import _lib
 from ._lib import (DENSE, DIR_AUTO, DIR_PULL, DIR_PUSH, NIL, OP_ALWAYS, OP_RECORD,
-                   OP_RELAX_MIN, SPARSE, W_F32, W_F64, W_U32, GfbError, SsspOpts, SsspStats,
-                   check)
+                   OP_RELAX_MIN, SPARSE, W_F32, W_F64, W_U32, GfbError, ParseError, SsspOpts,
+                   SsspStats, check)
 
 __all__ = ["Context", "Graph", "Frontier", "build_csr", "build_transpose", "rmat", "grid",
            "sssp", "sssp_stats", "neighbors_expand", "neighbors_expand_pull", "uniquify", "filter",
-           "DistanceMap", "Recorder", "NIL", "GfbError"]
+           "DistanceMap", "Recorder", "NIL", "GfbError", "ParseError", "EdgeList",
+           "parse_matrix_market", "read_matrix_market", "graph_from_edges", "write_distances"]
 
 _WT = {"u32": W_U32, "f32": W_F32, "f64": W_F64}
 _WT_NP = {W_U32: np.uint32, W_F32: np.float32, W_F64: np.float64}
@@ -467,3 +468,77 @@ def filter(f, pred, dist, threshold=0.0, policy="device"):
     out = Frontier(f.repr, f.num_vertices, ctx=f.ctx)
     check(f._lib.gfb_filter(f.ctx.h, f.h, out.h, _PRED[pred], dist.h, float(threshold)))
     return out
+
+
+# ------------------------------------------------------- Matrix Market I/O --
+
+class EdgeList:
+    """io.hpp:17-20 EdgeList: ``num_vertices`` and the edges as three arrays
+    (0-based src / dst, double weights) in file order."""
+
+    def __init__(self, num_vertices, src, dst, w):
+        self.num_vertices, self.src, self.dst, self.w = num_vertices, src, dst, w
+
+    @property
+    def edges(self):
+        return list(zip(self.src.tolist(), self.dst.tolist(), self.w.tolist()))
+
+
+def parse_matrix_market(text, force_unit_weights=False, expand_symmetric=False):
+    """io.hpp:43-129 parse_matrix_market (string overload) -> EdgeList; raises
+    ParseError (with ``.line``) at the reference's lines and messages."""
+    lib = _lib.load()
+    b = text.encode() if isinstance(text, str) else bytes(text)
+    h = C.c_void_p()
+    check(lib.gfb_mm_parse(b, len(b), int(force_unit_weights), int(expand_symmetric),
+                           C.byref(h)))
+    try:
+        n, m = C.c_uint64(), C.c_uint64()
+        check(lib.gfb_edge_list_info(h, C.byref(n), C.byref(m)))
+        src = np.empty(m.value, np.uint32); dst = np.empty(m.value, np.uint32)
+        w = np.empty(m.value, np.float64)
+        check(lib.gfb_edge_list_read(h, _ptr(src), _ptr(dst), _ptr(w)))
+    finally:
+        lib.gfb_edge_list_free(h)
+    return EdgeList(n.value, src, dst, w)
+
+
+def graph_from_edges(num_vertices, src, dst, w, wtype="f64", transpose=False, ctx=None):
+    """build_csr (graph.hpp:132-162) on the device from an edge list: same
+    validation and layout as the reference (rows sorted by (dst, weight))."""
+    ctx = ctx or Context.default()
+    src = np.ascontiguousarray(src, np.uint32)
+    dst = np.ascontiguousarray(dst, np.uint32)
+    w = np.ascontiguousarray(w, np.float64)
+    if not (len(src) == len(dst) == len(w)):
+        raise ValueError("graph_from_edges: src / dst / w lengths differ")
+    h = C.c_void_p()
+    check(ctx._lib.gfb_graph_from_edges(ctx.h, int(num_vertices), len(src), _ptr(src), _ptr(dst),
+                                        _ptr(w), _WT[wtype] if isinstance(wtype, str) else wtype,
+                                        int(transpose), C.byref(h)))
+    return Graph(h, ctx)
+
+
+def read_matrix_market(path_or_text, wtype="f64", transpose=False, force_unit_weights=False,
+                       expand_symmetric=False, ctx=None):
+    """A Matrix Market file (or its text) -> device Graph: the host parser
+    (io.hpp:43-123) then build_csr on the device."""
+    text = path_or_text
+    if not (isinstance(text, (bytes, bytearray)) or "\n" in text or text.startswith("%%")):
+        with open(path_or_text, "rb") as fh:
+            text = fh.read()
+    el = parse_matrix_market(text, force_unit_weights, expand_symmetric)
+    return graph_from_edges(el.num_vertices, el.src, el.dst, el.w, wtype=wtype,
+                            transpose=transpose, ctx=ctx)
+
+
+def write_distances(dist, pred):
+    """io.hpp:131-155: one line per vertex, ``<v> <dist %g|inf> <pred|->``."""
+    if len(dist) != len(pred):
+        raise ValueError("write_distances: array length mismatch")
+    out = []
+    for v, (d, p) in enumerate(zip(dist, pred)):
+        ds = "inf" if d == math.inf else "%g" % d
+        ps = "-" if p is None or p == NIL else str(int(p))
+        out.append(f"{v} {ds} {ps}\n")
+    return "".join(out)

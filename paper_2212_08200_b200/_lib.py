@@ -12,7 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GFB_LIB") or os.path.join(HERE, "lib", "libgfb.so")
 
-GFB_OK, GFB_EINVAL, GFB_ERANGE, GFB_ELOGIC, GFB_ECUDA, GFB_ENOMEM, GFB_ENCCL = range(7)
+GFB_OK, GFB_EINVAL, GFB_ERANGE, GFB_ELOGIC, GFB_ECUDA, GFB_ENOMEM, GFB_ENCCL, GFB_EPARSE = range(8)
 W_U32, W_F32, W_F64 = 0, 1, 2
 DIR_PUSH, DIR_PULL, DIR_AUTO = 0, 1, 2
 SPARSE, DENSE = 0, 1
@@ -73,6 +73,13 @@ SIGNATURES = {
     "gfb_advance_pull": ([_vp, _vp, _vp, _vp, _int, _vp], _int),
     "gfb_filter_unique": ([_vp, _vp, _vp], _int),
     "gfb_filter": ([_vp, _vp, _vp, _int, _vp, C.c_double], _int),
+    "gfb_mm_parse": ([C.c_char_p, C.c_size_t, _int, _int, C.POINTER(_vp)], _int),
+    "gfb_edge_list_info": ([_vp, _pu64, _pu64], _int),
+    "gfb_edge_list_read": ([_vp, _vp, _vp, _vp], _int),
+    "gfb_edge_list_free": ([_vp], _int),
+    "gfb_last_error_line": ([], C.c_uint64),
+    "gfb_graph_from_edges": ([_vp, _u64, _u64, _vp, _vp, _vp, _int, _int, C.POINTER(_vp)], _int),
+    "gfb_graph_from_edge_list": ([_vp, _vp, _int, _int, C.POINTER(_vp)], _int),
     "gfb_mg_create_ex": ([_int, _vp, _int, C.POINTER(_vp)], _int),
     "gfb_mg_uses_nccl": ([_vp, C.POINTER(_int)], _int),
     "gfb_sssp_opts_default": ([C.POINTER(SsspOpts)], None),
@@ -136,6 +143,8 @@ def _exc(code, msg):
         e = IndexError(msg)          # std::out_of_range
     elif code == GFB_ELOGIC:
         e = GfbLogicError(msg)       # std::logic_error
+    elif code == GFB_EPARSE:
+        e = ParseError(msg, int(load().gfb_last_error_line()))  # graflow::ParseError
     else:
         e = GfbError(msg)            # std::runtime_error
     e.gfb_code = code
@@ -144,6 +153,14 @@ def _exc(code, msg):
 
 class GfbLogicError(RuntimeError):
     pass
+
+
+class ParseError(RuntimeError):
+    """graflow::ParseError (io.hpp:27-36): message "line N: ...", .line."""
+
+    def __init__(self, msg, line):
+        super().__init__(msg)
+        self.line = line
 
 
 def check(code):

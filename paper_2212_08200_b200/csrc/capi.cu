@@ -26,6 +26,17 @@ Graph* graph_upload(Ctx*, uint64_t, uint64_t, const uint32_t*, const uint32_t*, 
 void graph_refill(Graph*, const uint32_t*, const uint32_t*, const void*, int);
 Graph* graph_generate_rmat(Ctx*, int, int, uint64_t, int, int);
 Graph* graph_generate_grid(Ctx*, uint32_t, uint64_t, int);
+Graph* graph_from_edges(Ctx*, uint64_t, uint64_t, const uint32_t*, const uint32_t*, const double*,
+                        int, int);
+struct EdgeList;
+EdgeList* mm_parse(const char*, size_t, bool, bool);
+void edge_list_free(EdgeList*);
+void edge_list_info(const EdgeList*, uint64_t*, uint64_t*);
+void edge_list_read(const EdgeList*, uint32_t*, uint32_t*, double*);
+const uint32_t* edge_list_src(const EdgeList*);
+const uint32_t* edge_list_dst(const EdgeList*);
+const double* edge_list_w(const EdgeList*);
+uint64_t parse_error_line();
 void graph_download(Graph*, uint32_t*, uint32_t*, void*);
 Frontier* frontier_create(Ctx*, uint64_t, int);
 void frontier_assign(Frontier*, const uint32_t*, uint64_t);
@@ -185,6 +196,66 @@ int gfb_graph_generate_rmat(gfb_ctx* ctx, int scale, int ef, uint64_t seed, int 
     NEED(out);
     set_device(ctx);
     *out = static_cast<gfb_graph*>(graph_generate_rmat(ctx, scale, ef, seed, wtype, csc));
+  });
+}
+
+// ---- Matrix Market ingest (mm.cu) + device build_csr (graph.cu) ----
+struct gfb_edge_list {};  // opaque: a gfb::EdgeList
+
+int gfb_mm_parse(const char* text, size_t len, int force_unit, int expand_symmetric,
+                 gfb_edge_list** out) {
+  return guard([&] {
+    NEED(out);
+    if (!text && len) gfb::fail(GFB_EINVAL, "mm: null text");
+    *out = reinterpret_cast<gfb_edge_list*>(
+        gfb::mm_parse(text ? text : "", len, force_unit != 0, expand_symmetric != 0));
+  });
+}
+
+int gfb_edge_list_info(const gfb_edge_list* e, uint64_t* n, uint64_t* m) {
+  return guard([&] {
+    NEED(e);
+    gfb::edge_list_info(reinterpret_cast<const gfb::EdgeList*>(e), n, m);
+  });
+}
+
+int gfb_edge_list_read(const gfb_edge_list* e, uint32_t* src, uint32_t* dst, double* w) {
+  return guard([&] {
+    NEED(e);
+    gfb::edge_list_read(reinterpret_cast<const gfb::EdgeList*>(e), src, dst, w);
+  });
+}
+
+int gfb_edge_list_free(gfb_edge_list* e) {
+  return guard([&] { gfb::edge_list_free(reinterpret_cast<gfb::EdgeList*>(e)); });
+}
+
+uint64_t gfb_last_error_line(void) { return gfb::parse_error_line(); }
+
+int gfb_graph_from_edges(gfb_ctx* ctx, uint64_t n, uint64_t m, const uint32_t* src,
+                         const uint32_t* dst, const double* w, int wtype, int build_csc,
+                         gfb_graph** out) {
+  return guard([&] {
+    NEED(ctx);
+    NEED(out);
+    set_device(ctx);
+    *out = static_cast<gfb_graph*>(graph_from_edges(ctx, n, m, src, dst, w, wtype, build_csc));
+  });
+}
+
+int gfb_graph_from_edge_list(gfb_ctx* ctx, const gfb_edge_list* e, int wtype, int build_csc,
+                             gfb_graph** out) {
+  return guard([&] {
+    NEED(ctx);
+    NEED(e);
+    NEED(out);
+    set_device(ctx);
+    const auto* el = reinterpret_cast<const gfb::EdgeList*>(e);
+    uint64_t n = 0, m = 0;
+    gfb::edge_list_info(el, &n, &m);
+    *out = static_cast<gfb_graph*>(graph_from_edges(ctx, n, m, gfb::edge_list_src(el),
+                                                    gfb::edge_list_dst(el), gfb::edge_list_w(el),
+                                                    wtype, build_csc));
   });
 }
 
