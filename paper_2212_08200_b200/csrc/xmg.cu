@@ -26,7 +26,8 @@
 //
 // NCCL needs one device per communicator rank; partitions sharing a device
 // (the one-GPU tests) exchange through device copies with the same protocol.
-#include <nccl.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is bound at first use (nccl_api())
 
 #include <algorithm>
 #include <chrono>
@@ -38,10 +39,50 @@
 
 namespace gfb {
 
-#define GFB_NCCL(x)                                                                       \
-  do {                                                                                    \
-    ncclResult_t r_ = (x);                                                                \
-    if (r_ != ncclSuccess) fail(GFB_ENCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+// NCCL is bound with dlopen at the first exchange that needs it, not linked:
+// libgfb.so loaded before torch must not pin the system libnccl.so.2 into the
+// process (torch's bundled NCCL has the same soname and newer symbols).  An
+// NCCL already in the process (torch's) is preferred.
+struct NcclApi {
+  decltype(&ncclCommInitAll) CommInitAll;
+  decltype(&ncclCommDestroy) CommDestroy;
+  decltype(&ncclGroupStart) GroupStart;
+  decltype(&ncclGroupEnd) GroupEnd;
+  decltype(&ncclSend) Send;
+  decltype(&ncclRecv) Recv;
+  decltype(&ncclAllReduce) AllReduce;
+  decltype(&ncclGetErrorString) GetErrorString;
+};
+
+static const NcclApi& nccl_api() {
+  static const NcclApi api = [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) fail(GFB_ENCCL, std::string("libnccl.so.2 not loadable: ") + dlerror());
+    auto sym = [h](const char* name) {
+      void* f = dlsym(h, name);
+      if (!f) fail(GFB_ENCCL, std::string("libnccl.so.2 lacks ") + name);
+      return f;
+    };
+    NcclApi a;
+    a.CommInitAll = (decltype(a.CommInitAll))sym("ncclCommInitAll");
+    a.CommDestroy = (decltype(a.CommDestroy))sym("ncclCommDestroy");
+    a.GroupStart = (decltype(a.GroupStart))sym("ncclGroupStart");
+    a.GroupEnd = (decltype(a.GroupEnd))sym("ncclGroupEnd");
+    a.Send = (decltype(a.Send))sym("ncclSend");
+    a.Recv = (decltype(a.Recv))sym("ncclRecv");
+    a.AllReduce = (decltype(a.AllReduce))sym("ncclAllReduce");
+    a.GetErrorString = (decltype(a.GetErrorString))sym("ncclGetErrorString");
+    return a;
+  }();
+  return api;
+}
+
+#define GFB_NCCL(x)                                                                         \
+  do {                                                                                      \
+    ncclResult_t r_ = (x);                                                                  \
+    if (r_ != ncclSuccess)                                                                  \
+      fail(GFB_ENCCL, std::string(#x) + ": " + nccl_api().GetErrorString(r_));                  \
   } while (0)
 
 unsigned long long* part_pending_launch(Part* p);
@@ -59,7 +100,7 @@ struct Xmg {
   int wtype = -1;
   ~Xmg() {
     for (Part* p : parts) delete p;
-    for (ncclComm_t c : comms) ncclCommDestroy(c);
+    for (ncclComm_t c : comms) nccl_api().CommDestroy(c);
   }
 };
 
@@ -75,7 +116,7 @@ Xmg* xmg_create(const std::vector<Ctx*>& ctx) {
   x->nccl = std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
   if (x->nccl) {
     x->comms.resize(devs.size());
-    GFB_NCCL(ncclCommInitAll(x->comms.data(), (int)devs.size(), devs.data()));
+    GFB_NCCL(nccl_api().CommInitAll(x->comms.data(), (int)devs.size(), devs.data()));
   }
   return x.release();
 }
@@ -140,18 +181,18 @@ static void exchange(Xmg* x, const std::vector<std::vector<uint32_t>>& counts,
     if (roff[p][P] > x->in_cap[p]) fail(GFB_ELOGIC, "xmg: inbox overflow");
   }
   if (x->nccl) {
-    GFB_NCCL(ncclGroupStart());
+    GFB_NCCL(nccl_api().GroupStart());
     for (int q = 0; q < P; ++q)
       for (int p = 0; p < P; ++p) {
         if (p == q) continue;
         if (counts[q][p])
-          GFB_NCCL(ncclSend(x->out[q].as<char>() + soff[q][p] * 16, counts[q][p] * 16, ncclUint8,
+          GFB_NCCL(nccl_api().Send(x->out[q].as<char>() + soff[q][p] * 16, counts[q][p] * 16, ncclUint8,
                             p, x->comms[q], x->ctx[q]->stream));
         if (counts[p][q])
-          GFB_NCCL(ncclRecv(x->in[q].as<char>() + roff[q][p] * 16, counts[p][q] * 16, ncclUint8,
+          GFB_NCCL(nccl_api().Recv(x->in[q].as<char>() + roff[q][p] * 16, counts[p][q] * 16, ncclUint8,
                             p, x->comms[q], x->ctx[q]->stream));
       }
-    GFB_NCCL(ncclGroupEnd());
+    GFB_NCCL(nccl_api().GroupEnd());
   } else {  // partitions sharing devices: the same all-to-all-v as copies
     for (int p = 0; p < P; ++p) {
       set_dev(x->ctx[p]);
@@ -179,11 +220,11 @@ static uint64_t global_pending(Xmg* x) {
   }
   unsigned long long total = 0;
   if (x->nccl) {
-    GFB_NCCL(ncclGroupStart());
+    GFB_NCCL(nccl_api().GroupStart());
     for (int q = 0; q < P; ++q)
-      GFB_NCCL(ncclAllReduce(cnt[q], cnt[q], 1, ncclUint64, ncclSum, x->comms[q],
+      GFB_NCCL(nccl_api().AllReduce(cnt[q], cnt[q], 1, ncclUint64, ncclSum, x->comms[q],
                              x->ctx[q]->stream));
-    GFB_NCCL(ncclGroupEnd());
+    GFB_NCCL(nccl_api().GroupEnd());
     set_dev(x->ctx[0]);
     GFB_CUDA(cudaMemcpyAsync(&total, cnt[0], 8, cudaMemcpyDeviceToHost, x->ctx[0]->stream));
     for (int q = 0; q < P; ++q) {
@@ -282,11 +323,11 @@ void xmg_sssp(Xmg* x, uint32_t source, const gfb_sssp_opts* o, double* dist, uin
         part_pred(x->parts[q], gd[q].p, gres[q].as<uint32_t>(), gcand[q].as<uint32_t>(), round);
       }
       if (x->nccl) {
-        GFB_NCCL(ncclGroupStart());
+        GFB_NCCL(nccl_api().GroupStart());
         for (int q = 0; q < P; ++q)
-          GFB_NCCL(ncclAllReduce(gcand[q].p, gcand[q].p, x->n, ncclUint32, ncclMin, x->comms[q],
+          GFB_NCCL(nccl_api().AllReduce(gcand[q].p, gcand[q].p, x->n, ncclUint32, ncclMin, x->comms[q],
                                  x->ctx[q]->stream));
-        GFB_NCCL(ncclGroupEnd());
+        GFB_NCCL(nccl_api().GroupEnd());
         set_dev(x->ctx[0]);
         GFB_CUDA(cudaMemcpyAsync(pmin.data(), gcand[0].p, x->n * 4, cudaMemcpyDeviceToHost,
                                  x->ctx[0]->stream));

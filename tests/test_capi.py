@@ -5,6 +5,7 @@ import ctypes as C
 import os
 import re
 import subprocess
+import sys
 
 import pytest
 
@@ -47,6 +48,20 @@ def test_library_exports_every_declared_symbol(lib):
 def test_python_binding_covers_header():
     from paper_2212_08200_b200 import _lib
     assert sorted(_lib.SIGNATURES) == declared()
+
+
+def test_library_does_not_link_nccl():
+    """NCCL is bound lazily (xmg.cu nccl_api()): a libgfb.so that linked the
+    system libnccl.so.2 and was loaded before torch made `import torch` fail
+    (torch's bundled NCCL shares the soname and has newer symbols)."""
+    out = subprocess.run(["readelf", "-d", LIB], capture_output=True, text=True,
+                         check=True).stdout
+    assert "libnccl" not in out
+    code = ("import ctypes; ctypes.CDLL(%r, mode=ctypes.RTLD_GLOBAL); import torch; "
+            "print('ok')" % LIB)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
 def test_library_is_sm100a(lib):
