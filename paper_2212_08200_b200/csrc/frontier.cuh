@@ -358,6 +358,8 @@ static __global__ void k_fscan_o(unsigned long long* btot, unsigned long long* b
   }
   if (lane == 31) {
     ctl->bcut = cut;
+    ctl->k_all = (uint32_t)(all >> 32);
+    ctl->t_all = T_all;
     plan_totals((uint32_t)(upto >> 32), (uint32_t)upto, plan, ctl, m, alpha, can_pull,
                 force_pull, loop_handle, mode_handle, set_loop, set_mode);
   }

@@ -449,6 +449,52 @@ static __global__ void k_rl_big(const uint32_t* __restrict__ ro, const EdgeRec<W
   }
 }
 
+// Rows of the relabelled CSR sorted by destination: on RMAT most edges point
+// into the first few hundred thousand relabelled ids, so a sorted row lets
+// neighbouring lanes' distance gathers share sectors and L1 lines (s24:
+// 3.80 -> 3.68 ms).  Records are split into (dst, weight) arrays for a
+// segmented sort and joined back.
+template <class W>
+static __global__ void k_split_recs(const EdgeRec<W>* r, uint32_t* k, W* v, uint64_t m) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const EdgeRec<W> x = r[e];
+    k[e] = x.v;
+    v[e] = x.w;
+  }
+}
+template <class W>
+static __global__ void k_join_recs(EdgeRec<W>* r, const uint32_t* k, const W* v, uint64_t m) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    EdgeRec<W> x{};
+    x.v = k[e];
+    x.w = v[e];
+    r[e] = x;
+  }
+}
+
+template <class W>
+static void sort_rows(Ctx* c, const uint32_t* ro, EdgeRec<W>* adj, uint64_t n, uint64_t m) {
+  cudaStream_t s = c->stream;
+  TBuf k0, k1, v0, v1, t;
+  k0.alloc(m * 4, s);
+  k1.alloc(m * 4, s);
+  v0.alloc(m * sizeof(W), s);
+  v1.alloc(m * sizeof(W), s);
+  k_split_recs<W><<<stride_grid(c), 256, 0, s>>>(adj, k0.as<uint32_t>(), v0.as<W>(), m);
+  size_t tb = 0;
+  GFB_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, k0.as<uint32_t>(), k1.as<uint32_t>(),
+                                               v0.as<W>(), v1.as<W>(), (int64_t)m, (int64_t)n, ro,
+                                               ro + 1, s));
+  t.alloc(tb, s);
+  GFB_CUDA(cub::DeviceSegmentedSort::SortPairs(t.p, tb, k0.as<uint32_t>(), k1.as<uint32_t>(),
+                                               v0.as<W>(), v1.as<W>(), (int64_t)m, (int64_t)n, ro,
+                                               ro + 1, s));
+  k_join_recs<W><<<stride_grid(c), 256, 0, s>>>(adj, k1.as<uint32_t>(), v1.as<W>(), m);
+  GFB_CUDA(cudaGetLastError());
+}
+
 void ensure_relabel(Graph* g) {
   if (g->rl_valid) return;
   Ctx* c = g->ctx;
@@ -548,6 +594,12 @@ void ensure_relabel(Graph* g) {
         g->rl_adj.as<EdgeRec<uint32_t>>(), big.as<uint32_t>(), nbig);
   }
   GFB_CUDA(cudaGetLastError());
+  if (g->wtype == GFB_W_F32)
+    sort_rows<float>(c, g->rl_ro.as<uint32_t>(), g->rl_adj.as<EdgeRec<float>>(), n, m);
+  else if (g->wtype == GFB_W_F64)
+    sort_rows<double>(c, g->rl_ro.as<uint32_t>(), g->rl_adj.as<EdgeRec<double>>(), n, m);
+  else
+    sort_rows<uint32_t>(c, g->rl_ro.as<uint32_t>(), g->rl_adj.as<EdgeRec<uint32_t>>(), n, m);
   c->sync();  // temporaries are stream-ordered frees; keep the build synchronous
   g->rl_valid = true;
 }

@@ -375,6 +375,7 @@ __device__ __forceinline__ T ldc(const T* p) {
 //      that otherwise compete with the 64 MB distance array for L2)
 //   4: L2 evict_last hint on the distance gathers and reductions
 //   8: distance gathers through ld.global.nc
+//  16: software-pipelined record loads (one edge per lane, no PEER / REC)
 template <int OPT, class D>
 __device__ __forceinline__ D test_gather(const D* p) {
   if constexpr ((OPT & 8) != 0) return __ldg(p);
@@ -455,6 +456,44 @@ __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, u
                                      : total;
     const uint32_t c0 = max(__shfl_sync(0xffffffffu, off, 0), e0);
     const uint32_t c1 = min(nxt, e1);
+    if constexpr ((OPT & 16) != 0 && !REC && !PEER && VT == 1) {
+      // software-pipelined: the record of chunk x + 32 is in flight while
+      // chunk x gathers and reduces (s24: 3.72 -> 3.55 ms together with 6
+      // CTAs per SM; 8 CTAs per SM spill; two edges per lane or 4 CTAs per
+      // SM are slower, profiles/r02_advance_variants.txt)
+      auto fetch = [&](uint32_t x, EdgeRec<W>& rec, D& sd, uint32_t& su) {
+        const uint32_t le = x + lane;
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          uint32_t o = __shfl_sync(0xffffffffu, off, lo + step);
+          if (o <= le) lo += step;
+        }
+        const uint32_t so = __shfl_sync(0xffffffffu, off, lo);
+        const uint32_t ss = __shfl_sync(0xffffffffu, start, lo);
+        sd = shfl_d(du, lo);
+        su = __shfl_sync(0xffffffffu, u, lo);
+        rec.v = NIL;
+        if (le < c1) rec = ld_rec(a.adj + (ss + (le - so)));
+      };
+      EdgeRec<W> rec;
+      D sd;
+      uint32_t su;
+      fetch(c0, rec, sd, su);
+      for (uint32_t x = c0; x < c1; x += 32) {
+        const uint32_t v = rec.v;
+        const D nd = dadd(sd, rec.w, err);
+        const uint32_t uv = su;
+        if (x + 32 < c1) fetch(x + 32, rec, sd, su);
+        if (v != NIL) {
+          const D cur = test_gather<OPT>(a.dist + v);
+          if (nd < cur) {
+            relax_reds<OPT>(a.dist, pkey, a.bm_out, v, nd, uv);
+            if (fmin) *fmin = min(*fmin, fkey(nd));
+          }
+        }
+      }
+    } else
     for (uint32_t x = c0; x < c1; x += 32 * VT) {
       uint32_t dst[VT], uu[VT];
       uint32_t eid[REC ? VT : 1];

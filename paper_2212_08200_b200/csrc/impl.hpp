@@ -39,7 +39,7 @@ struct Ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev[4] = {};
+  cudaEvent_t ev[7] = {};
   cudaStream_t aux[2] = {};  // graph-capture helpers (device loop)
   // operator-API scratch
   DBuf ctl, status, qstatus;

@@ -49,6 +49,8 @@ struct Ctl {
   // peer-memory partition (peer.cu): sums over all ranks from the last
   // cross-rank barrier (k_xbar) of k / flag / unresolved / resolved
   uint32_t gk, gflag, gunres, gresolved;
+  // ordered compaction: vertices / edges in the bitmap (placed + deferred)
+  uint32_t k_all, t_all;
 };
 
 // Expansion plan: the frontier restricted to vertices with out-degree > 0.

@@ -123,17 +123,20 @@ struct Runner {
   // bucket cursors, deferral cut, plan totals (+ loop / direction decision)
   // -> write the distance-ordered plan; deferred vertices stay in the bitmap
   void compact(cudaStream_t st, int dir, float alpha, cudaGraphConditionalHandle hloop,
-               cudaGraphConditionalHandle hmode, bool set_loop, bool set_mode) {
+               cudaGraphConditionalHandle hmode, bool set_loop, bool set_mode,
+               cudaEvent_t* split = nullptr) {
     const uint32_t tiles = ws->ftiles;
     unsigned long long* bt = ws->obuck.as<unsigned long long>();
     unsigned long long* cells = ws->oagg.as<unsigned long long>();
     uint32_t* tflag = reinterpret_cast<uint32_t*>(cells + (size_t)tiles * OB_N);
     k_fcount_o<D><<<tiles, F_WARPS * 32, 0, st>>>(lro(), ws->bm_next.as<uint32_t>(), nwords,
                                                   ldist(), ws->ctl.as<Ctl>(), cells, bt, tflag);
+    if (split) GFB_CUDA(cudaEventRecord(split[0], st));
     k_fscan_o<<<1, 32, 0, st>>>(bt, bt + OB_N, plan(), ws->ctl.as<Ctl>(), (uint32_t)g->m, alpha,
                                 dir == GFB_DIR_AUTO && g->has_csc ? 1 : 0,
                                 dir == GFB_DIR_PULL ? 1 : 0, hloop, hmode, set_loop ? 1 : 0,
                                 set_mode ? 1 : 0, defer_pct(), defer_min());
+    if (split) GFB_CUDA(cudaEventRecord(split[1], st));
     k_fwrite_o<D><<<tiles, F_WARPS * 32, 0, st>>>(lro(), ws->bm_next.as<uint32_t>(),
                                                   ws->bm_cur.as<uint32_t>(), nwords, ldist(),
                                                   ws->ctl.as<Ctl>(), cells, bt + OB_N, plan(),
@@ -153,12 +156,14 @@ struct Runner {
     ++kernels;
   }
 
-  // The push advance (hot.cuh k_push_range): 8 x 256-thread CTAs per SM,
-  // strided edge tiles, PTX red.*.  Measured at RMAT s24 / s22
+  // The push advance (hot.cuh k_push_range): 6 x 256-thread CTAs per SM,
+  // strided edge tiles, PTX red.*, the next chunk's records in flight while
+  // the current one gathers (OPT 16).  Measured at RMAT s24 / s22
   // (profiles/r01_variants_s24.txt): 128 / 256 / 512-edge tiles 3.91 / 3.86 /
   // 3.94 ms at s24, 1.27 / 1.31 / 1.35 at s22; one edge per lane 3.81 / 1.24
-  // vs two 3.85 / 1.27.  f64 (record mode): <2 edges/lane, 6 CTAs/SM>
-  // (<1,8> 5.94, <2,6> 5.82, <4,4> 6.29 ms without predecessors).
+  // vs two 3.85 / 1.27; pipelined at 6 CTAs/SM 3.72 -> 3.55 ms
+  // (profiles/r02_advance_variants.txt).  f64 (record mode): <2 edges/lane,
+  // 6 CTAs/SM> (<1,8> 5.94, <2,6> 5.82, <4,4> 6.29 ms without predecessors).
   int tile() const {
     if (o->advance_tile) return o->advance_tile;
     return g->m <= (1ull << 27) ? 128 : 256;
@@ -166,9 +171,9 @@ struct Runner {
   void push(cudaStream_t st) {
     if constexpr (key_mode()) {
       if (tile() == 128)
-        k_push_range<W, 1, 8, 128, 1><<<c->num_sms * 8, 256, 0, st>>>(args(false));
+        k_push_range<W, 1, 6, 128, 17><<<c->num_sms * 6, 256, 0, st>>>(args(false));
       else
-        k_push_range<W, 1, 8, 256, 1><<<c->num_sms * 8, 256, 0, st>>>(args(false));
+        k_push_range<W, 1, 6, 256, 17><<<c->num_sms * 6, 256, 0, st>>>(args(false));
     } else {
       k_push_range<W, 2, 6, 256, 1, false, true><<<c->num_sms * 6, 256, 0, st>>>(args(false));
     }
@@ -407,16 +412,24 @@ struct Runner {
         else push(s);
         GFB_CUDA(cudaEventRecord(c->ev[3], s));
         GFB_CUDA(cudaGetLastError());
-        compact(s, dir, alpha, none, none, false, false);
+        compact(s, dir, alpha, none, none, false, false, o->trace ? &c->ev[5] : nullptr);
+        GFB_CUDA(cudaEventRecord(c->ev[4], s));
         ++launches;
-        GFB_CUDA(cudaEventSynchronize(c->ev[3]));
-        float ms = 0;
+        GFB_CUDA(cudaEventSynchronize(c->ev[4]));
+        float ms = 0, fms = 0;
         GFB_CUDA(cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]));
+        GFB_CUDA(cudaEventElapsedTime(&fms, c->ev[3], c->ev[4]));
         adv_ms += ms;
-        if (o->trace)
-          fprintf(stderr, "[gfb] superstep %llu %s frontier=%u edges=%u advance=%.3f ms (%.1f G edges/s)\n",
+        if (o->trace) {  // filter split: count | scan | write; bitmap = placed + deferred
+          float f0 = 0, f1 = 0;
+          GFB_CUDA(cudaEventElapsedTime(&f0, c->ev[3], c->ev[5]));
+          GFB_CUDA(cudaEventElapsedTime(&f1, c->ev[5], c->ev[6]));
+          fprintf(stderr, "[gfb] superstep %llu %s frontier=%u edges=%u advance=%.3f ms (%.1f G edges/s) "
+                  "filter=%.3f ms (count %.3f scan %.3f write %.3f) bitmap=%u/%u\n",
                   (unsigned long long)launches, h.mode ? "pull" : "push", h.k, h.total, ms,
-                  (h.mode ? g->pull_total : h.total) / (ms * 1e-3) / 1e9);
+                  (h.mode ? g->pull_total : h.total) / (ms * 1e-3) / 1e9, fms, f0, f1,
+                  fms - f0 - f1, h.k_all, h.t_all);
+        }
       }
     }
     uint64_t fallback = 0;

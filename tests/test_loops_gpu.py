@@ -129,7 +129,8 @@ def test_headline_instantiation_rmat(ctx, scale, wt):
 
 
 def test_relabel_view_is_permuted_csr(ctx):
-    """ensure_relabel: rows keyed by descending in-degree, contents mapped."""
+    """ensure_relabel: rows keyed by descending in-degree, contents mapped,
+    each row sorted by destination."""
     import ctypes as C
     from paper_2212_08200_b200 import _lib
     g = gb.rmat(10, 16, seed=1, wtype="f32", transpose=True, ctx=ctx)
@@ -152,6 +153,7 @@ def test_relabel_view_is_permuted_csr(ctx):
         a = sorted(zip(perm[col[ro[p]:ro[p + 1]]].tolist(), w[ro[p]:ro[p + 1]].tolist()))
         b = sorted(zip(dst[ro2[i]:ro2[i + 1]].tolist(), ww[ro2[i]:ro2[i + 1]].tolist()))
         assert a == b
+        assert np.all(np.diff(dst[ro2[i]:ro2[i + 1]].astype(np.int64)) >= 0)  # rows by destination
 
 
 def test_default_path_rmat20_bit_exact(ctx):
