@@ -213,9 +213,10 @@ _RELABEL = {"auto": 0, "on": 1, "off": 2}
 
 
 def _opts(direction="push", pull_alpha=1.05, delta=0.0, device_loop=True, compute_pred=True,
-          loop="auto", relabel="auto", defer_pct=0, advance_tile=0, trace=False):
+          loop="auto", relabel="auto", defer_pct=0, advance_tile=0, trace=False, tail_edges=0):
     """gfb_sssp_opts (include/gfb.h).  The tuning knobs (loop, relabel,
-    defer_pct, advance_tile) never change the result, only the schedule."""
+    defer_pct, advance_tile, tail_edges) never change the result, only the
+    schedule."""
     o = SsspOpts()
     _lib.load().gfb_sssp_opts_default(C.byref(o))
     if direction not in _DIR:
@@ -232,6 +233,7 @@ def _opts(direction="push", pull_alpha=1.05, delta=0.0, device_loop=True, comput
     o.defer_pct = int(defer_pct)
     o.advance_tile = int(advance_tile)
     o.trace = int(bool(trace))
+    o.tail_edges = int(tail_edges)
     return o
 
 

@@ -31,7 +31,8 @@ class SsspOpts(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("direction", C.c_int32), ("pull_alpha", C.c_float),
                 ("device_loop", C.c_int32), ("delta", C.c_double), ("compute_pred", C.c_int32),
                 ("loop", C.c_int32), ("relabel", C.c_int32), ("defer_pct", C.c_int32),
-                ("advance_tile", C.c_int32), ("trace", C.c_int32), ("reserved", C.c_int32 * 2)]
+                ("advance_tile", C.c_int32), ("trace", C.c_int32), ("tail_edges", C.c_int32),
+                ("reserved", C.c_int32 * 1)]
 
 
 class SsspStats(C.Structure):

@@ -331,7 +331,9 @@ static __global__ void k_fscan_o(unsigned long long* btot, unsigned long long* b
                                  cudaGraphConditionalHandle loop_handle,
                                  cudaGraphConditionalHandle mode_handle, int set_loop,
                                  int set_mode, uint32_t defer_pct = 100,
-                                 uint32_t defer_min = 0) {
+                                 uint32_t defer_min = 0,
+                                 cudaGraphConditionalHandle tail_handle = {}, int set_tail = 0,
+                                 uint32_t tail_edges = 0) {
   const int lane = threadIdx.x;
   static_assert(OB_N <= 32, "one warp scans the bucket totals");
   const unsigned long long x = lane < OB_N ? btot[lane] : 0ull;
@@ -362,6 +364,11 @@ static __global__ void k_fscan_o(unsigned long long* btot, unsigned long long* b
     ctl->t_all = T_all;
     plan_totals((uint32_t)(upto >> 32), (uint32_t)upto, plan, ctl, m, alpha, can_pull,
                 force_pull, loop_handle, mode_handle, set_loop, set_mode);
+    // small plan, nothing deferred: the next superstep starts the tail kernel
+    const uint32_t tail = tail_edges && (upto >> 32) > 0 && upto == all &&
+                          (uint32_t)upto < tail_edges ? 1u : 0u;
+    ctl->tail = tail;
+    if (set_tail) cudaGraphSetConditional(tail_handle, tail);
   }
 }
 

@@ -413,7 +413,8 @@ __device__ __forceinline__ void relax_reds(D* dist, unsigned long long* pkey, ui
 // stores {u, csr edge} into predrec and sets the frontier bit.  A later,
 // smaller relaxation may land its record first: k_pred_verify checks every
 // record's tightness and the repair rounds fix the rest.
-template <class W, int VT, bool COH = false, int OPT = 0, bool PEER = false, bool REC = false>
+template <class W, int VT, bool COH = false, int OPT = 0, bool PEER = false, bool REC = false,
+          bool ENQ = false>
 __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, uint32_t e1,
                                              uint32_t k, uint32_t total, unsigned* err,
                                              uint32_t* fmin = nullptr,
@@ -425,7 +426,8 @@ __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, u
   uint32_t cs = ldc<COH>(a.plan.tseg + e0 / PLAN_GRAIN);
   for (;;) {
     uint32_t cand = cs + lane;
-    uint32_t end = cand < k ? ldc<COH>(a.plan.off + cand + 1) : 0xFFFFFFFFu;
+    // (the last segment ends at total: plans built in-kernel carry no off[k] sentinel)
+    uint32_t end = cand + 1 < k ? ldc<COH>(a.plan.off + cand + 1) : total;
     unsigned msk = __ballot_sync(0xffffffffu, cand < k && end > e0);
     if (msk) {
       cs += __ffs(msk) - 1;
@@ -482,7 +484,9 @@ __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, u
       fetch(c0, rec, sd, su);
       for (uint32_t x = c0; x < c1; x += 32) {
         const uint32_t v = rec.v;
-        const D nd = dadd(sd, rec.w, err);
+        // (only a loaded record: a lane past the chunk end holds no weight, and a
+        // u32 sum with a stale register would raise the overflow flag)
+        const D nd = v != NIL ? dadd(sd, rec.w, err) : D(0);
         const uint32_t uv = su;
         if (x + 32 < c1) fetch(x + 32, rec, sd, su);
         if (v != NIL) {
@@ -562,7 +566,23 @@ __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, u
         if (dst[r] != NIL) cur[r] = test_gather<OPT>(a.dist + dst[r]);
 #pragma unroll
       for (int r = 0; r < VT; ++r) {  // C: fire-and-forget reductions
-        if (dst[r] != NIL && nd[r] < cur[r]) {
+        if constexpr (ENQ) {  // tail: dedup with a returning OR, warp-aggregated append
+          bool fresh = false;
+          if (dst[r] != NIL && nd[r] < cur[r]) {
+            red_min_u32(reinterpret_cast<unsigned*>(a.dist + dst[r]), dbits(nd[r]));
+            red_min_u64(pkey + dst[r], pred_key(nd[r], uu[r]));
+            const uint32_t bit = 1u << (dst[r] & 31);
+            fresh = (atomicOr(a.tq_bm + (dst[r] >> 5), bit) & bit) == 0;
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, fresh);
+          if (m) {
+            const int leader = __ffs(m) - 1;
+            uint32_t base = 0;
+            if (lane == leader) base = atomicAdd(a.tq_cnt, (uint32_t)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (fresh) a.tq_out[base + __popc(m & lanemask_lt())] = dst[r];
+          }
+        } else if (dst[r] != NIL && nd[r] < cur[r]) {
           relax_reds<OPT>(a.dist, pkey, a.bm_out, dst[r], nd[r], uu[r]);
           if (fmin) *fmin = min(*fmin, fkey(nd[r]));  // for the distance-ordered plan
         }
@@ -601,7 +621,7 @@ __global__ void __launch_bounds__(256, MINB) k_push_range(AdvArgs<W> a) {
   const uint32_t total = a.ctl->total;
   const uint32_t k = a.ctl->k;
   unsigned* err = &a.ctl->err;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && total) {  // (empty after a tail hand-back)
     a.ctl->relax += total;
     a.ctl->supersteps += 1;
     a.ctl->push_steps += 1;

@@ -115,6 +115,8 @@ struct Workspace {
   DBuf ctl;
   DBuf agg;        // per-tile (count, edges) of bfs.cu's frontier compaction
   DBuf oagg, obuck; // distance-ordered filter: (tile, bucket) cells, bucket totals / cursors
+  DBuf tq, tctr;    // tail kernel (tail.cuh): two vertex queues, rotating counters
+  int tail_grid = 0;
   DBuf src_dev;    // the source vertex (read by k_init)
   DBuf dist_int, pkey_int;          // loop state in relabelled ids (ensure_relabel)
   DBuf nf_q, nf_bm, nf_cnt;         // near-far queues / bitmaps / counters (nearfar.cuh)
@@ -124,7 +126,7 @@ struct Workspace {
   // this workspace's buffers: invalidate_loop_graphs() on every reallocation.
   cudaGraphExec_t loop_exec = nullptr;
   cudaGraph_t loop_graph = nullptr;
-  int loop_key[5] = {-1, -1, -1, -1, -1};
+  int loop_key[6] = {-1, -1, -1, -1, -1, -1};
   cudaGraphExec_t bfs_exec = nullptr;  // bfs.cu device loop
   cudaGraph_t bfs_graph = nullptr;
   int bfs_key = -1;

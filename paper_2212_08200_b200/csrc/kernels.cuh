@@ -51,6 +51,7 @@ struct Ctl {
   uint32_t gk, gflag, gunres, gresolved;
   // ordered compaction: vertices / edges in the bitmap (placed + deferred)
   uint32_t k_all, t_all;
+  uint32_t tail;       // k_fscan_o: the next superstep starts the tail kernel (tail.cuh)
 };
 
 // Expansion plan: the frontier restricted to vertices with out-degree > 0.
@@ -369,6 +370,11 @@ struct AdvArgs {
   uint32_t* rbm;
   int op;                    // gfb_op
   const PeerTab* peers;      // k_push_range<PEER>: owner-addressed destinations
+  // tail queue (range_expand<ENQ>, tail.cuh): a relaxation that lowers v sets
+  // v's bit in tq_bm with a returning OR; the first one appends v to tq_out
+  uint32_t* tq_out;
+  uint32_t* tq_cnt;
+  uint32_t* tq_bm;
 };
 
 // Warp-aggregated append of `x` (one atomicAdd per warp).

@@ -11,6 +11,8 @@
 //             k_fscan_o, k_fwrite_o (frontier.cuh)
 //   loop      while (f.size() != 0) (algorithms.hpp:167): a CUDA graph with a
 //             conditional WHILE node whose condition k_fscan_o sets
+//   tail      small frontiers: one persistent launch with vertex queues
+//             (tail.cuh k_tail), entered through an IF node the filter sets
 //   preds     repair_predecessors (algorithms.hpp:77-93): k_pred_* (kernels.cuh)
 // High-diameter meshes take the near-far loop instead (nearfar.cuh).
 #include <cub/cub.cuh>
@@ -26,6 +28,7 @@
 #include "hot.cuh"
 #include "impl.hpp"
 #include "nearfar.cuh"
+#include "tail.cuh"
 
 namespace gfb {
 
@@ -124,7 +127,8 @@ struct Runner {
   // -> write the distance-ordered plan; deferred vertices stay in the bitmap
   void compact(cudaStream_t st, int dir, float alpha, cudaGraphConditionalHandle hloop,
                cudaGraphConditionalHandle hmode, bool set_loop, bool set_mode,
-               cudaEvent_t* split = nullptr) {
+               cudaEvent_t* split = nullptr, cudaGraphConditionalHandle htail = {},
+               bool set_tail = false) {
     const uint32_t tiles = ws->ftiles;
     unsigned long long* bt = ws->obuck.as<unsigned long long>();
     unsigned long long* cells = ws->oagg.as<unsigned long long>();
@@ -135,7 +139,8 @@ struct Runner {
     k_fscan_o<<<1, 32, 0, st>>>(bt, bt + OB_N, plan(), ws->ctl.as<Ctl>(), (uint32_t)g->m, alpha,
                                 dir == GFB_DIR_AUTO && g->has_csc ? 1 : 0,
                                 dir == GFB_DIR_PULL ? 1 : 0, hloop, hmode, set_loop ? 1 : 0,
-                                set_mode ? 1 : 0, defer_pct(), defer_min());
+                                set_mode ? 1 : 0, defer_pct(), defer_min(), htail,
+                                set_tail ? 1 : 0, tail_edges(dir));
     if (split) GFB_CUDA(cudaEventRecord(split[1], st));
     k_fwrite_o<D><<<tiles, F_WARPS * 32, 0, st>>>(lro(), ws->bm_next.as<uint32_t>(),
                                                   ws->bm_cur.as<uint32_t>(), nwords, ldist(),
@@ -154,6 +159,59 @@ struct Runner {
       k_pull_relax<W, false><<<grid, H_BLOCK, 0, st>>>(args(true), g->pull_total, g->pull_k);
     }
     ++kernels;
+  }
+
+  // Tail kernel threshold (tail.cuh): 4-byte distances, push-only loops on
+  // the BSP driver; a plan below it with nothing deferred hands over.
+  uint32_t tail_edges(int dir) const {
+    if (!key_mode() || pullable(dir) || o->tail_edges < 0) return 0;
+    if (o->tail_edges > 0) return (uint32_t)o->tail_edges;
+    return (uint32_t)std::max<uint64_t>(g->m >> 8, 4096);
+  }
+  // queues + grid size (outside any stream capture)
+  void tail_prepare() {
+    if constexpr (key_mode()) {
+      if (ws->tq.bytes < (size_t)n * 8 + 8) {
+        invalidate_loop_graphs(g);
+        ws->tq.alloc((size_t)n * 8 + 8, s);
+        ws->tctr.alloc(64, s);
+      }
+      if (!ws->tail_grid) {
+        int per_sm = 0;
+        GFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail<W>, TL_THREADS, 0));
+        if (per_sm <= 0) fail(GFB_ECUDA, "sssp: tail kernel does not fit an SM");
+        ws->tail_grid = std::min(per_sm, 2) * c->num_sms;
+      }
+    }
+  }
+  void tail_launch(cudaStream_t st, cudaGraphConditionalHandle hloop, bool set_loop) {
+    if constexpr (key_mode()) {
+      TailArgs<W> t{};
+      t.a = args(false);
+      t.ro = lro();
+      t.q[0] = ws->tq.as<uint32_t>();
+      t.q[1] = t.q[0] + n;
+      t.qcnt = ws->tctr.as<uint32_t>();
+      t.cell = reinterpret_cast<unsigned long long*>(ws->tctr.as<char>() + 16);
+      t.bm[0] = ws->bm_next.as<uint32_t>();
+      t.bm[1] = ws->bm_cur.as<uint32_t>();
+      t.nwords = nwords;
+      // hand back above the entry threshold (in vertices: no ping-pong)
+      t.qmax = std::max<uint32_t>(std::max<uint32_t>(4096, n >> 7), tail_edges(GFB_DIR_PUSH));
+      t.hloop = hloop;
+      t.set_loop = set_loop ? 1 : 0;
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(ws->tail_grid);
+      cfg.blockDim = dim3(TL_THREADS);
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      GFB_CUDA(cudaLaunchKernelEx(&cfg, k_tail<W>, t));
+      ++kernels;
+    }
   }
 
   // The push advance (hot.cuh k_push_range): 6 x 256-thread CTAs per SM,
@@ -272,6 +330,7 @@ struct Runner {
   //      graph holds raw pointers into the graph's / workspace's buffers:
   //      every reallocation of those destroys it (invalidate_loop_graphs).
   void build_loop_graph(int dir, float alpha) {
+    if (tail_edges(dir) > 0) tail_prepare();
     invalidate_loop_graphs(g);
     for (auto& a : c->aux)
       if (!a) GFB_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
@@ -334,7 +393,28 @@ struct Runner {
     } else {
       push(b);
     }
-    compact(b, dir, alpha, hloop, hmode, true, pull_ok);
+    const bool tail_ok = tail_edges(dir) > 0;
+    cudaGraphConditionalHandle htail{};
+    if (tail_ok)
+      GFB_CUDA(cudaGraphConditionalHandleCreate(&htail, body, 0, cudaGraphCondAssignDefault));
+    compact(b, dir, alpha, hloop, hmode, true, pull_ok, nullptr, htail, tail_ok);
+    if (tail_ok) {  // IF(tail) { k_tail } -- the rest of the run in one launch
+      GFB_CUDA(cudaStreamGetCaptureInfo(b, &cst, nullptr, &capG, &deps, &ndeps));
+      cudaGraphNodeParams tp{};
+      tp.type = cudaGraphNodeTypeConditional;
+      tp.conditional.handle = htail;
+      tp.conditional.type = cudaGraphCondTypeIf;
+      tp.conditional.size = 1;
+      cudaGraphNode_t tnode;
+      GFB_CUDA(cudaGraphAddNode(&tnode, capG, deps, ndeps, &tp));
+      cudaGraph_t gtail = tp.conditional.phGraph_out[0];
+      GFB_CUDA(cudaStreamUpdateCaptureDependencies(b, &tnode, 1, cudaStreamSetCaptureDependencies));
+      cudaStream_t x = c->aux[1];
+      GFB_CUDA(cudaStreamBeginCaptureToGraph(x, gtail, nullptr, nullptr, 0,
+                                             cudaStreamCaptureModeRelaxed));
+      tail_launch(x, hloop, true);
+      GFB_CUDA(cudaStreamEndCapture(x, &tmp));
+    }
     GFB_CUDA(cudaStreamEndCapture(b, &tmp));
     GFB_CUDA(cudaGraphInstantiate(&ws->loop_exec, G, 0));
     ws->loop_graph = G;
@@ -391,7 +471,8 @@ struct Runner {
     if (done) {
     } else if (o->device_loop) {
       // the graph's key: everything its captured launches depend on
-      const int key[5] = {dir, (int)(alpha * 1000), rl ? 1 : 0, (int)defer_pct(), tile()};
+      const int key[6] = {dir, (int)(alpha * 1000), rl ? 1 : 0, (int)defer_pct(), tile(),
+                          (int)tail_edges(dir)};
       if (!ws->loop_exec || memcmp(key, ws->loop_key, sizeof(key)) != 0) {
         GFB_CUDA(cudaStreamSynchronize(s));
         build_loop_graph(dir, alpha);
@@ -406,6 +487,19 @@ struct Runner {
       for (;;) {
         Ctl h = c->read_ctl(ws->ctl.as<Ctl>());
         if (h.err & 1u) fail(GFB_ERANGE, "sssp: u32 distance overflow (use f64 weights)");
+        if (h.tail == 1 && tail_edges(dir) > 0) {  // the rest of the run in one launch
+          tail_prepare();
+          tail_launch(s, none, false);
+          ++launches;
+          h = c->read_ctl(ws->ctl.as<Ctl>());
+          if (o->trace)
+            fprintf(stderr, "[gfb] tail kernel: %u supersteps so far, %s\n", h.supersteps,
+                    h.tail == 2 ? "handed back (queue above qmax)" : "converged");
+          if (h.tail != 2) break;
+          compact(s, dir, alpha, none, none, false, false);
+
+          continue;
+        }
         if (h.k == 0) break;
         GFB_CUDA(cudaEventRecord(c->ev[2], s));
         if (h.mode == 1) pull_launch(s);
@@ -425,10 +519,10 @@ struct Runner {
           GFB_CUDA(cudaEventElapsedTime(&f0, c->ev[3], c->ev[5]));
           GFB_CUDA(cudaEventElapsedTime(&f1, c->ev[5], c->ev[6]));
           fprintf(stderr, "[gfb] superstep %llu %s frontier=%u edges=%u advance=%.3f ms (%.1f G edges/s) "
-                  "filter=%.3f ms (count %.3f scan %.3f write %.3f) bitmap=%u/%u\n",
+                  "filter=%.3f ms (count %.3f scan %.3f write %.3f) bitmap=%u/%u tail=%u\n",
                   (unsigned long long)launches, h.mode ? "pull" : "push", h.k, h.total, ms,
                   (h.mode ? g->pull_total : h.total) / (ms * 1e-3) / 1e9, fms, f0, f1,
-                  fms - f0 - f1, h.k_all, h.t_all);
+                  fms - f0 - f1, h.k_all, h.t_all, h.tail);
         }
       }
     }

@@ -315,3 +315,59 @@ def test_auto_switch_pulls(ctx, kw):
     _check(g, dist, pred)
     _, _, st2 = gb.sssp_stats(g, 0, direction="auto", pull_alpha=1.0)
     assert st2.pull_steps == 0  # a plan's edges never exceed m
+
+
+# ---- the tail kernel (tail.cuh): small frontiers in one persistent launch ----
+
+@pytest.mark.parametrize("wt", ["f32", "u32"])
+@pytest.mark.parametrize("tail", [1 << 30, 50_000])
+def test_tail_kernel_rmat(ctx, wt, tail):
+    """tail_edges = 2^30: the tail takes over after the source's superstep and
+    hands back to the bitmap filter whenever a queue outgrows qmax; 50K: the
+    hand-over happens mid-run.  Same fixpoint either way, both loop drivers."""
+    g = gb.rmat(16, 16, seed=3, wtype=wt, transpose=False, ctx=ctx)
+    for dl in (True, False):
+        for src in (0, 77):
+            dist, pred, st = gb.sssp_stats(g, src, tail_edges=tail, device_loop=dl)
+            _check(g, dist, pred, source=src, wtype=wt)
+            assert st.supersteps > 0 and st.relaxations >= st.m_reach
+
+
+def test_tail_kernel_off_same_result(ctx):
+    """tail_edges = -1 (never) vs the default threshold vs always: identical
+    distances (a schedule change only)."""
+    g = gb.rmat(18, 16, seed=1, wtype="f32", transpose=False, ctx=ctx)
+    runs = [gb.sssp_stats(g, 0, tail_edges=t) for t in (-1, 0, 1 << 30)]
+    for dist, pred, _ in runs:
+        _check(g, dist, pred)
+    assert runs[0][2].supersteps > 0
+
+
+def test_tail_kernel_grid_bsp(ctx):
+    """A high-diameter mesh on the BSP loop: thousands of tiny supersteps, all
+    but the first few inside the tail kernel."""
+    g = gb.grid(256, seed=2, transpose=False, ctx=ctx)
+    dist, pred, st = gb.sssp_stats(g, 0, loop="bsp")
+    _check(g, dist, pred)
+    d2, p2, st2 = gb.sssp_stats(g, 0, loop="bsp", tail_edges=-1)
+    assert np.array_equal(dist, d2)
+
+
+def test_tail_kernel_corpus(ctx):
+    """The reference acceptance corpus (acceptance.cpp:95-122; every graph is
+    small, so the default threshold of 4096 edges runs each one almost
+    entirely in the tail), f32, two sources, both loop drivers."""
+    corpus = np.load(os.path.join(os.path.dirname(__file__), "golden", "corpus.npz"))
+    for i in range(0, 200, 7):
+        row = corpus["meta"][i]
+        n, seed = int(row[0]), int(row[1])
+        s_, d_, w_ = O.random_edges(n, seed)
+        g = gb.build_csr((s_, d_, w_), n, wtype="f32", ctx=ctx)
+        ro, col, w32 = g.csr()
+        for src in (0, n // 2):
+            want, _ = O.dijkstra(n, ro, col, w32, src, "f32")
+            for dl in (True, False):
+                dist, pred, st = gb.sssp_stats(g, src, device_loop=dl)
+                assert np.array_equal(dist.astype(np.float32), want), (i, src, dl)
+                assert O.check_pred_tree(n, ro, col, w32, dist.astype(np.float32), src,
+                                         pred) == -1, (i, src, dl)

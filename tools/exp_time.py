@@ -21,12 +21,14 @@ ap.add_argument("--runs", type=int, default=10)
 ap.add_argument("--trace", action="store_true")
 ap.add_argument("--pred", type=int, default=0)
 ap.add_argument("--defer", type=int, default=0)
+ap.add_argument("--tile", type=int, default=0)
 ap.add_argument("--tag", default=os.environ.get("GFB_LIB", "default"))
 args = ap.parse_args()
 
 ctx = gb.Context(0)
 g = gb.rmat(args.scale, 16, seed=1, wtype="f32", transpose=False, ctx=ctx)
-kw = dict(want_result=False, compute_pred=bool(args.pred), defer_pct=args.defer)
+kw = dict(want_result=False, compute_pred=bool(args.pred), defer_pct=args.defer,
+          advance_tile=args.tile)
 for _ in range(3):
     gb.sssp_stats(g, 0, **kw)
 ms = []
