@@ -303,7 +303,8 @@ def run_ours(args):
         "e2e": e2e,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None, "traffic": traffic,
-                     "kernel": "k_push_range (advance, hot.cuh)",
+                     "kernel": "k_push_range (advance, hot.cuh) + k_tail (the last supersteps' "
+                               "advances with their queue filter, tail.cuh)",
                      "algorithmic_bytes_per_step": alg_bytes,
                      "b_alg_bytes_per_te": b_alg, "m_reach": m_reach,
                      "advance_ms_per_step": ist.advance_ms,
@@ -311,9 +312,10 @@ def run_ours(args):
                      "advance_share_of_step": ist.advance_ms / t_ms,
                      "peak_kind": peak_kind,
                      "note": "achieved = B_alg x m_reach (SURVEY §8(d), redundant visits get "
-                             "no credit) / advance time per step (CUDA events, host-loop run); "
-                             "traffic = ncu dram read+write summed over one step's advance "
-                             "launches (profiles/advance_traffic.json)"},
+                             "no credit) / advance time per step (CUDA events, host-loop run; "
+                             "the tail kernel's whole time counted as advance); traffic = ncu "
+                             "dram read+write summed over one step's advance + tail launches "
+                             "(profiles/advance_traffic.json)"},
         "visits": {"relaxations_per_step": ist.relaxations,
                    "work_inflation": ist.relaxations / m_reach,
                    "visit_bw_gbs": ist.relaxations * 12 / (ist.advance_ms * 1e-3) / 1e9

@@ -365,8 +365,10 @@ static __global__ void k_fscan_o(unsigned long long* btot, unsigned long long* b
     plan_totals((uint32_t)(upto >> 32), (uint32_t)upto, plan, ctl, m, alpha, can_pull,
                 force_pull, loop_handle, mode_handle, set_loop, set_mode);
     // small plan, nothing deferred: the next superstep starts the tail kernel
-    const uint32_t tail = tail_edges && (upto >> 32) > 0 && upto == all &&
-                          (uint32_t)upto < tail_edges ? 1u : 0u;
+    // (not from the source's plan: its output is unknown -- the hub phase of
+    // a skewed graph must keep the deferral)
+    const uint32_t tail = tail_edges && ctl->supersteps > 0 && (upto >> 32) > 0 &&
+                          upto == all && (uint32_t)upto < tail_edges ? 1u : 0u;
     ctl->tail = tail;
     if (set_tail) cudaGraphSetConditional(tail_handle, tail);
   }

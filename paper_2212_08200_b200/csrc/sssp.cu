@@ -196,8 +196,8 @@ struct Runner {
       t.bm[0] = ws->bm_next.as<uint32_t>();
       t.bm[1] = ws->bm_cur.as<uint32_t>();
       t.nwords = nwords;
-      // hand back above the entry threshold (in vertices: no ping-pong)
-      t.qmax = std::max<uint32_t>(std::max<uint32_t>(4096, n >> 7), tail_edges(GFB_DIR_PUSH));
+      // hand back at twice the entry threshold (hysteresis: no ping-pong)
+      t.tmax = 2 * tail_edges(GFB_DIR_PUSH);
       t.hloop = hloop;
       t.set_loop = set_loop ? 1 : 0;
       cudaLaunchConfig_t cfg{};
@@ -489,12 +489,17 @@ struct Runner {
         if (h.err & 1u) fail(GFB_ERANGE, "sssp: u32 distance overflow (use f64 weights)");
         if (h.tail == 1 && tail_edges(dir) > 0) {  // the rest of the run in one launch
           tail_prepare();
+          GFB_CUDA(cudaEventRecord(c->ev[2], s));
           tail_launch(s, none, false);
+          GFB_CUDA(cudaEventRecord(c->ev[3], s));
           ++launches;
           h = c->read_ctl(ws->ctl.as<Ctl>());
+          float tms = 0;  // the tail's supersteps count as advance time (their filter included)
+          GFB_CUDA(cudaEventElapsedTime(&tms, c->ev[2], c->ev[3]));
+          adv_ms += tms;
           if (o->trace)
             fprintf(stderr, "[gfb] tail kernel: %u supersteps so far, %s\n", h.supersteps,
-                    h.tail == 2 ? "handed back (queue above qmax)" : "converged");
+                    h.tail == 2 ? "handed back (plan above 2 x tail_edges)" : "converged");
           if (h.tail != 2) break;
           compact(s, dir, alpha, none, none, false, false);
 

@@ -18,9 +18,10 @@
 //            vertices are cleared for the superstep after next    | grid sync
 //
 // The result is the same fixpoint (a label-correcting order change only);
-// predecessors use the packed (dist, u) keys of k_push_range.  A queue above
-// qmax vertices goes back to the bitmap filter: its vertices are marked in
-// bm_next, the plan is emptied and the loop continues (ctl->tail = 2).
+// predecessors use the packed (dist, u) keys of k_push_range.  A rebuilt plan
+// above tmax edges goes back to the bitmap filter: its vertices are marked in
+// bm_next (bm[0] holds no dedup bits after a build), the plan is emptied and
+// the loop continues (ctl->tail = 2).
 #pragma once
 
 #include <cooperative_groups.h>
@@ -41,7 +42,7 @@ struct TailArgs {
   unsigned long long* cell;   // [3] rotating (slots << 32 | edges) reservation cursors
   uint32_t* bm[2];            // dedup bitmaps: [0] bm_next, [1] bm_cur
   uint32_t nwords;
-  uint32_t qmax;
+  uint32_t tmax;              // a rebuilt plan above this many edges goes back to the filter
   cudaGraphConditionalHandle hloop;
   int set_loop;
 };
@@ -89,23 +90,6 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_tail(TailArgs<W> t) {
     const uint32_t Q = __ldcg(t.qcnt + s % 3);
     if (Q == 0) break;
     const uint32_t* qin = t.q[s & 1];
-    if (Q > t.qmax) {  // back to the bitmap filter: the queued vertices go to bm_next,
-      // their smallest distance to ctl->fmin (the filter's bucket base)
-      uint32_t fm = 0xFFFFFFFFu;
-      for (uint32_t b0 = gwarp * 32; b0 < Q; b0 += nwarps * 32) {
-        const uint32_t i = b0 + lane;
-        if (i < Q) {
-          const uint32_t v = __ldcg(qin + i);
-          fm = min(fm, fkey(__ldcg(a.dist + v)));
-          if (s & 1) atomicOr(t.bm[0] + (v >> 5), 1u << (v & 31));
-        }
-      }
-#pragma unroll
-      for (int d = 16; d > 0; d >>= 1) fm = min(fm, __shfl_xor_sync(0xffffffffu, fm, d));
-      if (lane == 0 && fm != 0xFFFFFFFFu) atomicMin(&a.ctl->fmin, fm);
-      escaped = 1;
-      break;
-    }
     unsigned long long* cell = t.cell + s % 3;
     for (uint32_t b0 = gwarp * 32; b0 < Q; b0 += nwarps * 32) {
       const uint32_t i = b0 + lane;
@@ -138,6 +122,24 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_tail(TailArgs<W> t) {
     K = (uint32_t)(tot >> 32);
     T = (uint32_t)tot;
     if (K == 0) break;  // only sinks were improved
+    if (T > t.tmax) {  // grown past the tail: back to the bitmap filter (its
+      // deferral and distance order), the plan's vertices marked in bm_next and
+      // their smallest distance in ctl->fmin (the filter's bucket base)
+      uint32_t fm = 0xFFFFFFFFu;
+      for (uint32_t b0 = gwarp * 32; b0 < K; b0 += nwarps * 32) {
+        const uint32_t i = b0 + lane;
+        if (i < K) {
+          const uint32_t v = __ldcg(a.plan.v + i);
+          fm = min(fm, fkey(__ldcg(a.dist + v)));
+          atomicOr(t.bm[0] + (v >> 5), 1u << (v & 31));
+        }
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) fm = min(fm, __shfl_xor_sync(0xffffffffu, fm, d));
+      if (lane == 0 && fm != 0xFFFFFFFFu) atomicMin(&a.ctl->fmin, fm);
+      escaped = 1;
+      break;
+    }
   }
   if (gtid == 0) {
     a.ctl->relax += relax;
