@@ -238,7 +238,7 @@ int NAME(size_t n, const uint32_t* ro, const uint32_t* col,                   \
   uint8_t* mark = dedup ? (uint8_t*)calloc(n, 1) : NULL;                      \
   uint64_t steps = 0, relax = 0;                                              \
   f[0] = source;                                                              \
-  while (fsz) { /* :602 while (f.size() != 0) */                              \
+  while (fsz) { /* algorithms.hpp:167 while (f.size() != 0) */                              \
     ++steps;                                                                  \
     size_t ocap = 1024;                                                       \
     osz = 0;                                                                  \
