@@ -33,9 +33,18 @@ def run(args, rank, world):
     if world == 1:  # --partitioned without torchrun: a single-rank group
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
-    # the only host collectives: the one-time IPC handle exchange, barriers and
-    # the final max/sum reductions of the measurements (gloo is enough)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # the only host-driven collectives: the one-time IPC handle exchange,
+    # barriers and the final max/sum reductions of the measurements -- over
+    # NCCL (the exchange itself is device-initiated through peer memory)
+    # NCCL with a GPU per rank; ranks sharing one GPU (one-GPU test boxes) fall
+    # back to gloo (NCCL rejects duplicate devices)
+    if torch.cuda.device_count() >= world:
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", dev))
+        cdev = torch.device("cuda", dev)
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        cdev = torch.device("cpu")
     ctx = gb.Context(dev)
     t0 = time.time()
     g = gb.rmat(args.scale, args.edgefactor, seed=args.seed, wtype="f32", transpose=False, ctx=ctx)
@@ -68,11 +77,11 @@ def run(args, rank, world):
         launches += st["kernel_launches"]
     clocks = sampler.stop() if sampler else None
     t_local = sum(times) / len(times)
-    tt = torch.tensor([t_local], dtype=torch.float64)
+    tt = torch.tensor([t_local], dtype=torch.float64, device=cdev)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_ms = float(tt.item())
     agg = torch.tensor([st["m_reach"], st["n_reach"], st["relaxations"], launches],
-                       dtype=torch.int64)
+                       dtype=torch.int64, device=cdev)
     dist.all_reduce(agg, op=dist.ReduceOp.SUM)
     m_reach, n_reach, relax, all_launches = (int(x) for x in agg.tolist())
 
@@ -84,7 +93,7 @@ def run(args, rank, world):
     fin = np.isfinite(du[src_rows])
     nd = du[src_rows][fin] + w_l[fin]
     relaxable = int(np.count_nonzero(nd < d_all[col_l[fin]].astype(np.float32)))
-    bad = torch.tensor([relaxable], dtype=torch.int64)
+    bad = torch.tensor([relaxable], dtype=torch.int64, device=cdev)
     dist.all_reduce(bad)
 
     # e2e: host slice (pinned) -> device upload + IPC link + SSSP + D2H of the
@@ -102,7 +111,7 @@ def run(args, rank, world):
         e2e_ms.append((time.perf_counter() - t1) * 1e3)
         dist.barrier()
         p2.free()
-    te = torch.tensor([e2e_ms[-1]], dtype=torch.float64)
+    te = torch.tensor([e2e_ms[-1]], dtype=torch.float64, device=cdev)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
 
     if rank == 0:
