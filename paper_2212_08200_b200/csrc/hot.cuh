@@ -4,15 +4,18 @@
 //
 //   k_push_range  push advance: warps claim TILE-edge tiles of the plan
 //                 round-robin (merge-path style segment search by shuffles
-//                 over a 32-segment window), 64 warps per SM; record stream
-//                 -> distance gather (test before atomic) -> fire-and-forget
-//                 red.* of the distance, the packed (dist, pred) key and the
-//                 frontier bit.  Shapes (sssp.cu Runner::push): 32-bit
-//                 distances one edge per lane, 128-edge tiles for m <= 2^27,
-//                 256 above (opts.advance_tile overrides); REC (f64):
-//                 returning 64-bit mins and {u, edge} records, two edges per
-//                 lane, 6 CTAs per SM; PEER (peer.cu): one edge per lane,
-//                 256-edge tiles, owner-addressed reductions.
+//                 over a 32-segment window); record stream -> distance gather
+//                 (test before atomic) -> fire-and-forget red.* of the
+//                 distance, the packed (dist, pred) key and the frontier bit.
+//                 Shapes (sssp.cu Runner::push): 32-bit distances one edge
+//                 per lane, 6 CTAs per SM, the next 32-edge chunk's records
+//                 in flight while the current chunk gathers (OPT 16),
+//                 128-edge tiles for m <= 2^27, 256 above (opts.advance_tile
+//                 overrides); REC (f64): returning 64-bit mins and {u, edge}
+//                 records, two edges per lane, 6 CTAs per SM; PEER (peer.cu):
+//                 one edge per lane, 8 CTAs per SM, 256-edge tiles,
+//                 owner-addressed reductions.  range_expand<ENQ> is the tail
+//                 kernel's variant (tail.cuh).
 //   k_push_warp   warp-tile kernel with atomicMin-with-return; only the
 //                 host-driven partitioned advance of mg.cu (PART) uses it.
 //   k_pull_relax  pull over the CSC plan (CTA tiles in shared memory).
