@@ -600,6 +600,8 @@ def main():
     ap.add_argument("--grid-delta", type=float, default=16.0)
     ap.add_argument("--partitioned", action="store_true",
                     help="force the 1-D partitioned path (default for N > 1)")
+    ap.add_argument("--no-relabel", action="store_true",
+                    help="partitioned path: keep the generator's vertex ids")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
                     help="partitioned path: device-initiated peer-memory exchange (default) "
                          "or the host-driven NCCL all-to-all")

@@ -50,8 +50,13 @@ def run(args, rank, world):
     g = gb.rmat(args.scale, args.edgefactor, seed=args.seed, wtype="f32", transpose=False, ctx=ctx)
     ro, col, w = g.csr()
     n = g.num_vertices
-    g.free()
     rs = peer.aligned_ranges(ro, world)
+    relabel = not getattr(args, "no_relabel", False)
+    if relabel:  # range-preserving in-degree relabel + destination-sorted rows (untimed setup,
+        # like the single-GPU loop's relabelled copy built in its warm-up)
+        ro, col, w, perm = peer.relabel_ranges(g, rs)
+    src = int(perm[0]) if relabel else 0  # source 0 of the generator's ids
+    g.free()
     lo, hi = int(rs[rank]), int(rs[rank + 1])
     ro_l, col_l, w_l = mg.slice_csr(ro, col, w, lo, hi)
     del col, w
@@ -67,12 +72,12 @@ def run(args, rank, world):
     i = 0
     while i < args.warmup or time.time() < t_end:
         dist.barrier()
-        p.sssp(0)
+        p.sssp(src)
         i += 1
     times, launches = [], 0
     for _ in range(args.steps):
         dist.barrier()  # host skew out of the device timing
-        st = p.sssp(0)
+        st = p.sssp(src)
         times.append(st["device_ms"])
         launches += st["kernel_launches"]
     clocks = sampler.stop() if sampler else None
@@ -106,7 +111,7 @@ def run(args, rank, world):
         t1 = time.perf_counter()
         p2 = peer.PeerSssp(rank, world, rs, *pin, ctx=ctx)
         p2.link()
-        p2.sssp(0)
+        p2.sssp(src)
         d2, _ = p2.read(native=True)
         e2e_ms.append((time.perf_counter() - t1) * 1e3)
         dist.barrier()
@@ -126,6 +131,9 @@ def run(args, rank, world):
             "config": {"workload": f"RMAT scale {args.scale} EF{args.edgefactor} fp32, source 0, "
                                    f"1-D edge-balanced partition over {world} GPU(s), "
                                    f"device-initiated exchange over peer memory",
+                       "relabel": "in-degree order inside each rank's range, rows sorted by "
+                                  "destination (gfb_graph_relabel_ranges, untimed setup)"
+                                  if relabel else "none (the generator's ids)",
                        "scale": args.scale, "edgefactor": args.edgefactor,
                        "parallelism": f"1d-partition{world}-peer",
                        "l2": "inputs larger than L2"},

@@ -282,6 +282,22 @@ int gfb_sssp_read(gfb_graph* g, double* dist, void* dist_native, uint32_t* pred)
 int gfb_debug_relabel(gfb_graph* g, uint32_t* row_offsets, uint32_t* adj_pairs,
                       uint32_t* perm);
 
+/* Range-preserving relabelled copy of g for the 1-D partitioned paths
+ * (gfb_peer_* / gfb_mg_*; the reference partitions by contiguous vertex
+ * ranges): inside each [range_starts[q], range_starts[q+1])
+ * vertices are ranked by descending in-degree (the hot destinations of one
+ * owner share cache lines, as in the single-GPU loop's relabelled CSR) and
+ * every row is sorted by destination; no vertex changes owner, so the same
+ * range_starts partition the result with the same per-owner edge counts.
+ * Writes row_offsets (n+1), col (m, new ids), weights (m, g's native type:
+ * u32 / f32 / f64) and perm (n, old id -> new id); any pointer may be 0.
+ * range_starts: nparts + 1 entries from 0 to n, non-decreasing (else
+ * GFB_EINVAL).  Distances of the relabelled graph map back as
+ * dist_old[v] = dist_new[perm[v]]. */
+int gfb_graph_relabel_ranges(gfb_graph* g, uint32_t nparts, const uint32_t* range_starts,
+                             uint32_t* row_offsets, uint32_t* col, void* weights,
+                             uint32_t* perm);
+
 /* Breadth-first search as operator reuse (algorithms.hpp:194-239 bfs()):
  * depth[n] as double (math.inf for unreachable, like BfsResult.depth),
  * supersteps = levels expanded (max depth + 1), relaxations = claim

@@ -55,6 +55,7 @@ SIGNATURES = {
     "gfb_graph_info": ([_vp, _pu64, _pu64, C.POINTER(_int), C.POINTER(_int)], _int),
     "gfb_graph_download": ([_vp, _vp, _vp, _vp], _int),
     "gfb_debug_relabel": ([_vp, _vp, _vp, _vp], _int),
+    "gfb_graph_relabel_ranges": ([_vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp], _int),
     "gfb_graph_generate_rmat": ([_vp, _int, _int, _u64, _int, _int, C.POINTER(_vp)], _int),
     "gfb_graph_generate_grid": ([_vp, _u32, _u64, _int, C.POINTER(_vp)], _int),
     "gfb_frontier_create": ([_vp, _u64, _int, C.POINTER(_vp)], _int),

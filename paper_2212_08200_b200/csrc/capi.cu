@@ -560,6 +560,17 @@ int gfb_debug_relabel(gfb_graph* g, uint32_t* ro, uint32_t* adj_pairs, uint32_t*
   });
 }
 
+int gfb_graph_relabel_ranges(gfb_graph* g, uint32_t nparts, const uint32_t* range_starts,
+                             uint32_t* row_offsets, uint32_t* col, void* weights,
+                             uint32_t* perm) {
+  return guard([&] {
+    NEED(g);
+    NEED(range_starts);
+    set_device(g->ctx);
+    gfb::relabel_ranges(g, nparts, range_starts, row_offsets, col, weights, perm);
+  });
+}
+
 // ---- peer-memory partitioned SSSP (include/gfb.h) ----
 static gfb::Peer* P(gfb_peer* p) { return reinterpret_cast<gfb::Peer*>(p); }
 

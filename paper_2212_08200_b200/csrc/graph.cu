@@ -495,17 +495,182 @@ static void sort_rows(Ctx* c, const uint32_t* ro, EdgeRec<W>* adj, uint64_t n, u
   GFB_CUDA(cudaGetLastError());
 }
 
+static __global__ void k_range_keys(const uint32_t* __restrict__ cnt,
+                                    const uint32_t* __restrict__ ranges, uint32_t nparts,
+                                    unsigned long long* keys, uint32_t n) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = nparts;  // the range holding v: ranges[lo] <= v < ranges[lo + 1]
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) / 2;
+      if (ranges[mid] <= v) lo = mid;
+      else hi = mid;
+    }
+    keys[v] = ((unsigned long long)(nparts - 1 - lo) << 32) | cnt[v];
+  }
+}
+
+// The relabelled CSR (new id = rank by descending in-degree cnt[], rows
+// sorted by destination) into perm / iperm / ro2 / adj2.  ranges (device,
+// nparts + 1 cut points): the ranking runs inside each vertex range, so a
+// 1-D partition of the new ids owns the same rows (relabel_ranges).
+static void build_relabelled(Graph* g, const uint32_t* cnt, uint32_t* perm, uint32_t* iperm,
+                             uint32_t* ro2, void* adj2, const uint32_t* ranges = nullptr,
+                             uint32_t nparts = 0) {
+  Ctx* c = g->ctx;
+  cudaStream_t s = c->stream;
+  const uint32_t n = (uint32_t)g->n;
+  const uint64_t m = g->m;
+  TBuf cnt2, ids, deg2, tmp;
+  cnt2.alloc((size_t)n * 4, s);
+  ids.alloc((size_t)n * 4, s);
+  deg2.alloc((size_t)(n + 1) * 4, s);
+  k_iota_rev<<<stride_grid(c), 256, 0, s>>>(ids.as<uint32_t>(), n);
+  size_t tb = 0;
+  TBuf k64, k64b;
+  if (ranges) {  // (nparts - 1 - range) << 32 | in-degree, descending: ranges in order
+    k64.alloc((size_t)n * 8, s);
+    k64b.alloc((size_t)n * 8, s);
+    k_range_keys<<<stride_grid(c), 256, 0, s>>>(cnt, ranges, nparts, k64.as<unsigned long long>(), n);
+    GFB_CUDA(cub::DeviceRadixSort::SortPairsDescending(
+        nullptr, tb, k64.as<unsigned long long>(), k64b.as<unsigned long long>(),
+        ids.as<uint32_t>(), iperm, (int64_t)n, 0, 64, s));
+  } else {
+    GFB_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, cnt, cnt2.as<uint32_t>(),
+                                                       ids.as<uint32_t>(), iperm, (int64_t)n, 0,
+                                                       32, s));
+  }
+  size_t tb2 = 0;
+  GFB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, deg2.as<uint32_t>(),
+                                         ro2, (int64_t)(n + 1), s));
+  tmp.alloc(std::max(tb, tb2), s);
+  if (ranges)
+    GFB_CUDA(cub::DeviceRadixSort::SortPairsDescending(
+        tmp.p, tb, k64.as<unsigned long long>(), k64b.as<unsigned long long>(),
+        ids.as<uint32_t>(), iperm, (int64_t)n, 0, 64, s));
+  else
+    GFB_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp.p, tb, cnt, cnt2.as<uint32_t>(),
+                                                       ids.as<uint32_t>(), iperm, (int64_t)n, 0,
+                                                       32, s));
+  k_rl_perm<<<stride_grid(c), 256, 0, s>>>(iperm, g->ro.as<uint32_t>(),
+                                           perm, deg2.as<uint32_t>(), n);
+  GFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, deg2.as<uint32_t>(), ro2,
+                                         (int64_t)(n + 1), s));
+  TBuf big;
+  big.alloc((size_t)n * 4 + 16, s);
+  uint32_t* nbig = big.as<uint32_t>() + n;
+  GFB_CUDA(cudaMemsetAsync(nbig, 0, 4, s));
+  if (g->wtype == GFB_W_F32) {
+    k_rl_rows<float><<<stride_grid(c), 256, 0, s>>>(
+        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<float>>(), ro2,
+        iperm, perm, reinterpret_cast<EdgeRec<float>*>(adj2), n,
+        big.as<uint32_t>(), nbig);
+    k_rl_big<float><<<stride_grid(c), 256, 0, s>>>(
+        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<float>>(), ro2,
+        iperm, perm, reinterpret_cast<EdgeRec<float>*>(adj2),
+        big.as<uint32_t>(), nbig);
+  } else if (g->wtype == GFB_W_F64) {
+    k_rl_rows<double><<<stride_grid(c), 256, 0, s>>>(
+        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<double>>(), ro2,
+        iperm, perm, reinterpret_cast<EdgeRec<double>*>(adj2), n,
+        big.as<uint32_t>(), nbig);
+    k_rl_big<double><<<stride_grid(c), 256, 0, s>>>(
+        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<double>>(), ro2,
+        iperm, perm, reinterpret_cast<EdgeRec<double>*>(adj2),
+        big.as<uint32_t>(), nbig);
+  } else {
+    k_rl_rows<uint32_t><<<stride_grid(c), 256, 0, s>>>(
+        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<uint32_t>>(), ro2,
+        iperm, perm,
+        reinterpret_cast<EdgeRec<uint32_t>*>(adj2), n, big.as<uint32_t>(), nbig);
+    k_rl_big<uint32_t><<<stride_grid(c), 256, 0, s>>>(
+        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<uint32_t>>(), ro2,
+        iperm, perm,
+        reinterpret_cast<EdgeRec<uint32_t>*>(adj2), big.as<uint32_t>(), nbig);
+  }
+  GFB_CUDA(cudaGetLastError());
+  if (g->wtype == GFB_W_F32)
+    sort_rows<float>(c, ro2, reinterpret_cast<EdgeRec<float>*>(adj2), n, m);
+  else if (g->wtype == GFB_W_F64)
+    sort_rows<double>(c, ro2, reinterpret_cast<EdgeRec<double>*>(adj2), n, m);
+  else
+    sort_rows<uint32_t>(c, ro2, reinterpret_cast<EdgeRec<uint32_t>*>(adj2), n, m);
+}
+
+static void indegrees(Graph* g, uint32_t* cnt) {
+  Ctx* c = g->ctx;
+  cudaStream_t s = c->stream;
+  const uint32_t n = (uint32_t)g->n;
+  const uint64_t m = g->m;
+  if (g->has_csc) {  // from the transpose's offsets
+    k_indeg_csc<<<stride_grid(c), 256, 0, s>>>(g->co.as<uint32_t>(), n, cnt);
+  } else {
+    GFB_CUDA(cudaMemsetAsync(cnt, 0, (size_t)n * 4, s));
+    if (g->wtype == GFB_W_F32)
+      k_indeg<float><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<float>>(), m, cnt);
+    else if (g->wtype == GFB_W_F64)
+      k_indeg<double><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<double>>(), m, cnt);
+    else
+      k_indeg<uint32_t><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<uint32_t>>(), m, cnt);
+  }
+  GFB_CUDA(cudaGetLastError());
+}
+
+// A range-preserving relabelled copy for the 1-D partitioned paths (peer.cu,
+// mg.cu): inside each [starts[q], starts[q+1]) the vertices are ranked by
+// descending in-degree, rows sorted by destination -- the single-GPU loop's
+// layout (ensure_relabel) without moving any vertex to another owner.
+// Written to host buffers: row offsets (n + 1), destinations and native
+// weights (m), perm (old id -> new id, n).
+void relabel_ranges(Graph* g, uint32_t nparts, const uint32_t* starts, uint32_t* ro_out,
+                    uint32_t* col_out, void* w_out, uint32_t* perm_out) {
+  check_usable(g);
+  const uint32_t n = (uint32_t)g->n;
+  const uint64_t m = g->m;
+  if (nparts < 1 || !starts || starts[0] != 0 || starts[nparts] != n)
+    fail(GFB_EINVAL, "relabel_ranges: range_starts must run from 0 to n");
+  for (uint32_t q = 0; q < nparts; ++q)
+    if (starts[q + 1] < starts[q]) fail(GFB_EINVAL, "relabel_ranges: range_starts must not decrease");
+  Ctx* c = g->ctx;
+  cudaStream_t s = c->stream;
+  TBuf cnt, perm, iperm, ro2, adj2, rg, kc, kw;
+  cnt.alloc((size_t)n * 4, s);
+  perm.alloc((size_t)n * 4 + 4, s);
+  iperm.alloc((size_t)n * 4 + 4, s);
+  ro2.alloc((size_t)(n + 1) * 4, s);
+  adj2.alloc(m * g->rec_bytes() + 16, s);
+  rg.alloc((size_t)(nparts + 1) * 4, s);
+  GFB_CUDA(cudaMemcpyAsync(rg.p, starts, (size_t)(nparts + 1) * 4, cudaMemcpyHostToDevice, s));
+  indegrees(g, cnt.as<uint32_t>());
+  build_relabelled(g, cnt.as<uint32_t>(), perm.as<uint32_t>(), iperm.as<uint32_t>(),
+                   ro2.as<uint32_t>(), adj2.p, rg.as<uint32_t>(), nparts);
+  const size_t wb = g->wtype == GFB_W_F64 ? 8 : 4;
+  kc.alloc(m * 4 + 4, s);
+  kw.alloc(m * wb + 8, s);
+  if (g->wtype == GFB_W_F32)
+    k_split_recs<float><<<stride_grid(c), 256, 0, s>>>(adj2.as<EdgeRec<float>>(), kc.as<uint32_t>(),
+                                                       kw.as<float>(), m);
+  else if (g->wtype == GFB_W_F64)
+    k_split_recs<double><<<stride_grid(c), 256, 0, s>>>(adj2.as<EdgeRec<double>>(),
+                                                        kc.as<uint32_t>(), kw.as<double>(), m);
+  else
+    k_split_recs<uint32_t><<<stride_grid(c), 256, 0, s>>>(adj2.as<EdgeRec<uint32_t>>(),
+                                                          kc.as<uint32_t>(), kw.as<uint32_t>(), m);
+  GFB_CUDA(cudaGetLastError());
+  if (ro_out) GFB_CUDA(cudaMemcpyAsync(ro_out, ro2.p, (size_t)(n + 1) * 4, cudaMemcpyDeviceToHost, s));
+  if (col_out) GFB_CUDA(cudaMemcpyAsync(col_out, kc.p, m * 4, cudaMemcpyDeviceToHost, s));
+  if (w_out) GFB_CUDA(cudaMemcpyAsync(w_out, kw.p, m * wb, cudaMemcpyDeviceToHost, s));
+  if (perm_out) GFB_CUDA(cudaMemcpyAsync(perm_out, perm.p, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+  c->sync();
+}
+
 void ensure_relabel(Graph* g) {
   if (g->rl_valid) return;
   Ctx* c = g->ctx;
   cudaStream_t s = c->stream;
   const uint32_t n = (uint32_t)g->n;
   const uint64_t m = g->m;
-  TBuf cnt, cnt2, ids, deg2, tmp;
+  TBuf cnt;
   cnt.alloc((size_t)n * 4, s);
-  cnt2.alloc((size_t)n * 4, s);
-  ids.alloc((size_t)n * 4, s);
-  deg2.alloc((size_t)(n + 1) * 4, s);
   if (g->rl_perm.bytes < (size_t)n * 4) {
     invalidate_loop_graphs(g);
     g->rl_perm.alloc((size_t)n * 4, s);
@@ -513,20 +678,7 @@ void ensure_relabel(Graph* g) {
     g->rl_ro.alloc((size_t)(n + 1) * 4, s);
     g->rl_adj.alloc(m * g->rec_bytes(), s);
   }
-  if (g->has_csc) {  // in-degrees from the transpose's offsets
-    k_indeg_csc<<<stride_grid(c), 256, 0, s>>>(g->co.as<uint32_t>(), n, cnt.as<uint32_t>());
-  } else {
-    GFB_CUDA(cudaMemsetAsync(cnt.p, 0, (size_t)n * 4, s));
-    if (g->wtype == GFB_W_F32)
-      k_indeg<float><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<float>>(), m,
-                                                    cnt.as<uint32_t>());
-    else if (g->wtype == GFB_W_F64)
-      k_indeg<double><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<double>>(), m,
-                                                     cnt.as<uint32_t>());
-    else
-      k_indeg<uint32_t><<<stride_grid(c), 256, 0, s>>>(g->adj.as<EdgeRec<uint32_t>>(), m,
-                                                       cnt.as<uint32_t>());
-  }
+  indegrees(g, cnt.as<uint32_t>());
   {  // only skewed in-degrees profit (grids lose their locality): max >= 32x mean
     TBuf mx, tmpr;
     mx.alloc(8, s);
@@ -543,63 +695,8 @@ void ensure_relabel(Graph* g) {
       return;
     }
   }
-  k_iota_rev<<<stride_grid(c), 256, 0, s>>>(ids.as<uint32_t>(), n);
-  size_t tb = 0;
-  GFB_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, cnt.as<uint32_t>(),
-                                                     cnt2.as<uint32_t>(), ids.as<uint32_t>(),
-                                                     g->rl_iperm.as<uint32_t>(), (int64_t)n, 0, 32,
-                                                     s));
-  size_t tb2 = 0;
-  GFB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, deg2.as<uint32_t>(),
-                                         g->rl_ro.as<uint32_t>(), (int64_t)(n + 1), s));
-  tmp.alloc(std::max(tb, tb2), s);
-  GFB_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp.p, tb, cnt.as<uint32_t>(),
-                                                     cnt2.as<uint32_t>(), ids.as<uint32_t>(),
-                                                     g->rl_iperm.as<uint32_t>(), (int64_t)n, 0, 32,
-                                                     s));
-  k_rl_perm<<<stride_grid(c), 256, 0, s>>>(g->rl_iperm.as<uint32_t>(), g->ro.as<uint32_t>(),
-                                           g->rl_perm.as<uint32_t>(), deg2.as<uint32_t>(), n);
-  GFB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, deg2.as<uint32_t>(), g->rl_ro.as<uint32_t>(),
-                                         (int64_t)(n + 1), s));
-  TBuf big;
-  big.alloc((size_t)n * 4 + 16, s);
-  uint32_t* nbig = big.as<uint32_t>() + n;
-  GFB_CUDA(cudaMemsetAsync(nbig, 0, 4, s));
-  if (g->wtype == GFB_W_F32) {
-    k_rl_rows<float><<<stride_grid(c), 256, 0, s>>>(
-        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<float>>(), g->rl_ro.as<uint32_t>(),
-        g->rl_iperm.as<uint32_t>(), g->rl_perm.as<uint32_t>(), g->rl_adj.as<EdgeRec<float>>(), n,
-        big.as<uint32_t>(), nbig);
-    k_rl_big<float><<<stride_grid(c), 256, 0, s>>>(
-        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<float>>(), g->rl_ro.as<uint32_t>(),
-        g->rl_iperm.as<uint32_t>(), g->rl_perm.as<uint32_t>(), g->rl_adj.as<EdgeRec<float>>(),
-        big.as<uint32_t>(), nbig);
-  } else if (g->wtype == GFB_W_F64) {
-    k_rl_rows<double><<<stride_grid(c), 256, 0, s>>>(
-        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<double>>(), g->rl_ro.as<uint32_t>(),
-        g->rl_iperm.as<uint32_t>(), g->rl_perm.as<uint32_t>(), g->rl_adj.as<EdgeRec<double>>(), n,
-        big.as<uint32_t>(), nbig);
-    k_rl_big<double><<<stride_grid(c), 256, 0, s>>>(
-        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<double>>(), g->rl_ro.as<uint32_t>(),
-        g->rl_iperm.as<uint32_t>(), g->rl_perm.as<uint32_t>(), g->rl_adj.as<EdgeRec<double>>(),
-        big.as<uint32_t>(), nbig);
-  } else {
-    k_rl_rows<uint32_t><<<stride_grid(c), 256, 0, s>>>(
-        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<uint32_t>>(), g->rl_ro.as<uint32_t>(),
-        g->rl_iperm.as<uint32_t>(), g->rl_perm.as<uint32_t>(),
-        g->rl_adj.as<EdgeRec<uint32_t>>(), n, big.as<uint32_t>(), nbig);
-    k_rl_big<uint32_t><<<stride_grid(c), 256, 0, s>>>(
-        g->ro.as<uint32_t>(), g->adj.as<EdgeRec<uint32_t>>(), g->rl_ro.as<uint32_t>(),
-        g->rl_iperm.as<uint32_t>(), g->rl_perm.as<uint32_t>(),
-        g->rl_adj.as<EdgeRec<uint32_t>>(), big.as<uint32_t>(), nbig);
-  }
-  GFB_CUDA(cudaGetLastError());
-  if (g->wtype == GFB_W_F32)
-    sort_rows<float>(c, g->rl_ro.as<uint32_t>(), g->rl_adj.as<EdgeRec<float>>(), n, m);
-  else if (g->wtype == GFB_W_F64)
-    sort_rows<double>(c, g->rl_ro.as<uint32_t>(), g->rl_adj.as<EdgeRec<double>>(), n, m);
-  else
-    sort_rows<uint32_t>(c, g->rl_ro.as<uint32_t>(), g->rl_adj.as<EdgeRec<uint32_t>>(), n, m);
+  build_relabelled(g, cnt.as<uint32_t>(), g->rl_perm.as<uint32_t>(), g->rl_iperm.as<uint32_t>(),
+                   g->rl_ro.as<uint32_t>(), g->rl_adj.p);
   c->sync();  // temporaries are stream-ordered frees; keep the build synchronous
   g->rl_valid = true;
 }

@@ -191,6 +191,8 @@ inline int stride_grid(const Ctx* c) { return c->num_sms * 8; }
 inline int persist_grid(const Ctx* c, int per_sm) { return c->num_sms * per_sm; }
 
 // graph.cu
+void relabel_ranges(Graph* g, uint32_t nparts, const uint32_t* starts, uint32_t* ro_out,
+                    uint32_t* col_out, void* w_out, uint32_t* perm_out);
 void build_csc(Graph* g);
 void ensure_csc(Graph* g);
 void ensure_ceid(Graph* g);

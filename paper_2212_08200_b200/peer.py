@@ -40,6 +40,44 @@ def aligned_ranges(row_offsets, parts, align=ALIGN):
     return np.maximum.accumulate(np.array(cuts, dtype=np.int64)).astype(np.uint32)
 
 
+def relabel_ranges(g, range_starts):
+    """Range-preserving relabelled copy of device graph ``g`` for the
+    partition ``range_starts`` (gfb_graph_relabel_ranges): inside each range
+    vertices are ranked by descending in-degree and rows are sorted by
+    destination -- the single-GPU loop's relabelled layout without moving a
+    vertex to another owner.  Returns ``(row_offsets, col, w, perm)`` with
+    ``perm[old] = new``; a distance of the relabelled graph maps back as
+    ``dist_old = dist_new[perm]`` (``unrelabel``)."""
+    from . import _WT_NP
+    rs = np.ascontiguousarray(range_starts, np.uint32)
+    n, m = g.num_vertices, g.num_edges
+    ro = np.empty(n + 1, np.uint32)
+    col = np.empty(max(m, 1), np.uint32)
+    w = np.empty(max(m, 1), _WT_NP[g.wtype])
+    perm = np.empty(max(n, 1), np.uint32)
+    _lib.check(g._lib.gfb_graph_relabel_ranges(g.h, len(rs) - 1, C.c_void_p(rs.ctypes.data),
+                                          C.c_void_p(ro.ctypes.data), C.c_void_p(col.ctypes.data),
+                                          C.c_void_p(w.ctypes.data),
+                                          C.c_void_p(perm.ctypes.data)))
+    return ro, col[:m], w[:m], perm[:n]
+
+
+def unrelabel(perm, dist_new, pred_new=None):
+    """Results of a relabelled run in the original ids: dist[v] =
+    dist_new[perm[v]], pred[v] = iperm[pred_new[perm[v]]] (NIL kept)."""
+    perm = np.asarray(perm)
+    dist = np.asarray(dist_new)[perm]
+    if pred_new is None:
+        return dist
+    iperm = np.empty_like(perm)
+    iperm[perm] = np.arange(len(perm), dtype=perm.dtype)
+    p = np.asarray(pred_new)[perm]
+    ok = p != NIL
+    out = np.full(len(perm), NIL, np.uint32)
+    out[ok] = iperm[p[ok]]
+    return dist, out
+
+
 class PeerSssp:
     """One rank's share: rows [range_starts[rank], range_starts[rank+1]) with
     global column ids (``mg.slice_csr``), on ``ctx``'s GPU."""

@@ -35,7 +35,26 @@ def main():
             pass
         mg.free()
     edge_cases(parts)
+    relabelled(parts)
     print(f"MG_OK parts {parts}", flush=True)
+
+
+def relabelled(parts):
+    """The partitioned path on a range-preserving relabelled copy
+    (gfb_graph_relabel_ranges, what bench.py --gpus N runs on): distances map
+    back to the oracle's on the original graph."""
+    import paper_2212_08200_b200 as gb
+    n, ro, col, w = W.rmat(13, 1, 5)
+    g = gb.Graph.from_csr(n, ro, col, w, wtype="f32")
+    rs = peer.aligned_ranges(ro, parts)
+    ro2, col2, w2, perm = peer.relabel_ranges(g, rs)
+    g.free()
+    mg = peer.MgSssp([0] * parts, ro2, col2, w2)
+    for src in (0, n - 1):
+        d2, p2, _ = mg.sssp(int(perm[src]))
+        d, p = peer.unrelabel(perm, d2, p2)
+        W.check("rmat13-relabelled", n, ro, col, w, src, d, p, 0)
+    mg.free()
 
 
 
