@@ -461,7 +461,7 @@ __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, u
                                      : total;
     const uint32_t c0 = max(__shfl_sync(0xffffffffu, off, 0), e0);
     const uint32_t c1 = min(nxt, e1);
-    if constexpr ((OPT & 16) != 0 && !REC && !PEER && VT == 1) {
+    if constexpr ((OPT & 16) != 0 && !REC && VT == 1) {
       // software-pipelined: the record of chunk x + 32 is in flight while
       // chunk x gathers and reduces (s24: 3.72 -> 3.55 ms together with 6
       // CTAs per SM; 8 CTAs per SM spill; two edges per lane or 4 CTAs per
@@ -492,7 +492,19 @@ __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, u
         const D nd = v != NIL ? dadd(sd, rec.w, err) : D(0);
         const uint32_t uv = su;
         if (x + 32 < c1) fetch(x + 32, rec, sd, su);
-        if (v != NIL) {
+        if (v == NIL) continue;
+        if constexpr (PEER) {  // owner-addressed (see the VT loop below)
+          const uint32_t q = v >> PEER_VBITS;
+          const uint32_t vl = v & PEER_VMASK;
+          const uint32_t* tp = q == pt->self ? pt->dist[q] : pt->rc;
+          const D cur = test_gather<OPT>(reinterpret_cast<const D*>(tp) + vl);
+          if (nd < cur) {
+            if (q != pt->self) red_min_u32(reinterpret_cast<unsigned*>(pt->rc + vl), dbits(nd));
+            relax_reds<OPT>(reinterpret_cast<D*>(pt->dist[q]), pt->pkey[q], pt->bm[q], vl, nd,
+                            uv + pt->self_lo);
+            if (fmin) *fmin = min(*fmin, fkey(nd));
+          }
+        } else {
           const D cur = test_gather<OPT>(a.dist + v);
           if (nd < cur) {
             relax_reds<OPT>(a.dist, pkey, a.bm_out, v, nd, uv);

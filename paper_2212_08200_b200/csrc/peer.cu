@@ -595,7 +595,7 @@ struct PeerRun {
     a.op = GFB_OP_RELAX_MIN;
     a.peers = p->tab_dev.as<PeerTab>();
     if constexpr (sizeof(D) == 4) {
-      k_push_range<W, 1, 8, 256, 1, true><<<c->num_sms * 8, 256, 0, st>>>(a);
+      k_push_range<W, 1, 6, 256, 17, true><<<c->num_sms * 6, 256, 0, st>>>(a);
     }
     ++p->launches;
   }
