@@ -532,8 +532,15 @@ struct Runner {
       }
     }
     uint64_t fallback = 0;
-    pred_pass(source, o->compute_pred != 0, &fallback);
-    GFB_CUDA(cudaEventRecord(c->ev[1], s));
+    if (o->trace) GFB_CUDA(cudaEventRecord(c->ev[4], s));
+    pred_pass(source, o->compute_pred != 0, &fallback);  // records ev[1]
+    if (o->trace) {
+      float pms = 0;
+      GFB_CUDA(cudaEventSynchronize(c->ev[1]));
+      GFB_CUDA(cudaEventElapsedTime(&pms, c->ev[4], c->ev[1]));
+      fprintf(stderr, "[gfb] predecessor pass %.3f ms (fallback %llu)\n", pms,
+              (unsigned long long)fallback);
+    }
     Ctl h = c->read_ctl(ws->ctl.as<Ctl>());
     if (h.err & 1u) fail(GFB_ERANGE, "sssp: u32 distance overflow (use f64 weights)");
     float ms = 0;
@@ -579,7 +586,13 @@ struct Runner {
         ws->repair_bm.as<uint32_t>(), ws->cand.as<uint32_t>(), n, source, ws->ctl.as<Ctl>(), pv);
     GFB_CUDA(cudaGetLastError());
     ++kernels;
-    if (!want) return;
+    // ev[1] = the end of the device work, recorded before every host read of
+    // the control block (the decision to continue is host-side; the SSSP's
+    // device time does not include that round trip)
+    if (!want) {
+      GFB_CUDA(cudaEventRecord(c->ev[1], s));
+      return;
+    }
     Ctl* dctl = ws->ctl.as<Ctl>();
     // key rounds first (no in-edge scan), queued in batches of
     // PRED_KEY_ROUNDS with one host read per batch; long zero-weight tie
@@ -598,6 +611,7 @@ struct Runner {
         kernels += PRED_KEY_ROUNDS;
         base += PRED_KEY_ROUNDS;
       }
+      GFB_CUDA(cudaEventRecord(c->ev[1], s));
       h = c->read_ctl(dctl);
       *fallback = h.unresolved;
       left = h.unresolved - std::min(h.unresolved, h.resolved);
@@ -616,6 +630,7 @@ struct Runner {
             base);
         GFB_CUDA(cudaGetLastError());
         ++kernels;
+        GFB_CUDA(cudaEventRecord(c->ev[1], s));
         Ctl r = c->read_ctl(dctl);
         // round 1 (strict edges) may resolve nothing when every unresolved
         // vertex sits in a zero-weight tie class; later rounds must progress
@@ -647,6 +662,7 @@ struct Runner {
             list.as<uint4>(), cap, big.as<uint32_t>(), dctl);
         kernels += 2;
       }
+      GFB_CUDA(cudaEventRecord(c->ev[1], s));
       const Ctl r = c->read_ctl(dctl);
       if (!(r.err & 4u)) break;
       if (attempt > 0) fail(GFB_ELOGIC, "sssp: predecessor repair list overflow");
@@ -664,6 +680,7 @@ struct Runner {
                                                   base);
       GFB_CUDA(cudaGetLastError());
       kernels += 2;
+      GFB_CUDA(cudaEventRecord(c->ev[1], s));
       Ctl r = c->read_ctl(dctl);
       if (r.err & 4u) fail(GFB_ELOGIC, "sssp: predecessor repair list overflow");
       if (r.flag == 0 && round > 1)
