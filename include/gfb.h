@@ -231,7 +231,7 @@ typedef struct gfb_sssp_opts {
                             0 = by size (128 for m <= 2^27, else 256), or
                             128 / 256 */
   int32_t trace;         /* 1: per-superstep lines on stderr (host loop) */
-  int32_t tail_edges;    /* BSP loop, 4-byte weights, push: a plan below this
+  int32_t tail_edges;    /* BSP loop, push: a plan below this
                             many edges with nothing deferred hands the rest of
                             the run to one persistent tail launch (vertex
                             queues, no per-superstep bitmap filter).  0 = by

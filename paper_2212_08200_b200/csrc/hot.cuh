@@ -549,7 +549,22 @@ __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, u
         }
 #pragma unroll
         for (int r = 0; r < VT; ++r) {  // D: winners record themselves
-          if (dst[r] != NIL && nd[r] < cur[r]) {
+          if constexpr (ENQ) {  // tail (tail.cuh): returning-OR dedup, warp-aggregated append
+            bool fresh = false;
+            if (dst[r] != NIL && nd[r] < cur[r]) {
+              a.predrec[dst[r]] = make_uint2(uu[r], eid[r]);
+              const uint32_t bit = 1u << (dst[r] & 31);
+              fresh = (atomicOr(a.tq_bm + (dst[r] >> 5), bit) & bit) == 0;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, fresh);
+            if (m) {
+              const int leader = __ffs(m) - 1;
+              uint32_t base = 0;
+              if (lane == leader) base = atomicAdd(a.tq_cnt, (uint32_t)__popc(m));
+              base = __shfl_sync(0xffffffffu, base, leader);
+              if (fresh) a.tq_out[base + __popc(m & lanemask_lt())] = dst[r];
+            }
+          } else if (dst[r] != NIL && nd[r] < cur[r]) {
             a.predrec[dst[r]] = make_uint2(uu[r], eid[r]);
             red_or_u32(a.bm_out + (dst[r] >> 5), 1u << (dst[r] & 31));
             if (fmin) *fmin = min(*fmin, fkey(nd[r]));

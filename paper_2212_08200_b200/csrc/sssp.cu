@@ -161,16 +161,16 @@ struct Runner {
     ++kernels;
   }
 
-  // Tail kernel threshold (tail.cuh): 4-byte distances, push-only loops on
-  // the BSP driver; a plan below it with nothing deferred hands over.
+  // Tail kernel threshold (tail.cuh): push-only loops on the BSP driver; a
+  // plan below it with nothing deferred hands over.
   uint32_t tail_edges(int dir) const {
-    if (!key_mode() || pullable(dir) || o->tail_edges < 0) return 0;
+    if (pullable(dir) || o->tail_edges < 0) return 0;
     if (o->tail_edges > 0) return (uint32_t)o->tail_edges;
     return (uint32_t)std::max<uint64_t>(g->m >> 8, 4096);
   }
   // queues + grid size (outside any stream capture)
   void tail_prepare() {
-    if constexpr (key_mode()) {
+    {
       if (ws->tq.bytes < (size_t)n * 8 + 8) {
         invalidate_loop_graphs(g);
         ws->tq.alloc((size_t)n * 8 + 8, s);
@@ -185,7 +185,7 @@ struct Runner {
     }
   }
   void tail_launch(cudaStream_t st, cudaGraphConditionalHandle hloop, bool set_loop) {
-    if constexpr (key_mode()) {
+    {
       TailArgs<W> t{};
       t.a = args(false);
       t.ro = lro();

@@ -1,5 +1,5 @@
 // tail.cuh -- the small-frontier tail of the BSP loop as ONE persistent
-// cooperative launch (4-byte distances, push loops).
+// cooperative launch (push loops; any arithmetic).
 //
 // After the big supersteps an RMAT SSSP still runs 6-8 supersteps whose
 // frontiers hold a few thousand edges; each costs the bitmap filter's three
@@ -49,7 +49,8 @@ struct TailArgs {
 
 template <class W>
 __global__ void __launch_bounds__(TL_THREADS, 2) k_tail(TailArgs<W> t) {
-  static_assert(sizeof(typename DT<W>::D) == 4, "the tail uses packed predecessor keys");
+  // 4-byte distances: packed (dist, pred) keys; f64: returning mins and {u, edge} records
+  constexpr bool REC = sizeof(typename DT<W>::D) == 8;
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   AdvArgs<W> a = t.a;
   const int lane = threadIdx.x & 31;
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_tail(TailArgs<W> t) {
     relax += T;
     ++steps;
     for (uint64_t e0 = (uint64_t)gwarp * TL_TILE; e0 < T; e0 += (uint64_t)nwarps * TL_TILE)
-      range_expand<W, 1, true, 1, false, false, true>(a, (uint32_t)e0,
+      range_expand<W, 1, true, 1, false, REC, true>(a, (uint32_t)e0,
                                                       (uint32_t)min(e0 + TL_TILE, (uint64_t)T),
                                                       K, T, err);
     if (gtid == 0) {  // the counters of superstep s + 1 (last read two barriers ago)

@@ -371,3 +371,19 @@ def test_tail_kernel_corpus(ctx):
                 assert np.array_equal(dist.astype(np.float32), want), (i, src, dl)
                 assert O.check_pred_tree(n, ro, col, w32, dist.astype(np.float32), src,
                                          pred) == -1, (i, src, dl)
+
+
+@pytest.mark.parametrize("tail", [1 << 30, 0])
+def test_tail_kernel_f64_records(ctx, tail):
+    """f64 (record mode: returning mins, {u, edge} records) through the tail
+    kernel, both loop drivers: bit-exact vs the f64 oracle, valid trees."""
+    g32 = gb.rmat(15, 16, seed=7, wtype="f32", transpose=False, ctx=ctx)
+    ro, col, w = g32.csr()
+    n = g32.num_vertices
+    g32.free()
+    g = gb.Graph.from_csr(n, ro, col, w.astype(np.float64), wtype="f64", ctx=ctx)
+    want, _ = O.dijkstra(n, ro, col, w.astype(np.float64), 0, "f64")
+    for dl in (True, False):
+        dist, pred, st = gb.sssp_stats(g, 0, tail_edges=tail, device_loop=dl)
+        assert np.array_equal(dist, want), dl
+        assert O.check_pred_tree(n, ro, col, w.astype(np.float64), dist, 0, pred) == -1, dl
