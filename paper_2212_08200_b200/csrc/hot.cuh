@@ -12,9 +12,8 @@
 //                 in flight while the current chunk gathers (OPT 16),
 //                 128-edge tiles for m <= 2^27, 256 above (opts.advance_tile
 //                 overrides); REC (f64): returning 64-bit mins and {u, edge}
-//                 records, two edges per lane, 6 CTAs per SM; PEER (peer.cu):
-//                 one edge per lane, 8 CTAs per SM, 256-edge tiles,
-//                 owner-addressed reductions.  range_expand<ENQ> is the tail
+//                 records, same pipelined shape, 256-edge tiles; PEER
+//                 (peer.cu): same shape, owner-addressed reductions.  range_expand<ENQ> is the tail
 //                 kernel's variant (tail.cuh).
 //   k_push_warp   warp-tile kernel with atomicMin-with-return; only the
 //                 host-driven partitioned advance of mg.cu (PART) uses it.
@@ -461,39 +460,51 @@ __device__ __forceinline__ void range_expand(const AdvArgs<W>& a, uint32_t e0, u
                                      : total;
     const uint32_t c0 = max(__shfl_sync(0xffffffffu, off, 0), e0);
     const uint32_t c1 = min(nxt, e1);
-    if constexpr ((OPT & 16) != 0 && !REC && VT == 1) {
+    if constexpr ((OPT & 16) != 0 && VT == 1) {
       // software-pipelined: the record of chunk x + 32 is in flight while
       // chunk x gathers and reduces (s24: 3.72 -> 3.55 ms together with 6
       // CTAs per SM; 8 CTAs per SM spill; two edges per lane or 4 CTAs per
       // SM are slower, profiles/r02_advance_variants.txt)
-      auto fetch = [&](uint32_t x, EdgeRec<W>& rec, D& sd, uint32_t& su) {
+      // segment of each lane's edge by one OR-reduction of the window's
+      // segment starts that fall in the chunk (bit p: a segment starts at
+      // x + p) and a popcount, instead of a 5-step shuffle search: 3 SHFL per
+      // 32 edges instead of 9 (they share the L1 data pipe with the gathers;
+      // 3.49 -> 3.42 ms at s24)
+      const uint32_t sbase = start - off;  // record index = sbase + plan edge
+      int bj = __shfl_sync(0xffffffffu, off, 0) >= c0 ? -1 : 0;  // segment of edge c0 - 1
+      auto fetch = [&](uint32_t x, EdgeRec<W>& rec, D& sd, uint32_t& su, uint32_t& se) {
         const uint32_t le = x + lane;
-        int lo = 0;
-#pragma unroll
-        for (int step = 16; step >= 1; step >>= 1) {
-          uint32_t o = __shfl_sync(0xffffffffu, off, lo + step);
-          if (o <= le) lo += step;
-        }
-        const uint32_t so = __shfl_sync(0xffffffffu, off, lo);
-        const uint32_t ss = __shfl_sync(0xffffffffu, start, lo);
+        const uint32_t p = off - x;  // (off >= x: unsigned wrap otherwise)
+        const uint32_t mk = __reduce_or_sync(0xffffffffu, off >= x && p < 32u ? 1u << p : 0u);
+        const int lo = bj + __popc(mk & (0xFFFFFFFFu >> (31 - lane)));
+        bj += __popc(mk);
+        const uint32_t sb = __shfl_sync(0xffffffffu, sbase, lo);
         sd = shfl_d(du, lo);
         su = __shfl_sync(0xffffffffu, u, lo);
+        se = sb + le;  // the CSR edge (record mode)
         rec.v = NIL;
-        if (le < c1) rec = ld_rec(a.adj + (ss + (le - so)));
+        if (le < c1) rec = ld_rec(a.adj + se);
       };
       EdgeRec<W> rec;
       D sd;
-      uint32_t su;
-      fetch(c0, rec, sd, su);
+      uint32_t su, se;
+      fetch(c0, rec, sd, su, se);
       for (uint32_t x = c0; x < c1; x += 32) {
         const uint32_t v = rec.v;
         // (only a loaded record: a lane past the chunk end holds no weight, and a
         // u32 sum with a stale register would raise the overflow flag)
         const D nd = v != NIL ? dadd(sd, rec.w, err) : D(0);
-        const uint32_t uv = su;
-        if (x + 32 < c1) fetch(x + 32, rec, sd, su);
+        const uint32_t uv = su, ev = se;
+        if (x + 32 < c1) fetch(x + 32, rec, sd, su, se);
         if (v == NIL) continue;
-        if constexpr (PEER) {  // owner-addressed (see the VT loop below)
+        if constexpr (REC) {  // f64: returning min, the winner records {u, edge}
+          const D cur = test_gather<OPT>(a.dist + v);
+          if (nd < cur && nd < atomic_min_d(a.dist + v, nd)) {
+            a.predrec[v] = make_uint2(uv, ev);
+            red_or_u32(a.bm_out + (v >> 5), 1u << (v & 31));
+            if (fmin) *fmin = min(*fmin, fkey(nd));
+          }
+        } else if constexpr (PEER) {  // owner-addressed (see the VT loop below)
           const uint32_t q = v >> PEER_VBITS;
           const uint32_t vl = v & PEER_VMASK;
           const uint32_t* tp = q == pt->self ? pt->dist[q] : pt->rc;
