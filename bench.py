@@ -416,6 +416,32 @@ def full_size_parity(gb, g, args, dist32, pred, st, f64_dist):
     return parity, cpu
 
 
+def sp_certificate(ro, col, w, dist, pred, source):
+    """Size-independent proof that fp32 distances are THE shortest-path
+    fixpoint (SURVEY §8c at sizes the oracle's Dijkstra is slow at): dist[src]
+    = 0, no edge can still relax (fl(dist[u] + w) >= dist[v] for every edge,
+    the device's own arithmetic) and the predecessor tree is tight and
+    acyclic (the reference checker's rules, oracle/graflow_oracle.c)."""
+    from oracle import oracle as O
+    n = len(ro) - 1
+    ok_src = dist[source] == 0
+    relaxable = 0
+    step = 1 << 26
+    for r0 in range(0, n, 1 << 22):  # row blocks (bounded temporaries)
+        r1 = min(n, r0 + (1 << 22))
+        e0, e1 = int(ro[r0]), int(ro[r1])
+        for a in range(e0, e1, step):
+            b = min(e1, a + step)
+            rows = np.searchsorted(ro[r0:r1 + 1], np.arange(a, b, dtype=np.int64),
+                                   side="right") - 1 + r0
+            du = dist[rows]
+            fin = np.isfinite(du)
+            nd = du[fin] + w[a:b][fin]
+            relaxable += int(np.count_nonzero(nd < dist[col[a:b][fin]]))
+    bad = int(O.check_pred_tree(n, ro, col, w, dist, source, pred))
+    return {"source_zero": bool(ok_src), "relaxable_edges": relaxable, "pred_tree_valid": bad == -1}
+
+
 def secondary_configs(gb, ctx, args, g_main=None):
     """The other BASELINE.json configs as extra measurements (not the headline):
     f64 arithmetic on the headline graph, configs[1] RMAT s22 push-only,
@@ -507,11 +533,19 @@ def secondary_configs(gb, ctx, args, g_main=None):
     if args.s26:
         g = gb.rmat(26, args.edgefactor, seed=args.seed, wtype="f32", transpose=False, ctx=ctx)
         ms, st = timed(g, 3)
-        out.append({"config": "BASELINE configs[4]'s graph on ONE GPU (the N=1 point of the "
-                              "scaling target): RMAT s26 EF16 fp32, default loop",
-                    "gteps": st.m_reach / (ms * 1e-3) / 1e9, "ms": ms,
-                    "supersteps": st.supersteps, "m_reach": st.m_reach,
-                    "work_inflation": st.relaxations / st.m_reach})
+        rec = {"config": "BASELINE configs[4]'s graph on ONE GPU (the N=1 point of the "
+                         "scaling target): RMAT s26 EF16 fp32, default loop",
+               "gteps": st.m_reach / (ms * 1e-3) / 1e9, "ms": ms,
+               "supersteps": st.supersteps, "m_reach": st.m_reach,
+               "work_inflation": st.relaxations / st.m_reach}
+        if not args.no_cpu:  # the last timed call's result, certified at full size
+            t0 = time.perf_counter()
+            d, p = gb.sssp_read(g, native=True)
+            ro, col, w = g.csr()
+            rec["parity"] = dict(sp_certificate(ro, col, w, d, p, 0),
+                                 seconds=round(time.perf_counter() - t0, 1))
+            del ro, col, w, d, p
+        out.append(rec)
         g.free()
     return out
 
