@@ -823,7 +823,7 @@ k_pred_verify(const uint32_t* __restrict__ ro, const EdgeRec<W>* __restrict__ ad
         if (pr[r].x != NIL) pr[r].x = pv.iperm[pr[r].x];
         if (v < n) {
           pv.dist_out[v] = dv[r];
-          pv.key_out[v] = ((unsigned long long)pr[r].y << 32) | pr[r].x;
+          if (pv.key_out) pv.key_out[v] = ((unsigned long long)pr[r].y << 32) | pr[r].x;
         }
       }
     }
@@ -979,13 +979,18 @@ template <class W>
 __global__ void k_pred_key_round(const uint32_t* __restrict__ list,
                                  const unsigned long long* __restrict__ key,
                                  const typename DT<W>::D* __restrict__ dist, uint32_t* pred,
-                                 uint32_t* res, uint32_t* repair_bm, uint32_t k, Ctl* ctl) {
+                                 uint32_t* res, uint32_t* repair_bm, uint32_t k, Ctl* ctl,
+                                 const uint32_t* __restrict__ perm = nullptr,
+                                 const uint32_t* __restrict__ iperm = nullptr) {
   const uint32_t count = ctl->unresolved;
   uint32_t done = 0;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
     const uint32_t v = list[i];
     if (res[v] != 0) continue;
-    const uint32_t u = (uint32_t)key[v];
+    // relabelled loop: the keys stay in loop ids (k_pred_verify<PERM> does not
+    // write them back for every vertex), mapped here for the few unresolved
+    uint32_t u = perm ? (uint32_t)key[perm[v]] : (uint32_t)key[v];
+    if (perm && u != NIL) u = iperm[u];
     if (u == NIL || !(dist[u] == dist[v])) continue;
     const uint32_t ru = res[u];
     if (ru != 0 && ru <= k) {

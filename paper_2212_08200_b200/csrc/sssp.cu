@@ -577,8 +577,7 @@ struct Runner {
     if (rl)  // back to the caller's ids, fused into the verification
       pv = PermView<D>{g->rl_perm.as<uint32_t>(), g->rl_iperm.as<uint32_t>(),
                        ws->dist_int.as<D>(), ws->pkey_int.as<unsigned long long>(),
-                       ws->dist.as<D>(), ws->predrec.as<unsigned long long>(),
-                       g->rl_adj.p};
+                       ws->dist.as<D>(), nullptr /* keys stay in loop ids */, g->rl_adj.p};
     verify<<<c->num_sms * 8, 256, 0, s>>>(
         g->ro.as<uint32_t>(), g->adj.as<EdgeRec<W>>(),
         g->has_csc ? g->co.as<uint32_t>() : nullptr,
@@ -605,9 +604,11 @@ struct Runner {
       if constexpr (key_mode()) {
         for (uint32_t k = base + 1; k <= base + PRED_KEY_ROUNDS; ++k)
           k_pred_key_round<W><<<c->num_sms, 256, 0, s>>>(
-              ws->cand.as<uint32_t>(), ws->predrec.as<unsigned long long>(), ws->dist.as<D>(),
-              ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(), ws->repair_bm.as<uint32_t>(), k,
-              dctl);
+              ws->cand.as<uint32_t>(),
+              rl ? ws->pkey_int.as<unsigned long long>() : ws->predrec.as<unsigned long long>(),
+              ws->dist.as<D>(), ws->pred.as<uint32_t>(), ws->res.as<uint32_t>(),
+              ws->repair_bm.as<uint32_t>(), k, dctl,
+              rl ? g->rl_perm.as<uint32_t>() : nullptr, rl ? g->rl_iperm.as<uint32_t>() : nullptr);
         GFB_CUDA(cudaGetLastError());
         kernels += PRED_KEY_ROUNDS;
         base += PRED_KEY_ROUNDS;
