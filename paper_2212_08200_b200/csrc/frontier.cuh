@@ -412,6 +412,14 @@ k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
   }
   const uint32_t base = ctl->blo >> OB_SHIFT;
   const uint32_t wbase = blockIdx.x * F_WORDS + warp * F_WPW;
+  // a tile whose set bits are all deferred: no row offsets / distances to
+  // load, its bitmap words stay (degree-0 bits included: the count pass
+  // ignores them), only the placed-set bitmap is cleared (s24: 3.43 -> 3.39 ms)
+  __syncthreads();
+  if (s_ws[F_WARPS] == 0) {
+    if (bm_cur && lane < F_WPW && wbase + lane < nwords) bm_cur[wbase + lane] = 0;
+    return;
+  }
   WarpWords w;
   uint32_t raw;
   load_warp_words(ro, bm_next, nwords, wbase, w, &raw);
