@@ -31,13 +31,26 @@ struct WarpWords {
   uint32_t deg[F_WPW];
 };
 
+// rbm (partitioned loop): the bits remote ranks set are ORed in; *chk_word
+// = those not also set locally (their relaxation may not have lowered v)
 template <bool COH = false>
 __device__ __forceinline__ void load_warp_words(const uint32_t* __restrict__ ro,
                                                 const uint32_t* bm, uint32_t nwords,
-                                                uint32_t wbase, WarpWords& w, uint32_t* raw_word) {
+                                                uint32_t wbase, WarpWords& w, uint32_t* raw_word,
+                                                const uint32_t* rbm = nullptr,
+                                                uint32_t* chk_word = nullptr) {
   const int lane = threadIdx.x & 31;
   uint32_t my = 0;
-  if (lane < F_WPW && wbase + lane < nwords) my = COH ? __ldcg(bm + wbase + lane) : bm[wbase + lane];
+  if (lane < F_WPW && wbase + lane < nwords) {
+    my = COH ? __ldcg(bm + wbase + lane) : bm[wbase + lane];
+    if (rbm) {
+      const uint32_t r = rbm[wbase + lane];
+      *chk_word = r & ~my;
+      my |= r;
+    }
+  } else if (rbm) {
+    *chk_word = 0;
+  }
   *raw_word = my;
   uint32_t words[F_WPW];
 #pragma unroll
@@ -264,21 +277,25 @@ __device__ __forceinline__ uint32_t obucket(const D* dist, uint32_t v, uint32_t 
   return k <= base ? 0u : min(k - base, (uint32_t)OB_N - 1);
 }
 
-// Partitioned loop (peer.cu): remote relaxations set the owner's frontier bit
-// without knowing whether they lowered its distance (the sender tested
-// against its own proposal cache).  dexp[v] = distance bits v was last
-// expanded with; a set bit whose distance is unchanged is dropped here.
-// nullptr (single GPU: a bit is only set by a relaxation that lowered v).
+// Partitioned loop (peer.cu): remote relaxations set the owner's remote
+// frontier bitmap (rbm) without knowing whether they lowered its distance
+// (the sender tested against its own proposal cache).  dexp[v] = distance
+// bits v was last expanded with; a bit set ONLY remotely (chk, lane j holds
+// word j's mask) whose distance is unchanged is dropped here.  Local bits
+// come from relaxations that lowered v and need no check (one rank: none of
+// the dexp reads).  DEXP = false: single GPU.
 template <bool DEXP, class D>
 __device__ __forceinline__ void drop_unchanged(WarpWords& w, const D* dist, const uint32_t* dexp,
-                                               uint32_t wbase) {
+                                               uint32_t wbase, uint32_t chk) {
   if constexpr (DEXP) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int j = 0; j < F_WPW; ++j) {
+      const uint32_t cw = __shfl_sync(0xffffffffu, chk, j);
+      if (cw == 0) continue;  // warp-uniform
       const uint32_t v = (wbase + j) * 32 + lane;
       bool k = (w.keep[j] >> lane) & 1u;
-      if (k) k = dbits(dist[v]) != dexp[v];
+      if (k && ((cw >> lane) & 1u)) k = dbits(dist[v]) != dexp[v];
       w.keep[j] = __ballot_sync(0xffffffffu, k);
     }
   }
@@ -292,7 +309,7 @@ __global__ void __launch_bounds__(F_WARPS * 32)
 k_fcount_o(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uint32_t nwords,
            const D* __restrict__ dist, const Ctl* __restrict__ ctl,
            unsigned long long* agg, unsigned long long* btot, uint32_t* tflag,
-           const uint32_t* dexp = nullptr) {
+           const uint32_t* dexp = nullptr, const uint32_t* rbm = nullptr) {
   __shared__ uint32_t s_c[OB_N], s_e[OB_N];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x < OB_N) s_c[threadIdx.x] = s_e[threadIdx.x] = 0;
@@ -300,9 +317,9 @@ k_fcount_o(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uin
   const uint32_t base = ctl->fmin >> OB_SHIFT;
   const uint32_t wbase = blockIdx.x * F_WORDS + warp * F_WPW;
   WarpWords w;
-  uint32_t raw;
-  load_warp_words(ro, bm, nwords, wbase, w, &raw);
-  drop_unchanged<DEXP>(w, dist, dexp, wbase);
+  uint32_t raw, chk = 0;
+  load_warp_words(ro, bm, nwords, wbase, w, &raw, DEXP ? rbm : nullptr, &chk);
+  drop_unchanged<DEXP>(w, dist, dexp, wbase, chk);
 #pragma unroll
   for (int j = 0; j < F_WPW; ++j) {
     if ((w.keep[j] >> lane) & 1u) {
@@ -312,8 +329,10 @@ k_fcount_o(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uin
     }
   }
   // any bit in this tile at all: k_fwrite_o skips tiles without one
+  // (+2: remotely set bits to merge -- no all-deferred shortcut)
   const int any = __syncthreads_or(raw != 0);
-  if (threadIdx.x == 0) tflag[blockIdx.x] = any;
+  const int anyr = DEXP ? __syncthreads_or(chk != 0) : 0;
+  if (threadIdx.x == 0) tflag[blockIdx.x] = any | (anyr << 1);
   if (threadIdx.x < OB_N) {
     const unsigned long long x = ((unsigned long long)s_c[threadIdx.x] << 32) | s_e[threadIdx.x];
     agg[(size_t)blockIdx.x * OB_N + threadIdx.x] = x;
@@ -387,14 +406,16 @@ __global__ void __launch_bounds__(F_WARPS * 32)
 k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur, uint32_t nwords,
             const D* __restrict__ dist, const Ctl* __restrict__ ctl,
             const unsigned long long* __restrict__ agg, unsigned long long* bcur, Plan plan,
-            const uint32_t* __restrict__ tflag, uint32_t* dexp = nullptr) {
+            const uint32_t* __restrict__ tflag, uint32_t* dexp = nullptr,
+            uint32_t* rbm = nullptr) {
   constexpr int TV = F_WORDS * 32, NT = F_WARPS * 32, VT = TV / NT;
   __shared__ uint32_t s_cb[OB_N], s_ce[OB_N], s_lb[OB_N], s_rank[OB_N];
   __shared__ uint32_t s_deg[TV], s_pre[TV];
   __shared__ uint8_t s_bk[TV];
   __shared__ uint32_t s_ws[F_WARPS + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (!tflag[blockIdx.x]) return;  // empty tile: nothing to place or clear
+  const uint32_t tf = tflag[blockIdx.x];
+  if (!tf) return;  // empty tile: nothing to place or clear
   const uint32_t cut = ctl->bcut;
   if (warp == 0) {
     const unsigned long long x =
@@ -416,14 +437,14 @@ k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
   // load, its bitmap words stay (degree-0 bits included: the count pass
   // ignores them), only the placed-set bitmap is cleared (s24: 3.43 -> 3.39 ms)
   __syncthreads();
-  if (s_ws[F_WARPS] == 0) {
+  if (s_ws[F_WARPS] == 0 && (tf & 2u) == 0) {
     if (bm_cur && lane < F_WPW && wbase + lane < nwords) bm_cur[wbase + lane] = 0;
     return;
   }
   WarpWords w;
-  uint32_t raw;
-  load_warp_words(ro, bm_next, nwords, wbase, w, &raw);
-  drop_unchanged<DEXP>(w, dist, dexp, wbase);
+  uint32_t raw, chk = 0;
+  load_warp_words(ro, bm_next, nwords, wbase, w, &raw, DEXP ? rbm : nullptr, &chk);
+  drop_unchanged<DEXP>(w, dist, dexp, wbase, chk);
   __syncthreads();
   uint32_t pend = 0;
 #pragma unroll
@@ -442,12 +463,15 @@ k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
       s_bk[p] = (uint8_t)b;
       plan.v[gi] = v;
       plan.start[gi] = w.st[j];
-      if constexpr (DEXP) dexp[v] = dbits(dist[v]);
+      if constexpr (DEXP) {
+        if (dexp) dexp[v] = dbits(dist[v]);
+      }
     }
   }
   if (lane < F_WPW && wbase + lane < nwords) {
     if (bm_cur) bm_cur[wbase + lane] = raw & ~pend;
     bm_next[wbase + lane] = pend;
+    if (DEXP && rbm && (tf & 2u)) rbm[wbase + lane] = 0;  // merged (or dropped)
   }
   __syncthreads();
   const uint32_t placed = s_ws[F_WARPS];
