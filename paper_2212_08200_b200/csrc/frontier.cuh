@@ -29,16 +29,20 @@ struct WarpWords {
   uint32_t keep[F_WPW];
   uint32_t st[F_WPW];
   uint32_t deg[F_WPW];
+  uint32_t fk[F_WPW];  // fkey(dist[v]) when a distance array is given
 };
 
 // rbm (partitioned loop): the bits remote ranks set are ORed in; *chk_word
 // = those not also set locally (their relaxation may not have lowered v)
-template <bool COH = false>
+// dist (distance-ordered filter): the set bits' distances are loaded in the
+// same batch as their row offsets (one dependent round trip fewer)
+template <bool COH = false, class D = float>
 __device__ __forceinline__ void load_warp_words(const uint32_t* __restrict__ ro,
                                                 const uint32_t* bm, uint32_t nwords,
                                                 uint32_t wbase, WarpWords& w, uint32_t* raw_word,
                                                 const uint32_t* rbm = nullptr,
-                                                uint32_t* chk_word = nullptr) {
+                                                uint32_t* chk_word = nullptr,
+                                                const D* __restrict__ dist = nullptr) {
   const int lane = threadIdx.x & 31;
   uint32_t my = 0;
   if (lane < F_WPW && wbase + lane < nwords) {
@@ -55,19 +59,22 @@ __device__ __forceinline__ void load_warp_words(const uint32_t* __restrict__ ro,
   uint32_t words[F_WPW];
 #pragma unroll
   for (int j = 0; j < F_WPW; ++j) words[j] = __shfl_sync(0xffffffffu, my, j);
-  // issue every row-offset load before consuming any (F_WPW x 2 in flight)
+  // issue every row-offset (and distance) load before consuming any
+  D dv[F_WPW];
 #pragma unroll
   for (int j = 0; j < F_WPW; ++j) {
     bool bit = (words[j] >> lane) & 1u;
     uint32_t v = (wbase + j) * 32 + lane;
     w.st[j] = bit ? ro[v] : 0u;
     w.deg[j] = bit ? ro[v + 1] : 0u;
+    if (dist) dv[j] = bit ? dist[v] : D(0);
   }
 #pragma unroll
   for (int j = 0; j < F_WPW; ++j) {
     bool bit = (words[j] >> lane) & 1u;
     w.deg[j] = bit ? w.deg[j] - w.st[j] : 0u;
     w.keep[j] = __ballot_sync(0xffffffffu, w.deg[j] > 0);
+    if (dist) w.fk[j] = fkey(dv[j]);
   }
 }
 
@@ -271,9 +278,8 @@ constexpr int OB_SHIFT = 22;      // float bits >> 22 = exponent + 1 mantissa bi
 // 1.36, 10% 3.92 / 1.42, 15% 3.99, 20% 4.50, 30% 4.72 (tools/variants.py).
 constexpr uint32_t DEFER_PCT = 5;
 
-template <class D>
-__device__ __forceinline__ uint32_t obucket(const D* dist, uint32_t v, uint32_t base) {
-  const uint32_t k = fkey(dist[v]) >> OB_SHIFT;
+__device__ __forceinline__ uint32_t obucket_k(uint32_t fk, uint32_t base) {
+  const uint32_t k = fk >> OB_SHIFT;
   return k <= base ? 0u : min(k - base, (uint32_t)OB_N - 1);
 }
 
@@ -318,12 +324,12 @@ k_fcount_o(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uin
   const uint32_t wbase = blockIdx.x * F_WORDS + warp * F_WPW;
   WarpWords w;
   uint32_t raw, chk = 0;
-  load_warp_words(ro, bm, nwords, wbase, w, &raw, DEXP ? rbm : nullptr, &chk);
+  load_warp_words(ro, bm, nwords, wbase, w, &raw, DEXP ? rbm : nullptr, &chk, dist);
   drop_unchanged<DEXP>(w, dist, dexp, wbase, chk);
 #pragma unroll
   for (int j = 0; j < F_WPW; ++j) {
     if ((w.keep[j] >> lane) & 1u) {
-      const uint32_t b = obucket(dist, (wbase + j) * 32 + lane, base);
+      const uint32_t b = obucket_k(w.fk[j], base);
       atomicAdd(&s_c[b], 1u);
       atomicAdd(&s_e[b], w.deg[j]);
     }
@@ -443,7 +449,7 @@ k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
   }
   WarpWords w;
   uint32_t raw, chk = 0;
-  load_warp_words(ro, bm_next, nwords, wbase, w, &raw, DEXP ? rbm : nullptr, &chk);
+  load_warp_words(ro, bm_next, nwords, wbase, w, &raw, DEXP ? rbm : nullptr, &chk, dist);
   drop_unchanged<DEXP>(w, dist, dexp, wbase, chk);
   __syncthreads();
   uint32_t pend = 0;
@@ -451,7 +457,7 @@ k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
   for (int j = 0; j < F_WPW; ++j) {
     const bool kept = (w.keep[j] >> lane) & 1u;
     const uint32_t v = (wbase + j) * 32 + lane;
-    const uint32_t b = kept ? obucket(dist, v, base) : 0u;
+    const uint32_t b = kept ? obucket_k(w.fk[j], base) : 0u;
     const bool place = kept && b <= cut;
     const unsigned dm = __ballot_sync(0xffffffffu, kept && !place);
     if (lane == j) pend = dm;
