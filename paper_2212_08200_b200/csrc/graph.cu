@@ -6,7 +6,12 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <immintrin.h>
+
+#include <cmath>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "impl.hpp"
 #include "rmat.cuh"
@@ -72,7 +77,10 @@ Ctl Ctx::read_ctl(const Ctl* dctl) {
   return *ctl_host;
 }
 
-Graph::~Graph() = default;
+Graph::~Graph() {
+  for (cudaEvent_t& e : hdone)
+    if (e) cudaEventDestroy(e);
+}
 
 void invalidate_loop_graphs(Graph* g) {
   Workspace* ws = g->ws.get();
@@ -201,6 +209,77 @@ static void launch_interleave(Graph* g, const uint32_t* dcol, const void* dw, in
 
 static size_t host_wsize(int htype) { return htype == GFB_W_F64 ? 8 : 4; }
 
+// f64 host weights into an f32 graph (the reference's values() on the
+// headline path): narrowed on the host, a slice per thread, into pinned
+// buffers, so PCIe carries 4 bytes per weight instead of 8 -- with exactly
+// the device conversion's rules (conv_weight<float>: a negative, NaN or
+// infinite double, or one that rounds to +inf, is invalid; -0.0 -> +0.0).
+// Returns the first invalid edge index of [0, cnt), or ~0.
+static constexpr uint64_t HOST_NARROW_MIN_EDGES = 1ull << 20;
+
+// scalar slice [a, b): first invalid index or ~0
+static uint64_t narrow_scalar(const double* src, float* dst, uint64_t a, uint64_t b) {
+  uint64_t first = ~0ull;
+  for (uint64_t i = a; i < b; ++i) {
+    const double d = src[i];
+    const float w = (float)d;  // round to nearest (SSE), like __double2float_rn
+    const bool ok = d >= 0 && !std::isinf(d) && w >= 0.0f && !std::isinf(w);
+    if (!ok && first == ~0ull) first = i;
+    dst[i] = w + 0.0f;
+  }
+  return first;
+}
+
+// AVX2 slice: 8 weights per step, streaming (non-temporal) stores -- the
+// pinned buffer is read next by the DMA engine, not by this core, so no
+// read-for-ownership of its lines (the narrowing is host-memory bound)
+__attribute__((target("avx2"))) static uint64_t narrow_avx2(const double* src, float* dst,
+                                                            uint64_t a, uint64_t b) {
+  uint64_t i = a;
+  uint64_t first = ~0ull;
+  while (i < b && ((uintptr_t)(dst + i) & 31u)) {  // align the stores
+    const uint64_t f = narrow_scalar(src, dst, i, i + 1);
+    if (first == ~0ull) first = f;
+    ++i;
+  }
+  const __m256d zd = _mm256_setzero_pd();
+  const __m256 zf = _mm256_setzero_ps();
+  const __m256 inf = _mm256_set1_ps(INFINITY);
+  for (; i + 8 <= b; i += 8) {
+    const __m256d d0 = _mm256_loadu_pd(src + i), d1 = _mm256_loadu_pd(src + i + 4);
+    const __m256 w = _mm256_set_m128(_mm256_cvtpd_ps(d1), _mm256_cvtpd_ps(d0));
+    // valid: d >= 0 (ordered: NaN and negatives fail; -0.0 passes) and w < +inf
+    const int okd = _mm256_movemask_pd(_mm256_cmp_pd(d0, zd, _CMP_GE_OQ)) |
+                    (_mm256_movemask_pd(_mm256_cmp_pd(d1, zd, _CMP_GE_OQ)) << 4);
+    const int okw = _mm256_movemask_ps(_mm256_cmp_ps(w, inf, _CMP_LT_OQ));
+    if ((okd & okw) != 0xFF && first == ~0ull) first = narrow_scalar(src, dst, i, i + 8);
+    _mm256_stream_ps(dst + i, _mm256_add_ps(w, zf));  // -0.0 -> +0.0
+  }
+  if (i < b) {
+    const uint64_t f = narrow_scalar(src, dst, i, b);
+    if (first == ~0ull) first = f;
+  }
+  _mm_sfence();
+  return first;
+}
+
+static uint64_t narrow_weights(const double* src, float* dst, uint64_t cnt) {
+  const unsigned hc = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  const bool avx2 = __builtin_cpu_supports("avx2");
+  // slices in multiples of 8 weights (32-byte aligned stores when dst is)
+  const uint64_t per = ((cnt + hc - 1) / hc + 7) & ~7ull;
+  std::vector<uint64_t> bad(hc, ~0ull);
+  std::vector<std::thread> th;
+  auto work = [&](unsigned t) {
+    const uint64_t a = std::min<uint64_t>(cnt, t * per), b = std::min<uint64_t>(cnt, a + per);
+    bad[t] = avx2 ? narrow_avx2(src, dst, a, b) : narrow_scalar(src, dst, a, b);
+  };
+  for (unsigned t = 1; t < hc; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+  return *std::min_element(bad.begin(), bad.end());
+}
+
 // H2D upload as a two-stream pipeline: chunk b+1 is copied (copy stream,
 // double-buffered staging kept on the graph for refills) while chunk b is
 // validated and interleaved into {dst, w} records (compute stream).
@@ -226,7 +305,10 @@ static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const 
   if (!ro || (m && (!col || !w))) fail(GFB_EINVAL, "graph: null CSR array");
   if (!c->aux[1]) GFB_CUDA(cudaStreamCreateWithFlags(&c->aux[1], cudaStreamNonBlocking));
   cudaStream_t cp = c->aux[1];
-  const size_t wsz = host_wsize(htype);
+  // f64 -> f32 narrowed on the host (large uploads; identical validation)
+  const bool narrow = htype == GFB_W_F64 && g->wtype == GFB_W_F32 && m >= HOST_NARROW_MIN_EDGES;
+  uint64_t host_bad_w = ~0ull;
+  const size_t wsz = narrow ? 4 : host_wsize(htype);
   // staging layout per buffer: col[chunk] | w[chunk]; chunk rounded to 64 so
   // every sub-array stays 16-byte aligned for any weight width
   const uint64_t chunk = (std::min<uint64_t>(UPLOAD_CHUNK, std::max<uint64_t>(m, 1)) + 63) & ~63ull;
@@ -241,6 +323,21 @@ static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const 
     GFB_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
   }
   GFB_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  if (narrow) {
+    if (g->hstage.bytes < 2 * chunk * 4) {
+      if (g->hstage.p) {
+        c->sync();
+        GFB_CUDA(cudaStreamSynchronize(cp));
+        cudaFreeHost(g->hstage.p);
+        g->hstage.p = nullptr;
+        g->hstage.bytes = 0;
+      }
+      GFB_CUDA(cudaHostAlloc(&g->hstage.p, 2 * chunk * 4, cudaHostAllocDefault));
+      g->hstage.bytes = 2 * chunk * 4;
+    }
+    for (cudaEvent_t& e : g->hdone)
+      if (!e) GFB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   GFB_CUDA(cudaEventRecord(start, s));  // staging / flags ready before any copy
   GFB_CUDA(cudaStreamWaitEvent(cp, start, 0));
   GFB_CUDA(cudaMemcpyAsync(g->ro.p, ro, (n + 1) * 4, cudaMemcpyHostToDevice, cp));
@@ -254,11 +351,23 @@ static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const 
     void* dw = g->stage.as<char>() + b * chunk * 12 + chunk * 4;
     if (k >= 2) GFB_CUDA(cudaStreamWaitEvent(cp, done[b], 0));  // buffer b consumed
     GFB_CUDA(cudaMemcpyAsync(dcol, col + e0, cnt * 4, cudaMemcpyHostToDevice, cp));
-    GFB_CUDA(cudaMemcpyAsync(dw, static_cast<const char*>(w) + e0 * wsz, cnt * wsz,
-                             cudaMemcpyHostToDevice, cp));
+    if (narrow) {
+      // host buffer b was last read by the copy of chunk k - 2: wait for it,
+      // then narrow this chunk while the previous chunk's copies run
+      float* hb = g->hstage.as<float>() + b * chunk;
+      if (k >= 2) GFB_CUDA(cudaEventSynchronize(g->hdone[b]));
+      const uint64_t bw = narrow_weights(static_cast<const double*>(w) + e0, hb, cnt);
+      if (bw != ~0ull) host_bad_w = std::min(host_bad_w, e0 + bw);
+      GFB_CUDA(cudaMemcpyAsync(dw, hb, cnt * 4, cudaMemcpyHostToDevice, cp));
+      GFB_CUDA(cudaEventRecord(g->hdone[b], cp));
+    } else {
+      GFB_CUDA(cudaMemcpyAsync(dw, static_cast<const char*>(w) + e0 * wsz, cnt * wsz,
+                               cudaMemcpyHostToDevice, cp));
+    }
     GFB_CUDA(cudaEventRecord(ready[b], cp));
     GFB_CUDA(cudaStreamWaitEvent(s, ready[b], 0));
-    if (g->wtype == GFB_W_F32) launch_interleave<float>(g, dcol, dw, htype, e0, cnt, f);
+    if (narrow) launch_interleave<float>(g, dcol, dw, GFB_W_F32, e0, cnt, f);
+    else if (g->wtype == GFB_W_F32) launch_interleave<float>(g, dcol, dw, htype, e0, cnt, f);
     else if (g->wtype == GFB_W_F64) launch_interleave<double>(g, dcol, dw, htype, e0, cnt, f);
     else launch_interleave<uint32_t>(g, dcol, dw, htype, e0, cnt, f);
     GFB_CUDA(cudaEventRecord(done[b], s));
@@ -272,6 +381,7 @@ static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const 
     cudaEventDestroy(done[b]);
   }
   cudaEventDestroy(start);
+  hf[1] = std::min<unsigned long long>(hf[1], host_bad_w);
   if (hf[2] != ~0ull)
     fail(GFB_EINVAL, "graph: row_offsets inconsistent at vertex " + std::to_string(hf[2]));
   // graph.hpp:134-142 reports the first offending edge

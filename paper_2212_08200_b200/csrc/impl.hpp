@@ -29,6 +29,19 @@ struct DBuf {
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
+// Owning pinned host buffer (cudaHostAlloc), grown on demand.
+struct HostBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  HostBuf() = default;
+  HostBuf(const HostBuf&) = delete;
+  HostBuf& operator=(const HostBuf&) = delete;
+  ~HostBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
 // Function-local temporary: freed stream-ordered at scope exit (its stream
 // is alive for the whole call), so temporaries never synchronise the device.
 struct TBuf : DBuf {
@@ -62,6 +75,8 @@ struct Graph {
   bool has_csc = false;     // ... and it is built for the current contents (ensure_csc)
   DBuf ro, adj, co, cadj, ceid;  // ceid built lazily (ensure_ceid) for the record op
   DBuf stage;                     // upload staging, kept for refills
+  HostBuf hstage;                 // pinned f64 -> f32 narrowing buffers (fill_graph)
+  cudaEvent_t hdone[2] = {};      // ... and the copies that last read them
   // A refill whose validation failed has already overwritten ro / adj: the
   // handle is unusable (every entry point rejects it) until a good refill.
   bool poisoned = false;

@@ -382,3 +382,52 @@ def test_frontier_semantics(ctx):
     assert dn.size() == 4 and list(dn.contents()) == [3, 7, 64, 99]
     with pytest.raises(IndexError):
         gb.Frontier("sparse", 10, ctx=ctx).assign([10])
+
+
+# ------------------------------------ f64 host weights into an f32 graph ---
+
+def _big_csr(n=1 << 16, deg=24, seed=5):
+    """m = 1.5 M edges: above graph.cu's HOST_NARROW_MIN_EDGES (f64 weights are
+    narrowed on the host, a slice per thread, before the H2D copy)."""
+    rng = np.random.default_rng(seed)
+    ro = np.arange(0, n * deg + 1, deg, dtype=np.uint32)
+    col = rng.integers(0, n, n * deg, dtype=np.uint32)
+    w = rng.random(n * deg)  # doubles, most not representable in f32
+    return n, ro, col, w
+
+
+def test_host_narrowed_upload_equals_device_conversion(ctx):
+    """The narrowed upload rounds like the device conversion (to nearest), so
+    the device CSR equals an upload of the same weights already rounded."""
+    n, ro, col, w = _big_csr()
+    w[7] = -0.0  # canonicalised to +0.0
+    w[9] = 3.4e38  # finite in f32
+    g = gb.Graph.from_csr(n, ro, col, w, wtype="f32", ctx=ctx)
+    g32 = gb.Graph.from_csr(n, ro, col, w.astype(np.float32) + np.float32(0), wtype="f32", ctx=ctx)
+    r1, c1, w1 = g.csr()
+    r2, c2, w2 = g32.csr()
+    assert np.array_equal(r1, r2) and np.array_equal(c1, c2)
+    assert np.array_equal(w1.view(np.uint32), w2.view(np.uint32))
+    assert not np.signbit(w1[7])
+    d, p, _, _ = gb.sssp(g, 0)
+    d2, p2, _, _ = gb.sssp(g32, 0)
+    assert np.array_equal(d, d2)
+
+
+@pytest.mark.parametrize("bad", [-1e-50, np.nan, np.inf, 1e300, -2.0])
+def test_host_narrowed_upload_validation(ctx, bad):
+    """Same first-offending-edge message as the device path (graph.hpp:134-142);
+    1e300 is finite as a double but rounds to +inf in f32: rejected like the
+    device conversion does; the refill path checks the same rules."""
+    n, ro, col, w = _big_csr()
+    at = 1_234_567
+    w[at] = bad
+    w[at + 100] = -1.0
+    with pytest.raises(ValueError, match=f"edge {at} has negative or non-finite weight"):
+        gb.Graph.from_csr(n, ro, col, w, wtype="f32", ctx=ctx)
+    n, ro, col, w_ok = _big_csr()
+    g = gb.Graph.from_csr(n, ro, col, w_ok, wtype="f32", ctx=ctx)
+    with pytest.raises(ValueError, match=f"edge {at} has negative or non-finite weight"):
+        g.refill(ro, col, w)
+    g.refill(ro, col, w_ok)  # a good refill clears the poisoned state
+    gb.sssp(g, 0)
