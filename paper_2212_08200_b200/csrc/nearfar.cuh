@@ -39,6 +39,7 @@ constexpr int NF_THREADS = 1024;
 // relaxation inside a phase (still the same fixpoint), fewer phases on
 // high-diameter graphs.
 constexpr uint32_t NF_LQ = 128;
+constexpr uint32_t NF_CHASE = 128;
 
 template <class W>
 struct NfArgs {
@@ -285,8 +286,15 @@ __global__ void __launch_bounds__(NF_THREADS, 1) k_nearfar(NfArgs<W> a) {
         expand(ok, ok ? __ldcg(qin + j) : make_uint2(0, 0));
         if constexpr (LH > 0) {
           // chase this warp's own near activations without a grid barrier
-          for (int hop = 0; hop < LH && lq_n > 0; ++hop) {
+          // at most NF_CHASE entries chased per queue chunk: bounds the
+          // longest warp's chain, whose end every other warp waits for at the
+          // grid barrier (78.7% of warp samples at barrier, 4096^2 grid,
+          // profiles/r02_nearfar_grid4096_full.txt; budget 32 / 64 / 128 /
+          // none: 41.2 / 32.7 / 31.1 / 31.9 ms)
+          uint32_t chased = 0;
+          for (int hop = 0; hop < LH && lq_n > 0 && chased < NF_CHASE; ++hop) {
             const uint32_t take = min(lq_n, 32u);
+            chased += take;
             const bool v = (uint32_t)lane < take;
             const uint2 e = v ? s_lq[warp][lq_n - take + lane] : make_uint2(0, 0);
             lq_n -= take;
