@@ -272,9 +272,20 @@ static uint64_t narrow_weights(const double* src, float* dst, uint64_t cnt) {
   std::vector<std::thread> th;
   auto work = [&](unsigned t) {
     const uint64_t a = std::min<uint64_t>(cnt, t * per), b = std::min<uint64_t>(cnt, a + per);
+    // IEEE round-to-nearest with denormals kept, like __double2float_rn on the
+    // device, whatever FTZ / DAZ / rounding mode the calling process has set
+    const unsigned csr = _mm_getcsr();
+    _mm_setcsr(0x1F80u);
     bad[t] = avx2 ? narrow_avx2(src, dst, a, b) : narrow_scalar(src, dst, a, b);
+    _mm_setcsr(csr);
   };
-  for (unsigned t = 1; t < hc; ++t) th.emplace_back(work, t);
+  for (unsigned t = 1; t < hc; ++t) {
+    try {
+      th.emplace_back(work, t);
+    } catch (...) {  // no thread available: this slice on the calling thread
+      work(t);
+    }
+  }
   work(0);
   for (auto& x : th) x.join();
   return *std::min_element(bad.begin(), bad.end());

@@ -431,3 +431,15 @@ def test_host_narrowed_upload_validation(ctx, bad):
         g.refill(ro, col, w)
     g.refill(ro, col, w_ok)  # a good refill clears the poisoned state
     gb.sssp(g, 0)
+
+
+def test_host_narrowed_upload_keeps_f32_denormals(ctx):
+    """Weights in the f32 denormal range round like __double2float_rn even when
+    the process runs with flush-to-zero (the narrowing pins its own MXCSR)."""
+    n, ro, col, w = _big_csr()
+    w[:1000] = np.ldexp(1.0, -140) * (1 + np.arange(1000) / 997.0)  # f32 denormals
+    g = gb.Graph.from_csr(n, ro, col, w, wtype="f32", ctx=ctx)
+    _, _, w1 = g.csr()
+    want = w[:1000].astype(np.float32)
+    assert np.all(want > 0)
+    assert np.array_equal(w1[:1000].view(np.uint32), want.view(np.uint32))
