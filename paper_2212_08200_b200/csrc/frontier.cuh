@@ -363,6 +363,7 @@ static __global__ void k_fscan_o(unsigned long long* btot, unsigned long long* b
                                  uint32_t tail_edges = 0) {
   const int lane = threadIdx.x;
   static_assert(OB_N <= 32, "one warp scans the bucket totals");
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (PDL launch: the count's totals)
   const unsigned long long x = lane < OB_N ? btot[lane] : 0ull;
   unsigned long long incl = x;
 #pragma unroll
@@ -422,6 +423,7 @@ k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
   __shared__ uint8_t s_bk[TV];
   __shared__ uint32_t s_ws[F_WARPS + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (PDL launch: the scan's cursors)
   const uint32_t tf = tflag[blockIdx.x];
   if (!tf) return;  // empty tile: nothing to place or clear
   const uint32_t cut = ctl->bcut;
