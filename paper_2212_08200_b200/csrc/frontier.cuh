@@ -410,8 +410,10 @@ static __global__ void k_fscan_o(unsigned long long* btot, unsigned long long* b
 // (Measured alternatives: per-lane 64-bit shared cursors -- a CAS loop --
 // 1-5% slower; full staging of v/start/deg 1.2x; a warp-aggregated atomic per
 // distinct bucket of a word 2.1x.)
+// (__launch_bounds__ minimum 7 CTAs/SM: 32 registers instead of 56 -- s24
+// 3.38 -> 3.33 ms; 6 / 8: 3.36 / 3.36, r02_rejected_filter_variants.txt)
 template <class D, bool DEXP = false>
-__global__ void __launch_bounds__(F_WARPS * 32)
+__global__ void __launch_bounds__(F_WARPS * 32, 7)
 k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur, uint32_t nwords,
             const D* __restrict__ dist, const Ctl* __restrict__ ctl,
             const unsigned long long* __restrict__ agg, unsigned long long* bcur, Plan plan,
