@@ -324,16 +324,52 @@ k_fcount_o(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uin
   __syncthreads();
   const uint32_t base = ctl->fmin >> OB_SHIFT;
   const uint32_t wbase = blockIdx.x * F_WORDS + warp * F_WPW;
-  WarpWords w;
   uint32_t raw, chk = 0;
-  load_warp_words(ro, bm, nwords, wbase, w, &raw, DEXP ? rbm : nullptr, &chk, dist);
-  drop_unchanged<DEXP>(w, dist, dexp, wbase, chk);
+#ifndef GFB_FC_HALF
+#define GFB_FC_HALF 1
+#endif
+  if constexpr (!DEXP && GFB_FC_HALF) {
+    // two halves of F_WPW / 2 words: 12 loads in flight per lane and no
+    // register spills at the 32-register cap
+    const int lane_ = lane;
+    uint32_t my = 0;
+    if (lane_ < F_WPW && wbase + lane_ < nwords) my = bm[wbase + lane_];
+    raw = my;
 #pragma unroll
-  for (int j = 0; j < F_WPW; ++j) {
-    if ((w.keep[j] >> lane) & 1u) {
-      const uint32_t b = obucket_k(w.fk[j], base);
-      atomicAdd(&s_c[b], 1u);
-      atomicAdd(&s_e[b], w.deg[j]);
+    for (int h = 0; h < 2; ++h) {
+      constexpr int HW = F_WPW / 2;
+      uint32_t st[HW], en[HW];
+      D dv[HW];
+#pragma unroll
+      for (int q = 0; q < HW; ++q) {
+        const int j = h * HW + q;
+        const bool bit = (__shfl_sync(0xffffffffu, my, j) >> lane_) & 1u;
+        const uint32_t v = (wbase + j) * 32 + lane_;
+        st[q] = bit ? ro[v] : 0u;
+        en[q] = bit ? ro[v + 1] : 0u;
+        dv[q] = bit ? dist[v] : D(0);
+      }
+#pragma unroll
+      for (int q = 0; q < HW; ++q) {
+        const uint32_t deg = en[q] - st[q];
+        if (deg > 0) {
+          const uint32_t b = obucket_k(fkey(dv[q]), base);
+          atomicAdd(&s_c[b], 1u);
+          atomicAdd(&s_e[b], deg);
+        }
+      }
+    }
+  } else {
+    WarpWords w;
+    load_warp_words(ro, bm, nwords, wbase, w, &raw, DEXP ? rbm : nullptr, &chk, dist);
+    drop_unchanged<DEXP>(w, dist, dexp, wbase, chk);
+#pragma unroll
+    for (int j = 0; j < F_WPW; ++j) {
+      if ((w.keep[j] >> lane) & 1u) {
+        const uint32_t b = obucket_k(w.fk[j], base);
+        atomicAdd(&s_c[b], 1u);
+        atomicAdd(&s_e[b], w.deg[j]);
+      }
     }
   }
   // any bit in this tile at all: k_fwrite_o skips tiles without one
@@ -453,17 +489,10 @@ k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
     if (bm_cur && lane < F_WPW && wbase + lane < nwords) bm_cur[wbase + lane] = 0;
     return;
   }
-  WarpWords w;
-  uint32_t raw, chk = 0;
-  load_warp_words(ro, bm_next, nwords, wbase, w, &raw, DEXP ? rbm : nullptr, &chk, dist);
-  drop_unchanged<DEXP>(w, dist, dexp, wbase, chk);
-  __syncthreads();
-  uint32_t pend = 0;
-#pragma unroll
-  for (int j = 0; j < F_WPW; ++j) {
-    const bool kept = (w.keep[j] >> lane) & 1u;
+  uint32_t raw, pend = 0;
+  // place one word's vertices (b: bucket of kept lanes)
+  auto place_word = [&](int j, bool kept, uint32_t b, uint32_t st, uint32_t deg) {
     const uint32_t v = (wbase + j) * 32 + lane;
-    const uint32_t b = kept ? obucket_k(w.fk[j], base) : 0u;
     const bool place = kept && b <= cut;
     const unsigned dm = __ballot_sync(0xffffffffu, kept && !place);
     if (lane == j) pend = dm;
@@ -471,13 +500,54 @@ k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
       const uint32_t r = atomicAdd(&s_rank[b], 1u);
       const uint32_t p = s_lb[b] + r;
       const uint32_t gi = s_cb[b] + r;
-      s_deg[p] = w.deg[j];
+      s_deg[p] = deg;
       s_bk[p] = (uint8_t)b;
       plan.v[gi] = v;
-      plan.start[gi] = w.st[j];
+      plan.start[gi] = st;
       if constexpr (DEXP) {
         if (dexp) dexp[v] = dbits(dist[v]);
       }
+    }
+  };
+#ifndef GFB_FW_HALF
+#define GFB_FW_HALF 1
+#endif
+  if constexpr (!DEXP && GFB_FW_HALF) {
+    // two halves of F_WPW / 2 words, loads then placements (no spills at
+    // the 32-register cap; like k_fcount_o)
+    uint32_t my = 0;
+    if (lane < F_WPW && wbase + lane < nwords) my = bm_next[wbase + lane];
+    raw = my;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      constexpr int HW = F_WPW / 2;
+      uint32_t st[HW], en[HW];
+      D dv[HW];
+#pragma unroll
+      for (int q = 0; q < HW; ++q) {
+        const int j = h * HW + q;
+        const bool bit = (__shfl_sync(0xffffffffu, my, j) >> lane) & 1u;
+        const uint32_t v = (wbase + j) * 32 + lane;
+        st[q] = bit ? ro[v] : 0u;
+        en[q] = bit ? ro[v + 1] : 0u;
+        dv[q] = bit ? dist[v] : D(0);
+      }
+#pragma unroll
+      for (int q = 0; q < HW; ++q) {
+        const uint32_t deg = en[q] - st[q];
+        const bool kept = deg > 0;
+        place_word(h * HW + q, kept, kept ? obucket_k(fkey(dv[q]), base) : 0u, st[q], deg);
+      }
+    }
+  } else {
+    WarpWords w;
+    uint32_t chk = 0;
+    load_warp_words(ro, bm_next, nwords, wbase, w, &raw, DEXP ? rbm : nullptr, &chk, dist);
+    drop_unchanged<DEXP>(w, dist, dexp, wbase, chk);
+#pragma unroll
+    for (int j = 0; j < F_WPW; ++j) {
+      const bool kept = (w.keep[j] >> lane) & 1u;
+      place_word(j, kept, kept ? obucket_k(w.fk[j], base) : 0u, w.st[j], w.deg[j]);
     }
   }
   if (lane < F_WPW && wbase + lane < nwords) {
