@@ -25,57 +25,38 @@ constexpr int F_WPW = 8;                     // bitmap words per warp
 constexpr int F_WORDS = F_WARPS * F_WPW;     // 64 words = 2048 vertices per tile
 constexpr int F_SCAN_THREADS = 1024;
 
-// The 8 words of this warp -> per-word (mask of kept bits, row start, degree).
+// The 8 words of this warp -> per-word (mask of kept bits, row start, degree)
+// (plain compaction of bfs.cu; the ordered filter below loads in halves).
 struct WarpWords {
   uint32_t keep[F_WPW];
   uint32_t st[F_WPW];
   uint32_t deg[F_WPW];
-  uint32_t fk[F_WPW];  // fkey(dist[v]) when a distance array is given
 };
 
-// rbm (partitioned loop): the bits remote ranks set are ORed in; *chk_word
-// = those not also set locally (their relaxation may not have lowered v)
-// dist (distance-ordered filter): the set bits' distances are loaded in the
-// same batch as their row offsets (one dependent round trip fewer)
-template <bool COH = false, class D = float>
+template <bool COH = false>
 __device__ __forceinline__ void load_warp_words(const uint32_t* __restrict__ ro,
                                                 const uint32_t* bm, uint32_t nwords,
-                                                uint32_t wbase, WarpWords& w, uint32_t* raw_word,
-                                                const uint32_t* rbm = nullptr,
-                                                uint32_t* chk_word = nullptr,
-                                                const D* __restrict__ dist = nullptr) {
+                                                uint32_t wbase, WarpWords& w, uint32_t* raw_word) {
   const int lane = threadIdx.x & 31;
   uint32_t my = 0;
-  if (lane < F_WPW && wbase + lane < nwords) {
-    my = COH ? __ldcg(bm + wbase + lane) : bm[wbase + lane];
-    if (rbm) {
-      const uint32_t r = rbm[wbase + lane];
-      *chk_word = r & ~my;
-      my |= r;
-    }
-  } else if (rbm) {
-    *chk_word = 0;
-  }
+  if (lane < F_WPW && wbase + lane < nwords) my = COH ? __ldcg(bm + wbase + lane) : bm[wbase + lane];
   *raw_word = my;
   uint32_t words[F_WPW];
 #pragma unroll
   for (int j = 0; j < F_WPW; ++j) words[j] = __shfl_sync(0xffffffffu, my, j);
-  // issue every row-offset (and distance) load before consuming any
-  D dv[F_WPW];
+  // issue every row-offset load before consuming any (F_WPW x 2 in flight)
 #pragma unroll
   for (int j = 0; j < F_WPW; ++j) {
     bool bit = (words[j] >> lane) & 1u;
     uint32_t v = (wbase + j) * 32 + lane;
     w.st[j] = bit ? ro[v] : 0u;
     w.deg[j] = bit ? ro[v + 1] : 0u;
-    if (dist) dv[j] = bit ? dist[v] : D(0);
   }
 #pragma unroll
   for (int j = 0; j < F_WPW; ++j) {
     bool bit = (words[j] >> lane) & 1u;
     w.deg[j] = bit ? w.deg[j] - w.st[j] : 0u;
     w.keep[j] = __ballot_sync(0xffffffffu, w.deg[j] > 0);
-    if (dist) w.fk[j] = fkey(dv[j]);
   }
 }
 
@@ -287,26 +268,10 @@ __device__ __forceinline__ uint32_t obucket_k(uint32_t fk, uint32_t base) {
 // Partitioned loop (peer.cu): remote relaxations set the owner's remote
 // frontier bitmap (rbm) without knowing whether they lowered its distance
 // (the sender tested against its own proposal cache).  dexp[v] = distance
-// bits v was last expanded with; a bit set ONLY remotely (chk, lane j holds
-// word j's mask) whose distance is unchanged is dropped here.  Local bits
-// come from relaxations that lowered v and need no check (one rank: none of
-// the dexp reads).  DEXP = false: single GPU.
-template <bool DEXP, class D>
-__device__ __forceinline__ void drop_unchanged(WarpWords& w, const D* dist, const uint32_t* dexp,
-                                               uint32_t wbase, uint32_t chk) {
-  if constexpr (DEXP) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int j = 0; j < F_WPW; ++j) {
-      const uint32_t cw = __shfl_sync(0xffffffffu, chk, j);
-      if (cw == 0) continue;  // warp-uniform
-      const uint32_t v = (wbase + j) * 32 + lane;
-      bool k = (w.keep[j] >> lane) & 1u;
-      if (k && ((cw >> lane) & 1u)) k = dbits(dist[v]) != dexp[v];
-      w.keep[j] = __ballot_sync(0xffffffffu, k);
-    }
-  }
-}
+// bits v was last expanded with; in the count and write passes below a bit
+// set ONLY remotely whose distance is unchanged is dropped.  Local bits come
+// from relaxations that lowered v and need no check (one rank: none of the
+// dexp reads).  DEXP = false: single GPU.
 
 // Count: per tile (the F_WORDS-word tiles of k_fcount) and bucket -> agg,
 // and the bucket totals accumulated in btot[OB_N] (64-bit: count << 32 | edges).
@@ -324,16 +289,20 @@ k_fcount_o(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uin
   __syncthreads();
   const uint32_t base = ctl->fmin >> OB_SHIFT;
   const uint32_t wbase = blockIdx.x * F_WORDS + warp * F_WPW;
+  // the tile's words in two halves of F_WPW / 2: 12 loads in flight per
+  // lane and no register spills at the 32-register cap (one batch of 8
+  // words spilled: s24 3.36 -> 3.26 ms with the halves)
   uint32_t raw, chk = 0;
-#ifndef GFB_FC_HALF
-#define GFB_FC_HALF 1
-#endif
-  if constexpr (!DEXP && GFB_FC_HALF) {
-    // two halves of F_WPW / 2 words: 12 loads in flight per lane and no
-    // register spills at the 32-register cap
-    const int lane_ = lane;
+  {
     uint32_t my = 0;
-    if (lane_ < F_WPW && wbase + lane_ < nwords) my = bm[wbase + lane_];
+    if (lane < F_WPW && wbase + lane < nwords) {
+      my = bm[wbase + lane];
+      if (DEXP && rbm) {  // peers' bits: checked against dexp below
+        const uint32_t r = rbm[wbase + lane];
+        chk = r & ~my;
+        my |= r;
+      }
+    }
     raw = my;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -343,32 +312,26 @@ k_fcount_o(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uin
 #pragma unroll
       for (int q = 0; q < HW; ++q) {
         const int j = h * HW + q;
-        const bool bit = (__shfl_sync(0xffffffffu, my, j) >> lane_) & 1u;
-        const uint32_t v = (wbase + j) * 32 + lane_;
+        const bool bit = (__shfl_sync(0xffffffffu, my, j) >> lane) & 1u;
+        const uint32_t v = (wbase + j) * 32 + lane;
         st[q] = bit ? ro[v] : 0u;
         en[q] = bit ? ro[v + 1] : 0u;
         dv[q] = bit ? dist[v] : D(0);
       }
 #pragma unroll
       for (int q = 0; q < HW; ++q) {
+        const int j = h * HW + q;
         const uint32_t deg = en[q] - st[q];
-        if (deg > 0) {
+        bool kept = deg > 0;
+        if constexpr (DEXP) {  // a bit set only by peers: did the distance move?
+          const uint32_t cw = __shfl_sync(0xffffffffu, chk, j);
+          if (kept && ((cw >> lane) & 1u)) kept = dbits(dv[q]) != dexp[(wbase + j) * 32 + lane];
+        }
+        if (kept) {
           const uint32_t b = obucket_k(fkey(dv[q]), base);
           atomicAdd(&s_c[b], 1u);
           atomicAdd(&s_e[b], deg);
         }
-      }
-    }
-  } else {
-    WarpWords w;
-    load_warp_words(ro, bm, nwords, wbase, w, &raw, DEXP ? rbm : nullptr, &chk, dist);
-    drop_unchanged<DEXP>(w, dist, dexp, wbase, chk);
-#pragma unroll
-    for (int j = 0; j < F_WPW; ++j) {
-      if ((w.keep[j] >> lane) & 1u) {
-        const uint32_t b = obucket_k(w.fk[j], base);
-        atomicAdd(&s_c[b], 1u);
-        atomicAdd(&s_e[b], w.deg[j]);
       }
     }
   }
@@ -509,14 +472,18 @@ k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
       }
     }
   };
-#ifndef GFB_FW_HALF
-#define GFB_FW_HALF 1
-#endif
-  if constexpr (!DEXP && GFB_FW_HALF) {
-    // two halves of F_WPW / 2 words, loads then placements (no spills at
-    // the 32-register cap; like k_fcount_o)
-    uint32_t my = 0;
-    if (lane < F_WPW && wbase + lane < nwords) my = bm_next[wbase + lane];
+  // two halves of F_WPW / 2 words, loads then placements (no spills at the
+  // 32-register cap, like k_fcount_o: s24 3.26 -> 3.20 ms)
+  {
+    uint32_t my = 0, chk = 0;
+    if (lane < F_WPW && wbase + lane < nwords) {
+      my = bm_next[wbase + lane];
+      if (DEXP && rbm && (tf & 2u)) {
+        const uint32_t r = rbm[wbase + lane];
+        chk = r & ~my;
+        my |= r;
+      }
+    }
     raw = my;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -534,20 +501,15 @@ k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
       }
 #pragma unroll
       for (int q = 0; q < HW; ++q) {
+        const int j = h * HW + q;
         const uint32_t deg = en[q] - st[q];
-        const bool kept = deg > 0;
-        place_word(h * HW + q, kept, kept ? obucket_k(fkey(dv[q]), base) : 0u, st[q], deg);
+        bool kept = deg > 0;
+        if constexpr (DEXP) {
+          const uint32_t cw = __shfl_sync(0xffffffffu, chk, j);
+          if (kept && ((cw >> lane) & 1u)) kept = dbits(dv[q]) != dexp[(wbase + j) * 32 + lane];
+        }
+        place_word(j, kept, kept ? obucket_k(fkey(dv[q]), base) : 0u, st[q], deg);
       }
-    }
-  } else {
-    WarpWords w;
-    uint32_t chk = 0;
-    load_warp_words(ro, bm_next, nwords, wbase, w, &raw, DEXP ? rbm : nullptr, &chk, dist);
-    drop_unchanged<DEXP>(w, dist, dexp, wbase, chk);
-#pragma unroll
-    for (int j = 0; j < F_WPW; ++j) {
-      const bool kept = (w.keep[j] >> lane) & 1u;
-      place_word(j, kept, kept ? obucket_k(w.fk[j], base) : 0u, w.st[j], w.deg[j]);
     }
   }
   if (lane < F_WPW && wbase + lane < nwords) {
