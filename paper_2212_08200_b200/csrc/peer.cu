@@ -677,11 +677,12 @@ struct PeerRun {
     if (o->direction == GFB_DIR_PULL) fail(GFB_EINVAL, "peer: the partitioned SSSP is push-only");
     if (o->delta > 0) fail(GFB_EINVAL, "peer: the near-far filter is single-GPU only");
     p->has_result = false;
-    // 10% (not the single-GPU loop's 5%): every extra superstep costs two
-    // cross-rank barriers here -- s24, one partition: 5.52-5.60 ms at 10% vs
-    // 5.79 at 5%; equal at four partitions sharing one GPU
+    // 5%, like the single-GPU loop: s24 at one partition on the relabelled
+    // copy 3.81 ms vs 4.00 at 10% with the same 22 supersteps (so the same
+    // number of cross-rank barriers; r01, before the relabel and the
+    // spill-free filter, 10% won: 5.52-5.60 vs 5.79 ms)
     if (o->defer_pct < 0 || o->defer_pct > 100) fail(GFB_EINVAL, "sssp: defer_pct must be 0..100");
-    defer = o->defer_pct ? (uint32_t)o->defer_pct : 10u;
+    defer = o->defer_pct ? (uint32_t)o->defer_pct : 5u;
     src_local = (source >= p->lo && source < p->lo + p->n) ? source - p->lo : NIL;
     if (!p->exec || p->graph_key != (int)defer) {
       GFB_CUDA(cudaStreamSynchronize(s));
