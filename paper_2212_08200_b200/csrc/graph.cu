@@ -8,6 +8,7 @@
 #include <cstring>
 #include <immintrin.h>
 
+#include <chrono>
 #include <cmath>
 #include <string>
 #include <thread>
@@ -319,7 +320,11 @@ static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const 
   // f64 -> f32 narrowed on the host (large uploads; identical validation)
   const bool narrow = htype == GFB_W_F64 && g->wtype == GFB_W_F32 && m >= HOST_NARROW_MIN_EDGES;
   uint64_t host_bad_w = ~0ull;
-  const size_t wsz = narrow ? 4 : host_wsize(htype);
+  const size_t wsz = host_wsize(htype);
+  // narrowing pays while a chunk narrows faster than PCIe would carry its
+  // doubles (~55 GB/s for col + 8-byte weights); on a busy host it falls
+  // back to the device conversion for the remaining chunks
+  bool narrow_now = narrow;
   // staging layout per buffer: col[chunk] | w[chunk]; chunk rounded to 64 so
   // every sub-array stays 16-byte aligned for any weight width
   const uint64_t chunk = (std::min<uint64_t>(UPLOAD_CHUNK, std::max<uint64_t>(m, 1)) + 63) & ~63ull;
@@ -362,12 +367,16 @@ static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const 
     void* dw = g->stage.as<char>() + b * chunk * 12 + chunk * 4;
     if (k >= 2) GFB_CUDA(cudaStreamWaitEvent(cp, done[b], 0));  // buffer b consumed
     GFB_CUDA(cudaMemcpyAsync(dcol, col + e0, cnt * 4, cudaMemcpyHostToDevice, cp));
-    if (narrow) {
+    const bool nk = narrow_now;  // this chunk narrowed on the host
+    if (nk) {
       // host buffer b was last read by the copy of chunk k - 2: wait for it,
       // then narrow this chunk while the previous chunk's copies run
       float* hb = g->hstage.as<float>() + b * chunk;
       if (k >= 2) GFB_CUDA(cudaEventSynchronize(g->hdone[b]));
+      const auto t0 = std::chrono::steady_clock::now();
       const uint64_t bw = narrow_weights(static_cast<const double*>(w) + e0, hb, cnt);
+      const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (sec > (double)cnt * 12.0 / 55e9) narrow_now = false;
       if (bw != ~0ull) host_bad_w = std::min(host_bad_w, e0 + bw);
       GFB_CUDA(cudaMemcpyAsync(dw, hb, cnt * 4, cudaMemcpyHostToDevice, cp));
       GFB_CUDA(cudaEventRecord(g->hdone[b], cp));
@@ -377,7 +386,7 @@ static void fill_graph(Graph* g, const uint32_t* ro, const uint32_t* col, const 
     }
     GFB_CUDA(cudaEventRecord(ready[b], cp));
     GFB_CUDA(cudaStreamWaitEvent(s, ready[b], 0));
-    if (narrow) launch_interleave<float>(g, dcol, dw, GFB_W_F32, e0, cnt, f);
+    if (nk) launch_interleave<float>(g, dcol, dw, GFB_W_F32, e0, cnt, f);
     else if (g->wtype == GFB_W_F32) launch_interleave<float>(g, dcol, dw, htype, e0, cnt, f);
     else if (g->wtype == GFB_W_F64) launch_interleave<double>(g, dcol, dw, htype, e0, cnt, f);
     else launch_interleave<uint32_t>(g, dcol, dw, htype, e0, cnt, f);
