@@ -286,12 +286,12 @@ k_fcount_o(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uin
   __shared__ uint32_t s_c[OB_N], s_e[OB_N];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x < OB_N) s_c[threadIdx.x] = s_e[threadIdx.x] = 0;
-  __syncthreads();
   const uint32_t base = ctl->fmin >> OB_SHIFT;
   const uint32_t wbase = blockIdx.x * F_WORDS + warp * F_WPW;
   // the tile's words in two halves of F_WPW / 2: 12 loads in flight per
   // lane and no register spills at the 32-register cap (one batch of 8
-  // words spilled: s24 3.36 -> 3.26 ms with the halves)
+  // words spilled: s24 3.36 -> 3.26 ms with the halves); the bitmap words
+  // are loaded before the barrier that publishes the cleared counters
   uint32_t raw, chk = 0;
   {
     uint32_t my = 0;
@@ -304,6 +304,7 @@ k_fcount_o(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ bm, uin
       }
     }
     raw = my;
+    __syncthreads();
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       constexpr int HW = F_WPW / 2;
@@ -444,6 +445,16 @@ k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
   }
   const uint32_t base = ctl->blo >> OB_SHIFT;
   const uint32_t wbase = blockIdx.x * F_WORDS + warp * F_WPW;
+  // this warp's bitmap words, loaded while warp 0 reserves the cells
+  uint32_t my = 0, chk = 0;
+  if (lane < F_WPW && wbase + lane < nwords) {
+    my = bm_next[wbase + lane];
+    if (DEXP && rbm && (tf & 2u)) {
+      const uint32_t r = rbm[wbase + lane];
+      chk = r & ~my;
+      my |= r;
+    }
+  }
   // a tile whose set bits are all deferred: no row offsets / distances to
   // load, its bitmap words stay (degree-0 bits included: the count pass
   // ignores them), only the placed-set bitmap is cleared (s24: 3.43 -> 3.39 ms)
@@ -475,15 +486,6 @@ k_fwrite_o(const uint32_t* __restrict__ ro, uint32_t* bm_next, uint32_t* bm_cur,
   // two halves of F_WPW / 2 words, loads then placements (no spills at the
   // 32-register cap, like k_fcount_o: s24 3.26 -> 3.20 ms)
   {
-    uint32_t my = 0, chk = 0;
-    if (lane < F_WPW && wbase + lane < nwords) {
-      my = bm_next[wbase + lane];
-      if (DEXP && rbm && (tf & 2u)) {
-        const uint32_t r = rbm[wbase + lane];
-        chk = r & ~my;
-        my |= r;
-      }
-    }
     raw = my;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
